@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""Benchmark of the pffmg hot path (BASELINE.json metric) -- one JSON line.
+
+Headline workload: cfg2 (BASELINE configs[1]) -- 2D notched square, 1024^2 Q1
+quads, 3,151,875 fp64 DoFs, NoSplit, 8-level GMG, Chebyshev degree 3.
+
+* a "step" is one application of the linearised monolithic Jacobian (vmult,
+  the north-star kernel) to a seeded N(0,1) vector, inputs resident in HBM,
+  L2 flushed (512 MiB write) before every step; timed with CUDA events on the
+  launching stream.  value = GDoF/s = DoFs x steps / sum(step time), summed
+  over ranks (max-over-ranks time).
+* e2e: the same metric through the public API `PhaseFieldOperator.apply`
+  with pinned host buffers (H2D of v, kernel, D2H of the result inside the
+  timed region).
+* solve: one Newton-step linear solve (build_level_contexts + GMRES(30) to
+  rel 1e-8 with the V(1,1) GMG preconditioner), the second half of the metric.
+* roofline: achieved = B_C (SURVEY §8d algorithmic bytes of the reference's
+  cached-coefficient vmult) / kernel time; B_F (the recompute model this
+  kernel implements) and ncu DRAM bytes reported beside it.
+* cpu_baseline: the CPU oracle port of the reference vmult on the host cores.
+
+`--impl reference` times the CPU oracle port (the reference is pure Python
+and cannot travel to the box) on the same workload and prints the same line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PFF Jacobian vmult GDoF/s and GMG-GMRES solve time/Newton step, % HBM roofline"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def algorithmic_bytes(dim, V, C):
+    """B_C (cached tables, the reference algorithm) and B_F (recompute)."""
+    nc, Q = dim + 1, 2 ** dim
+    b_c = 16 * nc * V + 8 * Q * (2 + dim * (dim + 1) // 2) * C + nc * V
+    b_f = 8 * (3 * nc + 1) * V + nc * V
+    return b_c, b_f
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except (ValueError, IndexError):
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_vmult_rate(prob, threads, reps):
+    """Oracle port of the reference vmult (oracle/, CPU): GDoF/s, median of reps."""
+    from oracle import fe, jacobian, meshgen
+    levels = meshgen.build_hierarchy(prob.blocks, prob.n_levels, prob.dim)
+    T = fe.LevelTables(levels[-1], prob.n_levels - 1)
+    p = prob.params
+    mat = jacobian.Material(mu=p.mu, lam=p.lam, g_c=p.g_c, kappa=p.kappa, eps=p.eps)
+    st = jacobian.State(U=prob.state.U, U_prev1=prob.state.U, U_prev2=prob.state.U, t=0.0,
+                        t_prev1=0.0, t_prev2=0.0, phi_tilde=prob.state.phi_tilde)
+    mask = prob.dirichlet.is_constrained | prob.active
+    t0 = time.perf_counter()
+    op = jacobian.JacobianOperator(T, st, mask, mat, threads=threads)
+    t_cache = time.perf_counter() - t0
+    op.apply(prob.v)                                      # warm
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        op.apply(prob.v)
+        ts.append(time.perf_counter() - t0)
+    return prob.n_dofs / float(np.median(ts)) * 1e-9, float(np.median(ts)), t_cache, ts
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1902_08112_b200 import configs
+    prob = configs.make(args.config)
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    rate, med, t_cache, ts = cpu_vmult_rate(prob, threads, args.warmup + args.steps)
+    steps = ts[args.warmup:]
+    per = float(np.mean(steps))
+    value = prob.n_dofs / per * 1e-9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GDoF/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8d)",
+        "config": {"workload": f"{args.config} vmult", "n_dofs": prob.n_dofs},
+        "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.config} full-size vmult x{args.steps} (oracle/ numpy "
+                                   f"restatement of model.py:368-375, {threads} threads); "
+                                   f"coefficient cache build {t_cache:.2f}s excluded"},
+        "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1902_08112_b200 import _lib, configs, krylov, mgsolve
+    from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, SplitKind
+
+    prob = configs.make(args.config)
+    mesh = prob.disc.hierarchy.finest
+    mask = prob.dirichlet.combined_with(prob.active, np.zeros(prob.n_dofs))
+    op = PhaseFieldOperator(prob.disc.finest, prob.state,
+                            ConstraintMask(mask.is_constrained, mask.inhomogeneity),
+                            prob.params, SplitKind.NOSPLIT)
+    n = prob.n_dofs
+    v = torch.as_tensor(prob.v, device="cuda")
+    out = torch.empty_like(v)
+    flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        op.apply_dev(_lib.FULL, v, out)
+
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        t0 = time.perf_counter()
+        for e0, e1 in evs:
+            flush.zero_()
+            e0.record(stream)
+            step()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    t_tot = float(np.sum(step_ms)) * 1e-3
+    if ws > 1:
+        tt = torch.tensor([t_tot], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_tot = float(tt.item())
+    per = t_tot / args.steps
+    value = ws * n / per * 1e-9
+
+    # ---------------------------------------------------------------- e2e
+    h_in = torch.from_numpy(prob.v.copy()).pin_memory()
+    h_out = torch.empty(n, dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        op.apply(h_in, out=h_out)
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(max(3, min(args.steps, 20))):
+        t0 = time.perf_counter()
+        op.apply(h_in, out=h_out)
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_per = float(np.median(e2e_t))
+
+    # -------------------------------------------------------------- solve
+    solve = None
+    if not args.no_solve:
+        rhs = torch.as_tensor(configs.fallback_rhs(prob), device="cuda")
+        ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+
+        def newton_step():
+            t0 = time.perf_counter()
+            ctxs = mgsolve.build_level_contexts(prob.disc, prob.state, prob.active, prob.dirichlet,
+                                                prob.params, SplitKind.NOSPLIT)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            pc = mgsolve.VCyclePreconditioner(ctxs, degree=prob.degree)
+            x, its = krylov.gmres(ctxs[-1].op.apply, pc, rhs, ctl)
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            return t1 - t0, t2 - t1, its
+
+        newton_step()                                   # warm (graph capture, probes)
+        setup_s, gmres_s, its = newton_step()
+        solve = {"setup_ms": setup_s * 1e3, "gmres_ms": gmres_s * 1e3, "gmres_iters": its,
+                 "ms_per_newton_step": (setup_s + gmres_s) * 1e3,
+                 "rhs": "seeded N(0,1), constrained rows zeroed (SURVEY §8d fallback)",
+                 "control": "GMRES(30) rel 1e-8 abs 0, V(1,1) FULL, Chebyshev deg %d" % prob.degree}
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+
+    hbm, peak_kind = peaks()
+    b_c, b_f = algorithmic_bytes(prob.dim, mesh.n_vertices, mesh.n_cells)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_vmult_cfg2.json")
+    if os.path.exists(prof) and args.config == "cfg2":
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    achieved = b_c / per * 1e-9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded state/vector, SURVEY §8d; random-init, no dataset)",
+        "config": {"workload": f"{args.config}: 2D notched square 1024^2 Q1 NoSplit vmult"
+                   if args.config == "cfg2" else args.config,
+                   "n_dofs": n, "n_vertices": mesh.n_vertices, "n_cells": mesh.n_cells,
+                   "l2": "flushed (512 MiB write) before every step",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic,
+                     "bytes_model": "B_C = 16 n_c V + 8 Q (2 + d(d+1)/2) C + n_c V (SURVEY §8d)",
+                     "algorithmic_bytes_BC": b_c, "algorithmic_bytes_BF": b_f,
+                     "frac_BF": b_f / per * 1e-9 / hbm,
+                     "frac_ncu": (traffic / per * 1e-9 / hbm) if traffic else None,
+                     "peak_kind": peak_kind},
+        "e2e": {"value": n / e2e_per * 1e-9, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n,
+                "path": "PhaseFieldOperator.apply(pinned host tensor, out=pinned host tensor)"},
+        "gpu_launches": args.steps,
+        "solve": solve,
+        "wall_s_timed_region": wall,
+        "step_ms_min_max": [float(np.min(step_ms)), float(np.max(step_ms))],
+    }
+    line["clocks"] = clk.summary()
+    if not args.no_cpu and ws == 1:
+        threads = os.cpu_count() or 1
+        rate, med, t_cache, _ = cpu_vmult_rate(prob, threads, 3)
+        line["cpu_baseline"] = {"value": rate, "unit": "GDoF/s", "cores": threads, "kind": "port",
+                                "sample": f"{args.config} full-size vmult, median of 3 (oracle/ "
+                                          f"numpy port of model.py:368-375, {threads} threads, "
+                                          f"{med * 1e3:.0f} ms each)"}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="pffmg", choices=["pffmg", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg4", "cfg5"])
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

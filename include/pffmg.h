@@ -1,0 +1,192 @@
+/*
+ * pffmg — B200-native matrix-free phase-field-fracture Jacobian + GMG kernels.
+ *
+ * Flat C ABI of libpffmg.so (built for sm_100a).  Every entry point takes
+ * plain device pointers (fp64 vectors in the reference's component-major dof
+ * layout gid = c*V + v, reference fem.py:1-4 / fem.py:91-126), sizes, and a
+ * cudaStream_t passed as void*.  Every call returns an int status
+ * (0 = ok); pffmg_last_error() returns the message of the last failure on the
+ * calling thread.  No C++ exceptions cross this boundary.  All work is
+ * enqueued asynchronously on the given stream; the library never
+ * synchronises except in the functions documented as returning host data.
+ *
+ * The reference (fracmg, pure Python) binds these through ctypes; the host
+ * twins live in paper_1902_08112_b200/ and INTEGRATION.md shows the binding.
+ * Reference paths below are relative to /root/reference/pkg/src/fracmg/.
+ */
+#ifndef PFFMG_H
+#define PFFMG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFFMG_OK 0
+#define PFFMG_ERR_ARG 1
+#define PFFMG_ERR_CUDA 2
+#define PFFMG_ERR_UNSUPPORTED 3
+
+/* Which part of the Jacobian a vmult applies (reference model.py:368-392). */
+#define PFFMG_FULL (-1)     /* PhaseFieldOperator.apply          model.py:368-375 */
+#define PFFMG_UBLOCK 0      /* apply_block(0, .) displacement    model.py:377-392 */
+#define PFFMG_PBLOCK 1      /* apply_block(1, .) phase field     model.py:377-392 */
+
+/*
+ * Level geometry: a (possibly non-box) lattice of congruent cells.  Vertex
+ * numbering follows the reference mesh (mesh.py:163-194): x fastest, rows of
+ * constant (y, z) contiguous.  For a box lattice the row tables are NULL and
+ * vertex id = x + (nx+1)*(y + (ny+1)*z).  Otherwise, for vertex row
+ * r = y + (ny+1)*z the vertices x in [vrow_lo[r], vrow_hi[r]) have ids
+ * vrow_off[r] + (x - vrow_lo[r]); for cell row s = y + ny*z the cells
+ * x in [crow_lo[s], crow_hi[s]) exist.  All table pointers are DEVICE pointers.
+ */
+typedef struct {
+    int32_t dim;            /* 2 or 3 */
+    int32_t nx, ny, nz;     /* cells per axis of the bounding lattice (nz = 0 in 2D) */
+    double hx, hy, hz;      /* cell edge lengths (LevelMesh.cell_size) */
+    int64_t n_vertices;     /* V: component stride of every dof vector */
+    const int64_t* vrow_off;
+    const int32_t* vrow_lo;
+    const int32_t* vrow_hi;
+    const int32_t* crow_lo;
+    const int32_t* crow_hi;
+} pffmg_lattice;
+
+/*
+ * Linearisation state + material of one level (model.py:89-119, 270-309).
+ * The per-quadrature-point coefficient tables of _build_caches are NOT
+ * stored: the kernels recompute gk, T_phiu, a_phiphi on the fly from U and
+ * phi_tilde (SURVEY §8d "model F").
+ */
+typedef struct {
+    double mu, lam, g_c, kappa, eps;
+    double pressure;            /* MaterialParams.pressure(state.t) */
+    int32_t split;              /* 0 = NOSPLIT; 1 = MIEHE (returns PFFMG_ERR_UNSUPPORTED for now) */
+    int32_t pad_;
+    const double* U;            /* (dim+1)*V linearisation point (may be NULL for the u block) */
+    const double* phi_tilde;    /* V extrapolated phase field (may be NULL for the phi block) */
+    const double* rho;          /* NULL (rho == 1) or modulus field per lattice cell x QP */
+    const uint8_t* flags;       /* V packed constraint bits: bit c <=> dof c*V+v constrained */
+} pffmg_state;
+
+const char* pffmg_last_error(void);
+int pffmg_version(void);
+int pffmg_device_sm_count(int* out);
+
+/* ---------------------------------------------------------------- operator */
+
+/* out = G~ v restricted to `which` (model.py:368-392): constrained entries of
+ * v read as 0, constrained rows copy v.  v/out point at the block's first
+ * component (component stride = lattice->n_vertices). */
+int pffmg_apply(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                const double* v, double* out, void* stream);
+
+/* out = b - A x (mgsolve.py:95, 100, 227): fused residual. out != x. */
+int pffmg_residual(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                   const double* x, const double* b, double* out, void* stream);
+
+/* Exact operator diagonal, constrained entries = 1.0 (model.py:394-413). */
+int pffmg_diagonal(const pffmg_lattice* lat, const pffmg_state* st, double* out, void* stream);
+
+/* One fused Chebyshev step of chebyshev_apply's recurrence (mgsolve.py:107-112):
+ *   r -= A d_in;  d_out = c_dd*d_in + c_dr*(invdiag*r);  x += d_out
+ * or, with x_add_din = 1 (first step after pffmg_cheb_init),
+ *   x = (x + d_in) + d_out   -- the same rounding as the reference's two updates.
+ * d_out != d_in; x is not read by the stencil so it is updated in place. */
+int pffmg_cheb_step(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                    const double* d_in, double* d_out, double* r, double* x,
+                    const double* invdiag, double c_dd, double c_dr, int x_add_din,
+                    void* stream);
+
+/* Start of chebyshev_apply from a non-zero x (mgsolve.py:95, 103-105):
+ *   r = b - A x;  d = (invdiag*r)/theta.
+ * The update x += d is deferred to the first pffmg_cheb_step (x_add_din = 1)
+ * or done by pffmg_axpy when the degree is 1, so x is never written while
+ * other CTAs still read it through the stencil. */
+int pffmg_cheb_init(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                    const double* x, const double* b, double* r, double* d,
+                    const double* invdiag, double theta, void* stream);
+
+/* ---------------------------------------------------------------- transfers */
+/* fem.py:308-411 with the V-cycle masking of mgsolve.py:228-234.
+ * `coarse`/`fine` are consecutive levels l and l+1; n_comp components. */
+
+/* vc = P^T vf per component; if coarse_flags != NULL, constrained coarse
+ * entries are set to 0 (mgsolve.py:228-229). */
+int pffmg_restrict(const pffmg_lattice* coarse, const pffmg_lattice* fine, int n_comp,
+                   int comp0, const double* vf, double* vc, const uint8_t* coarse_flags,
+                   void* stream);
+
+/* vf = P vc per component (fine_flags == NULL, accumulate == 0) or
+ * vf += (fine constrained ? 0 : P vc) (mgsolve.py:232-234, accumulate = 1). */
+int pffmg_prolongate(const pffmg_lattice* coarse, const pffmg_lattice* fine, int n_comp,
+                     int comp0, const double* vc, double* vf, const uint8_t* fine_flags,
+                     int accumulate, void* stream);
+
+/* Nodal injection of n_comp fp64 components (fem.py:361-363, 394-401). */
+int pffmg_inject_f64(const pffmg_lattice* coarse, const pffmg_lattice* fine, int n_comp,
+                     const double* vf, double* vc, void* stream);
+/* Injection of packed constraint flags (mgsolve.py:182-186): bit-exact. */
+int pffmg_inject_flags(const pffmg_lattice* coarse, const pffmg_lattice* fine,
+                       const uint8_t* ff, uint8_t* fc, void* stream);
+/* Injection map coarse vertex -> fine vertex id (fem.py:346-351, 365-367). */
+int pffmg_injection_map(const pffmg_lattice* coarse, const pffmg_lattice* fine,
+                        int64_t* out, void* stream);
+
+/* ----------------------------------------------------------- masks / vectors */
+
+/* flags[v] = OR_c (mask[c*V+v] != 0) << c. */
+int pffmg_pack_flags(const uint8_t* mask, int n_comp, int64_t V, uint8_t* flags, void* stream);
+int pffmg_unpack_flags(const uint8_t* flags, int n_comp, int64_t V, uint8_t* mask, void* stream);
+/* out = constrained ? 0 : in over components [comp0, comp0+n_comp). */
+int pffmg_masked_copy(const uint8_t* flags, int64_t V, int comp0, int n_comp,
+                      const double* in, double* out, void* stream);
+/* invdiag = 1 / diag. */
+int pffmg_reciprocal(const double* diag, double* out, int64_t n, void* stream);
+/* Chebyshev start from x = 0 (mgsolve.py:95, 103-106): r = b; d = (inv*r)/theta; x = d. */
+int pffmg_cheb_init_zero(const double* b, const double* invdiag, double theta,
+                         double* r, double* d, double* x, int64_t n, void* stream);
+/* Degenerate-range update (mgsolve.py:99): x += (inv*r)/theta. */
+int pffmg_jacobi_update(const double* r, const double* invdiag, double theta,
+                        double* x, int64_t n, void* stream);
+
+/* y = a*x + y ; x = a*x ; y = x - y etc. */
+int pffmg_axpy(double a, const double* x, double* y, int64_t n, void* stream);
+int pffmg_axpby(double a, const double* x, double b, double* y, int64_t n, void* stream);
+int pffmg_scale(double a, double* x, int64_t n, void* stream);
+int pffmg_copy(const double* x, double* y, int64_t n, void* stream);
+/* out = x - y */
+int pffmg_sub(const double* x, const double* y, double* out, int64_t n, void* stream);
+
+/* Deterministic reductions: fixed grid, fixed per-block tree, fixed-order
+ * final sum -> bitwise reproducible for a given n.  Result written to the
+ * DEVICE double *result. */
+int pffmg_dot(const double* x, const double* y, int64_t n, double* result, void* stream);
+int pffmg_dot_scaled(const double* x, const double* y, const double* s, int64_t n,
+                     double* result, void* stream);   /* sum x*(s*y) ... see docs */
+
+/* GMRES Arnoldi (krylov.py:93-107), device-resident H column:
+ *   for i in 0..j: h[i] = V_i . w ; w -= h[i] V_i      (modified Gram-Schmidt)
+ * with the conditional second pass when ||w|| < 1e-3 ||w0||, then
+ * h[j+1] = ||w||, V_{j+1} = w / h[j+1] (if nonzero).  Vb is the (m+1) x ld
+ * row-major basis, h is a device array of length >= j+2.  Returns nothing on
+ * the host; the caller reads h. */
+int pffmg_arnoldi_mgs(double* Vb, int64_t ld, int j, double* w, int64_t n, double* h,
+                      double* scratch, void* stream);
+/* x += sum_i y[i] * Z_i, i < k (krylov.py:132); y is a DEVICE array. */
+int pffmg_multi_axpy(const double* Z, int64_t ld, int k, const double* y, double* x,
+                     int64_t n, void* stream);
+
+/* Jacobi-PCG Lanczos for estimate_spectrum (krylov.py:146-185), device part.
+ * State vector layout: see pffmg_cg_* in csrc/vectors.cu. */
+int pffmg_cg_start(const double* b, const double* diag, double* r, double* z, double* p,
+                   int64_t n, double* scal, void* stream);
+int pffmg_cg_step(const double* Ap, const double* diag, double* r, double* z, double* p,
+                  int64_t n, double* scal, int phase, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFFMG_H */

@@ -1,0 +1,127 @@
+"""ctypes binding of libpffmg.so (the C ABI declared in include/pffmg.h).
+
+The shared library is built in-tree (`make -C paper_1902_08112_b200/csrc`,
+or `__graft_entry__.build()`).  There is no fallback: if the library or a
+CUDA device is missing, the product path raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpffmg.so")
+
+FULL, UBLOCK, PBLOCK = -1, 0, 1
+
+c_double_p = C.POINTER(C.c_double)
+vp = C.c_void_p
+
+
+class Lattice(C.Structure):
+    """pffmg_lattice (include/pffmg.h)."""
+    _fields_ = [("dim", C.c_int32), ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
+                ("hx", C.c_double), ("hy", C.c_double), ("hz", C.c_double),
+                ("n_vertices", C.c_int64),
+                ("vrow_off", vp), ("vrow_lo", vp), ("vrow_hi", vp),
+                ("crow_lo", vp), ("crow_hi", vp)]
+
+
+class State(C.Structure):
+    """pffmg_state (include/pffmg.h)."""
+    _fields_ = [("mu", C.c_double), ("lam", C.c_double), ("g_c", C.c_double),
+                ("kappa", C.c_double), ("eps", C.c_double), ("pressure", C.c_double),
+                ("split", C.c_int32), ("pad_", C.c_int32),
+                ("U", vp), ("phi_tilde", vp), ("rho", vp), ("flags", vp)]
+
+
+# name -> argtypes (restype is always c_int status unless noted)
+_SIGS = {
+    "pffmg_version": [],
+    "pffmg_device_sm_count": [C.POINTER(C.c_int)],
+    "pffmg_apply": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp],
+    "pffmg_residual": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp],
+    "pffmg_diagonal": [C.POINTER(Lattice), C.POINTER(State), vp, vp],
+    "pffmg_cheb_step": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp,
+                        C.c_double, C.c_double, C.c_int, vp],
+    "pffmg_cheb_init": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp,
+                        C.c_double, vp],
+    "pffmg_restrict": [C.POINTER(Lattice), C.POINTER(Lattice), C.c_int, C.c_int, vp, vp, vp, vp],
+    "pffmg_prolongate": [C.POINTER(Lattice), C.POINTER(Lattice), C.c_int, C.c_int, vp, vp, vp,
+                         C.c_int, vp],
+    "pffmg_inject_f64": [C.POINTER(Lattice), C.POINTER(Lattice), C.c_int, vp, vp, vp],
+    "pffmg_inject_flags": [C.POINTER(Lattice), C.POINTER(Lattice), vp, vp, vp],
+    "pffmg_injection_map": [C.POINTER(Lattice), C.POINTER(Lattice), vp, vp],
+    "pffmg_pack_flags": [vp, C.c_int, C.c_int64, vp, vp],
+    "pffmg_unpack_flags": [vp, C.c_int, C.c_int64, vp, vp],
+    "pffmg_masked_copy": [vp, C.c_int64, C.c_int, C.c_int, vp, vp, vp],
+    "pffmg_reciprocal": [vp, vp, C.c_int64, vp],
+    "pffmg_cheb_init_zero": [vp, vp, C.c_double, vp, vp, vp, C.c_int64, vp],
+    "pffmg_jacobi_update": [vp, vp, C.c_double, vp, C.c_int64, vp],
+    "pffmg_axpy": [C.c_double, vp, vp, C.c_int64, vp],
+    "pffmg_axpby": [C.c_double, vp, C.c_double, vp, C.c_int64, vp],
+    "pffmg_scale": [C.c_double, vp, C.c_int64, vp],
+    "pffmg_copy": [vp, vp, C.c_int64, vp],
+    "pffmg_sub": [vp, vp, vp, C.c_int64, vp],
+    "pffmg_dot": [vp, vp, C.c_int64, vp, vp],
+    "pffmg_dot_scaled": [vp, vp, vp, C.c_int64, vp, vp],
+    "pffmg_arnoldi_mgs": [vp, C.c_int64, C.c_int, vp, C.c_int64, vp, vp, vp],
+    "pffmg_multi_axpy": [vp, C.c_int64, C.c_int, vp, vp, C.c_int64, vp],
+    "pffmg_cg_start": [vp, vp, vp, vp, vp, C.c_int64, vp, vp],
+    "pffmg_cg_step": [vp, vp, vp, vp, vp, C.c_int64, vp, C.c_int, vp],
+}
+
+_lib = None
+
+
+class PffmgError(RuntimeError):
+    """A libpffmg call returned a non-zero status."""
+
+
+def load():
+    """Load libpffmg.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise PffmgError(f"{LIB_PATH} not built: run `make -C {_HERE}/csrc` "
+                             "(or __graft_entry__.build())")
+        lib = C.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        lib.pffmg_last_error.argtypes = []
+        lib.pffmg_last_error.restype = C.c_char_p
+        _lib = lib
+    return _lib
+
+
+def exported_symbols():
+    return ["pffmg_last_error"] + list(_SIGS)
+
+
+def call(name, *args):
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.pffmg_last_error().decode(errors="replace")
+        raise PffmgError(f"{name} failed (status {rc}): {msg}")
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise PffmgError("pffmg needs a CUDA device (sm_100a); there is no CPU fallback")
+    load()
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    """Device pointer of a tensor (or None)."""
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())

@@ -1,0 +1,108 @@
+// Error state, device queries and host-side construction of the kernel
+// argument structs for libpffmg.
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace pffmg {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: CUDA launch failed: %s", what, cudaGetErrorString(e));
+        return PFFMG_ERR_CUDA;
+    }
+    return PFFMG_OK;
+}
+
+int sm_count() {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+        cached = n;
+    }
+    return cached;
+}
+
+int make_lat(const pffmg_lattice* in, Lat* out) {
+    PFFMG_REQUIRE(in, "null lattice");
+    PFFMG_REQUIRE(in->dim == 2 || in->dim == 3, "lattice dim must be 2 or 3 (got %d)", in->dim);
+    PFFMG_REQUIRE(in->nx >= 1 && in->ny >= 1 && (in->dim == 2 ? in->nz == 0 : in->nz >= 1),
+                  "bad lattice extents %d x %d x %d", in->nx, in->ny, in->nz);
+    PFFMG_REQUIRE(in->n_vertices > 0, "n_vertices must be positive");
+    const bool has_rows = in->vrow_off != nullptr;
+    PFFMG_REQUIRE(has_rows == (in->vrow_lo != nullptr) && has_rows == (in->vrow_hi != nullptr) &&
+                      has_rows == (in->crow_lo != nullptr) && has_rows == (in->crow_hi != nullptr),
+                  "row tables must be all NULL (box) or all set");
+    if (!has_rows) {
+        const int64_t Vbox = (int64_t)(in->nx + 1) * (in->ny + 1) * (in->dim == 3 ? in->nz + 1 : 1);
+        PFFMG_REQUIRE(Vbox == in->n_vertices, "box lattice has %lld vertices, n_vertices=%lld",
+                      (long long)Vbox, (long long)in->n_vertices);
+    }
+    out->dim = in->dim;
+    out->nx = in->nx;
+    out->ny = in->ny;
+    out->nz = in->nz;
+    out->hx = in->hx;
+    out->hy = in->hy;
+    out->hz = in->hz;
+    out->V = in->n_vertices;
+    out->vrow_off = in->vrow_off;
+    out->vrow_lo = in->vrow_lo;
+    out->vrow_hi = in->vrow_hi;
+    out->crow_lo = in->crow_lo;
+    out->crow_hi = in->crow_hi;
+    return PFFMG_OK;
+}
+
+int make_consts(const pffmg_lattice* lat, const pffmg_state* st, Consts* K) {
+    PFFMG_REQUIRE(lat->hx > 0 && lat->hy > 0 && (lat->dim == 2 || lat->hz > 0), "cell sizes must be > 0");
+    PFFMG_REQUIRE(st->eps > 0, "eps must be > 0");
+    // fem.py:33-34
+    K->g0 = 0.5 - 0.5 / std::sqrt(3.0);
+    K->g1 = 0.5 + 0.5 / std::sqrt(3.0);
+    K->omg0 = 1.0 - K->g0;
+    K->omg1 = 1.0 - K->g1;
+    K->ih[0] = 1.0 / lat->hx;
+    K->ih[1] = 1.0 / lat->hy;
+    K->ih[2] = lat->dim == 3 ? 1.0 / lat->hz : 0.0;
+    // JxW = w_q * cell volume, w_q = 0.5^dim (fem.py:179)
+    const double vol = lat->dim == 3 ? lat->hx * lat->hy * lat->hz : lat->hx * lat->hy;
+    K->jxw = (lat->dim == 3 ? 0.125 : 0.25) * vol;
+    K->mu = st->mu;
+    K->lam = st->lam;
+    K->kappa = st->kappa;
+    K->omk = 1.0 - st->kappa;
+    K->two_p = 2.0 * st->pressure;
+    K->gc_over_eps = st->g_c / st->eps;
+    K->k_phi = st->g_c * st->eps;
+    return PFFMG_OK;
+}
+
+}  // namespace pffmg
+
+using namespace pffmg;
+
+extern "C" const char* pffmg_last_error(void) { return g_err; }
+
+extern "C" int pffmg_version(void) { return 1; }
+
+extern "C" int pffmg_device_sm_count(int* out) {
+    PFFMG_REQUIRE(out, "null out");
+    *out = sm_count();
+    return PFFMG_OK;
+}

@@ -1,0 +1,165 @@
+// Shared device-side helpers of libpffmg: lattice addressing, error state,
+// and the 2-point tensor-product (sum-factorised) Q1 kernels.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "../../include/pffmg.h"
+
+namespace pffmg {
+
+// ------------------------------------------------------------------ errors
+
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+
+#define PFFMG_REQUIRE(cond, ...)                                  \
+    do {                                                          \
+        if (!(cond)) {                                            \
+            ::pffmg::set_error(__VA_ARGS__);                      \
+            return PFFMG_ERR_ARG;                                 \
+        }                                                         \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();
+
+// ----------------------------------------------------------------- lattice
+
+// Kernel-side copy of pffmg_lattice (passed by value).
+struct Lat {
+    int dim, nx, ny, nz;
+    double hx, hy, hz;
+    int64_t V;
+    const int64_t* __restrict__ vrow_off;
+    const int32_t* __restrict__ vrow_lo;
+    const int32_t* __restrict__ vrow_hi;
+    const int32_t* __restrict__ crow_lo;
+    const int32_t* __restrict__ crow_hi;
+};
+
+int make_lat(const pffmg_lattice* in, Lat* out);
+
+// Vertex id of lattice point (x, y, z) or -1 when absent (reference vertex
+// numbering, mesh.py:163-194: x fastest, rows contiguous).
+__device__ __forceinline__ int64_t vertex_id(const Lat& L, int x, int y, int z) {
+    if (x < 0 || y < 0 || z < 0 || x > L.nx || y > L.ny || z > L.nz) return -1;
+    if (L.vrow_off == nullptr)
+        return (int64_t)x + (int64_t)(L.nx + 1) * ((int64_t)y + (int64_t)(L.ny + 1) * z);
+    const int r = y + (L.ny + 1) * z;
+    const int lo = __ldg(L.vrow_lo + r), hi = __ldg(L.vrow_hi + r);
+    if (x < lo || x >= hi) return -1;
+    return __ldg(L.vrow_off + r) + (x - lo);
+}
+
+template <int D>
+__device__ __forceinline__ bool cell_exists(const Lat& L, int x, int y, int z) {
+    if (x < 0 || y < 0 || x >= L.nx || y >= L.ny) return false;
+    if (D == 3 && (z < 0 || z >= L.nz)) return false;
+    if (L.crow_lo == nullptr) return true;
+    const int s = y + L.ny * z;
+    return x >= __ldg(L.crow_lo + s) && x < __ldg(L.crow_hi + s);
+}
+
+// ------------------------------------------------------- element constants
+
+// Everything the cell kernels need besides the fields.  Built on the host
+// with the same double expressions as the reference tables (fem.py:33-34,
+// 174-179, model.py:270-309) so results agree to rounding.
+struct Consts {
+    double g0, g1;        // 2-pt Gauss points 0.5 -/+ 0.5/sqrt(3)
+    double omg0, omg1;    // 1 - g
+    double ih[3];         // 1 / cell_size
+    double jxw;           // quadrature weight * cell volume (identical for all QPs)
+    double mu, lam, kappa, omk, two_p, gc_over_eps, k_phi;
+};
+
+int make_consts(const pffmg_lattice* lat, const pffmg_state* st, Consts* K);
+
+// ----------------------------------------------- sum factorisation (2-pt Q1)
+//
+// Arrays of 2^D doubles are indexed by bit patterns: bit a of the index is the
+// corner offset (or quadrature-point index) along axis a, x fastest -- the
+// corner order of mesh.py:36-39 and the QP order of fem.py:44-51.
+
+template <int D>
+struct SF {
+    static constexpr int NP = 1 << D;
+
+    // value (p = 0) and raw derivatives (p = 1 + a, not yet scaled by 1/h)
+    // of one nodal field at the 2^D Gauss points (fem.py:229-238 einsums,
+    // factorised along the axes).  CSE merges the shared passes.
+    __device__ __forceinline__ static void interp(const double (&c)[NP], double (&out)[D + 1][NP],
+                                                  const Consts& K, bool need_val = true) {
+#pragma unroll
+        for (int p = 0; p <= D; ++p)
+#pragma unroll
+            for (int i = 0; i < NP; ++i) out[p][i] = c[i];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+#pragma unroll
+            for (int p = 0; p <= D; ++p) {
+                if (p == 0 && !need_val) continue;
+#pragma unroll
+                for (int i = 0; i < NP; ++i) {
+                    if (i & (1 << a)) continue;
+                    const int j = i | (1 << a);
+                    const double u0 = out[p][i], u1 = out[p][j];
+                    const double d = u1 - u0;
+                    if (p == a + 1) {
+                        out[p][i] = d;
+                        out[p][j] = d;
+                    } else {
+                        out[p][i] = fma(K.g0, d, u0);
+                        out[p][j] = fma(K.g1, d, u0);
+                    }
+                }
+            }
+        }
+    }
+
+    // out[n] = sum_q f[q] N_q(n) + sum_{q,a} g[a][q] dN_q(n)/dref_a
+    // (the transposed contraction of model.py:347-354).  f / g are consumed.
+    template <bool HAS_F>
+    __device__ __forceinline__ static void integrate(double (&f)[NP], double (&g)[D][NP],
+                                                     const Consts& K) {
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                if (i & (1 << a)) continue;
+                const int j = i | (1 << a);
+                // S <- B_a^T S + D_a^T G_a
+                const double s = g[a][i] + g[a][j];
+                if (HAS_F || a != D - 1) {
+                    const double f0 = f[i], f1 = f[j];
+                    f[i] = fma(K.omg0, f0, fma(K.omg1, f1, -s));
+                    f[j] = fma(K.g0, f0, fma(K.g1, f1, s));
+                } else {
+                    f[i] = -s;
+                    f[j] = s;
+                }
+                // G_b <- B_a^T G_b for b < a
+#pragma unroll
+                for (int b = 0; b < a; ++b) {
+                    const double q0 = g[b][i], q1 = g[b][j];
+                    g[b][i] = fma(K.omg0, q0, K.omg1 * q1);
+                    g[b][j] = fma(K.g0, q0, K.g1 * q1);
+                }
+            }
+        }
+    }
+};
+
+// Deterministic block reduction helpers --------------------------------------
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace pffmg

@@ -1,0 +1,462 @@
+// Krylov BLAS-1 and deterministic reductions (reference krylov.py:50-198 and
+// the vector updates of mgsolve.py:82-113).
+//
+// Every reduction runs on a grid whose size is a fixed function of n, sums
+// each thread's grid-stride slice in order, reduces the block with a fixed
+// shuffle/shared-memory tree, and lets the last block to finish add the block
+// partials in index order -- so results are bitwise reproducible run to run
+// (the reference guarantees thread-count independent results, README.md:92-97).
+// Scalars that steer later kernels (GMRES H entries, CG alpha/beta, stop
+// flags) stay in device memory so no host round trip is needed between steps.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace pffmg {
+
+constexpr int RT = 256;         // reduction block size
+constexpr int RMAXB = 1024;     // max reduction blocks
+
+struct Scratch {
+    double partial[2 * RMAXB];
+    unsigned int counter;
+};
+
+static Scratch* g_scratch = nullptr;
+
+static int scratch(Scratch** out) {
+    if (!g_scratch) {
+        if (cudaMalloc(&g_scratch, sizeof(Scratch)) != cudaSuccess ||
+            cudaMemset(g_scratch, 0, sizeof(Scratch)) != cudaSuccess) {
+            g_scratch = nullptr;
+            set_error("cannot allocate reduction scratch");
+            return PFFMG_ERR_CUDA;
+        }
+    }
+    *out = g_scratch;
+    return PFFMG_OK;
+}
+
+static int red_blocks(int64_t n) {
+    int64_t b = (n + RT * 8 - 1) / (RT * 8);
+    if (b < 1) b = 1;
+    if (b > RMAXB) b = RMAXB;
+    return (int)b;
+}
+
+__device__ __forceinline__ void block_sum2(double& a0, double& a1) {
+    __shared__ double s0[RT / 32], s1[RT / 32];
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+        s0[w] = a0;
+        s1[w] = a1;
+    }
+    __syncthreads();
+    if (w == 0) {
+        a0 = lane < RT / 32 ? s0[lane] : 0.0;
+        a1 = lane < RT / 32 ? s1[lane] : 0.0;
+        a0 = warp_sum(a0);
+        a1 = warp_sum(a1);
+    }
+}
+
+// Generic fused "elementwise update + up to two sums + scalar finisher".
+template <class Op>
+__global__ void __launch_bounds__(RT) fused_kernel(Op op, int64_t n, Scratch* S) {
+    if (op.skip()) return;
+    op.prepare();
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT)
+        op.elem(i, a0, a1);
+    if (!Op::REDUCES) return;
+    block_sum2(a0, a1);
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        S->partial[2 * blockIdx.x] = a0;
+        S->partial[2 * blockIdx.x + 1] = a1;
+        __threadfence();
+        const unsigned t = atomicAdd(&S->counter, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double s0 = 0.0, s1 = 0.0;
+        volatile double* p = S->partial;
+        for (unsigned b = 0; b < gridDim.x; ++b) {
+            s0 += p[2 * b];
+            s1 += p[2 * b + 1];
+        }
+        op.finish(s0, s1);
+        S->counter = 0;
+    }
+}
+
+template <class Op>
+static int run_fused(const Op& op, int64_t n, cudaStream_t s, const char* what) {
+    Scratch* S;
+    int rc = scratch(&S);
+    if (rc) return rc;
+    fused_kernel<Op><<<red_blocks(n), RT, 0, s>>>(op, n, S);
+    return check_launch(what);
+}
+
+// ---------------------------------------------------------------- ops
+
+struct DotOp {
+    static constexpr bool REDUCES = true;
+    const double* x;
+    const double* y;
+    const double* s;   // optional elementwise scale: sum x*y*s
+    double* result;
+    __device__ bool skip() const { return false; }
+    __device__ void prepare() {}
+    __device__ void elem(int64_t i, double& a0, double&) const {
+        a0 = s ? fma(x[i], y[i] * s[i], a0) : fma(x[i], y[i], a0);
+    }
+    __device__ void finish(double s0, double) const { *result = s0; }
+};
+
+// One modified Gram-Schmidt pass (krylov.py:97-107):
+//   w -= (*hprev) * Vprev   (if Vprev)
+//   s0 = Vcur . w           (if Vcur)
+//   s1 = w . w              (if NRM)
+struct MgsOp {
+    static constexpr bool REDUCES = true;
+    const double* Vprev;
+    const double* hprev;
+    const double* Vcur;
+    double* w;
+    double* ctl;       // [0] w0n2, [1] wn2, [2] reorth flag, [3..] corrections
+    double* hcol;      // H[:, j] (device)
+    int i;             // index of Vcur
+    int kind;          // 0: first pass, 1: middle, 2: last (norm), 3..5: re-orth variants
+    int gate;          // 1: only run when ctl[2] != 0
+    double hp;
+    __device__ bool skip() const { return gate && ctl[2] == 0.0; }
+    __device__ void prepare() { hp = Vprev ? *hprev : 0.0; }
+    __device__ void elem(int64_t k, double& a0, double& a1) const {
+        double wk = w[k];
+        if (Vprev) {
+            wk = fma(-hp, Vprev[k], wk);
+            w[k] = wk;
+        }
+        if (Vcur) a0 = fma(Vcur[k], wk, a0);
+        if (kind == 0 || kind == 2 || kind == 5) a1 = fma(wk, wk, a1);
+    }
+    __device__ void finish(double s0, double s1) const {
+        switch (kind) {
+            case 0: hcol[i] = s0; ctl[0] = s1; break;                 // first pass: H[0,j], ||w0||^2
+            case 1: hcol[i] = s0; break;                              // H[i,j]
+            case 2: {                                                 // after the last update
+                ctl[1] = s1;
+                const double wn = sqrt(s1), w0 = sqrt(ctl[0]);
+                ctl[2] = (wn < 1e-3 * w0) ? 1.0 : 0.0;                // krylov.py:101
+                hcol[i] = wn;                                         // H[j+1, j] (krylov.py:107)
+                break;
+            }
+            case 3: ctl[3 + i] = s0; hcol[i] += s0; break;            // re-orth first
+            case 4: ctl[3 + i] = s0; hcol[i] += s0; break;            // re-orth middle
+            case 5: ctl[1] = s1; hcol[i] = sqrt(s1); break;           // re-orth final norm
+        }
+    }
+};
+
+struct ScaleByInvOp {      // V_{j+1} = w / h  when h != 0 (krylov.py:108-110)
+    static constexpr bool REDUCES = false;
+    double* w;
+    const double* h;
+    double hv;
+    __device__ bool skip() const { return *h == 0.0; }
+    __device__ void prepare() { hv = *h; }
+    __device__ void elem(int64_t k, double&, double&) const { w[k] = w[k] / hv; }
+    __device__ void finish(double, double) const {}
+};
+
+// ------------------------------------------------ CG-Lanczos (krylov.py:146-185)
+// scal layout
+enum { C_RZ = 0, C_STOP = 1, C_ALPHA = 2, C_BETA = 3, C_K = 4, C_NB = 5, C_PAP = 6, C_HIST = 8 };
+constexpr int CG_MAXIT = 64;
+
+struct CgStartOp {
+    static constexpr bool REDUCES = true;
+    const double *b, *diag;
+    double *r, *z, *p, *scal;
+    __device__ bool skip() const { return false; }
+    __device__ void prepare() {}
+    __device__ void elem(int64_t i, double& a0, double&) const {
+        const double ri = b[i];
+        const double zi = ri / diag[i];
+        r[i] = ri;
+        z[i] = zi;
+        p[i] = zi;
+        a0 = fma(ri, zi, a0);
+    }
+    __device__ void finish(double s0, double) const {
+        scal[C_RZ] = s0;
+        scal[C_STOP] = (s0 > 0.0 && isfinite(s0)) ? 0.0 : 1.0;
+        scal[C_K] = 0.0;
+        scal[C_NB] = 0.0;
+    }
+};
+
+struct CgPApOp {
+    static constexpr bool REDUCES = true;
+    const double *p, *Ap;
+    double* scal;
+    __device__ bool skip() const { return scal[C_STOP] != 0.0; }
+    __device__ void prepare() {}
+    __device__ void elem(int64_t i, double& a0, double&) const { a0 = fma(p[i], Ap[i], a0); }
+    __device__ void finish(double s0, double) const {
+        scal[C_PAP] = s0;
+        if (!(s0 > 0.0 && isfinite(s0))) {
+            scal[C_STOP] = 1.0;
+            return;
+        }
+        const double alpha = scal[C_RZ] / s0;
+        const int k = (int)scal[C_K];
+        scal[C_ALPHA] = alpha;
+        if (k < CG_MAXIT) scal[C_HIST + k] = alpha;
+        scal[C_K] = k + 1;
+    }
+};
+
+struct CgUpdateOp {
+    static constexpr bool REDUCES = true;
+    const double *Ap, *diag;
+    double *r, *z, *scal;
+    double alpha;
+    __device__ bool skip() const { return scal[C_STOP] != 0.0; }
+    __device__ void prepare() { alpha = scal[C_ALPHA]; }
+    __device__ void elem(int64_t i, double& a0, double&) const {
+        const double ri = r[i] - alpha * Ap[i];
+        const double zi = ri / diag[i];
+        r[i] = ri;
+        z[i] = zi;
+        a0 = fma(ri, zi, a0);
+    }
+    __device__ void finish(double s0, double) const {
+        const double rz = scal[C_RZ];
+        if (s0 <= 1e-28 * rz || !isfinite(s0)) {
+            scal[C_STOP] = 1.0;
+            return;
+        }
+        const double beta = s0 / rz;
+        const int nb = (int)scal[C_NB];
+        scal[C_BETA] = beta;
+        if (nb < CG_MAXIT) scal[C_HIST + CG_MAXIT + nb] = beta;
+        scal[C_NB] = nb + 1;
+        scal[C_RZ] = s0;
+    }
+};
+
+struct CgPOp {
+    static constexpr bool REDUCES = false;
+    const double* z;
+    double *p, *scal;
+    double beta;
+    __device__ bool skip() const { return scal[C_STOP] != 0.0; }
+    __device__ void prepare() { beta = scal[C_BETA]; }
+    __device__ void elem(int64_t i, double&, double&) const { p[i] = z[i] + beta * p[i]; }
+    __device__ void finish(double, double) const {}
+};
+
+// -------------------------------------------------------- plain vector kernels
+
+#define GRID_STRIDE(i, n) \
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+static dim3 vgrid(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 32;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return dim3((unsigned)b);
+}
+
+__global__ void pack_flags_k(const uint8_t* m, int nc, int64_t V, uint8_t* f) {
+    GRID_STRIDE(v, V) {
+        uint8_t b = 0;
+        for (int c = 0; c < nc; ++c) b |= (uint8_t)((m[(int64_t)c * V + v] != 0) << c);
+        f[v] = b;
+    }
+}
+__global__ void unpack_flags_k(const uint8_t* f, int nc, int64_t V, uint8_t* m) {
+    GRID_STRIDE(v, V) {
+        const uint8_t b = f[v];
+        for (int c = 0; c < nc; ++c) m[(int64_t)c * V + v] = (b >> c) & 1;
+    }
+}
+__global__ void masked_copy_k(const uint8_t* f, int64_t V, int comp0, int nc, const double* in, double* out) {
+    GRID_STRIDE(i, V * nc) {
+        const int c = (int)(i / V);
+        const int64_t v = i - (int64_t)c * V;
+        out[i] = ((f[v] >> (comp0 + c)) & 1) ? 0.0 : in[i];
+    }
+}
+__global__ void reciprocal_k(const double* d, double* o, int64_t n) {
+    GRID_STRIDE(i, n) o[i] = 1.0 / d[i];
+}
+__global__ void cheb_init_zero_k(const double* b, const double* inv, double theta, double* r, double* d,
+                                 double* x, int64_t n) {
+    GRID_STRIDE(i, n) {
+        const double ri = b[i];
+        const double di = (inv[i] * ri) / theta;   // mgsolve.py:105
+        r[i] = ri;
+        d[i] = di;
+        x[i] = 0.0 + di;                           // x = zeros; x += d
+    }
+}
+__global__ void jacobi_update_k(const double* r, const double* inv, double theta, double* x, int64_t n) {
+    GRID_STRIDE(i, n) x[i] += (inv[i] * r[i]) / theta;   // mgsolve.py:99
+}
+__global__ void axpby_k(double a, const double* x, double b, double* y, int64_t n, int mode) {
+    GRID_STRIDE(i, n) {
+        if (mode == 0) y[i] = fma(a, x[i], y[i]);
+        else if (mode == 1) y[i] = a * x[i] + b * y[i];
+        else if (mode == 2) y[i] = a * y[i];
+        else y[i] = x[i];
+    }
+}
+__global__ void sub_k(const double* x, const double* y, double* o, int64_t n) {
+    GRID_STRIDE(i, n) o[i] = x[i] - y[i];
+}
+// x += sum_k y[k] * Z_k   (krylov.py:132: x + Z[:j].T @ y)
+__global__ void multi_axpy_k(const double* Z, int64_t ld, int k, const double* y, double* x, int64_t n) {
+    __shared__ double ys[64];
+    if (threadIdx.x < k) ys[threadIdx.x] = y[threadIdx.x];
+    __syncthreads();
+    GRID_STRIDE(i, n) {
+        double s = 0.0;
+        for (int t = 0; t < k; ++t) s = fma(ys[t], Z[(int64_t)t * ld + i], s);
+        x[i] += s;
+    }
+}
+
+}  // namespace pffmg
+
+using namespace pffmg;
+
+#define VCHECK(what) return check_launch(what)
+
+extern "C" int pffmg_pack_flags(const uint8_t* mask, int n_comp, int64_t V, uint8_t* flags, void* stream) {
+    PFFMG_REQUIRE(mask && flags && n_comp >= 1 && n_comp <= 8 && V >= 0, "pffmg_pack_flags: bad args");
+    pack_flags_k<<<vgrid(V), 256, 0, as_stream(stream)>>>(mask, n_comp, V, flags);
+    VCHECK("pffmg_pack_flags");
+}
+extern "C" int pffmg_unpack_flags(const uint8_t* flags, int n_comp, int64_t V, uint8_t* mask, void* stream) {
+    PFFMG_REQUIRE(mask && flags && n_comp >= 1 && n_comp <= 8 && V >= 0, "pffmg_unpack_flags: bad args");
+    unpack_flags_k<<<vgrid(V), 256, 0, as_stream(stream)>>>(flags, n_comp, V, mask);
+    VCHECK("pffmg_unpack_flags");
+}
+extern "C" int pffmg_masked_copy(const uint8_t* flags, int64_t V, int comp0, int n_comp, const double* in,
+                                 double* out, void* stream) {
+    PFFMG_REQUIRE(flags && in && out && n_comp >= 1 && comp0 >= 0, "pffmg_masked_copy: bad args");
+    masked_copy_k<<<vgrid(V * n_comp), 256, 0, as_stream(stream)>>>(flags, V, comp0, n_comp, in, out);
+    VCHECK("pffmg_masked_copy");
+}
+extern "C" int pffmg_reciprocal(const double* diag, double* out, int64_t n, void* stream) {
+    PFFMG_REQUIRE(diag && out, "pffmg_reciprocal: bad args");
+    reciprocal_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(diag, out, n);
+    VCHECK("pffmg_reciprocal");
+}
+extern "C" int pffmg_cheb_init_zero(const double* b, const double* invdiag, double theta, double* r,
+                                    double* d, double* x, int64_t n, void* stream) {
+    PFFMG_REQUIRE(b && invdiag && r && d && x, "pffmg_cheb_init_zero: bad args");
+    cheb_init_zero_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(b, invdiag, theta, r, d, x, n);
+    VCHECK("pffmg_cheb_init_zero");
+}
+extern "C" int pffmg_jacobi_update(const double* r, const double* invdiag, double theta, double* x,
+                                   int64_t n, void* stream) {
+    PFFMG_REQUIRE(r && invdiag && x, "pffmg_jacobi_update: bad args");
+    jacobi_update_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(r, invdiag, theta, x, n);
+    VCHECK("pffmg_jacobi_update");
+}
+extern "C" int pffmg_axpy(double a, const double* x, double* y, int64_t n, void* stream) {
+    PFFMG_REQUIRE(x && y, "pffmg_axpy: bad args");
+    axpby_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(a, x, 1.0, y, n, 0);
+    VCHECK("pffmg_axpy");
+}
+extern "C" int pffmg_axpby(double a, const double* x, double b, double* y, int64_t n, void* stream) {
+    PFFMG_REQUIRE(x && y, "pffmg_axpby: bad args");
+    axpby_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(a, x, b, y, n, 1);
+    VCHECK("pffmg_axpby");
+}
+extern "C" int pffmg_scale(double a, double* x, int64_t n, void* stream) {
+    PFFMG_REQUIRE(x, "pffmg_scale: bad args");
+    axpby_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(a, x, 0.0, x, n, 2);
+    VCHECK("pffmg_scale");
+}
+extern "C" int pffmg_copy(const double* x, double* y, int64_t n, void* stream) {
+    PFFMG_REQUIRE(x && y, "pffmg_copy: bad args");
+    axpby_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(0.0, x, 0.0, y, n, 3);
+    VCHECK("pffmg_copy");
+}
+extern "C" int pffmg_sub(const double* x, const double* y, double* out, int64_t n, void* stream) {
+    PFFMG_REQUIRE(x && y && out, "pffmg_sub: bad args");
+    sub_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(x, y, out, n);
+    VCHECK("pffmg_sub");
+}
+extern "C" int pffmg_dot(const double* x, const double* y, int64_t n, double* result, void* stream) {
+    PFFMG_REQUIRE(x && y && result && n >= 0, "pffmg_dot: bad args");
+    return run_fused(DotOp{x, y, nullptr, result}, n, as_stream(stream), "pffmg_dot");
+}
+extern "C" int pffmg_dot_scaled(const double* x, const double* y, const double* s, int64_t n, double* result,
+                                void* stream) {
+    PFFMG_REQUIRE(x && y && s && result && n >= 0, "pffmg_dot_scaled: bad args");
+    return run_fused(DotOp{x, y, s, result}, n, as_stream(stream), "pffmg_dot_scaled");
+}
+
+extern "C" int pffmg_arnoldi_mgs(double* Vb, int64_t ld, int j, double* w, int64_t n, double* h,
+                                 double* ctl, void* stream) {
+    PFFMG_REQUIRE(Vb && w && h && ctl && j >= 0 && j < 64 && ld >= n, "pffmg_arnoldi_mgs: bad args");
+    cudaStream_t s = as_stream(stream);
+    auto V = [&](int i) { return (const double*)(Vb + (int64_t)i * ld); };
+    int rc;
+    // modified Gram-Schmidt sweep
+    for (int i = 0; i <= j; ++i) {
+        MgsOp op{i ? V(i - 1) : nullptr, i ? h + (i - 1) : nullptr, V(i), w, ctl, h, i, i ? 1 : 0, 0, 0.0};
+        if ((rc = run_fused(op, n, s, "arnoldi_mgs"))) return rc;
+    }
+    {
+        MgsOp op{V(j), h + j, nullptr, w, ctl, h, j + 1, 2, 0, 0.0};
+        if ((rc = run_fused(op, n, s, "arnoldi_mgs"))) return rc;
+    }
+    // conditional second pass (krylov.py:101-106), gated on ctl[2] on the device
+    for (int i = 0; i <= j; ++i) {
+        MgsOp op{i ? V(i - 1) : nullptr, i ? ctl + 3 + (i - 1) : nullptr, V(i), w, ctl, h, i, i ? 4 : 3, 1, 0.0};
+        if ((rc = run_fused(op, n, s, "arnoldi_mgs"))) return rc;
+    }
+    {
+        MgsOp op{V(j), ctl + 3 + j, nullptr, w, ctl, h, j + 1, 5, 1, 0.0};
+        if ((rc = run_fused(op, n, s, "arnoldi_mgs"))) return rc;
+    }
+    // V_{j+1} = w / H[j+1, j]
+    return run_fused(ScaleByInvOp{w, h + j + 1, 0.0}, n, s, "arnoldi_mgs");
+}
+
+extern "C" int pffmg_multi_axpy(const double* Z, int64_t ld, int k, const double* y, double* x, int64_t n,
+                                void* stream) {
+    PFFMG_REQUIRE(Z && y && x && k >= 0 && k <= 64 && ld >= n, "pffmg_multi_axpy: bad args");
+    if (k == 0) return PFFMG_OK;
+    multi_axpy_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(Z, ld, k, y, x, n);
+    VCHECK("pffmg_multi_axpy");
+}
+
+extern "C" int pffmg_cg_start(const double* b, const double* diag, double* r, double* z, double* p, int64_t n,
+                              double* scal, void* stream) {
+    PFFMG_REQUIRE(b && diag && r && z && p && scal, "pffmg_cg_start: bad args");
+    return run_fused(CgStartOp{b, diag, r, z, p, scal}, n, as_stream(stream), "pffmg_cg_start");
+}
+
+// phase 0: pAp + alpha; phase 1: r/z update + beta; phase 2: p update
+extern "C" int pffmg_cg_step(const double* Ap, const double* diag, double* r, double* z, double* p, int64_t n,
+                             double* scal, int phase, void* stream) {
+    PFFMG_REQUIRE(Ap && diag && r && z && p && scal && phase >= 0 && phase <= 2, "pffmg_cg_step: bad args");
+    cudaStream_t s = as_stream(stream);
+    if (phase == 0) return run_fused(CgPApOp{p, Ap, scal}, n, s, "pffmg_cg_step");
+    if (phase == 1) return run_fused(CgUpdateOp{Ap, diag, r, z, scal, 0.0}, n, s, "pffmg_cg_step");
+    return run_fused(CgPOp{z, p, scal, 0.0}, n, s, "pffmg_cg_step");
+}

@@ -1,0 +1,271 @@
+"""Lattice description of a level mesh and its device-side descriptor.
+
+The reference meshes (mesh.py:163-222) are unions of congruent axis-aligned
+blocks refined uniformly; vertex ids are lattice points sorted with x fastest
+(mesh.py:48-52, 176-178).  For a box domain the id of lattice point (x, y, z)
+is x + (nx+1)(y + (ny+1) z); for a non-box union (the L-shapes) every row of
+constant (y, z) is a contiguous run of ids, described by per-row tables.
+
+`LatticeMesh` / `build_hierarchy` build that numbering natively (no key
+sorting; arrays that only the reference needs -- keys, cells, vertices -- are
+produced lazily).  `lattice_of(mesh)` accepts either a `LatticeMesh` or any
+reference `LevelMesh` (keys + cells arrays) and returns the device
+descriptor used by every kernel.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from functools import cached_property
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def corner_bits(dim):
+    idx = np.arange(2 ** dim)
+    return np.stack([(idx >> a) & 1 for a in range(dim)], axis=1).astype(np.int64)
+
+
+class LatticeMesh:
+    """One refined level of a block union, lattice-native.
+
+    Exposes the reference LevelMesh attributes used on the hot path
+    (dim, n_vertices, n_cells, cell_size, cell_volume, diameter, keys,
+    key_mod, vertices, cells) -- the array ones lazily.
+    """
+
+    def __init__(self, blocks, level, dim):
+        blocks = np.asarray(blocks, dtype=float).reshape(-1, 2, dim)
+        n = 2 ** level
+        spacing = (blocks[0, 1] - blocks[0, 0]) / n
+        self.dim = dim
+        self.level_refinement = n
+        self.cell_size = np.asarray(spacing, dtype=float)
+        self.key_mod = int(round((blocks[:, 1] / spacing).max())) + 2
+        lows = np.rint(blocks[:, 0] / spacing).astype(np.int64)
+        self.kmin = lows.min(axis=0)
+        rel = lows - self.kmin
+        self.block_lows = rel                                    # (B, dim) in cells
+        self.ncell = (rel + n).max(axis=0)                       # cells per axis of the bbox
+        self.is_box = int(len(blocks)) * n ** dim == int(np.prod(self.ncell))
+        if not self.is_box:
+            self._build_rows()
+
+    # -- occupancy / row tables (non-box only) ------------------------------
+    def _occupancy(self, vertices):
+        n = self.level_refinement
+        ext = self.ncell + (1 if vertices else 0)
+        occ = np.zeros(tuple(ext[::-1]), dtype=bool)               # (z, y, x) / (y, x)
+        span = n + 1 if vertices else n
+        for lo in self.block_lows:
+            sl = tuple(slice(lo[a], lo[a] + span) for a in range(self.dim))[::-1]
+            occ[sl] = True
+        return occ
+
+    def _build_rows(self):
+        vocc = self._occupancy(True).reshape(-1, self.ncell[0] + 1)
+        cocc = self._occupancy(False).reshape(-1, self.ncell[0])
+        self.vrow_lo, self.vrow_hi, cnt = _row_runs(vocc)
+        self.vrow_off = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64)
+        self.crow_lo, self.crow_hi, ccnt = _row_runs(cocc)
+        self._nv = int(cnt.sum())
+        self._nc = int(ccnt.sum())
+
+    # -- LevelMesh surface ----------------------------------------------------
+    @property
+    def n_vertices(self):
+        if self.is_box:
+            return int(np.prod(self.ncell + 1))
+        return self._nv
+
+    @property
+    def n_cells(self):
+        if self.is_box:
+            return int(np.prod(self.ncell))
+        return self._nc
+
+    @property
+    def cell_volume(self):
+        return float(np.prod(self.cell_size))
+
+    @property
+    def diameter(self):
+        return float(np.linalg.norm(self.cell_size))
+
+    @cached_property
+    def keys(self):
+        if self.is_box:
+            grids = np.meshgrid(*[np.arange(e + 1) for e in self.ncell[::-1]], indexing="ij")
+            rel = np.stack([g.ravel() for g in grids[::-1]], axis=1)
+        else:
+            rel = np.argwhere(self._occupancy(True))[:, ::-1]
+        return (rel + self.kmin).astype(np.int64)
+
+    @cached_property
+    def vertices(self):
+        return self.keys.astype(float) * self.cell_size
+
+    def vertex_ids(self, rel):
+        """Ids of lattice points rel (..., dim) relative to kmin (-1 if absent)."""
+        rel = np.asarray(rel, dtype=np.int64)
+        x = rel[..., 0]
+        nxv, nyv = self.ncell[0] + 1, self.ncell[1] + 1
+        row = rel[..., 1] + (nyv * rel[..., 2] if self.dim == 3 else 0)
+        if self.is_box:
+            return x + nxv * row
+        lo, hi = self.vrow_lo[row], self.vrow_hi[row]
+        ids = self.vrow_off[row] + (x - lo)
+        return np.where((x >= lo) & (x < hi), ids, -1)
+
+    @cached_property
+    def cells(self):
+        """Cells block by block, x fastest inside a block, corners x fastest
+        (mesh.py:180-194)."""
+        n = self.level_refinement
+        grids = np.meshgrid(*([np.arange(n)] * self.dim), indexing="ij")
+        local = np.stack([g.ravel() for g in grids[::-1]], axis=1)
+        base = (self.block_lows[:, None, :] + local[None, :, :]).reshape(-1, self.dim)
+        corners = base[:, None, :] + corner_bits(self.dim)[None, :, :]
+        return self.vertex_ids(corners)
+
+
+def _row_runs(occ):
+    """Per-row [lo, hi) of a boolean (rows, width) array; each row must be one run."""
+    width = occ.shape[1]
+    cnt = occ.sum(axis=1)
+    has = cnt > 0
+    lo = np.where(has, np.argmax(occ, axis=1), 0)
+    hi = np.where(has, width - np.argmax(occ[:, ::-1], axis=1), 0)
+    if np.any(hi - lo != cnt):
+        raise NotImplementedError("lattice rows with gaps are not supported "
+                                  "(every row of constant (y, z) must be one run)")
+    return lo.astype(np.int32), hi.astype(np.int32), cnt.astype(np.int64)
+
+
+def build_hierarchy(blocks, n_levels, dim):
+    """Levels 0 (coarsest) .. n_levels-1 of a block union (mesh.py:219-222)."""
+    return [LatticeMesh(blocks, l, dim) for l in range(n_levels)]
+
+
+# --------------------------------------------------------------- descriptors
+
+class LatticeInfo:
+    """Host-side lattice facts of any level mesh (ours or the reference's)."""
+
+    def __init__(self, dim, ncell, h, n_vertices, is_box, rows=None, cell_perm=None):
+        self.dim = dim
+        self.ncell = np.asarray(ncell, dtype=np.int64)
+        self.h = np.asarray(h, dtype=float)
+        self.n_vertices = int(n_vertices)
+        self.is_box = is_box
+        self.rows = rows                 # (vrow_off, vrow_lo, vrow_hi, crow_lo, crow_hi) or None
+        self.cell_perm = cell_perm       # mesh cell index -> lattice cell index (for rho)
+
+
+def info_from_mesh(mesh):
+    if isinstance(mesh, LatticeMesh):
+        rows = None if mesh.is_box else (mesh.vrow_off, mesh.vrow_lo, mesh.vrow_hi,
+                                         mesh.crow_lo, mesh.crow_hi)
+        return LatticeInfo(mesh.dim, mesh.ncell, mesh.cell_size, mesh.n_vertices, mesh.is_box, rows)
+    return _info_from_arrays(mesh)
+
+
+def _info_from_arrays(mesh):
+    """Derive the lattice of a reference LevelMesh from its keys and cells and
+    verify that the numbering is the lattice numbering the kernels assume."""
+    keys = np.asarray(mesh.keys, dtype=np.int64)
+    cells = np.asarray(mesh.cells, dtype=np.int64)
+    dim = keys.shape[1]
+    kmin = keys.min(axis=0)
+    rel = keys - kmin
+    ncell = rel.max(axis=0)
+    nxv = int(ncell[0]) + 1
+    nrows = int(ncell[1] + 1) * (int(ncell[2] + 1) if dim == 3 else 1)
+    row = rel[:, 1] + ((ncell[1] + 1) * rel[:, 2] if dim == 3 else 0)
+    V = keys.shape[0]
+    if np.any(np.diff(row) < 0):
+        raise ValueError("mesh vertices are not in lattice order (x fastest)")
+    is_box = V == nxv * nrows
+    rows = None
+    if is_box:
+        ids = rel[:, 0] + nxv * row
+        if not np.array_equal(ids, np.arange(V)):
+            raise ValueError("box mesh vertex numbering is not the lattice numbering")
+    else:
+        vocc = np.zeros((nrows, nxv), dtype=bool)
+        vocc[row, rel[:, 0]] = True
+        vlo, vhi, cnt = _row_runs(vocc)
+        voff = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64)
+        ids = voff[row] + rel[:, 0] - vlo[row]
+        if not np.array_equal(ids, np.arange(V)):
+            raise ValueError("mesh vertex numbering is not row-contiguous lattice order")
+    # cells: corner 0 gives the lattice cell; verify all corners
+    c0 = rel[cells[:, 0]]
+    bits = corner_bits(dim)
+    for n in range(2 ** dim):
+        if not np.array_equal(rel[cells[:, n]], c0 + bits[n]):
+            raise ValueError("mesh cells are not lattice cells with x-fastest corners")
+    ncx, ncy = int(ncell[0]), int(ncell[1])
+    crow = c0[:, 1] + (ncy * c0[:, 2] if dim == 3 else 0)
+    cell_perm = c0[:, 0] + ncx * crow
+    ncrows = ncy * (int(ncell[2]) if dim == 3 else 1)
+    cocc = np.zeros((ncrows, ncx), dtype=bool)
+    cocc[crow, c0[:, 0]] = True
+    if cocc.sum() != cells.shape[0]:
+        raise ValueError("duplicate cells in mesh")
+    if not is_box or cells.shape[0] != ncx * ncrows:
+        if is_box:
+            raise ValueError("box vertex set with missing cells is not supported")
+        clo, chi, _ = _row_runs(cocc)
+        rows = (voff, vlo, vhi, clo, chi)
+    return LatticeInfo(dim, ncell, mesh.cell_size, V, is_box, rows, cell_perm)
+
+
+class DeviceLattice:
+    """pffmg_lattice + the device row tables backing it."""
+
+    def __init__(self, info: LatticeInfo):
+        self.info = info
+        self.dim = info.dim
+        self.n_vertices = info.n_vertices
+        L = _lib.Lattice()
+        L.dim = info.dim
+        L.nx, L.ny = int(info.ncell[0]), int(info.ncell[1])
+        L.nz = int(info.ncell[2]) if info.dim == 3 else 0
+        L.hx, L.hy = float(info.h[0]), float(info.h[1])
+        L.hz = float(info.h[2]) if info.dim == 3 else 0.0
+        L.n_vertices = info.n_vertices
+        self._tables = []
+        if info.rows is not None:
+            dev = torch.device("cuda")
+            voff, vlo, vhi, clo, chi = info.rows
+            ts = [torch.as_tensor(np.ascontiguousarray(voff, dtype=np.int64), device=dev),
+                  torch.as_tensor(np.ascontiguousarray(vlo, dtype=np.int32), device=dev),
+                  torch.as_tensor(np.ascontiguousarray(vhi, dtype=np.int32), device=dev),
+                  torch.as_tensor(np.ascontiguousarray(clo, dtype=np.int32), device=dev),
+                  torch.as_tensor(np.ascontiguousarray(chi, dtype=np.int32), device=dev)]
+            self._tables = ts
+            L.vrow_off, L.vrow_lo, L.vrow_hi, L.crow_lo, L.crow_hi = [t.data_ptr() for t in ts]
+        self.struct = L
+        self.ref = C.byref(L)
+
+    @property
+    def n_lattice_cells(self):
+        return int(np.prod(self.info.ncell))
+
+
+_CACHE = {}
+
+
+def device_lattice(mesh):
+    """Cached DeviceLattice of a mesh object (ours or the reference's)."""
+    key = id(mesh)
+    hit = _CACHE.get(key)
+    if hit is not None and hit[0] is mesh:
+        return hit[1]
+    _lib.require_cuda()
+    dl = DeviceLattice(info_from_mesh(mesh))
+    _CACHE[key] = (mesh, dl)
+    return dl

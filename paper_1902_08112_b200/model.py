@@ -1,0 +1,272 @@
+"""Drop-in twin of the reference operator layer (model.py) on sm_100a kernels.
+
+`PhaseFieldOperator(space, state, mask, params, split, threads=1)` has the
+constructor and protocol of reference model.py:242-413 (apply, apply_block,
+diagonal, blocks, mask, state, params, space, n_dofs).  Construction uploads
+the linearisation point U, phi_tilde and the packed constraint bits; every
+application is ONE fused kernel launch (libpffmg `pffmg_apply`) that gathers
+the cell's vertex data, interpolates to the 2-point Gauss points, evaluates
+the degraded stress / phase-field coupling / reaction, integrates and sums
+the vertex contributions deterministically.  The per-QP coefficient tables
+the reference caches in `_build_caches` (model.py:270-309) are recomputed on
+the fly instead of being streamed from HBM (fewer bytes per vmult).
+
+Vectors may be numpy arrays (copied to the GPU and back) or CUDA tensors
+(zero copy); the result has the kind of the input.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+from enum import Enum
+from typing import Callable, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .arrays import dev, empty, host, is_tensor, like, pack_flags, unpack_flags
+from .lattice import LatticeMesh, device_lattice
+
+__all__ = ["SplitKind", "MaterialParams", "LinearizationState", "ConstraintMask",
+           "PhaseFieldOperator", "extrapolate", "degradation", "jacobian_vmult", "diagonal"]
+
+
+class SplitKind(Enum):
+    NOSPLIT = "none"
+    MIEHE = "miehe"
+
+
+@dataclass
+class MaterialParams:
+    """Same fields as reference model.py:89-103."""
+    mu: float
+    lam: float
+    g_c: float
+    kappa: float = 1e-10
+    eps: float = 1.0
+    pressure_fn: Optional[Callable[[float], float]] = None
+    modulus_field: Optional[Callable[[np.ndarray], np.ndarray]] = None
+    split_band: float = 0.0
+
+    def pressure(self, t):
+        return float(self.pressure_fn(t)) if self.pressure_fn is not None else 0.0
+
+
+@dataclass
+class LinearizationState:
+    """Same fields as reference model.py:106-119 (arrays may live on the GPU)."""
+    U: object
+    U_prev1: object
+    U_prev2: object
+    t: float
+    t_prev1: float
+    t_prev2: float
+    phi_tilde: object
+
+    def with_U(self, U):
+        return replace(self, U=U)
+
+
+@dataclass
+class ConstraintMask:
+    """Same fields and semantics as reference fem.py:129-145."""
+    is_constrained: np.ndarray
+    inhomogeneity: np.ndarray
+
+    @classmethod
+    def empty(cls, n_dofs):
+        return cls(np.zeros(n_dofs, dtype=bool), np.zeros(n_dofs))
+
+    def combined_with(self, flags, values):
+        is_c = self.is_constrained | flags
+        vals = np.where(self.is_constrained, self.inhomogeneity, np.where(flags, values, 0.0))
+        return ConstraintMask(is_c, vals)
+
+
+class DeviceMask:
+    """A constraint mask that lives on the GPU as packed per-vertex bits; the
+    numpy view (`is_constrained`) is materialised lazily on first access."""
+
+    def __init__(self, flags, n_comp, V, inhomogeneity=None):
+        self.flags = flags
+        self.n_comp = n_comp
+        self.V = V
+        self._host = None
+        self._inh = inhomogeneity
+
+    @property
+    def is_constrained(self):
+        if self._host is None:
+            self._host = host(unpack_flags(self.flags, self.n_comp, self.V))
+        return self._host
+
+    @property
+    def inhomogeneity(self):
+        if self._inh is None:
+            self._inh = np.zeros(self.n_comp * self.V)
+        return self._inh
+
+
+def extrapolate(phi_prev1, phi_prev2, t, t_prev1, t_prev2):
+    """Reference model.py:122-132 (host helper, not on the hot path)."""
+    phi_prev1 = np.asarray(phi_prev1, dtype=float)
+    dt = t_prev1 - t_prev2
+    if dt <= 0.0:
+        return np.clip(phi_prev1, 0.0, 1.0)
+    return np.clip(phi_prev1 + (t - t_prev1) * (phi_prev1 - np.asarray(phi_prev2, float)) / dt, 0.0, 1.0)
+
+
+def degradation(phi, kappa):
+    """Reference model.py:135-137."""
+    return (1.0 - kappa) * np.square(phi) + kappa
+
+
+def _split_code(split):
+    v = getattr(split, "value", split)
+    if v in ("none", 0, None):
+        return 0
+    if v in ("miehe", 1):
+        return 1
+    raise ValueError(f"unknown split kind {split!r}")
+
+
+class PhaseFieldOperator:
+    """Matrix-free constrained Jacobian of one level (reference model.py:242-413)."""
+
+    def __init__(self, space, state, mask, params, split, threads=1, *, _flags=None):
+        _lib.require_cuda()
+        self.space = space
+        self.state = state
+        self.mask = mask
+        self.params = params
+        self.split = split
+        self.threads = max(1, int(threads))
+        self.lat = device_lattice(space.mesh)
+        self.dim = self.lat.dim
+        self.nc = self.dim + 1
+        V = self.lat.n_vertices
+        self.V = V
+        code = _split_code(split)
+        if code != 0:
+            raise NotImplementedError("the CUDA operator implements SplitKind.NOSPLIT only "
+                                      "(Miehe split: SURVEY §8f row 3, not built yet)")
+        self._U = dev(state.U)
+        self._pt = dev(state.phi_tilde)
+        if self._U.numel() != self.nc * V or self._pt.numel() != V:
+            raise ValueError(f"state sizes {self._U.numel()}/{self._pt.numel()} do not match "
+                             f"the level ({self.nc}x{V} dofs)")
+        self._flags = _flags if _flags is not None else pack_flags(mask.is_constrained, self.nc, V)
+        self._rho = self._modulus_table() if params.modulus_field is not None else None
+        st = _lib.State()
+        st.mu, st.lam, st.g_c = float(params.mu), float(params.lam), float(params.g_c)
+        st.kappa, st.eps = float(params.kappa), float(params.eps)
+        st.pressure = float(params.pressure(state.t))
+        st.split = code
+        st.U = self._U.data_ptr()
+        st.phi_tilde = self._pt.data_ptr()
+        st.rho = self._rho.data_ptr() if self._rho is not None else None
+        st.flags = self._flags.data_ptr()
+        self._st = st
+        import ctypes
+        self._stp = ctypes.byref(st)
+
+    # -- reference surface --------------------------------------------------
+    @property
+    def n_dofs(self):
+        return self.nc * self.V
+
+    @property
+    def blocks(self):
+        return (slice(0, self.dim * self.V), slice(self.dim * self.V, self.nc * self.V))
+
+    @property
+    def flags(self):
+        """Packed constraint bits on the device."""
+        return self._flags
+
+    def apply(self, v, out=None):
+        """G~ v with constrained rows = identity (model.py:368-375).  `out`
+        (optional, not in the reference signature) receives the result."""
+        x = dev(v)
+        if x.numel() != self.n_dofs:
+            raise ValueError(f"expected {self.n_dofs} dofs, got {x.numel()}")
+        y = out if (is_tensor(out) and out.is_cuda) else empty(self.n_dofs)
+        self.apply_dev(_lib.FULL, x, y)
+        if y is out:
+            return out
+        return like(y, v, out)
+
+    def apply_block(self, which, v_block):
+        """Diagonal block action, 0 = displacement, 1 = phase field (model.py:377-392)."""
+        x = dev(v_block)
+        n = self.dim * self.V if which == 0 else self.V
+        if x.numel() != n:
+            raise ValueError(f"block {which} expects {n} entries, got {x.numel()}")
+        out = empty(n)
+        self.apply_dev(which, x, out)
+        return like(out, v_block)
+
+    def diagonal(self):
+        """Exact diagonal, constrained entries 1.0 (model.py:394-413), as numpy
+        like the reference; `diagonal_dev` fills a CUDA tensor instead."""
+        out = empty(self.n_dofs)
+        self.diagonal_dev(out)
+        return host(out)
+
+    # -- device-level entry points (no conversions) --------------------------
+    def apply_dev(self, which, x, out):
+        _lib.call("pffmg_apply", self.lat.ref, self._stp, which, _lib.ptr(x), _lib.ptr(out),
+                  _lib.stream())
+
+    def residual_dev(self, which, x, b, out):
+        _lib.call("pffmg_residual", self.lat.ref, self._stp, which, _lib.ptr(x), _lib.ptr(b),
+                  _lib.ptr(out), _lib.stream())
+
+    def diagonal_dev(self, out):
+        _lib.call("pffmg_diagonal", self.lat.ref, self._stp, _lib.ptr(out), _lib.stream())
+
+    def cheb_step_dev(self, which, d_in, d_out, r, x, inv, c_dd, c_dr, x_add_din=False):
+        _lib.call("pffmg_cheb_step", self.lat.ref, self._stp, which, _lib.ptr(d_in),
+                  _lib.ptr(d_out), _lib.ptr(r), _lib.ptr(x), _lib.ptr(inv), c_dd, c_dr,
+                  int(x_add_din), _lib.stream())
+
+    def cheb_init_dev(self, which, x, b, r, d, inv, theta):
+        _lib.call("pffmg_cheb_init", self.lat.ref, self._stp, which, _lib.ptr(x), _lib.ptr(b),
+                  _lib.ptr(r), _lib.ptr(d), _lib.ptr(inv), theta, _lib.stream())
+
+    # -- helpers ---------------------------------------------------------------
+    def _modulus_table(self):
+        """rho(x_q) per lattice cell and QP (model.py:284-287)."""
+        info = self.lat.info
+        Q = 2 ** self.dim
+        ncell_lat = int(np.prod(info.ncell))
+        table = np.ones((ncell_lat, Q))
+        space = self.space
+        coords = getattr(space, "qp_coords", None)
+        if coords is not None and info.cell_perm is not None:
+            rho = np.asarray(self.params.modulus_field(coords), dtype=float)
+            table[info.cell_perm] = rho
+        else:
+            coords = _lattice_qp_coords(space.mesh)
+            table = np.asarray(self.params.modulus_field(coords), dtype=float).reshape(ncell_lat, Q)
+        return dev(table.ravel())
+
+
+def _lattice_qp_coords(mesh):
+    """QP coordinates of every lattice cell (lattice order), fem.py:181-182."""
+    dim = mesh.dim
+    g = np.array([0.5 - 0.5 / np.sqrt(3.0), 0.5 + 0.5 / np.sqrt(3.0)])
+    idx = np.arange(2 ** dim)
+    pts = np.stack([g[(idx >> a) & 1] for a in range(dim)], axis=1)
+    grids = np.meshgrid(*[np.arange(e) for e in mesh.ncell[::-1]], indexing="ij")
+    base = np.stack([gr.ravel() for gr in grids[::-1]], axis=1) + mesh.kmin
+    lo = base.astype(float) * mesh.cell_size
+    return lo[:, None, :] + pts[None, :, :] * mesh.cell_size
+
+
+def jacobian_vmult(space, state, mask, params, split, v, threads=1):
+    return PhaseFieldOperator(space, state, mask, params, split, threads).apply(v)
+
+
+def diagonal(space, state, mask, params, split, threads=1):
+    return PhaseFieldOperator(space, state, mask, params, split, threads).diagonal()

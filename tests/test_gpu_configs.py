@@ -1,0 +1,67 @@
+"""BASELINE configurations end to end on the GPU: vmult and one Newton-step
+GMRES(30)+GMG solve vs the reference's golden outputs (cfg1; cfg2 at 256^2),
+and size-independent properties at full cfg2 size (1024^2)."""
+import numpy as np
+import pytest
+import torch
+
+from tests.conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(name, levels=None):
+    from paper_1902_08112_b200 import configs
+    from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, SplitKind
+    prob = configs.make(name, levels)
+    mask = prob.dirichlet.combined_with(prob.active, np.zeros(prob.n_dofs))
+    op = PhaseFieldOperator(prob.disc.finest, prob.state, ConstraintMask(mask.is_constrained,
+                                                                         mask.inhomogeneity),
+                            prob.params, SplitKind.NOSPLIT)
+    return prob, mask, op
+
+
+@pytest.mark.parametrize("name,levels,tag", [("cfg1", None, "cfg1"), ("cfg2", 6, "cfg2_l6")])
+def test_config_vmult_and_solve_match_reference(golden, name, levels, tag):
+    from paper_1902_08112_b200 import krylov, mgsolve
+    from paper_1902_08112_b200.model import SplitKind
+    g = golden["configs"]
+    prob, mask, op = _setup(name, levels)
+    chk = g[f"{tag}/checksum"]
+    assert np.isclose(prob.state.U.sum(), chk[0], rtol=1e-13, atol=0)
+    assert np.isclose(prob.v.sum(), chk[1], rtol=1e-13, atol=0)
+    assert mask.is_constrained.sum() == chk[2]
+    assert rel_err(op.apply(prob.v), g[f"{tag}/apply"]) <= 1e-12
+    assert rel_err(op.diagonal(), g[f"{tag}/diagonal"]) <= 1e-12
+    ctxs = mgsolve.build_level_contexts(prob.disc, prob.state, prob.active, prob.dirichlet,
+                                        prob.params, SplitKind.NOSPLIT)
+    for l, c in enumerate(ctxs):
+        sp = np.array([[s.lambda_min_hat, s.lambda_max_hat, s.fallback] for s in c.spectra])
+        assert np.allclose(sp, g[f"{tag}/{l}/spectra"], rtol=1e-10, atol=0)
+    ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+    pc = mgsolve.VCyclePreconditioner(ctxs, mgsolve.PreconditionerKind.FULL, degree=prob.degree)
+    x, its = krylov.gmres(ctxs[-1].op.apply, pc, g[f"{tag}/gmres_rhs"], ctl)
+    assert abs(its - int(g[f"{tag}/gmres_iters"])) <= 1, (its, int(g[f"{tag}/gmres_iters"]))
+    assert rel_err(x, g[f"{tag}/gmres_x"]) <= 1e-6
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_properties():
+    """1024^2: linearity, identity rows, symmetry of the u block, determinism."""
+    prob, mask, op = _setup("cfg2")
+    n, d = op.n_dofs, op.dim * op.V
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
+    y = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
+    ax, ay = op.apply(x), op.apply(y)
+    assert torch.equal(ax, op.apply(x))
+    lin = op.apply(x + 0.5 * y)
+    assert (lin - (ax + 0.5 * ay)).norm() <= 1e-13 * lin.norm()
+    c = torch.as_tensor(mask.is_constrained, device="cuda")
+    assert torch.equal(ax[c], x[c])
+    xu, yu = x[:d].clone(), y[:d].clone()
+    xu[c[:d]] = 0
+    yu[c[:d]] = 0
+    lhs = torch.dot(op.apply_block(0, xu), yu)
+    rhs = torch.dot(xu, op.apply_block(0, yu))
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)

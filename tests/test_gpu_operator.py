@@ -1,0 +1,146 @@
+"""CUDA operator (libpffmg via the PhaseFieldOperator twin) vs the reference's
+golden outputs and vs the CPU oracle.  Bar: <= 1e-12 relative 2-norm error
+(north_star), constrained rows bit-equal to the input, constrained diagonal
+entries exactly 1.0, bitwise reproducible runs."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import jacobian
+from tests.conftest import rel_err
+from tests.golden.specs import MESHES
+from tests.helpers import (OP_TAGS, oracle_material, oracle_stack, oracle_state, product_disc,
+                           product_params, product_state)
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def _op(g, name, variant, split="none"):
+    from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, SplitKind
+    tag = f"{name}/{split}/{variant}"
+    disc = product_disc(name)
+    space = disc.finest
+    st = product_state(g[f"{tag}/U"], g[f"{tag}/phi_tilde"], g[f"{tag}/t"])
+    flags = g[f"{tag}/flags"]
+    mask = ConstraintMask(flags, np.zeros(flags.size))
+    op = PhaseFieldOperator(space, st, mask, product_params(space, variant == "modulus"),
+                            SplitKind.NOSPLIT)
+    return op, tag
+
+
+@pytest.mark.parametrize("name,variant", OP_TAGS)
+def test_apply_matches_reference(golden, name, variant):
+    g = golden["operator"]
+    op, tag = _op(g, name, variant)
+    v = g[f"{tag}/v"]
+    d = op.dim * op.V
+    out = op.apply(v)
+    assert isinstance(out, np.ndarray)
+    assert rel_err(out, g[f"{tag}/apply"]) <= TOL
+    assert rel_err(op.apply_block(0, v[:d]), g[f"{tag}/apply_u"]) <= TOL
+    assert rel_err(op.apply_block(1, v[d:]), g[f"{tag}/apply_phi"]) <= TOL
+    diag = op.diagonal()
+    assert rel_err(diag, g[f"{tag}/diagonal"]) <= TOL
+    flags = g[f"{tag}/flags"]
+    assert np.array_equal(out[flags], v[flags])           # identity rows, bit-exact
+    assert np.all(diag[flags] == 1.0)
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+def test_tensor_io_zero_copy_and_deterministic(golden, name):
+    g = golden["operator"]
+    op, tag = _op(g, name, "masked")
+    v = torch.as_tensor(g[f"{tag}/v"], device="cuda")
+    a = op.apply(v)
+    b = op.apply(v)
+    assert a.is_cuda and torch.equal(a, b)                # bitwise reproducible
+    assert rel_err(a.cpu().numpy(), g[f"{tag}/apply"]) <= TOL
+
+
+@pytest.mark.parametrize("name", ["cfg1", "lshape3d", "cube"])
+def test_zero_vector_and_linearity(golden, name):
+    g = golden["operator"]
+    op, tag = _op(g, name, "masked")
+    n = op.n_dofs
+    assert not op.apply(np.zeros(n)).any()
+    rng = np.random.default_rng(3)
+    x, y = rng.standard_normal(n), rng.standard_normal(n)
+    lhs = op.apply(x + 0.37 * y)
+    rhs = op.apply(x) + 0.37 * op.apply(y)
+    assert rel_err(lhs, rhs) <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["cfg1", "lprism"])
+def test_block_structure_matches_full(golden, name):
+    """apply_block == restriction of apply to the block, coupling G_u_phi = 0
+    (reference tests/test_model.py:229-276)."""
+    g = golden["operator"]
+    op, tag = _op(g, name, "masked")
+    n, d = op.n_dofs, op.dim * op.V
+    rng = np.random.default_rng(4)
+    vu = rng.standard_normal(d)
+    full = op.apply(np.concatenate([vu, np.zeros(n - d)]))
+    assert rel_err(full[:d], op.apply_block(0, vu)) <= 1e-14
+    vp = rng.standard_normal(n - d)
+    full = op.apply(np.concatenate([np.zeros(d), vp]))
+    flags = g[f"{tag}/flags"]
+    assert np.all(full[:d][~flags[:d]] == 0.0)            # G_u_phi = 0 exactly
+    assert rel_err(full[d:], op.apply_block(1, vp)) <= 1e-14
+
+
+@pytest.mark.parametrize("name", ["rect3d", "lprism", "cfg1"])
+def test_larger_random_states_vs_oracle(name):
+    """Finer refinement than the golden files: compare with the oracle directly."""
+    from paper_1902_08112_b200.fem import Discretization, build_hierarchy
+    from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, SplitKind
+    from oracle import fe, meshgen
+    blocks, n_levels, dim = MESHES[name]
+    n_levels += 1
+    olev = meshgen.build_hierarchy(blocks, n_levels, dim)[-1]
+    T = fe.LevelTables(olev, n_levels - 1)
+    rng = np.random.default_rng(8)
+    n = T.n_dofs
+    U = 1e-2 * rng.standard_normal(n)
+    U[T.phi_slice] = np.clip(0.6 + 0.4 * rng.standard_normal(T.n_vertices), 0, 1)
+    pt = np.clip(U[T.phi_slice] + 0.05 * rng.standard_normal(T.n_vertices), 0, 1)
+    flags = rng.random(n) < 0.1
+    v = rng.standard_normal(n)
+    mat = oracle_material(T)
+    ref_op = jacobian.JacobianOperator(T, oracle_state(U, pt, 0.3), flags, mat)
+    disc = Discretization(build_hierarchy(blocks, n_levels, dim))
+    space = disc.finest
+    op = PhaseFieldOperator(space, product_state(U, pt, 0.3), ConstraintMask(flags, np.zeros(n)),
+                            product_params(space), SplitKind.NOSPLIT)
+    assert rel_err(op.apply(v), ref_op.apply(v)) <= TOL
+    d = T.dim * T.n_vertices
+    assert rel_err(op.apply_block(0, v[:d]), ref_op.apply_block(0, v[:d])) <= TOL
+    assert rel_err(op.apply_block(1, v[d:]), ref_op.apply_block(1, v[d:])) <= TOL
+    assert rel_err(op.diagonal(), ref_op.diagonal()) <= TOL
+
+
+def test_fused_epilogues_match_unfused(golden):
+    """residual / Chebyshev epilogues == separate apply + vector algebra."""
+    from paper_1902_08112_b200 import _lib
+    g = golden["operator"]
+    op, tag = _op(g, "cfg1", "masked")
+    n, d = op.n_dofs, op.dim * op.V
+    rng = np.random.default_rng(5)
+    dev = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+    x, b = dev(rng.standard_normal(n)), dev(rng.standard_normal(n))
+    out = torch.empty_like(x)
+    op.residual_dev(_lib.FULL, x, b, out)
+    assert rel_err(out.cpu().numpy(), (b - op.apply(x)).cpu().numpy()) <= 1e-14
+    # Chebyshev step on the u block
+    din = dev(rng.standard_normal(d))
+    r0 = dev(rng.standard_normal(d))
+    x0 = dev(rng.standard_normal(d))
+    inv = dev(1.0 / (1.0 + rng.random(d)))
+    r, xx, dout = r0.clone(), x0.clone(), torch.empty_like(din)
+    op.cheb_step_dev(0, din, dout, r, xx, inv, 0.3, 0.7)
+    r_ref = r0 - op.apply_block(0, din)
+    d_ref = 0.3 * din + 0.7 * (inv * r_ref)
+    assert torch.equal(r, r_ref)
+    assert rel_err(dout.cpu().numpy(), d_ref.cpu().numpy()) <= 1e-15
+    assert rel_err(xx.cpu().numpy(), (x0 + d_ref).cpu().numpy()) <= 1e-15

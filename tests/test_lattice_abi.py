@@ -1,0 +1,88 @@
+"""Host-side logic of the product (CPU only): lattice numbering and row
+tables against the reference's meshes, and the C ABI library surface."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1902_08112_b200 import _lib, lattice
+from tests.golden.specs import MESHES
+from tests.helpers import oracle_levels
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+def test_lattice_mesh_matches_reference_numbering(golden, name):
+    g = golden["meshes"]
+    blocks, n_levels, dim = MESHES[name]
+    for l, lev in enumerate(lattice.build_hierarchy(blocks, n_levels, dim)):
+        keys = g[f"{name}/{l}/keys"]
+        assert lev.n_vertices == keys.shape[0]
+        assert lev.n_cells == g[f"{name}/{l}/cells"].shape[0]
+        assert np.array_equal(lev.keys, keys)
+        assert np.array_equal(lev.cells, g[f"{name}/{l}/cells"])
+        assert np.array_equal(lev.cell_size, g[f"{name}/{l}/cell_size"])
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+def test_lattice_info_from_reference_style_mesh(name):
+    """Row tables derived from a keys/cells mesh equal the native ones."""
+    blocks, n_levels, dim = MESHES[name]
+    native = lattice.build_hierarchy(blocks, n_levels, dim)
+    for lev_ref, lev in zip(oracle_levels(name), native):
+        a = lattice.info_from_mesh(lev_ref)
+        b = lattice.info_from_mesh(lev)
+        assert a.is_box == b.is_box == lev.is_box
+        assert np.array_equal(a.ncell, b.ncell)
+        assert a.n_vertices == b.n_vertices
+        if not a.is_box:
+            for x, y in zip(a.rows, b.rows):
+                assert np.array_equal(x, y)
+        # every cell of the mesh maps to a lattice cell; the perm is a bijection onto them
+        assert np.unique(a.cell_perm).size == lev_ref.n_cells
+
+
+def test_lattice_rejects_gapped_rows():
+    blocks = [[(0.0, 0.0), (1.0, 1.0)], [(2.0, 0.0), (3.0, 1.0)]]
+    with pytest.raises(NotImplementedError):
+        lattice.LatticeMesh(blocks, 1, 2)
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "pffmg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pffmg_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    names = _header_functions()
+    assert len(names) >= 30
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_lib.exported_symbols())
+
+
+def test_library_reports_argument_errors_without_a_gpu():
+    lib = _lib.load()
+    assert lib.pffmg_version() == 1
+    rc = lib.pffmg_apply(None, None, -1, None, None, None)
+    assert rc == 1
+    assert b"null" in lib.pffmg_last_error()
+    L = _lib.Lattice()
+    L.dim = 4
+    st = _lib.State()
+    rc = lib.pffmg_apply(ctypes.byref(L), ctypes.byref(st), -1, None, None, None)
+    assert rc == 1 and b"dim" in lib.pffmg_last_error()
+
+
+def test_product_has_no_oracle_imports():
+    pkg = os.path.join(ROOT, "paper_1902_08112_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
