@@ -68,7 +68,9 @@ typedef struct {
     const double* U;            /* (dim+1)*V linearisation point (may be NULL for the u block) */
     const double* phi_tilde;    /* V extrapolated phase field (may be NULL for the phi block) */
     const double* rho;          /* NULL (rho == 1) or modulus field per lattice cell x QP */
-    const uint8_t* flags;       /* V packed constraint bits: bit c <=> dof c*V+v constrained */
+    const uint8_t* flags;       /* V packed constraint bits: bit c <=> dof c*V+v constrained;
+                                   the buffer must stay readable (any content) up to
+                                   4*ceil(V/4) + 40 bytes: kernels read aligned 32-bit words */
 } pffmg_state;
 
 const char* pffmg_last_error(void);

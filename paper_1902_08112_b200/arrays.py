@@ -95,7 +95,7 @@ def pack_flags(mask_bool, n_comp, V):
         else mask_bool.to(torch.uint8).contiguous()
     if m.numel() != n_comp * V:
         raise ValueError(f"mask has {m.numel()} entries, expected {n_comp * V}")
-    out = empty(V, torch.uint8)
+    out = flags_buffer(V)
     _lib.call("pffmg_pack_flags", _lib.ptr(m), n_comp, V, _lib.ptr(out), _lib.stream())
     return out
 
@@ -129,3 +129,13 @@ def dot(x, y, out=None, offset=0):
 
 def norm(x):
     return float(np.sqrt(dot(x, x).item()))
+
+
+FLAG_PAD = 64
+
+
+def flags_buffer(V):
+    """Packed-flag buffer of V bytes; the kernels read flags as aligned 32-bit
+    words, so the allocation is padded (include/pffmg.h) and the pad zeroed."""
+    buf = torch.zeros(int(V) + FLAG_PAD, dtype=torch.uint8, device="cuda")
+    return buf[:int(V)]

@@ -1,0 +1,50 @@
+// 2D instantiations of the fused operator kernels (see op_kernels.cuh).
+#include "op_launch.cuh"
+
+namespace pffmg {
+
+constexpr int NW2D = 4;   // warps per CTA of the warp-independent 2D kernel
+
+template <int MODE, int EPI, bool ISO, bool RHO>
+static void launch_w(const OpArgs& A, dim3 grid, size_t smem, cudaStream_t s) {
+    static size_t done = 0;
+    if (smem > 48 * 1024 && done < smem) {
+        cudaFuncSetAttribute(op2dw_kernel<MODE, EPI, NW2D, ISO, RHO>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        done = smem;
+    }
+    op2dw_kernel<MODE, EPI, NW2D, ISO, RHO><<<grid, 32 * NW2D, smem, s>>>(A);
+}
+
+template <int MODE, int EPI>
+int launch2d(const OpArgs& A0, bool iso, cudaStream_t s) {
+    OpArgs A = A0;
+    const Lat& L = A.L;
+    using MI = ModeInfo<2, MODE>;
+    const int sms = sm_count();
+    const int nseg = (L.nx + 1 + 30) / 31;
+    const int rows = L.ny + 1;
+    // strips of H vertex rows: aim for ~24 resident warps per SM in one wave,
+    // H in [4, 64] (the first cell row of a strip is recomputed: overhead 1/H)
+    int64_t per = ((int64_t)rows * nseg + 24LL * sms - 1) / (24LL * sms);
+    per = per < 4 ? 4 : (per > 64 ? 64 : per);
+    A.planes_per_cta = (int)per;
+    A.nseg = nseg;
+    const int64_t warps = (int64_t)nseg * ((rows + per - 1) / per);
+    dim3 grid((unsigned)((warps + NW2D - 1) / NW2D));
+    const size_t smem = NW2D * (sizeof(double) * 4 * MI::NF * 33 + 4 * 40 + 4 * sizeof(int));
+    const bool rho = A.rho != nullptr;
+    if (iso && rho)
+        launch_w<MODE, EPI, true, true>(A, grid, smem, s);
+    else if (iso)
+        launch_w<MODE, EPI, true, false>(A, grid, smem, s);
+    else if (rho)
+        launch_w<MODE, EPI, false, true>(A, grid, smem, s);
+    else
+        launch_w<MODE, EPI, false, false>(A, grid, smem, s);
+    return PFFMG_OK;
+}
+
+PFFMG_INSTANTIATE_LAUNCH(launch2d)
+
+}  // namespace pffmg

@@ -1,414 +1,21 @@
-// The fused matrix-free vmult of the linearised PFF Jacobian on a lattice
-// level: stage vertex rows/planes in shared memory, one thread per cell
-// (gather -> sum-factorised interpolation -> pointwise physics -> integrate),
-// then a deterministic vertex sum (warp shuffles in x, shared memory in y,
-// registers carried in the marching direction) and a fused epilogue
-// (store / residual / Chebyshev step / diagonal).
-//
-// Replaces reference model.py:368-413 (apply, apply_block, diagonal) with
-// fem.py:203-225 (masked gather, bincount scatter) and the vector updates of
-// mgsolve.py:82-113 (chebyshev_apply) and 227 (residual) fused in.
-#include <cstdarg>
+// C ABI of the fused matrix-free operator: argument checking and dispatch to
+// the per-dimension kernel instantiations (op2d.cu, op3d.cu; kernels in
+// op_kernels.cuh).  Replaces reference model.py:368-413 and the vector
+// updates of mgsolve.py:82-113 / 227 (fused epilogues).
 #include <cmath>
 
-#include "cellops.cuh"
+#include "op_launch.cuh"
 
 namespace pffmg {
 
-enum Epi { E_STORE = 0, E_RESID = 1, E_CHEB = 2, E_CHEB0 = 3, E_DIAG = 4 };
-
-struct OpArgs {
-    Lat L;
-    Consts K;
-    const double* __restrict__ v;      // block base of the input field (component stride V)
-    double* __restrict__ out;          // STORE / RESID / DIAG output
-    const double* __restrict__ U;
-    const double* __restrict__ pt;
-    const double* __restrict__ rho;
-    const uint8_t* __restrict__ flags;
-    // epilogue operands (block base pointers, component stride V)
-    const double* __restrict__ b;
-    double* __restrict__ r;
-    double* __restrict__ x;            // CHEB: updated in place; CHEB0: x_out
-    double* __restrict__ dout;
-    const double* __restrict__ inv;
-    double c1, c2;                     // CHEB: c_dd, c_dr   CHEB0: theta
-    int x_add_din;                     // CHEB: x = (x + d_in) + d_out instead of x += d_out
-    int planes_per_cta;
-};
-
-// ------------------------------------------------------------ epilogue
-
-template <int NCO, int COMP0, int EPI>
-__device__ __forceinline__ void epilogue(const OpArgs& A, int64_t vid, uint8_t fl,
-                                         const double (&acc)[NCO], const double (&vin)[NCO]) {
-    const int64_t V = A.L.V;
-#pragma unroll
-    for (int k = 0; k < NCO; ++k) {
-        const bool con = (fl >> (COMP0 + k)) & 1;
-        const int64_t g = (int64_t)k * V + vid;
-        if (EPI == E_DIAG) {
-            A.out[g] = con ? 1.0 : acc[k];                       // model.py:412
-            continue;
-        }
-        const double Av = con ? vin[k] : acc[k];                 // model.py:373-374, 390-391
-        if (EPI == E_STORE) {
-            A.out[g] = Av;
-        } else if (EPI == E_RESID) {
-            A.out[g] = A.b[g] - Av;                              // mgsolve.py:227
-        } else if (EPI == E_CHEB) {                              // mgsolve.py:108-111
-            const double rr = A.r[g] - Av;
-            const double dn = A.c1 * vin[k] + A.c2 * (A.inv[g] * rr);
-            A.r[g] = rr;
-            A.dout[g] = dn;
-            const double xo = A.x[g];
-            A.x[g] = A.x_add_din ? (xo + vin[k]) + dn : xo + dn;
-        } else {                                                 // E_CHEB0: mgsolve.py:95, 105
-            const double rr = A.b[g] - Av;                       // (x += d deferred to the
-            A.r[g] = rr;                                         //  next step, see pffmg.h)
-            A.dout[g] = (A.inv[g] * rr) / A.c1;
-        }
-    }
-}
-
-// Load one staged vertex: all NF fields (raw) + flags.
-template <int D, int MODE>
-__device__ __forceinline__ void load_vertex(const OpArgs& A, int64_t vid,
-                                            double (&f)[ModeInfo<D, MODE>::NF], uint8_t& fl) {
-    using MI = ModeInfo<D, MODE>;
-    const int64_t V = A.L.V;
-    if (vid < 0) {
-#pragma unroll
-        for (int i = 0; i < MI::NF; ++i) f[i] = 0.0;
-        fl = 0;
-        return;
-    }
-#pragma unroll
-    for (int i = 0; i < MI::NV; ++i) f[MI::F_V + i] = __ldg(A.v + (int64_t)i * V + vid);
-#pragma unroll
-    for (int i = 0; i < MI::NU; ++i) f[MI::F_U + i] = __ldg(A.U + (int64_t)i * V + vid);
-    if (MI::PT) f[MI::F_PT] = __ldg(A.pt + vid);
-    fl = __ldg(A.flags + vid);
-}
-
-// ======================================================================= 2D
-// CTA = NW warps along x.  Warp w computes cells cx0 + 31 w + lane (lane 0 of
-// warp w and lane 31 of warp w-1 share a cell) and finalises the vertex
-// columns of lanes 1..31.  The CTA marches over a strip of vertex rows.
-
-template <int MODE, int EPI, int NW>
-__global__ void __launch_bounds__(32 * NW) op2d_kernel(const OpArgs A) {
-    constexpr int D = 2, NP = 4;
-    using MI = ModeInfo<D, MODE>;
-    constexpr int NF = MI::NF, NCO = MI::NCO;
-    constexpr int TW = 31 * NW + 2;            // staged vertices per row
-    constexpr int NT = 32 * NW;
-    constexpr int SLOTS = (TW + NT - 1) / NT;
-
-    __shared__ double sv[2][NF][TW];
-    __shared__ uint8_t sfl[2][TW];
-
-    const Lat& L = A.L;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int cx0 = -1 + (int)blockIdx.x * 31 * NW;
-    const int vy0 = (int)blockIdx.y * A.planes_per_cta;
-    const int vy1 = min(vy0 + A.planes_per_cta, L.ny + 1);
-    const int jc = 31 * w + lane;              // staged column of this thread's left corner
-    const int cx = cx0 + jc;
-
-    auto stage_now = [&](int y, int buf) {
-#pragma unroll
-        for (int s = 0; s < SLOTS; ++s) {
-            const int j = tid + s * NT;
-            if (j < TW) {
-                double f[NF];
-                uint8_t fl;
-                load_vertex<D, MODE>(A, vertex_id(L, cx0 + j, y, 0), f, fl);
-#pragma unroll
-                for (int i = 0; i < NF; ++i) sv[buf][i][j] = f[i];
-                sfl[buf][j] = fl;
-            }
-        }
-    };
-
-    stage_now(vy0 - 1, 0);
-    stage_now(vy0, 1);
-    __syncthreads();
-
-    double carry[NCO];
-#pragma unroll
-    for (int k = 0; k < NCO; ++k) carry[k] = 0.0;
-
-    int b0 = 0;
-    for (int cy = vy0 - 1; cy < vy1; ++cy) {
-        const int b1 = b0 ^ 1;
-        // prefetch row cy + 2 into registers
-        double pf[SLOTS][NF];
-        uint8_t pfl[SLOTS];
-        const bool need_next = (cy + 2 <= vy1);
-        if (need_next) {
-#pragma unroll
-            for (int s = 0; s < SLOTS; ++s) {
-                const int j = tid + s * NT;
-                load_vertex<D, MODE>(A, j < TW ? vertex_id(L, cx0 + j, cy + 2, 0) : -1, pf[s], pfl[s]);
-            }
-        }
-
-        // ---- cell (cx, cy)
-        double o[NCO][NP];
-        if (cell_exists<D>(L, cx, cy, 0)) {
-            double cv[NF][NP];
-#pragma unroll
-            for (int n = 0; n < NP; ++n) {
-                const int bb = (n >> 1) ? b1 : b0;
-                const int j = jc + (n & 1);
-                const uint8_t fl = sfl[bb][j];
-#pragma unroll
-                for (int i = 0; i < NF; ++i) {
-                    double val = sv[bb][i][j];
-                    if (i < MI::NV && ((fl >> (MI::COMP0 + i)) & 1)) val = 0.0;   // fem.py:205-206
-                    cv[i][n] = val;
-                }
-            }
-            const double* rq = A.rho ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * NP : nullptr;
-            cell_kernel<D, MODE>(cv, rq, A.K, o);
-        } else {
-#pragma unroll
-            for (int k = 0; k < NCO; ++k)
-#pragma unroll
-                for (int n = 0; n < NP; ++n) o[k][n] = 0.0;
-        }
-
-        // ---- x-combine: vertex column cx gets own corners (x=0) + left cell's (x=1)
-        double bot[NCO], top[NCO];
-#pragma unroll
-        for (int k = 0; k < NCO; ++k) {
-            const double r0 = __shfl_up_sync(0xffffffffu, o[k][1], 1);
-            const double r1 = __shfl_up_sync(0xffffffffu, o[k][3], 1);
-            bot[k] = o[k][0] + r0;
-            top[k] = o[k][2] + r1;
-        }
-        if (cy >= vy0 && lane >= 1) {
-            const int64_t vid = vertex_id(L, cx, cy, 0);
-            if (vid >= 0) {
-                double acc[NCO], vin[NCO];
-                const uint8_t fl = sfl[b0][jc];
-#pragma unroll
-                for (int k = 0; k < NCO; ++k) {
-                    acc[k] = carry[k] + bot[k];
-                    vin[k] = (MODE == M_DIAG) ? 0.0 : sv[b0][MI::F_V + k][jc];
-                }
-                epilogue<NCO, MI::COMP0, EPI>(A, vid, fl, acc, vin);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < NCO; ++k) carry[k] = top[k];
-
-        __syncthreads();                      // all reads of buffer b0 done
-        if (need_next) {
-#pragma unroll
-            for (int s = 0; s < SLOTS; ++s) {
-                const int j = tid + s * NT;
-                if (j < TW) {
-#pragma unroll
-                    for (int i = 0; i < NF; ++i) sv[b0][i][j] = pf[s][i];
-                    sfl[b0][j] = pfl[s];
-                }
-            }
-        }
-        __syncthreads();
-        b0 = b1;
-    }
-}
-
-// ======================================================================= 3D
-// CTA = TY warps; warp w <-> cell row cy0 + w, lane <-> cell column cx0 + lane.
-// Finalises vertices (cx0 + lane, cy0 + w) for lane >= 1, w >= 1; marches in z.
-
-template <int MODE, int EPI, int TY>
-__global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
-    constexpr int D = 3, NP = 8;
-    using MI = ModeInfo<D, MODE>;
-    constexpr int NF = MI::NF, NCO = MI::NCO;
-    constexpr int TXV = 33, TYV = TY + 1, TV = TXV * TYV;
-    constexpr int NT = 32 * TY;
-    constexpr int SLOTS = (TV + NT - 1) / NT;
-
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* sv = reinterpret_cast<double*>(smem_raw);                 // [2][NF][TV]
-    double* sy = sv + 2 * NF * TV;                                     // [TY][2][NCO][32]
-    uint8_t* sfl = reinterpret_cast<uint8_t*>(sy + TY * 2 * NCO * 32); // [2][TV]
-
-    const Lat& L = A.L;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int cx0 = -1 + (int)blockIdx.x * 31;
-    const int cy0 = -1 + (int)blockIdx.y * (TY - 1);
-    const int vz0 = (int)blockIdx.z * A.planes_per_cta;
-    const int vz1 = min(vz0 + A.planes_per_cta, L.nz + 1);
-    const int cx = cx0 + lane, cy = cy0 + w;
-
-    auto SV = [&](int buf, int f, int j) -> double& { return sv[(buf * NF + f) * TV + j]; };
-    auto stage_now = [&](int z, int buf) {
-#pragma unroll
-        for (int s = 0; s < SLOTS; ++s) {
-            const int j = tid + s * NT;
-            if (j < TV) {
-                const int jx = j % TXV, jy = j / TXV;
-                double f[NF];
-                uint8_t fl;
-                load_vertex<D, MODE>(A, vertex_id(L, cx0 + jx, cy0 + jy, z), f, fl);
-#pragma unroll
-                for (int i = 0; i < NF; ++i) SV(buf, i, j) = f[i];
-                sfl[buf * TV + j] = fl;
-            }
-        }
-    };
-
-    stage_now(vz0 - 1, 0);
-    stage_now(vz0, 1);
-    __syncthreads();
-
-    double carry[NCO];
-#pragma unroll
-    for (int k = 0; k < NCO; ++k) carry[k] = 0.0;
-
-    int b0 = 0;
-    for (int cz = vz0 - 1; cz < vz1; ++cz) {
-        const int b1 = b0 ^ 1;
-        double pf[SLOTS][NF];
-        uint8_t pfl[SLOTS];
-        const bool need_next = (cz + 2 <= vz1);
-        if (need_next) {
-#pragma unroll
-            for (int s = 0; s < SLOTS; ++s) {
-                const int j = tid + s * NT;
-                const int64_t vid = j < TV ? vertex_id(L, cx0 + j % TXV, cy0 + j / TXV, cz + 2) : -1;
-                load_vertex<D, MODE>(A, vid, pf[s], pfl[s]);
-            }
-        }
-
-        double o[NCO][NP];
-        if (cell_exists<D>(L, cx, cy, cz)) {
-            double cv[NF][NP];
-#pragma unroll
-            for (int n = 0; n < NP; ++n) {
-                const int bb = (n >> 2) ? b1 : b0;
-                const int j = (lane + (n & 1)) + TXV * (w + ((n >> 1) & 1));
-                const uint8_t fl = sfl[bb * TV + j];
-#pragma unroll
-                for (int i = 0; i < NF; ++i) {
-                    double val = SV(bb, i, j);
-                    if (i < MI::NV && ((fl >> (MI::COMP0 + i)) & 1)) val = 0.0;
-                    cv[i][n] = val;
-                }
-            }
-            const double* rq =
-                A.rho ? A.rho + ((int64_t)cx + (int64_t)L.nx * (cy + (int64_t)L.ny * cz)) * NP : nullptr;
-            cell_kernel<D, MODE>(cv, rq, A.K, o);
-        } else {
-#pragma unroll
-            for (int k = 0; k < NCO; ++k)
-#pragma unroll
-                for (int n = 0; n < NP; ++n) o[k][n] = 0.0;
-        }
-
-        // x-combine -> part[yb][zb][k] at vertex column x = cx
-        double part[2][2][NCO];
-#pragma unroll
-        for (int yb = 0; yb < 2; ++yb)
-#pragma unroll
-            for (int zb = 0; zb < 2; ++zb)
-#pragma unroll
-                for (int k = 0; k < NCO; ++k) {
-                    const int nl = (yb << 1) | (zb << 2);
-                    const double rr = __shfl_up_sync(0xffffffffu, o[k][nl | 1], 1);
-                    part[yb][zb][k] = o[k][nl] + rr;
-                }
-        // y-combine through shared memory: row w publishes its y=1 partials
-#pragma unroll
-        for (int zb = 0; zb < 2; ++zb)
-#pragma unroll
-            for (int k = 0; k < NCO; ++k) sy[((w * 2 + zb) * NCO + k) * 32 + lane] = part[1][zb][k];
-        __syncthreads();
-        if (w >= 1) {
-            double vp[2][NCO];
-#pragma unroll
-            for (int zb = 0; zb < 2; ++zb)
-#pragma unroll
-                for (int k = 0; k < NCO; ++k)
-                    vp[zb][k] = part[0][zb][k] + sy[(((w - 1) * 2 + zb) * NCO + k) * 32 + lane];
-            if (cz >= vz0 && lane >= 1) {
-                const int64_t vid = vertex_id(L, cx, cy, cz);
-                if (vid >= 0) {
-                    const int j = lane + TXV * w;
-                    const uint8_t fl = sfl[b0 * TV + j];
-                    double acc[NCO], vin[NCO];
-#pragma unroll
-                    for (int k = 0; k < NCO; ++k) {
-                        acc[k] = carry[k] + vp[0][k];
-                        vin[k] = (MODE == M_DIAG) ? 0.0 : SV(b0, MI::F_V + k, j);
-                    }
-                    epilogue<NCO, MI::COMP0, EPI>(A, vid, fl, acc, vin);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < NCO; ++k) carry[k] = vp[1][k];
-        }
-        __syncthreads();
-        if (need_next) {
-#pragma unroll
-            for (int s = 0; s < SLOTS; ++s) {
-                const int j = tid + s * NT;
-                if (j < TV) {
-#pragma unroll
-                    for (int i = 0; i < NF; ++i) SV(b0, i, j) = pf[s][i];
-                    sfl[b0 * TV + j] = pfl[s];
-                }
-            }
-        }
-        __syncthreads();
-        b0 = b1;
-    }
-}
-
-// ================================================================ launchers
-
-constexpr int NW2D = 4;
-constexpr int TY3D = 8;
-
 template <int MODE, int EPI>
-static int launch(const OpArgs& A0, cudaStream_t s, const char* what) {
-    OpArgs A = A0;
+static int launch(const OpArgs& A, cudaStream_t s, const char* what) {
     const Lat& L = A.L;
-    const int sms = sm_count();
-    if (L.dim == 2) {
-        const int gx = (L.nx + 1 + 31 * NW2D - 1) / (31 * NW2D);
-        const int rows = L.ny + 1;
-        // enough CTAs for ~4 per SM, strips of at least 4 rows
-        int per = (int)(((int64_t)rows * gx + 4LL * sms - 1) / (4LL * sms));
-        per = per < 4 ? 4 : (per > 32 ? 32 : per);
-        A.planes_per_cta = per;
-        dim3 grid(gx, (rows + per - 1) / per, 1);
-        op2d_kernel<MODE, EPI, NW2D><<<grid, 32 * NW2D, 0, s>>>(A);
-    } else {
-        using MI = ModeInfo<3, MODE>;
-        constexpr int TV = 33 * (TY3D + 1);
-        const size_t smem = sizeof(double) * (2 * MI::NF * TV + TY3D * 2 * MI::NCO * 32) + 2 * TV;
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(op3d_kernel<MODE, EPI, TY3D>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr_set = true;
-        }
-        const int gx = (L.nx + 1 + 30) / 31;
-        const int gy = (L.ny + 1 + TY3D - 2) / (TY3D - 1);
-        const int planes = L.nz + 1;
-        int per = (int)(((int64_t)planes * gx * gy + 2LL * sms - 1) / (2LL * sms));
-        per = per < 4 ? 4 : (per > 32 ? 32 : per);
-        A.planes_per_cta = per;
-        dim3 grid(gx, gy, (planes + per - 1) / per);
-        op3d_kernel<MODE, EPI, TY3D><<<grid, 32 * TY3D, smem, s>>>(A);
-    }
+    const bool iso = L.hx == L.hy && (L.dim == 2 || L.hz == L.hx);
+    if (L.dim == 2)
+        launch2d<MODE, EPI>(A, iso, s);
+    else
+        launch3d<MODE, EPI>(A, iso, s);
     return check_launch(what);
 }
 
@@ -418,6 +25,8 @@ static int fill_args(const pffmg_lattice* lat, const pffmg_state* st, OpArgs* A)
     int rc = make_lat(lat, &A->L);
     if (rc) return rc;
     rc = make_consts(lat, st, &A->K);
+    if (rc) return rc;
+    A->I = make_iso_host(A->K);
     if (rc) return rc;
     if (st->split != 0) {
         set_error("split kind %d not supported by the CUDA operator yet (NoSplit only)", st->split);

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .arrays import DeviceCallable, dev, empty, host, is_tensor, like, pack_flags, zeros
+from .arrays import DeviceCallable, dev, empty, flags_buffer, host, is_tensor, like, pack_flags, zeros
 from .fem import Discretization
 from .krylov import cg_lanczos_dev, estimate_spectrum, lanczos_extremes, probe_vector
 from .model import DeviceMask, LinearizationState, PhaseFieldOperator
@@ -221,7 +221,7 @@ def build_level_contexts(disc, state, active_mask, dirichlet_mask, params, split
     U[-1], P1[-1], P2[-1], PT[-1] = (dev(state.U), dev(state.U_prev1), dev(state.U_prev2),
                                      dev(state.phi_tilde))
     for l in range(L - 2, -1, -1):                      # mgsolve.py:173-186
-        flags[l] = torch.empty(Vs[l], dtype=torch.uint8, device="cuda")
+        flags[l] = flags_buffer(Vs[l])
         D.inject_flags_dev(flags[l + 1], flags[l], l)
         U[l], P1[l], P2[l] = (empty(nc * Vs[l]) for _ in range(3))
         PT[l] = empty(Vs[l])

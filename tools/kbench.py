@@ -1,0 +1,67 @@
+"""Kernel microbenchmark: time one operator mode on a config (CUDA events,
+L2 flushed between reps).  Used for tuning and under ncu."""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1902_08112_b200 import _lib, configs  # noqa: E402
+from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, SplitKind  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg2")
+ap.add_argument("--levels", type=int, default=None)
+ap.add_argument("--mode", default="full", choices=["full", "u", "phi", "diag", "chebu", "chebp", "resid"])
+ap.add_argument("--reps", type=int, default=20)
+args = ap.parse_args()
+
+prob = configs.make(args.config, args.levels)
+mask = prob.dirichlet.combined_with(prob.active, np.zeros(prob.n_dofs))
+op = PhaseFieldOperator(prob.disc.finest, prob.state, ConstraintMask(mask.is_constrained, mask.inhomogeneity),
+                        prob.params, SplitKind.NOSPLIT)
+n, d, V = op.n_dofs, op.dim * op.V, op.V
+v = torch.as_tensor(prob.v, device="cuda")
+out = torch.empty_like(v)
+r = torch.randn(n, dtype=torch.float64, device="cuda")
+x = torch.randn(n, dtype=torch.float64, device="cuda")
+inv = torch.rand(n, dtype=torch.float64, device="cuda") + 1.0
+d2 = torch.empty_like(v)
+flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+
+
+def run():
+    if args.mode == "full":
+        op.apply_dev(_lib.FULL, v, out)
+    elif args.mode == "u":
+        op.apply_dev(0, v[:d], out[:d])
+    elif args.mode == "phi":
+        op.apply_dev(1, v[d:], out[d:])
+    elif args.mode == "diag":
+        op.diagonal_dev(out)
+    elif args.mode == "resid":
+        op.residual_dev(_lib.FULL, v, r, out)
+    elif args.mode == "chebu":
+        op.cheb_step_dev(0, v[:d], d2[:d], r[:d], x[:d], inv[:d], 0.3, 0.2)
+    elif args.mode == "chebp":
+        op.cheb_step_dev(1, v[d:], d2[d:], r[d:], x[d:], inv[d:], 0.3, 0.2)
+
+
+for _ in range(3):
+    flush.zero_()
+    run()
+torch.cuda.synchronize()
+ts = []
+for _ in range(args.reps):
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run()
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+ndof = {"full": n, "resid": n, "diag": n, "u": d, "chebu": d, "phi": V, "chebp": V}[args.mode]
+print(f"{args.config} {args.mode}: median {np.median(ts)*1e3:.1f} us  min {np.min(ts)*1e3:.1f} us  "
+      f"{ndof / np.median(ts) * 1e-6:.1f} GDoF/s")
