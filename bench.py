@@ -194,10 +194,20 @@ def run_gpu(args):
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
+    def load_for(seconds):
+        """Keep the GPU busy with the same work so nvidia-smi sees it under load."""
+        t_end = time.perf_counter() + seconds
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                flush.zero_()
+                step()
+            torch.cuda.synchronize()
+
     with Clocks(local) as clk:
+        load_for(0.4)
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
         for e0, e1 in evs:
             flush.zero_()
@@ -206,6 +216,9 @@ def run_gpu(args):
             e1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+        if ws > 1:
+            torch.distributed.barrier()
+        load_for(0.4)
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     t_tot = float(np.sum(step_ms)) * 1e-3
     if ws > 1:

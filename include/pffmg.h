@@ -33,6 +33,8 @@ extern "C" {
 #define PFFMG_UBLOCK 0      /* apply_block(0, .) displacement    model.py:377-392 */
 #define PFFMG_PBLOCK 1      /* apply_block(1, .) phase field     model.py:377-392 */
 
+#define PFFMG_HINT_PREMASKED 1
+
 /*
  * Level geometry: a (possibly non-box) lattice of congruent cells.  Vertex
  * numbering follows the reference mesh (mesh.py:163-194): x fastest, rows of
@@ -64,7 +66,10 @@ typedef struct {
     double mu, lam, g_c, kappa, eps;
     double pressure;            /* MaterialParams.pressure(state.t) */
     int32_t split;              /* 0 = NOSPLIT; 1 = MIEHE (returns PFFMG_ERR_UNSUPPORTED for now) */
-    int32_t pad_;
+    int32_t hints;              /* bit 0 (PFFMG_HINT_PREMASKED): every input vector of the
+                                   call is already zero at constrained dofs, so the masked
+                                   gather (fem.py:205-206) can be skipped.  Results are
+                                   identical; a wrong hint gives wrong results. */
     const double* U;            /* (dim+1)*V linearisation point (may be NULL for the u block) */
     const double* phi_tilde;    /* V extrapolated phase field (may be NULL for the phi block) */
     const double* rho;          /* NULL (rho == 1) or modulus field per lattice cell x QP */

@@ -33,7 +33,7 @@ class State(C.Structure):
     """pffmg_state (include/pffmg.h)."""
     _fields_ = [("mu", C.c_double), ("lam", C.c_double), ("g_c", C.c_double),
                 ("kappa", C.c_double), ("eps", C.c_double), ("pressure", C.c_double),
-                ("split", C.c_int32), ("pad_", C.c_int32),
+                ("split", C.c_int32), ("hints", C.c_int32),
                 ("U", vp), ("phi_tilde", vp), ("rho", vp), ("flags", vp)]
 
 

@@ -1,8 +1,10 @@
 // Cell kernel for isotropic cells (h equal on every axis -- every BASELINE
 // configuration and every reference test mesh).  Same physics as the generic
 // cell_kernel in cellops.cuh (reference model.py:270-355), with the 1/h and
-// JxW factors folded into per-level constants (IsoK, built on the host) and
-// the symmetric tensor algebra written out.
+// JxW factors folded into per-level constants (IsoK, built on the host), the
+// symmetric tensor algebra written out, gradients kept in reduced form (a
+// derivative along j is constant along j) and the constant-coefficient
+// k_phi Laplacian applied in closed form at the corners.
 //
 // With raw reference derivatives r_ij = d_j^ref U_i, w_ij = d_j^ref v_i, and
 // the raw "stress" of U   S_ii = 2 mu r_ii + lam tr r,  S_ij = mu (r_ij + r_ji):
@@ -12,8 +14,7 @@
 //                                = ih^2 rho (1-k) phi S : w + 2 p phi ih tr w
 //   u-row stress (model.py:313-330)
 //     G_ii = JxW ih^2 gk rho (2 mu w_ii + lam tr w),  G_ij = JxW ih^2 gk rho mu (w_ij + w_ji)
-// and the k_phi Laplacian (constant per cell) is applied at the corners as
-// sum_j (D^T D)_j (x) (B^T B)_others (model.py:337, 353-354).
+//   k_phi Laplacian (model.py:337, 353-354): sum_j (D^T D)_j (x) (B^T B)_others
 #pragma once
 
 #include "cellops.cuh"
@@ -29,7 +30,9 @@ struct IsoK {
     double ctr;            // JxW 2 p ih                      -> pressure coupling (times phi)
     double clap;           // JxW k_phi ih^2
     double two_mu, lam, mu;
-    double bb_lo, bb_hi;   // sum_q B_qa B_qb: (2/3, 1/3) for the 2-point Gauss rule
+    double lapA, lapB, lapK1;   // 2D Laplacian: out_n += A u_n + B u_{n^3} + K1 sum(u)
+    double lam3[8];             // 3D Laplacian eigenvalues in the Walsh basis (scaled, / 8)
+    double dlo, dhi;            // diagonal helpers: sum_q B_qa B_qb (same / different corner)
 };
 
 inline IsoK make_iso_host(const Consts& K) {
@@ -47,40 +50,70 @@ inline IsoK make_iso_host(const Consts& K) {
     I.two_mu = 2.0 * K.mu;
     I.lam = K.lam;
     I.mu = K.mu;
-    I.bb_lo = K.omg0 * K.omg0 + K.omg1 * K.omg1;
-    I.bb_hi = K.omg0 * K.g0 + K.omg1 * K.g1;
+    // 1D tensor factors of the Laplacian: D^T D = 2 [[1,-1],[-1,1]], B^T B = [[lo,hi],[hi,lo]]
+    const double lo = K.omg0 * K.omg0 + K.omg1 * K.omg1;
+    const double hi = K.omg0 * K.g0 + K.omg1 * K.g1;
+    I.dlo = lo;
+    I.dhi = hi;
+    // 2D: K[n][m] = k_{popcount(n^m)}: k0 = 4 lo, k1 = 2 (hi - lo), k2 = -4 hi
+    const double k0 = 4.0 * lo, k1 = 2.0 * (hi - lo), k2 = -4.0 * hi;
+    I.lapA = I.clap * (k0 - k1);
+    I.lapB = I.clap * (k2 - k1);
+    I.lapK1 = I.clap * k1;
+    // 3D: Walsh basis s (bit a = difference mode along a): lambda(s) =
+    // sum_j [s_j] 4 prod_{a != j} (s_a ? lo - hi : lo + hi); scaled by clap / 8
+    for (int s = 0; s < 8; ++s) {
+        double lamv = 0.0;
+        for (int j = 0; j < 3; ++j) {
+            if (!((s >> j) & 1)) continue;
+            double p = 4.0;
+            for (int a = 0; a < 3; ++a)
+                if (a != j) p *= ((s >> a) & 1) ? (lo - hi) : (lo + hi);
+            lamv += p;
+        }
+        I.lam3[s] = I.clap * lamv * 0.125;
+    }
     return I;
 }
 
-// out[n] += scale * sum_j ((D^T D)_j (x) (B^T B)_{other axes}) c   (Q1 cell Laplacian)
+// out[n] += k_phi JxW ih^2 sum_q grad N_m . grad N_n  u_m   (Q1 cell Laplacian)
 template <int D>
-__device__ __forceinline__ void corner_laplacian(const double (&c)[1 << D], double scale,
-                                                 const IsoK& I, double (&out)[1 << D]) {
-    constexpr int NP = 1 << D;
+__device__ __forceinline__ void corner_laplacian(const double (&c)[1 << D], const IsoK& I,
+                                                 double (&out)[1 << D]) {
+    if (D == 2) {
+        const double s = (c[0] + c[1]) + (c[2] + c[3]);
+        const double ks = I.lapK1 * s;
 #pragma unroll
-    for (int j = 0; j < D; ++j) {
-        double t[NP];
+        for (int n = 0; n < 4; ++n) out[n] = fma(I.lapA, c[n], fma(I.lapB, c[n ^ 3], out[n] + ks));
+    } else {
+        double t[1 << D];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) t[i] = c[i];
+        for (int i = 0; i < (1 << D); ++i) t[i] = c[i];
 #pragma unroll
-        for (int a = 0; a < D; ++a) {
+        for (int a = 0; a < D; ++a)
 #pragma unroll
-            for (int i = 0; i < NP; ++i) {
+            for (int i = 0; i < (1 << D); ++i) {
                 if (i & (1 << a)) continue;
                 const int k = i | (1 << a);
                 const double u0 = t[i], u1 = t[k];
-                if (a == j) {            // D^T D = [[2, -2], [-2, 2]]
-                    const double d = 2.0 * (u1 - u0);
-                    t[i] = -d;
-                    t[k] = d;
-                } else {                 // B^T B = [[lo, hi], [hi, lo]]
-                    t[i] = fma(I.bb_lo, u0, I.bb_hi * u1);
-                    t[k] = fma(I.bb_hi, u0, I.bb_lo * u1);
-                }
+                t[i] = u0 + u1;
+                t[k] = u0 - u1;
             }
-        }
+        t[0] = 0.0;
 #pragma unroll
-        for (int i = 0; i < NP; ++i) out[i] = fma(scale, t[i], out[i]);
+        for (int s = 1; s < (1 << D); ++s) t[s] *= I.lam3[s];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int i = 0; i < (1 << D); ++i) {
+                if (i & (1 << a)) continue;
+                const int k = i | (1 << a);
+                const double u0 = t[i], u1 = t[k];
+                t[i] = u0 + u1;
+                t[k] = u0 - u1;
+            }
+#pragma unroll
+        for (int i = 0; i < (1 << D); ++i) out[i] += t[i];
     }
 }
 
@@ -106,8 +139,8 @@ __device__ __forceinline__ void cell_kernel_iso(const double (&cv)[ModeInfo<D, M
                                                 const IsoK& I,
                                                 double (&o)[ModeInfo<D, MODE>::NCO][1 << D]) {
     using MI = ModeInfo<D, MODE>;
-    constexpr int NP = 1 << D;
-    using S = SF<D>;
+    constexpr int NP = 1 << D, NR = 1 << (D - 1);
+    using S = SFr<D>;
 
     double rho[NP];
 #pragma unroll
@@ -115,47 +148,46 @@ __device__ __forceinline__ void cell_kernel_iso(const double (&cv)[ModeInfo<D, M
 
     double gks[NP];                                 // JxW ih^2 gk rho   (model.py:282, 295)
     if (MI::PT) {
-        double pv[D + 1][NP];
-        S::interp(cv[MI::F_PT], pv, K);
+        double pv[NP];
+        S::value(cv[MI::F_PT], pv, K);
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
-            const double ph = pv[0][q];
-            const double g = fma(I.gk_a * ph, ph, I.gk_b);
+            const double g = fma(I.gk_a * pv[q], pv[q], I.gk_b);
             gks[q] = RHO ? g * rho[q] : g;
         }
     }
 
-    // raw gradient of U's displacement part -> stress S, a_phiphi * JxW
-    double Sd[NP][D], So[NP][D * (D - 1) / 2], aj[NP];
+    // U's displacement gradient -> stress S, a_phiphi * JxW
+    double Sd[NP][D], So[NP][D * (D - 1) / 2 > 0 ? D * (D - 1) / 2 : 1], aj[NP];
     if (MI::NU > 0) {
-        double r[NP][D][D];
+        double rr[D][D][NR];
 #pragma unroll
-        for (int i = 0; i < D; ++i) {
-            double t[D + 1][NP];
-            S::interp(cv[MI::F_U + i], t, K, false);
+        for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int q = 0; q < NP; ++q)
-#pragma unroll
-                for (int j = 0; j < D; ++j) r[q][i][j] = t[1 + j][q];
-        }
+            for (int j = 0; j < D; ++j) S::deriv(cv[MI::F_U + i], j, rr[i][j], K);
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
-            double dv = 0.0;
+            double r[D][D];
 #pragma unroll
-            for (int i = 0; i < D; ++i) dv += r[q][i][i];
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = 0; j < D; ++j) r[i][j] = rr[i][j][drop_bit(q, j)];
+            double dv = r[0][0];
+#pragma unroll
+            for (int i = 1; i < D; ++i) dv += r[i][i];
             const double ld = I.lam * dv;
             double e2 = 0.0;                           // S : sym(r) = 2 E+ / ih^2
 #pragma unroll
             for (int i = 0; i < D; ++i) {
-                Sd[q][i] = fma(I.two_mu, r[q][i][i], ld);
-                e2 = fma(Sd[q][i], r[q][i][i], e2);
+                Sd[q][i] = fma(I.two_mu, r[i][i], ld);
+                e2 = fma(Sd[q][i], r[i][i], e2);
             }
             int k = 0;
 #pragma unroll
             for (int i = 0; i < D; ++i)
 #pragma unroll
                 for (int j = i + 1; j < D; ++j, ++k) {
-                    const double s = r[q][i][j] + r[q][j][i];
+                    const double s = r[i][j] + r[j][i];
                     So[q][k] = I.mu * s;
                     e2 = fma(So[q][k], s, e2);
                 }
@@ -171,7 +203,7 @@ __device__ __forceinline__ void cell_kernel_iso(const double (&cv)[ModeInfo<D, M
             double du[D];
 #pragma unroll
             for (int i = 0; i < D; ++i) du[i] = 0.0;
-            double dp = 0.0, g2 = 0.0;
+            double dp = 0.0;
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
                 double Nv = 1.0, gN[D];
@@ -198,46 +230,44 @@ __device__ __forceinline__ void cell_kernel_iso(const double (&cv)[ModeInfo<D, M
                 for (int i = 0; i < D; ++i)
                     du[i] = fma(gks[q], fma(I.mu, gg, (I.mu + I.lam) * (gN[i] * gN[i])), du[i]);
                 dp = fma(aj[q], Nv * Nv, dp);
-                g2 += gg;
             }
 #pragma unroll
             for (int i = 0; i < D; ++i) o[i][n] = du[i];
-            o[D][n] = fma(I.clap, g2, dp);
+            // Laplacian diagonal: k_phi JxW ih^2 * D * 2 * lo^(D-1)
+            double lap = 2.0 * D;
+#pragma unroll
+            for (int a = 1; a < D; ++a) lap *= I.dlo;
+            o[D][n] = fma(I.clap, lap, dp);
         }
         return;
     }
 
     double coup[NP];
     if (MODE == M_FULL || MODE == M_UBLK) {
-        double w[NP][D][D];
+        double ww[D][D][NR];
 #pragma unroll
-        for (int i = 0; i < D; ++i) {
-            double t[D + 1][NP];
-            S::interp(cv[MI::F_V + i], t, K, false);
+        for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int q = 0; q < NP; ++q)
-#pragma unroll
-                for (int j = 0; j < D; ++j) w[q][i][j] = t[1 + j][q];
-        }
+            for (int j = 0; j < D; ++j) S::deriv(cv[MI::F_V + i], j, ww[i][j], K);
         double phq[NP];
-        if (MODE == M_FULL) {
-            double t[D + 1][NP];
-            S::interp(cv[MI::F_U + D], t, K);
-#pragma unroll
-            for (int q = 0; q < NP; ++q) phq[q] = t[0][q];
-        }
+        if (MODE == M_FULL) S::value(cv[MI::F_U + D], phq, K);
         double G[D][D][NP];
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
-            double trw = 0.0;
+            double w[D][D];
 #pragma unroll
-            for (int i = 0; i < D; ++i) trw += w[q][i][i];
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = 0; j < D; ++j) w[i][j] = ww[i][j][drop_bit(q, j)];
+            double trw = w[0][0];
+#pragma unroll
+            for (int i = 1; i < D; ++i) trw += w[i][i];
             const double lt = I.lam * trw;
             double Y = 0.0;                            // S : w
 #pragma unroll
             for (int i = 0; i < D; ++i) {
-                G[i][i][q] = gks[q] * fma(I.two_mu, w[q][i][i], lt);
-                if (MODE == M_FULL) Y = fma(Sd[q][i], w[q][i][i], Y);
+                G[i][i][q] = gks[q] * fma(I.two_mu, w[i][i], lt);
+                if (MODE == M_FULL) Y = fma(Sd[q][i], w[i][i], Y);
             }
             const double cm = gks[q] * I.mu;
             int k = 0;
@@ -245,7 +275,7 @@ __device__ __forceinline__ void cell_kernel_iso(const double (&cv)[ModeInfo<D, M
             for (int i = 0; i < D; ++i)
 #pragma unroll
                 for (int j = i + 1; j < D; ++j, ++k) {
-                    const double sw = w[q][i][j] + w[q][j][i];
+                    const double sw = w[i][j] + w[j][i];
                     const double g = cm * sw;
                     G[i][j][q] = g;
                     G[j][i][q] = g;
@@ -258,22 +288,19 @@ __device__ __forceinline__ void cell_kernel_iso(const double (&cv)[ModeInfo<D, M
         }
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-            double f[NP];
-            S::template integrate<false>(f, G[i], K);
+            S::template deriv_T<false>(G[i][0], 0, o[i], K);
 #pragma unroll
-            for (int n = 0; n < NP; ++n) o[i][n] = f[n];
+            for (int j = 1; j < D; ++j) S::template deriv_T<true>(G[i][j], j, o[i], K);
         }
     }
     if (MODE == M_FULL || MODE == M_PBLK) {
         const double(&cp)[NP] = cv[MODE == M_FULL ? MI::F_V + D : MI::F_V];
-        double t[D + 1][NP];
-        S::interp(cp, t, K);
         double f[NP];
+        S::value(cp, f, K);
 #pragma unroll
-        for (int q = 0; q < NP; ++q)
-            f[q] = MODE == M_FULL ? fma(aj[q], t[0][q], coup[q]) : aj[q] * t[0][q];
+        for (int q = 0; q < NP; ++q) f[q] = MODE == M_FULL ? fma(aj[q], f[q], coup[q]) : aj[q] * f[q];
         mass_transpose<D>(f, K);
-        corner_laplacian<D>(cp, I.clap, I, f);
+        corner_laplacian<D>(cp, I, f);
         constexpr int slot = MODE == M_FULL ? D : 0;
 #pragma unroll
         for (int n = 0; n < NP; ++n) o[slot][n] = f[n];

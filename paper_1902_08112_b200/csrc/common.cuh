@@ -170,6 +170,89 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// Leaner factorisations used by the isotropic kernels.  A derivative along j
+// of a Q1 field is constant along j, so it is stored "reduced": an array of
+// 2^(D-1) values indexed by the other axes' bits (compile-time helpers
+// below).  Gradients take the pair difference first and interpolate the
+// reduced array; transposed gradient terms sum the pairs first.
+__host__ __device__ constexpr int drop_bit(int i, int j) {       // remove bit j
+    return (i & ((1 << j) - 1)) | ((i >> (j + 1)) << j);
+}
+__host__ __device__ constexpr int put_bit(int r, int j, int b) {  // insert bit b at j
+    return (r & ((1 << j) - 1)) | (b << j) | ((r >> j) << (j + 1));
+}
+
+template <int D>
+struct SFr {
+    static constexpr int NP = 1 << D, NR = 1 << (D - 1);
+
+    // values at the QPs (B along every axis)
+    __device__ __forceinline__ static void value(const double (&c)[NP], double (&v)[NP], const Consts& K) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) v[i] = c[i];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                if (i & (1 << a)) continue;
+                const int k = i | (1 << a);
+                const double u0 = v[i], d = v[k] - u0;
+                v[i] = fma(K.g0, d, u0);
+                v[k] = fma(K.g1, d, u0);
+            }
+    }
+
+    // raw derivative along j, reduced: g[r] = d_j^ref c at QPs with other bits r
+    __device__ __forceinline__ static void deriv(const double (&c)[NP], int j, double (&g)[NR],
+                                                 const Consts& K) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) g[r] = c[put_bit(r, j, 1)] - c[put_bit(r, j, 0)];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            if (a == j) continue;
+            const int ab = a < j ? a : a - 1;     // bit position in the reduced index
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                if (r & (1 << ab)) continue;
+                const int k = r | (1 << ab);
+                const double u0 = g[r], d = g[k] - u0;
+                g[r] = fma(K.g0, d, u0);
+                g[k] = fma(K.g1, d, u0);
+            }
+        }
+    }
+
+    // out[n] (=|+=) sum_q G[q] dN_n/dref_j (q): pairs summed along j, then B^T on the others
+    template <bool ACC>
+    __device__ __forceinline__ static void deriv_T(const double (&G)[NP], int j, double (&out)[NP],
+                                                   const Consts& K) {
+        double r[NR];
+#pragma unroll
+        for (int i = 0; i < NR; ++i) r[i] = G[put_bit(i, j, 0)] + G[put_bit(i, j, 1)];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            if (a == j) continue;
+            const int ab = a < j ? a : a - 1;
+#pragma unroll
+            for (int i = 0; i < NR; ++i) {
+                if (i & (1 << ab)) continue;
+                const int k = i | (1 << ab);
+                const double f0 = r[i], f1 = r[k];
+                r[i] = fma(K.omg0, f0, K.omg1 * f1);
+                r[k] = fma(K.g0, f0, K.g1 * f1);
+            }
+        }
+#pragma unroll
+        for (int n = 0; n < NP; ++n) {
+            const double t = r[drop_bit(n, j)];
+            if (ACC)
+                out[n] = ((n >> j) & 1) ? out[n] + t : out[n] - t;
+            else
+                out[n] = ((n >> j) & 1) ? t : -t;
+        }
+    }
+};
+
 // Deterministic block reduction helpers --------------------------------------
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -1,19 +1,34 @@
 // 2D instantiations of the fused operator kernels (see op_kernels.cuh).
+#include <cstdlib>
+
 #include "op_launch.cuh"
 
 namespace pffmg {
 
 constexpr int NW2D = 4;   // warps per CTA of the warp-independent 2D kernel
 
-template <int MODE, int EPI, bool ISO, bool RHO>
+template <int MODE, int EPI, bool ISO, bool RHO, bool BOX, bool PRE>
 static void launch_w(const OpArgs& A, dim3 grid, size_t smem, cudaStream_t s) {
     static size_t done = 0;
     if (smem > 48 * 1024 && done < smem) {
-        cudaFuncSetAttribute(op2dw_kernel<MODE, EPI, NW2D, ISO, RHO>,
+        cudaFuncSetAttribute(op2dw_kernel<MODE, EPI, NW2D, ISO, RHO, BOX, PRE>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         done = smem;
     }
-    op2dw_kernel<MODE, EPI, NW2D, ISO, RHO><<<grid, 32 * NW2D, smem, s>>>(A);
+    op2dw_kernel<MODE, EPI, NW2D, ISO, RHO, BOX, PRE><<<grid, 32 * NW2D, smem, s>>>(A);
+}
+
+template <int MODE, int EPI, bool ISO, bool RHO>
+static void launch_box(const OpArgs& A, bool pre, dim3 grid, size_t smem, cudaStream_t s) {
+    const bool box = A.L.vrow_off == nullptr;
+    if (box && pre)
+        launch_w<MODE, EPI, ISO, RHO, true, true>(A, grid, smem, s);
+    else if (box)
+        launch_w<MODE, EPI, ISO, RHO, true, false>(A, grid, smem, s);
+    else if (pre)
+        launch_w<MODE, EPI, ISO, RHO, false, true>(A, grid, smem, s);
+    else
+        launch_w<MODE, EPI, ISO, RHO, false, false>(A, grid, smem, s);
 }
 
 template <int MODE, int EPI>
@@ -22,26 +37,32 @@ int launch2d(const OpArgs& A0, bool iso, cudaStream_t s) {
     const Lat& L = A.L;
     using MI = ModeInfo<2, MODE>;
     const int sms = sm_count();
-    const int nseg = (L.nx + 1 + 30) / 31;
+    const int nseg = (L.nx + 1 + 29) / 30;
     const int rows = L.ny + 1;
     // strips of H vertex rows: aim for ~24 resident warps per SM in one wave,
     // H in [4, 64] (the first cell row of a strip is recomputed: overhead 1/H)
     int64_t per = ((int64_t)rows * nseg + 24LL * sms - 1) / (24LL * sms);
     per = per < 4 ? 4 : (per > 64 ? 64 : per);
+    static const int forced = [] {
+        const char* e = getenv("PFFMG_2D_ROWS");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced > 0) per = forced;
     A.planes_per_cta = (int)per;
     A.nseg = nseg;
     const int64_t warps = (int64_t)nseg * ((rows + per - 1) / per);
     dim3 grid((unsigned)((warps + NW2D - 1) / NW2D));
-    const size_t smem = NW2D * (sizeof(double) * 4 * MI::NF * 33 + 4 * 40 + 4 * sizeof(int));
+    const size_t smem = NW2D * (sizeof(double) * 4 * MI::NF * 32 + 4 * 48 + 4 * sizeof(int));
     const bool rho = A.rho != nullptr;
+    const bool pre = A.premasked != 0;
     if (iso && rho)
-        launch_w<MODE, EPI, true, true>(A, grid, smem, s);
+        launch_box<MODE, EPI, true, true>(A, pre, grid, smem, s);
     else if (iso)
-        launch_w<MODE, EPI, true, false>(A, grid, smem, s);
+        launch_box<MODE, EPI, true, false>(A, pre, grid, smem, s);
     else if (rho)
-        launch_w<MODE, EPI, false, true>(A, grid, smem, s);
+        launch_box<MODE, EPI, false, true>(A, pre, grid, smem, s);
     else
-        launch_w<MODE, EPI, false, false>(A, grid, smem, s);
+        launch_box<MODE, EPI, false, false>(A, pre, grid, smem, s);
     return PFFMG_OK;
 }
 

@@ -37,7 +37,8 @@ struct OpArgs {
     double c1, c2;                     // CHEB: c_dd, c_dr   CHEB0: theta
     int x_add_din;                     // CHEB: x = (x + d_in) + d_out instead of x += d_out
     int planes_per_cta;
-    int nseg;                          // 2D warp kernel: 31-column segments per row
+    int nseg;                          // 2D warp kernel: 30-column segments per row
+    int premasked;                     // PFFMG_HINT_PREMASKED
 };
 
 // ------------------------------------------------------------ epilogue
@@ -227,26 +228,58 @@ __global__ void __launch_bounds__(32 * NW) op2d_kernel(const OpArgs A) {
 }
 
 // ================================================================ 2D (warps)
-// Warp-independent variant: each warp owns a 31-column segment and a strip of
-// vertex rows; lane L computes cell cx = 31*seg - 1 + L (lane 0 computes the
-// cell shared with the neighbouring segment and finalises nothing).  Vertex
-// rows are staged into a warp-private 4-slot shared-memory ring with cp.async
-// two rows ahead of the cell row being computed; flags arrive as the 9
-// aligned 32-bit words covering the row segment.  No block-wide barriers.
-// Requires the flags buffer to be readable up to round_up(V, 4) + 36 bytes.
+// Warp-independent 2D kernel.  Each warp owns a segment of 30 vertex columns
+// and a strip of vertex rows.  Lanes load columns x0..x0+31 (x0 = 30*seg - 1);
+// lanes 0..30 compute cells cx = x0 + L (lane 0's cell is shared with the
+// neighbouring segment), lanes 1..30 finalise their vertex column.  Rows are
+// staged into a warp-private 4-slot shared-memory ring with cp.async three
+// rows ahead (fp64 fields: one 8-byte copy per lane and field; constraint
+// flags: the 9 aligned 32-bit words covering the row's 32 flag bytes, ids of a
+// lattice row being contiguous).  No block-wide barriers.  Unless the caller
+// promises pre-masked inputs (PFFMG_HINT_PREMASKED -- true inside the V-cycle,
+// CG-Lanczos and GMRES, whose vectors are always zero at constrained dofs),
+// every lane zeroes its own constrained entries once the row has landed
+// (the masked gather of fem.py:205-206, once per vertex).
 
-template <int MODE, int EPI, int NW, bool ISO, bool RHO>
-__global__ void __launch_bounds__(32 * NW) op2dw_kernel(const OpArgs A) {
+template <bool BOX>
+struct RowAddr {
+    // vertex id of (x, y) or -1 (32-bit: every supported level has < 2^31 dofs)
+    __device__ __forceinline__ static int id(const Lat& L, int x, int y) {
+        if (BOX) {
+            if ((unsigned)x > (unsigned)L.nx || (unsigned)y > (unsigned)L.ny) return -1;
+            return y * (L.nx + 1) + x;
+        }
+        return (int)vertex_id(L, x, y, 0);
+    }
+    // "virtual" id of column x in row y: ids of a row are contiguous, so this
+    // extends the row's numbering to columns outside the row (flag staging)
+    __device__ __forceinline__ static int vid_virtual(const Lat& L, int x, int y) {
+        if (BOX) return y * (L.nx + 1) + x;
+        if ((unsigned)y > (unsigned)L.ny) return 0;
+        return (int)__ldg(L.vrow_off + y) + (x - __ldg(L.vrow_lo + y));
+    }
+};
+
+template <int MODE, int EPI, int NW, bool ISO, bool RHO, bool BOX, bool PRE>
+#ifndef PFFMG_MINB_FULL
+#define PFFMG_MINB_FULL 4
+#endif
+#ifndef PFFMG_MINB_BLK
+#define PFFMG_MINB_BLK 8
+#endif
+__global__ void __launch_bounds__(32 * NW, MODE == M_FULL ? PFFMG_MINB_FULL : PFFMG_MINB_BLK)
+op2dw_kernel(const OpArgs A) {
     constexpr int D = 2, NP = 4;
     using MI = ModeInfo<D, MODE>;
-    constexpr int NF = MI::NF, NCO = MI::NCO;
-    constexpr int RING = 4, W = 33, FW = 40;
+    constexpr int NF = MI::NF, NCO = MI::NCO, NV = MI::NV;
+    constexpr int RING = 4, W = 32, SLOT = NF * W;
+    constexpr int FB = 48;                      // flag bytes per slot (9 words + pad)
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    double* sv = reinterpret_cast<double*>(smem_raw) + w * (RING * NF * W);
-    uint8_t* sf = smem_raw + sizeof(double) * NW * RING * NF * W + w * (RING * FW);
-    int* sfb = reinterpret_cast<int*>(smem_raw + sizeof(double) * NW * RING * NF * W + NW * RING * FW) +
+    double* sv = reinterpret_cast<double*>(smem_raw) + w * (RING * SLOT);
+    unsigned char* sfl = smem_raw + sizeof(double) * NW * RING * SLOT + w * (RING * FB);
+    int* sfo = reinterpret_cast<int*>(smem_raw + sizeof(double) * NW * RING * SLOT + NW * RING * FB) +
                w * RING;
 
     const Lat& L = A.L;
@@ -255,48 +288,61 @@ __global__ void __launch_bounds__(32 * NW) op2dw_kernel(const OpArgs A) {
     const int vy0 = strip * A.planes_per_cta;
     if (vy0 > L.ny) return;
     const int vy1 = min(vy0 + A.planes_per_cta, L.ny + 1);
-    const int x0 = 31 * seg - 1;
+    const int x0 = 30 * seg - 1;
     const int cx = x0 + lane;
-    const int64_t V = L.V;
+    const int V = (int)L.V;
+    const int nwords = (V + 3) / 4 + 8;          // readable flag words (padded buffer)
+    const bool col_cell = lane <= 30 && cx >= 0 && cx < L.nx;
+    const bool col_fin = lane >= 1 && lane <= 30;
 
     const double* fsrc[NF];
 #pragma unroll
-    for (int i = 0; i < MI::NV; ++i) fsrc[MI::F_V + i] = A.v + (int64_t)i * V;
+    for (int i = 0; i < NV; ++i) fsrc[MI::F_V + i] = A.v + (int64_t)i * V;
 #pragma unroll
     for (int i = 0; i < MI::NU; ++i) fsrc[MI::F_U + i] = A.U + (int64_t)i * V;
     if (MI::PT) fsrc[MI::F_PT] = A.pt;
+    const uint32_t* fw = reinterpret_cast<const uint32_t*>(A.flags);
 
     auto issue = [&](int y, int slot) {
-        double* dst = sv + slot * (NF * W);
-        const int64_t vid = vertex_id(L, cx, y, 0);
+        double* dst = sv + slot * SLOT + lane;
+        const int vid = RowAddr<BOX>::id(L, cx, y);
+        const bool ok = vid >= 0;
+        const int off = ok ? vid : 0;
 #pragma unroll
-        for (int f = 0; f < NF; ++f) cp_async8(dst + f * W + lane, fsrc[f] + (vid < 0 ? 0 : vid), vid >= 0);
-        if (lane == 31) {
-            const int64_t v2 = vertex_id(L, cx + 1, y, 0);
-#pragma unroll
-            for (int f = 0; f < NF; ++f) cp_async8(dst + f * W + 32, fsrc[f] + (v2 < 0 ? 0 : v2), v2 >= 0);
+        for (int f = 0; f < NF; ++f) cp_async8(dst + f * W, fsrc[f] + off, ok);
+        const int v0 = RowAddr<BOX>::vid_virtual(L, x0, y);
+        const int w0 = v0 >> 2;                  // floor division (v0 may be -1)
+        if (lane < 9) {
+            const int wi = w0 + lane;
+            const bool okw = wi >= 0 && wi < nwords && (unsigned)y <= (unsigned)L.ny;
+            cp_async4(sfl + slot * FB + 4 * lane, fw + (okw ? wi : 0), okw);
         }
-        // flag bytes of columns x0 .. x0+32 (contiguous ids inside a lattice row)
-        int lo = 0, hi = L.nx + 1;
-        const bool yin = y >= 0 && y <= L.ny;
-        if (yin && L.vrow_off) {
-            const int r = y;
-            lo = __ldg(L.vrow_lo + r);
-            hi = __ldg(L.vrow_hi + r);
-        }
-        const int xf = max(x0, lo);
-        const bool any = yin && xf <= min(x0 + 32, hi - 1);
-        int64_t vf = any ? vertex_id(L, xf, y, 0) : 0;
-        const int64_t wbase = vf >> 2;
-        if (lane < 9)
-            cp_async4(sf + slot * FW + 4 * lane, reinterpret_cast<const uint32_t*>(A.flags) + wbase + lane, any);
-        if (lane == 0) sfb[slot] = any ? (int)(vf & 3) - (xf - x0) : 0;
+        if (lane == 0) sfo[slot] = v0 - 4 * w0;  // byte of column x0 inside the staged words
         cp_async_commit();
+    };
+    auto flag = [&](int slot) -> unsigned { return sfl[slot * FB + sfo[slot] + lane]; };
+    auto mask_row = [&](int slot) {              // fem.py:205-206, once per vertex
+        if (PRE || NV == 0) return;
+        const unsigned fl = flag(slot);
+        double* row = sv + slot * SLOT;
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+            if ((fl >> (MI::COMP0 + i)) & 1) row[i * W + lane] = 0.0;
     };
 
     issue(vy0 - 1, 0);
     issue(vy0, 1);
     issue(vy0 + 1, 2);
+    cp_async_wait<1>();                          // rows vy0-1, vy0 landed
+    __syncwarp();
+    double raw_bot[NV > 0 ? NV : 1];             // raw own-column v of the bottom row
+#pragma unroll
+    for (int i = 0; i < NV; ++i) raw_bot[i] = sv[0 * SLOT + i * W + lane];
+    mask_row(0);
+    double raw_top[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) raw_top[i] = sv[1 * SLOT + i * W + lane];
+    mask_row(1);
 
     double carry[NCO];
 #pragma unroll
@@ -304,35 +350,35 @@ __global__ void __launch_bounds__(32 * NW) op2dw_kernel(const OpArgs A) {
 
     int it = 0;
     for (int cy = vy0 - 1; cy < vy1; ++cy, ++it) {
+        const int s0 = it & 3, s1 = (it + 1) & 3;
+        if (it > 0) {                            // row cy+1 becomes the top row
+            cp_async_wait<1>();
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                raw_bot[i] = raw_top[i];
+                raw_top[i] = sv[s1 * SLOT + i * W + lane];
+            }
+            mask_row(s1);
+        }
         if (cy + 3 <= vy1)
             issue(cy + 3, (it + 3) & 3);
         else
             cp_async_commit();
-        cp_async_wait<2>();
-        __syncwarp();
-        const int s0 = it & 3, s1 = (it + 1) & 3;
-        const double* r0 = sv + s0 * (NF * W);
-        const double* r1 = sv + s1 * (NF * W);
-        const int fb0 = sfb[s0], fb1 = sfb[s1];
-        auto flag = [&](int s, int fb, int j) -> uint8_t {
-            const int k = fb + j;
-            return sf[s * FW + (k < 0 ? 0 : k)];
-        };
+        if (!PRE) __syncwarp();                  // neighbour lanes' masking visible
 
+        const double* r0 = sv + s0 * SLOT;
+        const double* r1 = sv + s1 * SLOT;
         double o[NCO][NP];
-        if (cell_exists<D>(L, cx, cy, 0)) {
+        const bool cell = col_cell && (BOX ? (cy >= 0 && cy < L.ny) : cell_exists<D>(L, cx, cy, 0));
+        if (cell) {
             double cv[NF][NP];
 #pragma unroll
-            for (int n = 0; n < NP; ++n) {
-                const double* rr = (n >> 1) ? r1 : r0;
-                const int j = lane + (n & 1);
-                const uint8_t fl = (n >> 1) ? flag(s1, fb1, j) : flag(s0, fb0, j);
-#pragma unroll
-                for (int i = 0; i < NF; ++i) {
-                    double val = rr[i * W + j];
-                    if (i < MI::NV && ((fl >> (MI::COMP0 + i)) & 1)) val = 0.0;   // fem.py:205-206
-                    cv[i][n] = val;
-                }
+            for (int i = 0; i < NF; ++i) {
+                cv[i][0] = r0[i * W + lane];
+                cv[i][1] = r0[i * W + lane + 1];
+                cv[i][2] = r1[i * W + lane];
+                cv[i][3] = r1[i * W + lane + 1];
             }
             const double* rq = RHO ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * NP : nullptr;
             if (ISO)
@@ -354,22 +400,21 @@ __global__ void __launch_bounds__(32 * NW) op2dw_kernel(const OpArgs A) {
             bot[k] = o[k][0] + q0;
             top[k] = o[k][2] + q1;
         }
-        if (cy >= vy0 && lane >= 1) {
-            const int64_t vid = vertex_id(L, cx, cy, 0);
+        if (cy >= vy0 && col_fin) {
+            const int vid = RowAddr<BOX>::id(L, cx, cy);
             if (vid >= 0) {
                 double acc[NCO], vin[NCO];
-                const uint8_t fl = flag(s0, fb0, lane);
 #pragma unroll
                 for (int k = 0; k < NCO; ++k) {
                     acc[k] = carry[k] + bot[k];
-                    vin[k] = (MODE == M_DIAG) ? 0.0 : r0[(MI::F_V + k) * W + lane];
+                    vin[k] = (MODE == M_DIAG) ? 0.0 : raw_bot[k < NV ? k : 0];
                 }
-                epilogue<NCO, MI::COMP0, EPI>(A, vid, fl, acc, vin);
+                epilogue<NCO, MI::COMP0, EPI>(A, vid, (uint8_t)flag(s0), acc, vin);
             }
         }
 #pragma unroll
         for (int k = 0; k < NCO; ++k) carry[k] = top[k];
-        __syncwarp();
+        __syncwarp();                            // slot s0 free for the next issue
     }
     cp_async_wait<0>();
 }

@@ -37,6 +37,7 @@ static int fill_args(const pffmg_lattice* lat, const pffmg_state* st, OpArgs* A)
     A->pt = st->phi_tilde;
     A->rho = st->rho;
     A->flags = st->flags;
+    A->premasked = (st->hints & PFFMG_HINT_PREMASKED) ? 1 : 0;
     return PFFMG_OK;
 }
 

@@ -171,7 +171,7 @@ def _estimate_blocks(op, diag_dev, eig_iters, seed):
             ncomp = op.dim if k == 0 else 1
             _lib.call("pffmg_masked_copy", _lib.ptr(op.flags), op.V, comp0, ncomp, _lib.ptr(b),
                       _lib.ptr(b), _lib.stream())
-            scal = cg_lanczos_dev(lambda s_, d_, k=k: op.apply_dev(k, s_, d_), diag_dev[blk], b,
+            scal = cg_lanczos_dev(lambda s_, d_, k=k: op.apply_dev(k, s_, d_, pre=True), diag_dev[blk], b,
                                   eig_iters)
             spectra.append(lanczos_extremes(host(scal), eig_iters))
         else:
@@ -403,7 +403,7 @@ class _NativeCycle:
         self.x_out = None
 
     # one Chebyshev sweep on block k of level L: x (zero or not) -> smoothed x
-    def _cheb(self, L, k, prm, x_is_zero):
+    def _cheb(self, L, k, prm, x_is_zero, pre=True):
         op = L.op
         b = L.blk(k)
         x, r, rhs, inv = L.x[b], L.cr[b], L.r[b], L.inv[b]
@@ -416,10 +416,10 @@ class _NativeCycle:
                 x.zero_()
                 r.copy_(rhs)
             else:
-                op.residual_dev(k, x, rhs, r)
+                op.residual_dev(k, x, rhs, r, pre=pre)
             for _ in range(prm.degree):
                 _lib.call("pffmg_jacobi_update", _lib.ptr(r), _lib.ptr(inv), theta, _lib.ptr(x), nb, s)
-                op.residual_dev(k, x, rhs, r)
+                op.residual_dev(k, x, rhs, r, pre=pre)
             return
         sigma = theta / delta
         rho_old = 1.0 / sigma
@@ -428,11 +428,12 @@ class _NativeCycle:
                       _lib.ptr(d_in), _lib.ptr(x), nb, s)
             pending = False
         else:                                              # r = b - A x; d = inv r / theta
-            op.cheb_init_dev(k, x, rhs, r, d_in, inv, theta)
+            op.cheb_init_dev(k, x, rhs, r, d_in, inv, theta, pre=pre)
             pending = True                                 # x += d folded into the next step
         for _ in range(prm.degree - 1):
             rho = 1.0 / (2.0 * sigma - rho_old)
-            op.cheb_step_dev(k, d_in, d_out, r, x, inv, rho * rho_old, 2.0 * rho / delta, pending)
+            op.cheb_step_dev(k, d_in, d_out, r, x, inv, rho * rho_old, 2.0 * rho / delta, pending,
+                             pre=pre)
             pending = False
             d_in, d_out = d_out, d_in
             rho_old = rho
@@ -444,10 +445,10 @@ class _NativeCycle:
         for k in range(2):
             self._cheb(L, k, self.smooth_prm[l][k], x_is_zero)
 
-    def _coarse_into_x(self):
+    def _coarse_into_x(self, pre=True):
         L = self.levels[0]
         for k in range(2):
-            self._cheb(L, k, self.coarse_prm[k], True)
+            self._cheb(L, k, self.coarse_prm[k], True, pre)
 
     def _cycle(self, l):                                   # mgsolve.py:221-235
         if l == 0:
@@ -455,7 +456,7 @@ class _NativeCycle:
             return
         L, Lc = self.levels[l], self.levels[l - 1]
         self._smooth(l, True)
-        L.op.residual_dev(_lib.FULL, L.x, L.r, L.res)
+        L.op.residual_dev(_lib.FULL, L.x, L.r, L.res, pre=True)
         self.disc.restrict_dev(L.res, Lc.r, l - 1, L.dim + 1, 0, Lc.flags)
         self._cycle(l - 1)
         self.disc.prolongate_dev(Lc.x, L.x, l - 1, L.dim + 1, 0, L.flags, accumulate=True)
@@ -469,7 +470,7 @@ class _NativeCycle:
         Lc = self.levels[l - 1]
         b = L.blk(k)
         self._cheb(L, k, self.smooth_prm[l][k], True)
-        L.op.residual_dev(k, L.x[b], L.r[b], L.res[b])
+        L.op.residual_dev(k, L.x[b], L.r[b], L.res[b], pre=True)
         ncomp = L.dim if k == 0 else 1
         comp0 = 0 if k == 0 else L.dim
         self.disc.restrict_dev(L.res[b], Lc.r[Lc.blk(k)], l - 1, ncomp, comp0, Lc.flags)
@@ -509,9 +510,10 @@ class _NativeCycle:
         out.copy_(self.x_out)
 
     def coarse(self, r, out):
+        """Public coarse_solve: r is arbitrary (not masked), so no pre-mask hint."""
         L = self.levels[0]
         L.r.copy_(r)
-        self._coarse_into_x()
+        self._coarse_into_x(pre=False)
         out.copy_(L.x)
 
 

@@ -169,6 +169,13 @@ class PhaseFieldOperator:
         self._st = st
         import ctypes
         self._stp = ctypes.byref(st)
+        # same state with PFFMG_HINT_PREMASKED: for internal callers whose input
+        # vectors are zero at constrained dofs by construction (V-cycle, CG)
+        st_pre = _lib.State()
+        ctypes.pointer(st_pre)[0] = st
+        st_pre.hints = 1
+        self._st_pre = st_pre
+        self._stp_pre = ctypes.byref(st_pre)
 
     # -- reference surface --------------------------------------------------
     @property
@@ -214,24 +221,27 @@ class PhaseFieldOperator:
         return host(out)
 
     # -- device-level entry points (no conversions) --------------------------
-    def apply_dev(self, which, x, out):
-        _lib.call("pffmg_apply", self.lat.ref, self._stp, which, _lib.ptr(x), _lib.ptr(out),
+    def _sp(self, pre):
+        return self._stp_pre if pre else self._stp
+
+    def apply_dev(self, which, x, out, pre=False):
+        _lib.call("pffmg_apply", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(out),
                   _lib.stream())
 
-    def residual_dev(self, which, x, b, out):
-        _lib.call("pffmg_residual", self.lat.ref, self._stp, which, _lib.ptr(x), _lib.ptr(b),
+    def residual_dev(self, which, x, b, out, pre=False):
+        _lib.call("pffmg_residual", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
                   _lib.ptr(out), _lib.stream())
 
     def diagonal_dev(self, out):
         _lib.call("pffmg_diagonal", self.lat.ref, self._stp, _lib.ptr(out), _lib.stream())
 
-    def cheb_step_dev(self, which, d_in, d_out, r, x, inv, c_dd, c_dr, x_add_din=False):
-        _lib.call("pffmg_cheb_step", self.lat.ref, self._stp, which, _lib.ptr(d_in),
+    def cheb_step_dev(self, which, d_in, d_out, r, x, inv, c_dd, c_dr, x_add_din=False, pre=False):
+        _lib.call("pffmg_cheb_step", self.lat.ref, self._sp(pre), which, _lib.ptr(d_in),
                   _lib.ptr(d_out), _lib.ptr(r), _lib.ptr(x), _lib.ptr(inv), c_dd, c_dr,
                   int(x_add_din), _lib.stream())
 
-    def cheb_init_dev(self, which, x, b, r, d, inv, theta):
-        _lib.call("pffmg_cheb_init", self.lat.ref, self._stp, which, _lib.ptr(x), _lib.ptr(b),
+    def cheb_init_dev(self, which, x, b, r, d, inv, theta, pre=False):
+        _lib.call("pffmg_cheb_init", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
                   _lib.ptr(r), _lib.ptr(d), _lib.ptr(inv), theta, _lib.stream())
 
     # -- helpers ---------------------------------------------------------------

@@ -120,6 +120,24 @@ def test_larger_random_states_vs_oracle(name):
     assert rel_err(op.diagonal(), ref_op.diagonal()) <= TOL
 
 
+@pytest.mark.parametrize("name", ["cfg1", "lshape", "lprism", "cube"])
+def test_premasked_hint_is_exact(golden, name):
+    """PFFMG_HINT_PREMASKED (used inside the V-cycle / CG) gives bit-identical
+    results when the input is zero at constrained dofs."""
+    from paper_1902_08112_b200 import _lib
+    g = golden["operator"]
+    op, tag = _op(g, name, "masked")
+    flags = torch.as_tensor(g[f"{tag}/flags"], device="cuda")
+    v = torch.as_tensor(g[f"{tag}/v"], device="cuda").clone()
+    v[flags] = 0.0
+    d = op.dim * op.V
+    for which, vin, n in ((_lib.FULL, v, op.n_dofs), (0, v[:d], d), (1, v[d:], op.V)):
+        a, b = torch.empty(n, dtype=torch.float64, device="cuda"), torch.empty(n, dtype=torch.float64, device="cuda")
+        op.apply_dev(which, vin, a)
+        op.apply_dev(which, vin, b, pre=True)
+        assert torch.equal(a, b)
+
+
 def test_fused_epilogues_match_unfused(golden):
     """residual / Chebyshev epilogues == separate apply + vector algebra."""
     from paper_1902_08112_b200 import _lib
