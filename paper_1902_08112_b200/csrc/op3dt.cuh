@@ -1,0 +1,194 @@
+// 3D fused operator for isotropic hexahedra: CTA = TY warps, a tile of
+// 31 (x) x TY (y) cells marching in z.  Lanes load lattice columns
+// x0..x0+31 (x0 = 30*bx - 1); lanes 0..30 compute cells, lanes 1..30 /
+// warps 1..TY-1 finalise vertices.  Vertex planes are staged with cp.async
+// into a 4-slot shared-memory ring two planes ahead; the cell work is the
+// streaming cell3_iso kernel; vertex sums: x by shuffles, y through shared
+// memory, z by a register carry.  Replaces reference model.py:368-392 (+ the
+// fused epilogues of mgsolve.py:82-113, 227) for 3D levels.
+#pragma once
+
+#include "cell3_iso.cuh"
+#include "op_kernels.cuh"
+
+namespace pffmg {
+
+template <int MODE, int EPI, int TY, bool RHO, bool BOX, bool PRE>
+#ifndef PFFMG_3D_FULL_MINB
+#define PFFMG_3D_FULL_MINB 1
+#endif
+__global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB : 2) op3dt_kernel(const OpArgs A) {
+    using MI = ModeInfo<3, MODE>;
+    constexpr int NF = MI::NF, NCO = MI::NCO, NV = MI::NV;
+    constexpr int RING = 4, ROWS = TY + 1, W = 32;
+    constexpr int SLOT = NF * ROWS * W;          // doubles per staged plane
+    constexpr int FB = 48;                       // flag bytes per staged row
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* sv = reinterpret_cast<double*>(smem_raw);                          // [RING][NF][ROWS][W]
+    double* sy = sv + RING * SLOT;                                              // [TY][NCO][2][W]
+    unsigned char* sfl = reinterpret_cast<unsigned char*>(sy + TY * NCO * 2 * W);  // [RING][ROWS][FB]
+    int* sfo = reinterpret_cast<int*>(sfl + RING * ROWS * FB);                 // [RING][ROWS]
+
+    const Lat& L = A.L;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int x0 = 30 * (int)blockIdx.x - 1;
+    const int y0 = (TY - 1) * (int)blockIdx.y - 1;
+    const int vz0 = (int)blockIdx.z * A.planes_per_cta;
+    const int vz1 = min(vz0 + A.planes_per_cta, L.nz + 1);
+    const int cx = x0 + lane, cy = y0 + w;
+    const int V = (int)L.V;
+    const int nwords = (V + 3) / 4 + 8;
+    const bool lane_cell = lane <= 30;
+
+    const double* fsrc[NF];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) fsrc[MI::F_V + i] = A.v + (int64_t)i * V;
+#pragma unroll
+    for (int i = 0; i < MI::NU; ++i) fsrc[MI::F_U + i] = A.U + (int64_t)i * V;
+    if (MI::PT) fsrc[MI::F_PT] = A.pt;
+    const uint32_t* fw = reinterpret_cast<const uint32_t*>(A.flags);
+
+    auto vid_of = [&](int x, int y, int z) -> int {
+        if (BOX) {
+            if ((unsigned)x > (unsigned)L.nx || (unsigned)y > (unsigned)L.ny || (unsigned)z > (unsigned)L.nz)
+                return -1;
+            return (z * (L.ny + 1) + y) * (L.nx + 1) + x;
+        }
+        return (int)vertex_id(L, x, y, z);
+    };
+    auto vid_virtual = [&](int x, int y, int z) -> int {
+        if (BOX) return (z * (L.ny + 1) + y) * (L.nx + 1) + x;
+        if ((unsigned)y > (unsigned)L.ny || (unsigned)z > (unsigned)L.nz) return 0;
+        const int r = y + (L.ny + 1) * z;
+        return (int)__ldg(L.vrow_off + r) + (x - __ldg(L.vrow_lo + r));
+    };
+
+    // stage plane z into slot: row rr of the tile (rr = 0..TY), column = lane
+    auto issue = [&](int z, int slot) {
+        double* dst = sv + slot * SLOT;
+        for (int e = tid; e < ROWS * W; e += 32 * TY) {
+            const int rr = e / W, col = e % W;
+            const int vid = vid_of(x0 + col, y0 + rr, z);
+            const bool ok = vid >= 0;
+            const int off = ok ? vid : 0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) cp_async8(dst + (f * ROWS + rr) * W + col, fsrc[f] + off, ok);
+        }
+        for (int e = tid; e < ROWS * 9; e += 32 * TY) {
+            const int rr = e / 9, k = e % 9;
+            const int v0 = vid_virtual(x0, y0 + rr, z);
+            const int w0 = v0 >> 2;
+            const int wi = w0 + k;
+            const bool okw = wi >= 0 && wi < nwords && (unsigned)(y0 + rr) <= (unsigned)L.ny &&
+                             (unsigned)z <= (unsigned)L.nz;
+            cp_async4(sfl + (slot * ROWS + rr) * FB + 4 * k, fw + (okw ? wi : 0), okw);
+            if (k == 0) sfo[slot * ROWS + rr] = v0 - 4 * w0;
+        }
+        cp_async_commit();
+    };
+    auto flag = [&](int slot, int rr, int col) -> unsigned {
+        return sfl[(slot * ROWS + rr) * FB + sfo[slot * ROWS + rr] + col];
+    };
+    auto mask_plane = [&](int slot) {            // fem.py:205-206, once per staged vertex
+        if (PRE || NV == 0) return;
+        double* p = sv + slot * SLOT;
+        for (int e = tid; e < ROWS * W; e += 32 * TY) {
+            const int rr = e / W, col = e % W;
+            const unsigned fl = flag(slot, rr, col);
+#pragma unroll
+            for (int i = 0; i < NV; ++i)
+                if ((fl >> (MI::COMP0 + i)) & 1) p[(i * ROWS + rr) * W + col] = 0.0;
+        }
+    };
+
+    issue(vz0 - 1, 0);
+    issue(vz0, 1);
+    double carry[NCO];
+#pragma unroll
+    for (int k = 0; k < NCO; ++k) carry[k] = 0.0;
+
+    int it = 0;
+    for (int cz = vz0 - 1; cz < vz1; ++cz, ++it) {
+        const int s0 = it & 3, s1 = (it + 1) & 3;
+        if (cz + 2 <= vz1)
+            issue(cz + 2, (it + 2) & 3);
+        else
+            cp_async_commit();
+        cp_async_wait<1>();                      // planes cz, cz+1 landed (this thread's copies)
+        __syncthreads();                         // ... and everyone else's
+        if (!PRE) {
+            if (it == 0) mask_plane(s0);
+            mask_plane(s1);
+            __syncthreads();
+        }
+
+        const double* p0 = sv + s0 * SLOT;
+        const double* p1 = sv + s1 * SLOT;
+        struct Corners {
+            const double* p0;
+            const double* p1;
+            int lane, w;
+            __device__ __forceinline__ void load(int f, double (&c)[8]) const {
+#pragma unroll
+                for (int n = 0; n < 8; ++n) {
+                    const double* p = (n >> 2) ? p1 : p0;
+                    c[n] = p[(f * ROWS + w + ((n >> 1) & 1)) * W + lane + (n & 1)];
+                }
+            }
+        } C{p0, p1, lane < 31 ? lane : 30, w};
+
+        const bool cell = lane_cell && (BOX ? ((unsigned)cx < (unsigned)L.nx && (unsigned)cy < (unsigned)L.ny &&
+                                               (unsigned)cz < (unsigned)L.nz)
+                                            : cell_exists<3>(L, cx, cy, cz));
+        const double* rq = (RHO && cell) ? A.rho + ((int64_t)cx + (int64_t)L.nx * (cy + (int64_t)L.ny * cz)) * 8
+                                         : A.rho;
+        double vp[NCO][2];                       // this vertex column's (y=0) partials, per z corner
+        auto emit = [&](int k, double (&o)[8]) {
+#pragma unroll
+            for (int n = 0; n < 8; ++n) o[n] = cell ? o[n] : 0.0;
+#pragma unroll
+            for (int zb = 0; zb < 2; ++zb)
+#pragma unroll
+                for (int yb = 0; yb < 2; ++yb) {
+                    const int nl = (yb << 1) | (zb << 2);
+                    const double part = o[nl] + __shfl_up_sync(0xffffffffu, o[nl | 1], 1);
+                    if (yb)
+                        sy[((w * NCO + k) * 2 + zb) * W + lane] = part;
+                    else
+                        vp[k][zb] = part;
+                }
+        };
+        cell3_iso<MODE, RHO>(C, rq, A.K, A.I, emit);
+        __syncthreads();                         // y partials visible; planes fully read
+
+        if (w >= 1) {
+            double acc[NCO], top[NCO];
+#pragma unroll
+            for (int k = 0; k < NCO; ++k) {
+                acc[k] = carry[k] + (vp[k][0] + sy[(((w - 1) * NCO + k) * 2 + 0) * W + lane]);
+                top[k] = vp[k][1] + sy[(((w - 1) * NCO + k) * 2 + 1) * W + lane];
+            }
+            if (cz >= vz0 && lane >= 1 && lane <= 30) {
+                const int vid = vid_of(cx, cy, cz);
+                if (vid >= 0) {
+                    const unsigned fl = flag(s0, w, lane);
+                    double vin[NCO];
+#pragma unroll
+                    for (int k = 0; k < NCO; ++k) {
+                        // raw v (for identity rows): the staged copy was masked unless PRE
+                        vin[k] = PRE ? p0[((MI::F_V + k) * ROWS + w) * W + lane]
+                                     : (((fl >> (MI::COMP0 + k)) & 1) ? A.v[(int64_t)k * V + vid]
+                                                                      : p0[((MI::F_V + k) * ROWS + w) * W + lane]);
+                    }
+                    epilogue<NCO, MI::COMP0, EPI>(A, vid, (uint8_t)fl, acc, vin);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NCO; ++k) carry[k] = top[k];
+        }
+    }
+    cp_async_wait<0>();
+}
+
+}  // namespace pffmg

@@ -4,7 +4,7 @@
 //   -I../paper_1902_08112_b200/csrc -o cellbench cellbench.cu ../paper_1902_08112_b200/csrc/capi.cu
 #include <cstdio>
 
-#include "cellops_iso.cuh"
+#include "cell3_iso.cuh"
 
 using namespace pffmg;
 
@@ -32,6 +32,50 @@ __global__ void __launch_bounds__(128) bench(Consts K, IsoK I, int iters, double
             for (int n = 0; n < NP; ++n) cv[i][n] += eps;
     }
     if (acc == 1234.5) out[0] = acc;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(64) bench3(Consts K, IsoK I, int iters, double* out) {
+    using MI = ModeInfo<3, MODE>;
+    __shared__ double sm[MI::NF][8][64];
+    for (int i = 0; i < MI::NF; ++i)
+        for (int n = 0; n < 8; ++n) sm[i][n][threadIdx.x] = 1e-3 * (threadIdx.x + 3 * i + n) + (i == MI::F_PT ? 0.5 : 0.0);
+    struct Cn {
+        double (*sm)[8][64];
+        double eps;
+        __device__ void load(int f, double (&c)[8]) const {
+            for (int n = 0; n < 8; ++n) c[n] = sm[f][n][threadIdx.x] + eps;
+        }
+    };
+    double acc = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        Cn C{sm, 1e-30 * acc};
+        cell3_iso<MODE, false>(C, nullptr, K, I, [&](int k, double (&o)[8]) {
+#pragma unroll
+            for (int n = 0; n < 8; ++n) acc += o[n];
+        });
+    }
+    if (acc == 1234.5) out[0] = acc;
+}
+
+template <int MODE>
+void run3(const char* name, Consts K, IsoK I, double* d) {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int blocks = sms * 8, iters = 100;
+    bench3<MODE><<<blocks, 64>>>(K, I, 2, d);
+    cudaDeviceSynchronize();
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    bench3<MODE><<<blocks, 64>>>(K, I, iters, d);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    double cells = (double)blocks * 64 * iters;
+    printf("%s: %.1f Gcell/s  -> 1.08M cells in %.1f us\n", name, cells / ms * 1e-6, 1.08e6 / (cells / ms * 1e-3));
 }
 
 template <int D, int MODE>
@@ -73,5 +117,8 @@ int main() {
     run<3, M_FULL>("3D full", K, I, d);
     run<3, M_UBLK>("3D ublk", K, I, d);
     run<3, M_PBLK>("3D pblk", K, I, d);
+    run3<M_FULL>("3D stream full", K, I, d);
+    run3<M_UBLK>("3D stream ublk", K, I, d);
+    run3<M_PBLK>("3D stream pblk", K, I, d);
     return 0;
 }
