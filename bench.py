@@ -173,20 +173,37 @@ def run_gpu(args):
     from paper_1902_08112_b200 import _lib, configs, krylov, mgsolve
     from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, SplitKind
 
-    prob = configs.make(args.config)
+    if ws > 1 and args.config == "cfg2":
+        # weak scaling: one cfg2 slab (1024^2 cells) per GPU, stacked in y
+        prob = configs.notched_square(8, 3, "cfg2", stack=ws)
+    else:
+        prob = configs.make(args.config)
     mesh = prob.disc.hierarchy.finest
     mask = prob.dirichlet.combined_with(prob.active, np.zeros(prob.n_dofs))
-    op = PhaseFieldOperator(prob.disc.finest, prob.state,
-                            ConstraintMask(mask.is_constrained, mask.inhomogeneity),
-                            prob.params, SplitKind.NOSPLIT)
+    cmask = ConstraintMask(mask.is_constrained, mask.inhomogeneity)
     n = prob.n_dofs
-    v = torch.as_tensor(prob.v, device="cuda")
-    out = torch.empty_like(v)
+    if ws > 1:
+        from paper_1902_08112_b200 import distributed as D
+        from paper_1902_08112_b200.lattice import info_from_mesh
+        levels = prob.disc.hierarchy.levels
+        part = D.SlabPartition([int(info_from_mesh(m).ncell[-1]) for m in levels], ws, rank)
+        dop = D.DistributedOperator(mesh, len(levels) - 1, part, prob.state, cmask, prob.params,
+                                    SplitKind.NOSPLIT)
+        op = dop.local
+        v = torch.as_tensor(dop.to_local(prob.v), device="cuda")
+        out = torch.empty_like(v)
+
+        def step():                       # halo exchange (NCCL) + fused vmult of the owned rows
+            dop.apply_local(v, out)
+    else:
+        op = PhaseFieldOperator(prob.disc.finest, prob.state, cmask, prob.params, SplitKind.NOSPLIT)
+        v = torch.as_tensor(prob.v, device="cuda")
+        out = torch.empty_like(v)
+
+        def step():
+            op.apply_dev(_lib.FULL, v, out)
     flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
-
-    def step():
-        op.apply_dev(_lib.FULL, v, out)
 
     for _ in range(max(args.warmup, 3)):
         flush.zero_()
@@ -226,25 +243,44 @@ def run_gpu(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_tot = float(tt.item())
     per = t_tot / args.steps
-    value = ws * n / per * 1e-9
+    value = n / per * 1e-9                  # global DoFs per step (all ranks) / max-over-ranks time
 
     # ---------------------------------------------------------------- e2e
-    h_in = torch.from_numpy(prob.v.copy()).pin_memory()
-    h_out = torch.empty(n, dtype=torch.float64).pin_memory()
+    if ws > 1:
+        h_in = torch.from_numpy(dop.to_local(prob.v)).pin_memory()
+        h_out = torch.empty(v.numel(), dtype=torch.float64).pin_memory()
+
+        def e2e_call():
+            v.copy_(h_in, non_blocking=True)
+            step()
+            h_out.copy_(out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+    else:
+        h_in = torch.from_numpy(prob.v.copy()).pin_memory()
+        h_out = torch.empty(n, dtype=torch.float64).pin_memory()
+
+        def e2e_call():
+            op.apply(h_in, out=h_out)
+            torch.cuda.synchronize()
     for _ in range(2):
-        op.apply(h_in, out=h_out)
-    torch.cuda.synchronize()
+        e2e_call()
     e2e_t = []
     for _ in range(max(3, min(args.steps, 20))):
+        if ws > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
-        op.apply(h_in, out=h_out)
-        torch.cuda.synchronize()
+        e2e_call()
         e2e_t.append(time.perf_counter() - t0)
     e2e_per = float(np.median(e2e_t))
+    if ws > 1:
+        tt = torch.tensor([e2e_per], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_per = float(tt.item())
+    e2e_bytes = 8 * h_in.numel()
 
     # -------------------------------------------------------------- solve
     solve = None
-    if not args.no_solve:
+    if not args.no_solve and ws == 1:
         rhs = torch.as_tensor(configs.fallback_rhs(prob), device="cuda")
         ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
 
@@ -283,26 +319,30 @@ def run_gpu(args):
         except Exception:
             traffic = None
     achieved = b_c / per * 1e-9
+    peak_all = hbm * ws                           # aggregate over the ranks
+    workload = (f"{args.config}: 2D notched square 1024^2 Q1 NoSplit vmult" if ws == 1 else
+                f"{args.config} x{ws}: {ws} stacked 1024^2 notched squares (1024 x {1024 * ws} Q1), "
+                f"y-slab per GPU, NCCL halo exchange + fused vmult") if args.config == "cfg2" else args.config
     line = {
         "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded state/vector, SURVEY §8d; random-init, no dataset)",
-        "config": {"workload": f"{args.config}: 2D notched square 1024^2 Q1 NoSplit vmult"
-                   if args.config == "cfg2" else args.config,
+        "config": {"workload": workload,
                    "n_dofs": n, "n_vertices": mesh.n_vertices, "n_cells": mesh.n_cells,
                    "l2": "flushed (512 MiB write) before every step",
-                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic,
+                   "parallelism": f"slabs x{ws} (halo exchange)" if ws > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_all, "unit": "GB/s",
+                     "frac": achieved / peak_all, "traffic": traffic if ws == 1 else None,
                      "bytes_model": "B_C = 16 n_c V + 8 Q (2 + d(d+1)/2) C + n_c V (SURVEY §8d)",
                      "algorithmic_bytes_BC": b_c, "algorithmic_bytes_BF": b_f,
-                     "frac_BF": b_f / per * 1e-9 / hbm,
-                     "frac_ncu": (traffic / per * 1e-9 / hbm) if traffic else None,
-                     "peak_kind": peak_kind},
-        "e2e": {"value": n / e2e_per * 1e-9, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * n,
-                "d2h_bytes_per_step": 8 * n,
-                "path": "PhaseFieldOperator.apply(pinned host tensor, out=pinned host tensor)"},
+                     "frac_BF": b_f / per * 1e-9 / peak_all,
+                     "frac_ncu": (traffic / per * 1e-9 / hbm) if (traffic and ws == 1) else None,
+                     "peak_kind": peak_kind + (f" x{ws} GPUs" if ws > 1 else "")},
+        "e2e": {"value": n / e2e_per * 1e-9, "unit": "GDoF/s", "h2d_bytes_per_step": e2e_bytes,
+                "d2h_bytes_per_step": e2e_bytes,
+                "path": ("PhaseFieldOperator.apply(pinned host tensor, out=pinned host tensor)" if ws == 1
+                         else "per rank: pinned H2D of the slab, halo exchange + vmult, D2H; bytes per rank")},
         "gpu_launches": args.steps,
         "solve": solve,
         "wall_s_timed_region": wall,

@@ -54,6 +54,11 @@ typedef struct {
     const int32_t* vrow_hi;
     const int32_t* crow_lo;
     const int32_t* crow_hi;
+    /* Slab decomposition (multi-GPU): operator kernels finalise only vertex
+     * planes [own_lo, own_hi) of the last axis (y in 2D, z in 3D); the planes
+     * own_lo-1 and own_hi, if inside the lattice, are ghost planes that must
+     * hold the neighbours' values.  own_lo = own_hi = 0 means the whole lattice. */
+    int32_t own_lo, own_hi;
 } pffmg_lattice;
 
 /*

@@ -26,7 +26,8 @@ class Lattice(C.Structure):
                 ("hx", C.c_double), ("hy", C.c_double), ("hz", C.c_double),
                 ("n_vertices", C.c_int64),
                 ("vrow_off", vp), ("vrow_lo", vp), ("vrow_hi", vp),
-                ("crow_lo", vp), ("crow_hi", vp)]
+                ("crow_lo", vp), ("crow_hi", vp),
+                ("own_lo", C.c_int32), ("own_hi", C.c_int32)]
 
 
 class State(C.Structure):

@@ -72,9 +72,11 @@ def _material(h):
     return MaterialParams(mu=80.77, lam=121.15, g_c=2.7e-3, kappa=1e-8, eps=2.0 * h)
 
 
-def notched_square(n_levels, degree, name):
-    """cfg1/cfg2 (BASELINE configs[0], [1])."""
-    blocks = tiled_blocks((8, 8), 1.0 / 8)
+def notched_square(n_levels, degree, name, stack=1):
+    """cfg1/cfg2 (BASELINE configs[0], [1]).  `stack` > 1 stacks
+    that many unit squares in y (weak-scaling workload: one cfg slab per GPU;
+    the slit stays in the bottom square, Dirichlet rows at y = 0 and y = stack)."""
+    blocks = tiled_blocks((8, 8 * stack), 1.0 / 8)
     disc = Discretization(build_hierarchy(blocks, n_levels, 2))
     mesh = disc.hierarchy.finest
     V = mesh.n_vertices
@@ -90,7 +92,7 @@ def notched_square(n_levels, degree, name):
     flags = np.zeros(3 * V, dtype=bool)
     vals = np.zeros(3 * V)
     bottom = np.isclose(y, 0.0)
-    top = np.isclose(y, 1.0)
+    top = np.isclose(y, float(stack))
     flags[np.nonzero(bottom)[0]] = True
     flags[V + np.nonzero(bottom)[0]] = True
     flags[np.nonzero(top)[0]] = True

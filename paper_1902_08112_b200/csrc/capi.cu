@@ -66,6 +66,16 @@ int make_lat(const pffmg_lattice* in, Lat* out) {
     out->vrow_hi = in->vrow_hi;
     out->crow_lo = in->crow_lo;
     out->crow_hi = in->crow_hi;
+    const int nplanes = (in->dim == 3 ? in->nz : in->ny) + 1;
+    if (in->own_lo == 0 && in->own_hi == 0) {
+        out->own_lo = 0;
+        out->own_hi = nplanes;
+    } else {
+        PFFMG_REQUIRE(in->own_lo >= 0 && in->own_lo < in->own_hi && in->own_hi <= nplanes,
+                      "bad owned plane range [%d, %d) of %d planes", in->own_lo, in->own_hi, nplanes);
+        out->own_lo = in->own_lo;
+        out->own_hi = in->own_hi;
+    }
     return PFFMG_OK;
 }
 

@@ -39,6 +39,7 @@ struct Lat {
     const int32_t* __restrict__ vrow_hi;
     const int32_t* __restrict__ crow_lo;
     const int32_t* __restrict__ crow_hi;
+    int own_lo, own_hi;    // finalised vertex planes of the last axis (always set by make_lat)
 };
 
 int make_lat(const pffmg_lattice* in, Lat* out);

@@ -285,9 +285,9 @@ op2dw_kernel(const OpArgs A) {
     const Lat& L = A.L;
     const int gw = (int)blockIdx.x * NW + w;
     const int seg = gw % A.nseg, strip = gw / A.nseg;
-    const int vy0 = strip * A.planes_per_cta;
-    if (vy0 > L.ny) return;
-    const int vy1 = min(vy0 + A.planes_per_cta, L.ny + 1);
+    const int vy0 = L.own_lo + strip * A.planes_per_cta;
+    if (vy0 >= L.own_hi) return;
+    const int vy1 = min(vy0 + A.planes_per_cta, L.own_hi);
     const int x0 = 30 * seg - 1;
     const int cx = x0 + lane;
     const int V = (int)L.V;
@@ -441,8 +441,8 @@ __global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int cx0 = -1 + (int)blockIdx.x * 31;
     const int cy0 = -1 + (int)blockIdx.y * (TY - 1);
-    const int vz0 = (int)blockIdx.z * A.planes_per_cta;
-    const int vz1 = min(vz0 + A.planes_per_cta, L.nz + 1);
+    const int vz0 = L.own_lo + (int)blockIdx.z * A.planes_per_cta;
+    const int vz1 = min(vz0 + A.planes_per_cta, L.own_hi);
     const int cx = cx0 + lane, cy = cy0 + w;
 
     auto SV = [&](int buf, int f, int j) -> double& { return sv[(buf * NF + f) * TV + j]; };

@@ -1,0 +1,243 @@
+"""Slab decomposition of a level across ranks.
+
+The lattice is cut along its last axis (y in 2D, z in 3D) into contiguous
+slabs of vertex planes.  Rank r *owns* planes [own_lo, own_hi) and stores
+planes [own_lo - 1, own_hi] (ghost planes included when they exist), so the
+fused operator kernel can compute every cell layer touching an owned plane
+and finalise exactly the owned rows (`pffmg_lattice.own_lo/own_hi`).  Before
+each stencil application the ghost planes of the input are refreshed by a
+halo exchange: each rank sends its first owned plane down and its last owned
+plane up -- one plane per neighbour and component, the only data-path
+communication of a vmult.  Inner products sum the owned planes locally
+(deterministic device reduction) and all-reduce one small vector.
+
+Partitions of a hierarchy are nested: level l+1 owns planes [2a, 2b) when
+level l owns [a, b) (the last rank also owns the closing plane), so
+injection is rank-local and restriction/prolongation only need the ghost
+planes that the halo exchange already provides.  Levels too thin to give
+every rank `min_layers` cell layers are replicated on every rank.
+
+Communication goes through torch.distributed (NCCL over NVLink on GPUs,
+gloo on CPUs for the tests); the per-rank compute is a pluggable "local
+operator" (the CUDA PhaseFieldOperator on the slab by default).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .lattice import LatticeInfo, info_from_mesh
+
+
+@dataclass
+class Slab:
+    """One rank's share of one level."""
+    n_cells: int          # cell layers of the level along the cut axis
+    own_lo: int           # owned vertex planes [own_lo, own_hi) (global numbers)
+    own_hi: int
+    lo: int               # stored planes [lo, hi] (owned + ghosts)
+    hi: int
+    replicated: bool = False
+
+    @property
+    def has_lower(self):
+        return self.lo < self.own_lo
+
+    @property
+    def has_upper(self):
+        return self.hi >= self.own_hi
+
+
+def split_layers(n, world):
+    """Balanced cut points c_0 = 0 <= ... <= c_world = n."""
+    return [(n * r) // world for r in range(world + 1)]
+
+
+class SlabPartition:
+    """Nested slab partition of a hierarchy with `n_cells[l]` cell layers on level l."""
+
+    def __init__(self, n_cells, world, rank, min_layers=2):
+        self.world, self.rank = world, rank
+        self.n_cells = list(n_cells)
+        L = len(self.n_cells)
+        # coarsest level that gives every rank at least min_layers layers
+        self.first_sharded = L - 1
+        for l in range(L):
+            if self.n_cells[l] >= min_layers * world:
+                self.first_sharded = l
+                break
+        ls = self.first_sharded
+        cuts = split_layers(self.n_cells[ls], world)
+        self.slabs = []
+        for l in range(L):
+            n = self.n_cells[l]
+            if l < ls or world == 1:
+                self.slabs.append(Slab(n, 0, n + 1, 0, n, replicated=world > 1))
+                continue
+            k = 2 ** (l - ls)
+            a, b = cuts[rank] * k, cuts[rank + 1] * k
+            own_hi = b if rank < world - 1 else n + 1
+            self.slabs.append(Slab(n, a, own_hi, max(a - 1, 0), min(own_hi, n)))
+
+    def slab(self, l):
+        return self.slabs[l]
+
+
+def local_info(info: LatticeInfo, slab: Slab) -> LatticeInfo:
+    """The rank-local lattice (owned + ghost planes) of a global level."""
+    return info.slab(slab.lo, slab.hi, (slab.own_lo, slab.own_hi))
+
+
+class SlabMesh:
+    """Minimal mesh object for a rank-local slab (consumed by device_lattice)."""
+
+    def __init__(self, info: LatticeInfo, global_mesh=None):
+        self.lattice_info = info
+        self.dim = info.dim
+        self.n_vertices = info.n_vertices
+        self.cell_size = info.h
+        self.global_mesh = global_mesh
+
+    @property
+    def cell_volume(self):
+        return float(np.prod(self.cell_size))
+
+
+class SlabSpace:
+    def __init__(self, mesh, level):
+        self.mesh = mesh
+        self.level = level
+
+
+# ---------------------------------------------------------------- vectors
+
+def to_local(vec, n_comp, info_global: LatticeInfo, slab: Slab):
+    """Global component-major vector -> the rank's slab (owned + ghosts)."""
+    offs = info_global.plane_offsets()
+    V = info_global.n_vertices
+    a, b = int(offs[slab.lo]), int(offs[slab.hi + 1])
+    if isinstance(vec, torch.Tensor):
+        return torch.cat([vec[c * V + a:c * V + b] for c in range(n_comp)])
+    vec = np.asarray(vec)
+    return np.concatenate([vec[c * V + a:c * V + b] for c in range(n_comp)])
+
+
+def owned_slices(n_comp, info_local: LatticeInfo):
+    """Slices of a local vector covering the owned planes, one per component."""
+    offs = info_local.plane_offsets()
+    V = info_local.n_vertices
+    lo, hi = info_local.own
+    if lo == 0 and hi == 0:
+        lo, hi = 0, info_local.n_planes
+    a, b = int(offs[lo]), int(offs[hi])
+    return [slice(c * V + a, c * V + b) for c in range(n_comp)]
+
+
+class Halo:
+    """Ghost-plane exchange of component-major local vectors."""
+
+    def __init__(self, info_local: LatticeInfo, slab: Slab, rank, world, group=None):
+        self.offs = info_local.plane_offsets()
+        self.V = info_local.n_vertices
+        self.slab = slab
+        self.rank, self.world, self.group = rank, world, group
+        lo_own = slab.own_lo - slab.lo          # local index of the first owned plane
+        hi_own = slab.own_hi - slab.lo          # one past the last owned plane
+        self.send_down = (int(self.offs[lo_own]), int(self.offs[lo_own + 1])) if slab.has_lower else None
+        self.recv_down = (int(self.offs[0]), int(self.offs[1])) if slab.has_lower else None
+        self.send_up = (int(self.offs[hi_own - 1]), int(self.offs[hi_own])) if slab.has_upper else None
+        self.recv_up = (int(self.offs[hi_own]), int(self.offs[hi_own + 1])) if slab.has_upper else None
+
+    def exchange(self, vec, n_comp):
+        """Refresh ghost planes of `vec` (a 1-D tensor of n_comp * V entries) in place."""
+        if self.world == 1 or self.slab.replicated:
+            return vec
+        ops = []
+        V = self.V
+        for c in range(n_comp):
+            base = c * V
+            if self.send_down is not None:
+                a, b = self.send_down
+                ops.append(dist.P2POp(dist.isend, vec[base + a:base + b], self.rank - 1, self.group))
+                a, b = self.recv_down
+                ops.append(dist.P2POp(dist.irecv, vec[base + a:base + b], self.rank - 1, self.group))
+            if self.send_up is not None:
+                a, b = self.send_up
+                ops.append(dist.P2POp(dist.isend, vec[base + a:base + b], self.rank + 1, self.group))
+                a, b = self.recv_up
+                ops.append(dist.P2POp(dist.irecv, vec[base + a:base + b], self.rank + 1, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return vec
+
+
+def dist_dot(x, y, n_comp, info_local, group=None, local_dot=None):
+    """Sum over owned dofs of x*y across ranks (deterministic for a fixed world size)."""
+    parts = []
+    for s in owned_slices(n_comp, info_local):
+        if local_dot is not None:
+            parts.append(local_dot(x[s], y[s]))
+        else:
+            parts.append(torch.dot(x[s], y[s]))
+    t = torch.stack([torch.as_tensor(p, dtype=torch.float64, device=x.device) for p in parts]).sum()
+    t = t.reshape(1)
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, group=group)
+    return float(t.item())
+
+
+class DistributedOperator:
+    """Slab-sharded fused vmult of one level.
+
+    `local_factory(space, state, mask, params, split)` builds the per-rank
+    compute (default: the CUDA PhaseFieldOperator).  State vectors, masks and
+    flags are sliced to the slab once; `apply_local` refreshes the input's
+    ghost planes and applies the operator to the owned rows."""
+
+    def __init__(self, global_mesh, level, partition: SlabPartition, state, mask, params, split,
+                 local_factory=None, group=None):
+        info = info_from_mesh(global_mesh)
+        self.info_global = info
+        self.slab = partition.slab(level)
+        self.info = local_info(info, self.slab)
+        self.n_comp = info.dim + 1
+        self.rank, self.world = partition.rank, partition.world
+        self.halo = Halo(self.info, self.slab, self.rank, self.world, group)
+        self.group = group
+        nc = self.n_comp
+        loc = lambda v, k: to_local(v, k, info, self.slab)  # noqa: E731
+        from .model import ConstraintMask, LinearizationState
+        st = LinearizationState(U=loc(state.U, nc), U_prev1=loc(state.U_prev1, nc),
+                                U_prev2=loc(state.U_prev2, nc), t=state.t, t_prev1=state.t_prev1,
+                                t_prev2=state.t_prev2, phi_tilde=loc(state.phi_tilde, 1))
+        m = ConstraintMask(loc(mask.is_constrained, nc), loc(mask.inhomogeneity, nc))
+        space = SlabSpace(SlabMesh(self.info, global_mesh), level)
+        if local_factory is None:
+            from .model import PhaseFieldOperator
+            local_factory = PhaseFieldOperator
+        self.local = local_factory(space, st, m, params, split)
+        self.owned = owned_slices(nc, self.info)
+
+    @property
+    def n_local(self):
+        return self.n_comp * self.info.n_vertices
+
+    def to_local(self, vec):
+        return to_local(vec, self.n_comp, self.info_global, self.slab)
+
+    def apply_local(self, v_loc, out_loc):
+        """out (owned rows) = G~ v, after refreshing v's ghost planes."""
+        self.halo.exchange(v_loc, self.n_comp)
+        if hasattr(self.local, "apply_dev") and v_loc.is_cuda:
+            from . import _lib
+            self.local.apply_dev(_lib.FULL, v_loc, out_loc)
+        else:
+            out_loc.copy_(torch.as_tensor(self.local.apply(v_loc), dtype=out_loc.dtype))
+        return out_loc
+
+    def dot(self, x, y):
+        return dist_dot(x, y, self.n_comp, self.info, self.group)

@@ -162,9 +162,46 @@ class LatticeInfo:
         self.is_box = is_box
         self.rows = rows                 # (vrow_off, vrow_lo, vrow_hi, crow_lo, crow_hi) or None
         self.cell_perm = cell_perm       # mesh cell index -> lattice cell index (for rho)
+        self.own = (0, 0)                # finalised planes of the last axis; (0, 0) = all
+
+    @property
+    def n_planes(self):
+        return int(self.ncell[-1]) + 1
+
+    def plane_offsets(self):
+        """Vertex id of the first vertex of every plane of the last axis (+ V)."""
+        if self.rows is None:
+            per = int(np.prod(self.ncell[:-1] + 1))
+            return np.arange(self.n_planes + 1, dtype=np.int64) * per
+        voff, vlo, vhi = self.rows[0], self.rows[1], self.rows[2]
+        rows_per_plane = int(self.ncell[1]) + 1 if self.dim == 3 else 1
+        counts = (np.asarray(vhi, np.int64) - np.asarray(vlo, np.int64)).reshape(self.n_planes, -1).sum(1)
+        return np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+
+    def slab(self, lo, hi, own):
+        """Sub-lattice of vertex planes [lo, hi] (inclusive) with the finalised
+        planes `own` = (own_lo, own_hi) given in global plane numbers."""
+        offs = self.plane_offsets()
+        ncell = self.ncell.copy()
+        ncell[-1] = hi - lo
+        rows = None
+        if self.rows is not None:
+            voff, vlo, vhi, clo, chi = self.rows
+            rpp = int(self.ncell[1]) + 1 if self.dim == 3 else 1           # vertex rows per plane
+            cpp = int(self.ncell[1]) if self.dim == 3 else 1                # cell rows per plane
+            vs = slice(lo * rpp, (hi + 1) * rpp)
+            cs = slice(lo * cpp, hi * cpp)
+            rows = (np.asarray(voff[vs], np.int64) - offs[lo], vlo[vs], vhi[vs], clo[cs], chi[cs])
+        out = LatticeInfo(self.dim, ncell, self.h, int(offs[hi + 1] - offs[lo]), self.is_box, rows)
+        out.own = (own[0] - lo, own[1] - lo)
+        out.global_offset = int(offs[lo])
+        out.plane_lo = int(lo)
+        return out
 
 
 def info_from_mesh(mesh):
+    if hasattr(mesh, "lattice_info"):
+        return mesh.lattice_info
     if isinstance(mesh, LatticeMesh):
         rows = None if mesh.is_box else (mesh.vrow_off, mesh.vrow_lo, mesh.vrow_hi,
                                          mesh.crow_lo, mesh.crow_hi)
@@ -248,6 +285,7 @@ class DeviceLattice:
                   torch.as_tensor(np.ascontiguousarray(chi, dtype=np.int32), device=dev)]
             self._tables = ts
             L.vrow_off, L.vrow_lo, L.vrow_hi, L.crow_lo, L.crow_hi = [t.data_ptr() for t in ts]
+        L.own_lo, L.own_hi = int(info.own[0]), int(info.own[1])
         self.struct = L
         self.ref = C.byref(L)
 

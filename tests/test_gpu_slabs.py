@@ -1,0 +1,58 @@
+"""The CUDA operator on slab sub-lattices (own_lo/own_hi): every rank's
+owned rows, computed from its slab with ghost planes filled from the global
+vector, must stitch to the single-GPU result.  Ranks are emulated one after
+another in one process (no inter-rank waiting); the communication layer is
+covered by tests/test_distributed_cpu.py."""
+import numpy as np
+import pytest
+import torch
+
+from tests.conftest import rel_err
+from tests.golden.specs import MESHES
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name,world", [("cfg1", 2), ("cfg1", 5), ("cube", 2), ("lprism", 2),
+                                        ("rect3d", 3), ("lshape3d", 2)])
+def test_slab_operator_stitches(name, world):
+    from paper_1902_08112_b200 import _lib, distributed as D, lattice
+    from paper_1902_08112_b200.fem import Discretization, build_hierarchy
+    from paper_1902_08112_b200.model import ConstraintMask, LinearizationState, MaterialParams, \
+        PhaseFieldOperator, SplitKind
+    blocks, n_levels, dim = MESHES[name]
+    n_levels += 1
+    disc = Discretization(build_hierarchy(blocks, n_levels, dim))
+    levels = disc.hierarchy.levels
+    fine = levels[-1]
+    V = fine.n_vertices
+    n = (dim + 1) * V
+    rng = np.random.default_rng(11)
+    U = 1e-2 * rng.standard_normal(n)
+    U[dim * V:] = np.clip(0.6 + 0.4 * rng.standard_normal(V), 0, 1)
+    st = LinearizationState(U=U, U_prev1=U, U_prev2=U, t=0.2, t_prev1=0.0, t_prev2=0.0,
+                            phi_tilde=U[dim * V:].copy())
+    flags = rng.random(n) < 0.1
+    mask = ConstraintMask(flags, np.zeros(n))
+    params = MaterialParams(mu=1.3, lam=0.9, g_c=0.7, kappa=1e-10, eps=0.5, pressure_fn=lambda t: 10 * t)
+    v = rng.standard_normal(n)
+    ref = PhaseFieldOperator(disc.finest, st, mask, params, SplitKind.NOSPLIT).apply(v)
+    info = lattice.info_from_mesh(fine)
+    n_cells = [int(lattice.info_from_mesh(m).ncell[-1]) for m in levels]
+    offs = info.plane_offsets()
+    got = np.full(n, np.nan)
+    for rank in range(world):
+        part = D.SlabPartition(n_cells, world, rank, min_layers=2)
+        L = n_levels - 1
+        op = D.DistributedOperator(fine, L, part, st, mask, params, SplitKind.NOSPLIT)
+        v_loc = torch.as_tensor(op.to_local(v), device="cuda")     # ghosts already true values
+        out = torch.zeros(op.n_local, dtype=torch.float64, device="cuda")
+        op.local.apply_dev(_lib.FULL, v_loc, out)
+        s = part.slab(L)
+        a, b = int(offs[s.own_lo]), int(offs[s.own_hi])
+        per = b - a
+        owned = torch.cat([out[sl] for sl in op.owned]).cpu().numpy()
+        for c in range(dim + 1):
+            got[c * V + a:c * V + b] = owned[c * per:(c + 1) * per]
+    assert not np.isnan(got).any()
+    assert rel_err(got, ref) <= 1e-14

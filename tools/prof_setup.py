@@ -1,0 +1,48 @@
+"""Time the pieces of one Newton-step linear solve at cfg2 (host-side view)."""
+import cProfile
+import pstats
+import sys
+import os
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1902_08112_b200 import configs, krylov, mgsolve  # noqa: E402
+from paper_1902_08112_b200.model import SplitKind  # noqa: E402
+
+prob = configs.make(sys.argv[1] if len(sys.argv) > 1 else "cfg2")
+rhs = torch.as_tensor(configs.fallback_rhs(prob), device="cuda")
+
+
+def setup():
+    return mgsolve.build_level_contexts(prob.disc, prob.state, prob.active, prob.dirichlet,
+                                        prob.params, SplitKind.NOSPLIT)
+
+
+ctxs = setup()
+torch.cuda.synchronize()
+for _ in range(2):
+    t0 = time.perf_counter()
+    ctxs = setup()
+    torch.cuda.synchronize()
+    print("setup", time.perf_counter() - t0)
+pr = cProfile.Profile()
+pr.enable()
+ctxs = setup()
+torch.cuda.synchronize()
+pr.disable()
+pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
+pc = mgsolve.VCyclePreconditioner(ctxs, degree=prob.degree)
+ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8)
+x, its = krylov.gmres(ctxs[-1].op.apply, pc, rhs, ctl)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+x, its = krylov.gmres(ctxs[-1].op.apply, pc, rhs, ctl)
+torch.cuda.synchronize()
+print("gmres", its, time.perf_counter() - t0)
+t0 = time.perf_counter()
+for _ in range(10):
+    pc._pffmg_into(rhs, x)
+torch.cuda.synchronize()
+print("vcycle", (time.perf_counter() - t0) / 10)
