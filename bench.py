@@ -281,27 +281,42 @@ def run_gpu(args):
     # -------------------------------------------------------------- solve
     solve = None
     if not args.no_solve and ws == 1:
-        rhs = torch.as_tensor(configs.fallback_rhs(prob), device="cuda")
+        from paper_1902_08112_b200 import model as M
         ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+        cmask_dev = torch.as_tensor(mask.is_constrained, device="cuda")
+        state_dev = M.LinearizationState(
+            U=torch.as_tensor(prob.state.U, device="cuda"), U_prev1=torch.as_tensor(prob.state.U_prev1, device="cuda"),
+            U_prev2=torch.as_tensor(prob.state.U_prev2, device="cuda"), t=prob.state.t,
+            t_prev1=prob.state.t_prev1, t_prev2=prob.state.t_prev2,
+            phi_tilde=torch.as_tensor(prob.state.phi_tilde, device="cuda"))
 
         def newton_step():
+            """One linear Newton step of ActiveSetSolver.solve_step (nonlinear.py:146-181):
+            R~ = -A(U) with constrained rows zeroed, GMG setup, GMRES(30)."""
             t0 = time.perf_counter()
-            ctxs = mgsolve.build_level_contexts(prob.disc, prob.state, prob.active, prob.dirichlet,
+            R = M.residual(prob.disc.finest, state_dev, prob.dirichlet, prob.params, SplitKind.NOSPLIT)
+            R.neg_()
+            R[cmask_dev] = 0.0
+            ctxs = mgsolve.build_level_contexts(prob.disc, state_dev, prob.active, prob.dirichlet,
                                                 prob.params, SplitKind.NOSPLIT)
             torch.cuda.synchronize()
             t1 = time.perf_counter()
             pc = mgsolve.VCyclePreconditioner(ctxs, degree=prob.degree)
-            x, its = krylov.gmres(ctxs[-1].op.apply, pc, rhs, ctl)
+            x, its = krylov.gmres(ctxs[-1].op.apply, pc, R, ctl)
             torch.cuda.synchronize()
             t2 = time.perf_counter()
             return t1 - t0, t2 - t1, its
 
         newton_step()                                   # warm (graph capture, probes)
-        setup_s, gmres_s, its = newton_step()
+        runs = [newton_step() for _ in range(3)]
+        setup_s = float(np.median([r[0] for r in runs]))
+        gmres_s = float(np.median([r[1] for r in runs]))
+        its = runs[-1][2]
         solve = {"setup_ms": setup_s * 1e3, "gmres_ms": gmres_s * 1e3, "gmres_iters": its,
                  "ms_per_newton_step": (setup_s + gmres_s) * 1e3,
-                 "rhs": "seeded N(0,1), constrained rows zeroed (SURVEY §8d fallback)",
-                 "control": "GMRES(30) rel 1e-8 abs 0, V(1,1) FULL, Chebyshev deg %d" % prob.degree}
+                 "rhs": "Newton RHS -A(U), constrained rows zeroed, from the GPU residual kernel",
+                 "control": "GMRES(30) rel 1e-8 abs 0, V(1,1) FULL, Chebyshev deg %d" % prob.degree,
+                 "timing": "wall clock, median of 3 after one warm-up"}
 
     if rank != 0:
         if ws > 1:

@@ -99,6 +99,11 @@ int pffmg_apply(const pffmg_lattice* lat, const pffmg_state* st, int which,
 int pffmg_residual(const pffmg_lattice* lat, const pffmg_state* st, int which,
                    const double* x, const double* b, double* out, void* stream);
 
+/* Semilinear form A(U) of the linearisation state (NoSplit), constrained
+ * rows zeroed (model.py:420-460): the Newton right-hand side is -out. */
+int pffmg_semilinear_residual(const pffmg_lattice* lat, const pffmg_state* st, double* out,
+                              void* stream);
+
 /* Exact operator diagonal, constrained entries = 1.0 (model.py:394-413). */
 int pffmg_diagonal(const pffmg_lattice* lat, const pffmg_state* st, double* out, void* stream);
 

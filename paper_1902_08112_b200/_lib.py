@@ -45,6 +45,7 @@ _SIGS = {
     "pffmg_apply": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp],
     "pffmg_residual": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp],
     "pffmg_diagonal": [C.POINTER(Lattice), C.POINTER(State), vp, vp],
+    "pffmg_semilinear_residual": [C.POINTER(Lattice), C.POINTER(State), vp, vp],
     "pffmg_cheb_step": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp,
                         C.c_double, C.c_double, C.c_int, vp],
     "pffmg_cheb_init": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp,

@@ -1,13 +1,14 @@
 // Register-lean 3D cell kernel for isotropic hexahedra (NoSplit).
 //
 // Same physics as cell_kernel_iso<3> (cellops_iso.cuh; reference
-// model.py:270-355), reorganised as a stream over gradient components so that
-// only O(8)-sized per-QP arrays are live at a time: every reduced derivative
-// array (4 values: d_j of a trilinear field is bilinear in the other two
-// axes) is produced from the staged corners when it is needed, consumed by
-// the u-row stress terms, the S:w coupling and the E+ energy, and dropped.
-// Outputs are handed to `emit(k, o[8])` component by component so the caller
-// can start the vertex reduction (x-shuffle) early.
+// model.py:270-355 for the Jacobian, model.py:420-460 for the residual
+// mode), reorganised as a stream over gradient components so that only
+// O(8)-sized per-QP arrays are live at a time: every reduced derivative array
+// (4 values: d_j of a trilinear field is bilinear in the other two axes) is
+// produced from the staged corners when it is needed, consumed by the u-row
+// stress terms, the S:w coupling and the E+ energy, and dropped.  Outputs are
+// handed to `emit(k, o[8])` component by component so the caller can start
+// the vertex reduction (x-shuffle) early.
 #pragma once
 
 #include "cellops_iso.cuh"
@@ -20,6 +21,10 @@ __device__ __forceinline__ void cell3_iso(const Corners& C, const double* __rest
     using MI = ModeInfo<3, MODE>;
     using S = SFr<3>;
     constexpr int NP = 8;
+    constexpr bool RES = MODE == M_RES;
+    constexpr bool HAS_W = MODE == M_FULL || MODE == M_UBLK;     // v displacement gradient
+    constexpr bool HAS_R = MODE == M_FULL || MODE == M_PBLK || RES;   // U displacement gradient
+    constexpr bool HAS_G = HAS_W || RES;                         // u rows
 
     double rho[NP];
 #pragma unroll
@@ -33,9 +38,9 @@ __device__ __forceinline__ void cell3_iso(const Corners& C, const double* __rest
     };
 
     // ------------------------------------------------------------ gk rho
-    double gks[NP];
+    double gks[NP], pv[NP];
     if (MI::PT) {
-        double c[NP], pv[NP];
+        double c[NP];
         C.load(MI::F_PT, c);
         S::value(c, pv, K);
 #pragma unroll
@@ -44,9 +49,6 @@ __device__ __forceinline__ void cell3_iso(const Corners& C, const double* __rest
             gks[q] = RHO ? g * rho[q] : g;
         }
     }
-
-    constexpr bool HAS_W = MODE == M_FULL || MODE == M_UBLK;
-    constexpr bool HAS_R = MODE == M_FULL || MODE == M_PBLK;
 
     // ----------------------------------------------- diagonal gradient terms
     double wd[3][4], rd[3][4];
@@ -88,6 +90,14 @@ __device__ __forceinline__ void cell3_iso(const Corners& C, const double* __rest
             for (int q = 0; q < NP; ++q) G[q] = gks[q] * fma(I.two_mu, expand(wd[i], i, q), I.lam * trw[q]);
             S::template deriv_T<false>(G, i, ou[i], K);
         }
+        if (RES) {                                    // gk sigma+_ii + p phi~^2   (model.py:445-448)
+            double G[NP];
+#pragma unroll
+            for (int q = 0; q < NP; ++q)
+                G[q] = fma(gks[q], fma(I.two_mu, expand(rd[i], i, q), I.lam * trr[q]),
+                           I.cpres * (pv[q] * pv[q]));
+            S::template deriv_T<false>(G, i, ou[i], K);
+        }
         if (HAS_R) {
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
@@ -127,9 +137,16 @@ __device__ __forceinline__ void cell3_iso(const Corners& C, const double* __rest
                     e2[q] = fma(ms, s[q], e2[q]);                       // mu s_ij^2
                     if (MODE == M_FULL) Y[q] = fma(ms, sw[q], Y[q]);    // mu s_ij sw_ij
                 }
+                if (RES) {                             // gk sigma+_ij
+                    double G[NP];
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) G[q] = (gks[q] * I.mu) * s[q];
+                    S::template deriv_T<true>(G, j, ou[i], K);
+                    S::template deriv_T<true>(G, i, ou[j], K);
+                }
             }
         }
-    if (HAS_W) {
+    if (HAS_G) {
 #pragma unroll
         for (int i = 0; i < 3; ++i) emit(i, ou[i]);
     }
@@ -137,7 +154,7 @@ __device__ __forceinline__ void cell3_iso(const Corners& C, const double* __rest
     // ------------------------------------------------------------ phi row
     if (HAS_R) {
         double cp[NP], f[NP];
-        C.load(MODE == M_FULL ? MI::F_V + 3 : MI::F_V, cp);
+        C.load(MODE == M_FULL ? MI::F_V + 3 : (RES ? MI::F_U + 3 : MI::F_V), cp);
         S::value(cp, f, K);
         double phq[NP];
         if (MODE == M_FULL) {
@@ -148,6 +165,11 @@ __device__ __forceinline__ void cell3_iso(const Corners& C, const double* __rest
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
             const double ce = RHO ? I.cS * rho[q] : I.cS;
+            if (RES) {                                  // model.py:450-452
+                const double a = fma(ce, e2[q], I.cdiv * trr[q]);
+                f[q] = fma(f[q], a, -I.c0 * (1.0 - f[q]));
+                continue;
+            }
             const double aj = fma(ce, e2[q], fma(I.cdiv, trr[q], I.c0));   // JxW a_phiphi
             if (MODE == M_FULL) {
                 const double cc = RHO ? I.cc * rho[q] : I.cc;
@@ -159,7 +181,7 @@ __device__ __forceinline__ void cell3_iso(const Corners& C, const double* __rest
         }
         mass_transpose<3>(f, K);
         corner_laplacian<3>(cp, I, f);
-        emit(MODE == M_FULL ? 3 : 0, f);
+        emit(MODE == M_FULL || RES ? 3 : 0, f);
     }
 }
 

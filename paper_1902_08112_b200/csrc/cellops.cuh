@@ -8,18 +8,20 @@
 
 namespace pffmg {
 
-enum Mode { M_FULL = 0, M_UBLK = 1, M_PBLK = 2, M_DIAG = 3 };
+enum Mode { M_FULL = 0, M_UBLK = 1, M_PBLK = 2, M_DIAG = 3, M_RES = 4 };
 
 // Number of staged fp64 fields per vertex and of output components.
 template <int D, int MODE>
 struct ModeInfo {
     // FULL: v[0..D], U[0..D], phi_tilde;  UBLK: v[0..D-1], phi_tilde
     // PBLK: v[D], U[0..D-1];              DIAG: U[0..D-1], phi_tilde
-    static constexpr int NF = MODE == M_FULL ? 2 * D + 3 : D + 1;
+    // RES (semilinear form A(U), model.py:420-460): U[0..D], phi_tilde
+    static constexpr int NF = MODE == M_FULL ? 2 * D + 3 : (MODE == M_RES ? D + 2 : D + 1);
     static constexpr int NV = MODE == M_FULL ? D + 1 : (MODE == M_UBLK ? D : (MODE == M_PBLK ? 1 : 0));
-    static constexpr int NU = MODE == M_FULL ? D + 1 : (MODE == M_UBLK ? 0 : D);
+    static constexpr int NU = MODE == M_FULL || MODE == M_RES ? D + 1 : (MODE == M_UBLK ? 0 : D);
     static constexpr bool PT = MODE != M_PBLK;
-    static constexpr int NCO = MODE == M_FULL || MODE == M_DIAG ? D + 1 : (MODE == M_UBLK ? D : 1);
+    static constexpr int NCO =
+        MODE == M_FULL || MODE == M_DIAG || MODE == M_RES ? D + 1 : (MODE == M_UBLK ? D : 1);
     static constexpr int COMP0 = MODE == M_PBLK ? D : 0;   // global component of v/out slot 0
     // field slots in the staged tile
     static constexpr int F_V = 0;
@@ -61,6 +63,55 @@ __device__ __forceinline__ void cell_kernel(const double (&cv)[ModeInfo<D, MODE>
     using MI = ModeInfo<D, MODE>;
     constexpr int NP = 1 << D;
     using S = SF<D>;
+    if (MODE == M_RES) {
+        // semilinear form A(U), NoSplit, general box cells (model.py:420-460)
+        double rho[NP], pt[D + 1][NP], ph[D + 1][NP];
+#pragma unroll
+        for (int q = 0; q < NP; ++q) rho[q] = rho_q ? __ldg(rho_q + q) : 1.0;
+        S::interp(cv[MI::F_PT], pt, K);
+        S::interp(cv[MI::F_U + D], ph, K);
+        double G[D][D][NP], f[NP], g[D][NP];
+        {
+            double gu[NP][D][D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                double t[D + 1][NP];
+                S::interp(cv[MI::F_U + i], t, K, false);
+#pragma unroll
+                for (int q = 0; q < NP; ++q)
+#pragma unroll
+                    for (int j = 0; j < D; ++j) gu[q][i][j] = t[1 + j][q] * K.ih[j];
+            }
+            const double p = 0.5 * K.two_p;
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                double div, Ep, sp[D][D];
+                strain_stuff<D>(gu[q], div, Ep, sp, K);
+                const double gk = (K.omk * (pt[0][q] * pt[0][q]) + K.kappa) * rho[q];
+                const double pp = pt[0][q] * pt[0][q] * p;
+#pragma unroll
+                for (int i = 0; i < D; ++i)
+#pragma unroll
+                    for (int j = 0; j < D; ++j)
+                        G[i][j][q] = K.jxw * (gk * sp[i][j] + (i == j ? pp : 0.0)) * K.ih[j];
+                const double phi = ph[0][q];
+                f[q] = K.jxw * (K.omk * phi * rho[q] * Ep + K.two_p * phi * div - K.gc_over_eps * (1.0 - phi));
+#pragma unroll
+                for (int j = 0; j < D; ++j) g[j][q] = K.jxw * K.k_phi * (ph[1 + j][q] * K.ih[j]) * K.ih[j];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double t[NP];
+            S::template integrate<false>(t, G[i], K);
+#pragma unroll
+            for (int n = 0; n < NP; ++n) o[i][n] = t[n];
+        }
+        S::template integrate<true>(f, g, K);
+#pragma unroll
+        for (int n = 0; n < NP; ++n) o[D][n] = f[n];
+        return;
+    }
 
     // ---- state-dependent per-QP data
     double gkr[NP];      // gk * rho       (FULL, UBLK, DIAG)

@@ -29,6 +29,7 @@ struct IsoK {
     double cc;             // JxW ih^2 (1-k)                  -> coupling (times rho phi)
     double ctr;            // JxW 2 p ih                      -> pressure coupling (times phi)
     double clap;           // JxW k_phi ih^2
+    double cpres;          // JxW p ih                        -> residual pressure stress (times phi~^2)
     double two_mu, lam, mu;
     double lapA, lapB, lapK1;   // 2D Laplacian: out_n += A u_n + B u_{n^3} + K1 sum(u)
     double lam3[8];             // 3D Laplacian eigenvalues in the Walsh basis (scaled, / 8)
@@ -47,6 +48,7 @@ inline IsoK make_iso_host(const Consts& K) {
     I.cc = jh2 * K.omk;
     I.ctr = K.jxw * K.two_p * K.ih[0];
     I.clap = K.jxw * K.k_phi * ih2;
+    I.cpres = 0.5 * K.jxw * K.two_p * K.ih[0];
     I.two_mu = 2.0 * K.mu;
     I.lam = K.lam;
     I.mu = K.mu;
@@ -147,8 +149,8 @@ __device__ __forceinline__ void cell_kernel_iso(const double (&cv)[ModeInfo<D, M
     for (int q = 0; q < NP; ++q) rho[q] = RHO ? __ldg(rho_q + q) : 1.0;
 
     double gks[NP];                                 // JxW ih^2 gk rho   (model.py:282, 295)
+    double pv[NP];                                  // phi_tilde at the QPs
     if (MI::PT) {
-        double pv[NP];
         S::value(cv[MI::F_PT], pv, K);
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
@@ -192,8 +194,46 @@ __device__ __forceinline__ void cell_kernel_iso(const double (&cv)[ModeInfo<D, M
                     e2 = fma(So[q][k], s, e2);
                 }
             const double ce = RHO ? I.cS * rho[q] : I.cS;
-            aj[q] = fma(ce, e2, fma(I.cdiv, dv, I.c0));
+            aj[q] = fma(ce, e2, MODE == M_RES ? I.cdiv * dv : fma(I.cdiv, dv, I.c0));
         }
+    }
+
+    if (MODE == M_RES) {
+        // semilinear form A(U), NoSplit (model.py:420-460): u rows integrate
+        // gk rho sigma+ + p phi~^2 I against grad N; the phi row integrates
+        // (1-k) phi rho E+ + 2 p phi div u - Gc/eps (1 - phi) against N plus
+        // the Gc eps Laplacian of phi.
+        double G[D][D][NP];
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            const double pp = I.cpres * (pv[q] * pv[q]);
+#pragma unroll
+            for (int i = 0; i < D; ++i) G[i][i][q] = fma(gks[q], Sd[q][i], pp);
+            int k = 0;
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = i + 1; j < D; ++j, ++k) {
+                    G[i][j][q] = gks[q] * So[q][k];
+                    G[j][i][q] = G[i][j][q];
+                }
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            S::template deriv_T<false>(G[i][0], 0, o[i], K);
+#pragma unroll
+            for (int j = 1; j < D; ++j) S::template deriv_T<true>(G[i][j], j, o[i], K);
+        }
+        const double(&cu)[NP] = cv[MI::F_U + D];
+        double f[NP];
+        S::value(cu, f, K);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) f[q] = fma(f[q], aj[q], -I.c0 * (1.0 - f[q]));
+        mass_transpose<D>(f, K);
+        corner_laplacian<D>(cu, I, f);
+#pragma unroll
+        for (int n = 0; n < NP; ++n) o[D][n] = f[n];
+        return;
     }
 
     if (MODE == M_DIAG) {

@@ -16,7 +16,7 @@
 
 namespace pffmg {
 
-enum Epi { E_STORE = 0, E_RESID = 1, E_CHEB = 2, E_CHEB0 = 3, E_DIAG = 4 };
+enum Epi { E_STORE = 0, E_RESID = 1, E_CHEB = 2, E_CHEB0 = 3, E_DIAG = 4, E_RESZ = 5 };
 
 struct OpArgs {
     Lat L;
@@ -53,6 +53,10 @@ __device__ __forceinline__ void epilogue(const OpArgs& A, int64_t vid, uint8_t f
         const int64_t g = (int64_t)k * V + vid;
         if (EPI == E_DIAG) {
             A.out[g] = con ? 1.0 : acc[k];                       // model.py:412
+            continue;
+        }
+        if (EPI == E_RESZ) {
+            A.out[g] = con ? 0.0 : acc[k];                       // model.py:459
             continue;
         }
         const double Av = con ? vin[k] : acc[k];                 // model.py:373-374, 390-391

@@ -18,6 +18,6 @@ int launch3d(const OpArgs& A, bool iso, cudaStream_t s);
     PFFMG_INST1(F, M_UBLK, E_CHEB) PFFMG_INST1(F, M_UBLK, E_CHEB0)                           \
     PFFMG_INST1(F, M_PBLK, E_STORE) PFFMG_INST1(F, M_PBLK, E_RESID)                          \
     PFFMG_INST1(F, M_PBLK, E_CHEB) PFFMG_INST1(F, M_PBLK, E_CHEB0)                           \
-    PFFMG_INST1(F, M_DIAG, E_DIAG)
+    PFFMG_INST1(F, M_DIAG, E_DIAG) PFFMG_INST1(F, M_RES, E_RESZ)
 
 }  // namespace pffmg

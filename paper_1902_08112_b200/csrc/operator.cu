@@ -86,6 +86,17 @@ extern "C" int pffmg_residual(const pffmg_lattice* lat, const pffmg_state* st, i
     return dispatch_which<E_RESID>(A, which, as_stream(stream), "pffmg_residual");
 }
 
+extern "C" int pffmg_semilinear_residual(const pffmg_lattice* lat, const pffmg_state* st, double* out,
+                                         void* stream) {
+    OpArgs A;
+    int rc = fill_args(lat, st, &A);
+    if (rc) return rc;
+    PFFMG_REQUIRE(out && A.U && A.pt, "pffmg_semilinear_residual: needs out, U and phi_tilde");
+    A.out = out;
+    A.v = A.U;   // unused (no v fields in residual mode)
+    return launch<M_RES, E_RESZ>(A, as_stream(stream), "pffmg_semilinear_residual");
+}
+
 extern "C" int pffmg_diagonal(const pffmg_lattice* lat, const pffmg_state* st, double* out,
                               void* stream) {
     OpArgs A;

@@ -27,7 +27,7 @@ from . import _lib
 from .arrays import dev, empty, host, is_tensor, like, pack_flags, unpack_flags
 from .lattice import LatticeMesh, device_lattice
 
-__all__ = ["SplitKind", "MaterialParams", "LinearizationState", "ConstraintMask",
+__all__ = ["SplitKind", "MaterialParams", "LinearizationState", "ConstraintMask", "residual",
            "PhaseFieldOperator", "extrapolate", "degradation", "jacobian_vmult", "diagonal"]
 
 
@@ -232,6 +232,10 @@ class PhaseFieldOperator:
         _lib.call("pffmg_residual", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
                   _lib.ptr(out), _lib.stream())
 
+    def semilinear_dev(self, out):
+        """out = A(U) of the linearisation state, constrained rows zeroed (model.py:420-460)."""
+        _lib.call("pffmg_semilinear_residual", self.lat.ref, self._stp, _lib.ptr(out), _lib.stream())
+
     def diagonal_dev(self, out):
         _lib.call("pffmg_diagonal", self.lat.ref, self._stp, _lib.ptr(out), _lib.stream())
 
@@ -272,6 +276,15 @@ def _lattice_qp_coords(mesh):
     base = np.stack([gr.ravel() for gr in grids[::-1]], axis=1) + mesh.kmin
     lo = base.astype(float) * mesh.cell_size
     return lo[:, None, :] + pts[None, :, :] * mesh.cell_size
+
+
+def residual(space, state, mask, params, split, threads=1):
+    """Discrete semilinear form A_h(U) with constrained rows zeroed (reference
+    model.py:420-460), on the GPU.  Returns the kind of `state.U`."""
+    op = PhaseFieldOperator(space, state, mask, params, split, threads)
+    out = empty(op.n_dofs)
+    op.semilinear_dev(out)
+    return like(out, state.U)
 
 
 def jacobian_vmult(space, state, mask, params, split, v, threads=1):

@@ -65,3 +65,14 @@ def test_cfg2_full_size_properties():
     lhs = torch.dot(op.apply_block(0, xu), yu)
     rhs = torch.dot(xu, op.apply_block(0, yu))
     assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+
+
+@pytest.mark.parametrize("name,levels,tag", [("cfg1", None, "cfg1"), ("cfg2", 6, "cfg2_l6")])
+def test_newton_rhs_on_gpu_matches_reference(golden, name, levels, tag):
+    """R~ = -A(U) with constrained rows zeroed (nonlinear.py:146-160) from the GPU residual."""
+    from paper_1902_08112_b200 import model as M
+    g = golden["configs"]
+    prob, mask, op = _setup(name, levels)
+    R = -M.residual(prob.disc.finest, prob.state, prob.dirichlet, prob.params, M.SplitKind.NOSPLIT)
+    R[mask.is_constrained] = 0.0
+    assert rel_err(R, g[f"{tag}/gmres_rhs"]) <= 1e-12

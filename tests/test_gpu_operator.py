@@ -162,3 +162,20 @@ def test_fused_epilogues_match_unfused(golden):
     assert torch.equal(r, r_ref)
     assert rel_err(dout.cpu().numpy(), d_ref.cpu().numpy()) <= 1e-15
     assert rel_err(xx.cpu().numpy(), (x0 + d_ref).cpu().numpy()) <= 1e-15
+
+
+@pytest.mark.parametrize("name,variant", OP_TAGS)
+def test_semilinear_residual_matches_reference(golden, name, variant):
+    """model.residual twin (NoSplit) vs the reference's A(U) (model.py:420-460)."""
+    from paper_1902_08112_b200 import model as M
+    g = golden["operator"]
+    tag = f"{name}/none/{variant}"
+    disc = product_disc(name)
+    space = disc.finest
+    st = product_state(g[f"{tag}/U"], g[f"{tag}/phi_tilde"], g[f"{tag}/t"])
+    flags = g[f"{tag}/flags"]
+    mask = M.ConstraintMask(flags, np.zeros(flags.size))
+    out = M.residual(space, st, mask, product_params(space, variant == "modulus"), M.SplitKind.NOSPLIT)
+    assert isinstance(out, np.ndarray)
+    assert rel_err(out, g[f"{tag}/residual"]) <= TOL
+    assert np.all(out[flags] == 0.0)
