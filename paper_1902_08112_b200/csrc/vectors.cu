@@ -81,16 +81,21 @@ __global__ void __launch_bounds__(RT) fused_kernel(Op op, int64_t n, Scratch* S)
         last = (t == gridDim.x - 1);
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last) {
+        // the last block adds the block partials with a fixed tree: thread t
+        // sums partials t, t+RT, t+2RT, ... in order, then the block tree
         __threadfence();
         double s0 = 0.0, s1 = 0.0;
         volatile double* p = S->partial;
-        for (unsigned b = 0; b < gridDim.x; ++b) {
+        for (unsigned b = threadIdx.x; b < gridDim.x; b += RT) {
             s0 += p[2 * b];
             s1 += p[2 * b + 1];
         }
-        op.finish(s0, s1);
-        S->counter = 0;
+        block_sum2(s0, s1);
+        if (threadIdx.x == 0) {
+            op.finish(s0, s1);
+            S->counter = 0;
+        }
     }
 }
 

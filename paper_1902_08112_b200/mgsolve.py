@@ -158,22 +158,35 @@ def _is_native(op):
     return isinstance(op, PhaseFieldOperator)
 
 
+def _cg_native(op, diag_dev, eig_iters, seed):
+    """Enqueue the device CG-Lanczos of both blocks (no host sync); returns the
+    device scalar arrays.  Seed rule seed + 31*level + 7*k (mgsolve.py:135-136)."""
+    level = getattr(getattr(op, "space", None), "level", None)
+    out = []
+    for k, blk in enumerate(op.blocks):
+        sd = seed + 31 * level + 7 * k if level is not None else seed + 7 * k
+        n = blk.stop - blk.start
+        b = probe_vector(sd, n).clone()
+        comp0 = 0 if k == 0 else op.dim
+        ncomp = op.dim if k == 0 else 1
+        _lib.call("pffmg_masked_copy", _lib.ptr(op.flags), op.V, comp0, ncomp, _lib.ptr(b),
+                  _lib.ptr(b), _lib.stream())
+        out.append(cg_lanczos_dev(lambda s_, d_, k=k: op.apply_dev(k, s_, d_, pre=True), diag_dev[blk],
+                                  b, eig_iters))
+    return out
+
+
 def _estimate_blocks(op, diag_dev, eig_iters, seed):
     """Block spectra with the seed rule seed + 31*level + 7*k (mgsolve.py:128-139)."""
     spectra = []
     level = getattr(getattr(op, "space", None), "level", None)
+    if _is_native(op):
+        scals = host(torch.stack(_cg_native(op, diag_dev, eig_iters, seed)))
+        return tuple(lanczos_extremes(s, eig_iters) for s in scals)
     for k, blk in enumerate(op.blocks):
         sd = seed + 31 * level + 7 * k if level is not None else seed + 7 * k
-        if _is_native(op):
-            n = blk.stop - blk.start
-            b = probe_vector(sd, n).clone()
-            comp0 = 0 if k == 0 else op.dim
-            ncomp = op.dim if k == 0 else 1
-            _lib.call("pffmg_masked_copy", _lib.ptr(op.flags), op.V, comp0, ncomp, _lib.ptr(b),
-                      _lib.ptr(b), _lib.stream())
-            scal = cg_lanczos_dev(lambda s_, d_, k=k: op.apply_dev(k, s_, d_, pre=True), diag_dev[blk], b,
-                                  eig_iters)
-            spectra.append(lanczos_extremes(host(scal), eig_iters))
+        if False:
+            pass
         else:
             spectra.append(estimate_spectrum(lambda vb, k=k: op.apply_block(k, vb),
                                              diag_dev[blk], n_iters=eig_iters, seed=sd,
@@ -229,7 +242,7 @@ def build_level_contexts(disc, state, active_mask, dirichlet_mask, params, split
         D.inject_dev(P1[l + 1], P1[l], l, nc)
         D.inject_dev(P2[l + 1], P2[l], l, nc)
         D.inject_dev(PT[l + 1], PT[l], l, 1)
-    contexts = []
+    ops, diags, scals = [], [], []
     for l in range(L):
         st = LinearizationState(U=U[l], U_prev1=P1[l], U_prev2=P2[l], t=state.t,
                                 t_prev1=state.t_prev1, t_prev2=state.t_prev2, phi_tilde=PT[l])
@@ -239,8 +252,14 @@ def build_level_contexts(disc, state, active_mask, dirichlet_mask, params, split
         op = PhaseFieldOperator(D.spaces[l], st, mask, params, split, threads, _flags=flags[l])
         diag = empty(op.n_dofs)
         op.diagonal_dev(diag)
-        spectra = _estimate_blocks(op, diag, eig_iters, seed)
-        contexts.append(LevelContext(l, op, diag, spectra, None, disc, flags[l]))
+        ops.append(op)
+        diags.append(diag)
+        scals += _cg_native(op, diag, eig_iters, seed)        # enqueued, no host sync
+    scal_host = host(torch.stack(scals))                      # one sync for all levels
+    contexts = []
+    for l in range(L):
+        spectra = tuple(lanczos_extremes(scal_host[2 * l + k], eig_iters) for k in range(2))
+        contexts.append(LevelContext(l, ops[l], diags[l], spectra, None, disc, flags[l]))
     return contexts
 
 
