@@ -196,6 +196,15 @@ int pffmg_arnoldi_mgs(double* Vb, int64_t ld, int j, double* w, int64_t n, doubl
 int pffmg_multi_axpy(const double* Z, int64_t ld, int k, const double* y, double* x,
                      int64_t n, void* stream);
 
+/* Primal-dual active set of the phase-field dofs (nonlinear.py:75-89):
+ * active[v] = (mass_inv[v]*R[v] + c*(U[v] - phi_old[v]) > 0) && !(dirichlet bit phi_comp),
+ * evaluated with the reference's rounding (no FMA contraction): bit-exact for
+ * identical inputs.  Pointers are the phase-field parts (length V);
+ * dirichlet_flags (packed per-vertex bits) may be NULL. */
+int pffmg_active_set(const double* R_phi, const double* U_phi, const double* phi_old,
+                     const double* mass_inv_phi, double c, const uint8_t* dirichlet_flags,
+                     int phi_comp, int64_t V, uint8_t* active_phi, void* stream);
+
 /* Jacobi-PCG Lanczos for estimate_spectrum (krylov.py:146-185), device part.
  * State vector layout: see pffmg_cg_* in csrc/vectors.cu. */
 int pffmg_cg_start(const double* b, const double* diag, double* r, double* z, double* p,

@@ -71,6 +71,7 @@ _SIGS = {
     "pffmg_dot_scaled": [vp, vp, vp, C.c_int64, vp, vp],
     "pffmg_arnoldi_mgs": [vp, C.c_int64, C.c_int, vp, C.c_int64, vp, vp, vp],
     "pffmg_multi_axpy": [vp, C.c_int64, C.c_int, vp, vp, C.c_int64, vp],
+    "pffmg_active_set": [vp, vp, vp, vp, C.c_double, vp, C.c_int, C.c_int64, vp, vp],
     "pffmg_cg_start": [vp, vp, vp, vp, vp, C.c_int64, vp, vp],
     "pffmg_cg_step": [vp, vp, vp, vp, vp, C.c_int64, vp, C.c_int, vp],
 }

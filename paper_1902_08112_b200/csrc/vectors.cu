@@ -328,6 +328,20 @@ __global__ void axpby_k(double a, const double* x, double b, double* y, int64_t 
 __global__ void sub_k(const double* x, const double* y, double* o, int64_t n) {
     GRID_STRIDE(i, n) o[i] = x[i] - y[i];
 }
+// Primal-dual active set of the phase field (nonlinear.py:75-89):
+//   active_phi[v] = (minv[v] * R[v] + c * (U[v] - phi_old[v])) > 0  and not Dirichlet.
+// Explicit _rn intrinsics keep the reference's rounding (no FMA contraction),
+// so the set is bit-exact for identical inputs.
+__global__ void active_set_k(const double* R, const double* U, const double* phi_old, const double* minv,
+                             double c, const uint8_t* dflags, int comp, int64_t V, uint8_t* active) {
+    GRID_STRIDE(v, V) {
+        const double ind = __dadd_rn(__dmul_rn(minv[v], R[v]), __dmul_rn(c, __dsub_rn(U[v], phi_old[v])));
+        bool a = ind > 0.0;
+        if (dflags && ((dflags[v] >> comp) & 1)) a = false;
+        active[v] = a ? 1 : 0;
+    }
+}
+
 // x += sum_k y[k] * Z_k   (krylov.py:132: x + Z[:j].T @ y)
 __global__ void multi_axpy_k(const double* Z, int64_t ld, int k, const double* y, double* x, int64_t n) {
     __shared__ double ys[64];
@@ -448,6 +462,17 @@ extern "C" int pffmg_multi_axpy(const double* Z, int64_t ld, int k, const double
     if (k == 0) return PFFMG_OK;
     multi_axpy_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(Z, ld, k, y, x, n);
     VCHECK("pffmg_multi_axpy");
+}
+
+extern "C" int pffmg_active_set(const double* R_phi, const double* U_phi, const double* phi_old,
+                                const double* mass_inv_phi, double c, const uint8_t* dirichlet_flags,
+                                int phi_comp, int64_t V, uint8_t* active_phi, void* stream) {
+    PFFMG_REQUIRE(R_phi && U_phi && phi_old && mass_inv_phi && active_phi && V >= 0 && phi_comp >= 0 &&
+                      phi_comp < 8,
+                  "pffmg_active_set: bad args");
+    active_set_k<<<vgrid(V), 256, 0, as_stream(stream)>>>(R_phi, U_phi, phi_old, mass_inv_phi, c,
+                                                          dirichlet_flags, phi_comp, V, active_phi);
+    VCHECK("pffmg_active_set");
 }
 
 extern "C" int pffmg_cg_start(const double* b, const double* diag, double* r, double* z, double* p, int64_t n,
