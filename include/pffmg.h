@@ -59,6 +59,10 @@ typedef struct {
      * own_lo-1 and own_hi, if inside the lattice, are ghost planes that must
      * hold the neighbours' values.  own_lo = own_hi = 0 means the whole lattice. */
     int32_t own_lo, own_hi;
+    /* Global index of local plane 0 along the cut axis (0 unless this is a
+     * slab of a larger level); transfers use it to pair coarse and fine slabs. */
+    int32_t plane0;
+    int32_t pad_;
 } pffmg_lattice;
 
 /*

@@ -27,7 +27,8 @@ class Lattice(C.Structure):
                 ("n_vertices", C.c_int64),
                 ("vrow_off", vp), ("vrow_lo", vp), ("vrow_hi", vp),
                 ("crow_lo", vp), ("crow_hi", vp),
-                ("own_lo", C.c_int32), ("own_hi", C.c_int32)]
+                ("own_lo", C.c_int32), ("own_hi", C.c_int32),
+                ("plane0", C.c_int32), ("pad_", C.c_int32)]
 
 
 class State(C.Structure):

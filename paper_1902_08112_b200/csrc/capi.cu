@@ -66,6 +66,7 @@ int make_lat(const pffmg_lattice* in, Lat* out) {
     out->vrow_hi = in->vrow_hi;
     out->crow_lo = in->crow_lo;
     out->crow_hi = in->crow_hi;
+    out->plane0 = in->plane0;
     const int nplanes = (in->dim == 3 ? in->nz : in->ny) + 1;
     if (in->own_lo == 0 && in->own_hi == 0) {
         out->own_lo = 0;

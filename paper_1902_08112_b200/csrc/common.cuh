@@ -40,6 +40,7 @@ struct Lat {
     const int32_t* __restrict__ crow_lo;
     const int32_t* __restrict__ crow_hi;
     int own_lo, own_hi;    // finalised vertex planes of the last axis (always set by make_lat)
+    int plane0;            // global index of local plane 0 along the last axis
 };
 
 int make_lat(const pffmg_lattice* in, Lat* out);

@@ -152,27 +152,59 @@ class Halo:
         self.recv_up = (int(self.offs[hi_own]), int(self.offs[hi_own + 1])) if slab.has_upper else None
 
     def exchange(self, vec, n_comp):
-        """Refresh ghost planes of `vec` (a 1-D tensor of n_comp * V entries) in place."""
+        """Refresh ghost planes of `vec` (a 1-D tensor of n_comp * V entries) in place.
+
+        With NCCL the planes go device to device; with gloo (CPU tests, or
+        ranks sharing one GPU in tests) CUDA planes are staged through host memory."""
         if self.world == 1 or self.slab.replicated:
             return vec
-        ops = []
+        stage = vec.is_cuda and _backend(self.group) != "nccl"
+        ops, back = [], []
         V = self.V
+
+        def buf(t):
+            return t.cpu() if stage else t
+
         for c in range(n_comp):
             base = c * V
-            if self.send_down is not None:
-                a, b = self.send_down
-                ops.append(dist.P2POp(dist.isend, vec[base + a:base + b], self.rank - 1, self.group))
-                a, b = self.recv_down
-                ops.append(dist.P2POp(dist.irecv, vec[base + a:base + b], self.rank - 1, self.group))
-            if self.send_up is not None:
-                a, b = self.send_up
-                ops.append(dist.P2POp(dist.isend, vec[base + a:base + b], self.rank + 1, self.group))
-                a, b = self.recv_up
-                ops.append(dist.P2POp(dist.irecv, vec[base + a:base + b], self.rank + 1, self.group))
+            for send, recv, peer in ((self.send_down, self.recv_down, self.rank - 1),
+                                     (self.send_up, self.recv_up, self.rank + 1)):
+                if send is None:
+                    continue
+                a, b = send
+                ops.append(dist.P2POp(dist.isend, buf(vec[base + a:base + b]), peer, self.group))
+                a, b = recv
+                r = buf(vec[base + a:base + b])
+                ops.append(dist.P2POp(dist.irecv, r, peer, self.group))
+                if stage:
+                    back.append((vec[base + a:base + b], r))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        for dst, src in back:
+            dst.copy_(src)
         return vec
+
+
+def _backend(group=None):
+    try:
+        return dist.get_backend(group)
+    except Exception:
+        return "none"
+
+
+def allreduce_(t, group=None, op=None):
+    """In-place sum (or `op`) all-reduce; CUDA tensors staged through the host under gloo."""
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return t
+    op = op or dist.ReduceOp.SUM
+    if t.is_cuda and _backend(group) != "nccl":
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+    return t
 
 
 def dist_dot(x, y, n_comp, info_local, group=None, local_dot=None):
@@ -185,8 +217,7 @@ def dist_dot(x, y, n_comp, info_local, group=None, local_dot=None):
             parts.append(torch.dot(x[s], y[s]))
     t = torch.stack([torch.as_tensor(p, dtype=torch.float64, device=x.device) for p in parts]).sum()
     t = t.reshape(1)
-    if dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(t, group=group)
+    allreduce_(t, group)
     return float(t.item())
 
 

@@ -286,6 +286,7 @@ class DeviceLattice:
             self._tables = ts
             L.vrow_off, L.vrow_lo, L.vrow_hi, L.crow_lo, L.crow_hi = [t.data_ptr() for t in ts]
         L.own_lo, L.own_hi = int(info.own[0]), int(info.own[1])
+        L.plane0 = int(getattr(info, "plane_lo", 0))
         self.struct = L
         self.ref = C.byref(L)
 
