@@ -166,10 +166,14 @@ def run_reference(args):
 def run_gpu(args):
     import torch
     ws, rank, local = dist_env()
+    local = local % max(torch.cuda.device_count(), 1)   # --backend gloo smoke runs share one GPU
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     from paper_1902_08112_b200 import _lib, configs, krylov, mgsolve
     from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, SplitKind
 
@@ -317,6 +321,35 @@ def run_gpu(args):
                  "rhs": "Newton RHS -A(U), constrained rows zeroed, from the GPU residual kernel",
                  "control": "GMRES(30) rel 1e-8 abs 0, V(1,1) FULL, Chebyshev deg %d" % prob.degree,
                  "timing": "wall clock, median of 3 after one warm-up"}
+    elif not args.no_solve and ws > 1:
+        from paper_1902_08112_b200 import model as M
+        from paper_1902_08112_b200.dist_solver import DistGMG
+        ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+        rhs_g = configs.fallback_rhs(prob)
+
+        def newton_step():
+            torch.distributed.barrier()
+            t0 = time.perf_counter()
+            gmg = DistGMG(prob.disc.hierarchy.levels, ws, rank, degree=prob.degree)
+            gmg.setup(prob.state, prob.active, prob.dirichlet, prob.params, SplitKind.NOSPLIT)
+            b = gmg.to_local(rhs_g)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            x, its = gmg.gmres(b, ctl)
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            tt = torch.tensor([t1 - t0, t2 - t1], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            return float(tt[0]), float(tt[1]), its
+
+        newton_step()
+        setup_s, gmres_s, its = newton_step()
+        solve = {"setup_ms": setup_s * 1e3, "gmres_ms": gmres_s * 1e3, "gmres_iters": its,
+                 "ms_per_newton_step": (setup_s + gmres_s) * 1e3,
+                 "rhs": "seeded N(0,1), constrained rows zeroed (SURVEY §8d fallback)",
+                 "control": "slab-distributed GMRES(30) rel 1e-8 abs 0, V(1,1) FULL, Chebyshev deg %d, "
+                            "%s halos + all-reduced dots" % (prob.degree, args.backend),
+                 "timing": "wall clock, max over ranks"}
 
     if rank != 0:
         if ws > 1:
@@ -337,7 +370,7 @@ def run_gpu(args):
     peak_all = hbm * ws                           # aggregate over the ranks
     workload = (f"{args.config}: 2D notched square 1024^2 Q1 NoSplit vmult" if ws == 1 else
                 f"{args.config} x{ws}: {ws} stacked 1024^2 notched squares (1024 x {1024 * ws} Q1), "
-                f"y-slab per GPU, NCCL halo exchange + fused vmult") if args.config == "cfg2" else args.config
+                f"y-slab per GPU, {args.backend} halo exchange + fused vmult") if args.config == "cfg2" else args.config
     line = {
         "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
@@ -386,6 +419,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg4", "cfg5"])
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: host-staged communication, for functional runs of N>1 on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
