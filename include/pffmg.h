@@ -74,7 +74,7 @@ typedef struct {
 typedef struct {
     double mu, lam, g_c, kappa, eps;
     double pressure;            /* MaterialParams.pressure(state.t) */
-    int32_t split;              /* 0 = NOSPLIT; 1 = MIEHE (returns PFFMG_ERR_UNSUPPORTED for now) */
+    int32_t split;              /* 0 = NOSPLIT; 1 = MIEHE (2D; 3D returns PFFMG_ERR_UNSUPPORTED) */
     int32_t hints;              /* bit 0 (PFFMG_HINT_PREMASKED): every input vector of the
                                    call is already zero at constrained dofs, so the masked
                                    gather (fem.py:205-206) can be skipped.  Results are
@@ -82,9 +82,14 @@ typedef struct {
     const double* U;            /* (dim+1)*V linearisation point (may be NULL for the u block) */
     const double* phi_tilde;    /* V extrapolated phase field (may be NULL for the phi block) */
     const double* rho;          /* NULL (rho == 1) or modulus field per lattice cell x QP */
-    const uint8_t* flags;       /* V packed constraint bits: bit c <=> dof c*V+v constrained;
-                                   the buffer must stay readable (any content) up to
-                                   4*ceil(V/4) + 40 bytes: kernels read aligned 32-bit words */
+    const uint8_t* flags;       /* (see below) */
+    double split_band;          /* MaterialParams.split_band: C^1 blend half-width of the
+                                   spectral split (model.py:56-86); 0 = hard split */
+    /* flags: V packed constraint bits: bit c <=> dof c*V+v constrained; the
+     * buffer must stay readable (any content) up to 4*ceil(V/4) + 40 bytes:
+     * kernels read aligned 32-bit words.
+     * split = 1 (Miehe spectral split, model.py:174-219) is implemented for 2D
+     * levels; 3D returns PFFMG_ERR_UNSUPPORTED. */
 } pffmg_state;
 
 const char* pffmg_last_error(void);

@@ -36,7 +36,8 @@ class State(C.Structure):
     _fields_ = [("mu", C.c_double), ("lam", C.c_double), ("g_c", C.c_double),
                 ("kappa", C.c_double), ("eps", C.c_double), ("pressure", C.c_double),
                 ("split", C.c_int32), ("hints", C.c_int32),
-                ("U", vp), ("phi_tilde", vp), ("rho", vp), ("flags", vp)]
+                ("U", vp), ("phi_tilde", vp), ("rho", vp), ("flags", vp),
+                ("split_band", C.c_double)]
 
 
 # name -> argtypes (restype is always c_int status unless noted)

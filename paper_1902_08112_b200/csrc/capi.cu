@@ -101,6 +101,7 @@ int make_consts(const pffmg_lattice* lat, const pffmg_state* st, Consts* K) {
     K->two_p = 2.0 * st->pressure;
     K->gc_over_eps = st->g_c / st->eps;
     K->k_phi = st->g_c * st->eps;
+    K->band = st->split_band;
     return PFFMG_OK;
 }
 

@@ -11,14 +11,16 @@ namespace pffmg {
 enum Mode { M_FULL = 0, M_UBLK = 1, M_PBLK = 2, M_DIAG = 3, M_RES = 4 };
 
 // Number of staged fp64 fields per vertex and of output components.
-template <int D, int MODE>
+template <int D, int MODE, bool SPLIT = false>
 struct ModeInfo {
     // FULL: v[0..D], U[0..D], phi_tilde;  UBLK: v[0..D-1], phi_tilde
     // PBLK: v[D], U[0..D-1];              DIAG: U[0..D-1], phi_tilde
     // RES (semilinear form A(U), model.py:420-460): U[0..D], phi_tilde
-    static constexpr int NF = MODE == M_FULL ? 2 * D + 3 : (MODE == M_RES ? D + 2 : D + 1);
+    // With the spectral split (SPLIT) the u block also needs U[0..D-1]: its
+    // tangent depends on the strain of the linearisation state.
+    static constexpr int NU = MODE == M_FULL || MODE == M_RES ? D + 1 : (MODE == M_UBLK && !SPLIT ? 0 : D);
     static constexpr int NV = MODE == M_FULL ? D + 1 : (MODE == M_UBLK ? D : (MODE == M_PBLK ? 1 : 0));
-    static constexpr int NU = MODE == M_FULL || MODE == M_RES ? D + 1 : (MODE == M_UBLK ? 0 : D);
+    static constexpr int NF = NV + NU + (MODE != M_PBLK ? 1 : 0);
     static constexpr bool PT = MODE != M_PBLK;
     static constexpr int NCO =
         MODE == M_FULL || MODE == M_DIAG || MODE == M_RES ? D + 1 : (MODE == M_UBLK ? D : 1);

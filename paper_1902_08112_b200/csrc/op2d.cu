@@ -7,28 +7,28 @@ namespace pffmg {
 
 constexpr int NW2D = 4;   // warps per CTA of the warp-independent 2D kernel
 
-template <int MODE, int EPI, bool ISO, bool RHO, bool BOX, bool PRE>
+template <int MODE, int EPI, bool ISO, bool RHO, bool BOX, bool PRE, bool MIE>
 static void launch_w(const OpArgs& A, dim3 grid, size_t smem, cudaStream_t s) {
     static size_t done = 0;
     if (smem > 48 * 1024 && done < smem) {
-        cudaFuncSetAttribute(op2dw_kernel<MODE, EPI, NW2D, ISO, RHO, BOX, PRE>,
+        cudaFuncSetAttribute(op2dw_kernel<MODE, EPI, NW2D, ISO, RHO, BOX, PRE, MIE>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         done = smem;
     }
-    op2dw_kernel<MODE, EPI, NW2D, ISO, RHO, BOX, PRE><<<grid, 32 * NW2D, smem, s>>>(A);
+    op2dw_kernel<MODE, EPI, NW2D, ISO, RHO, BOX, PRE, MIE><<<grid, 32 * NW2D, smem, s>>>(A);
 }
 
-template <int MODE, int EPI, bool ISO, bool RHO>
+template <int MODE, int EPI, bool ISO, bool RHO, bool MIE = false>
 static void launch_box(const OpArgs& A, bool pre, dim3 grid, size_t smem, cudaStream_t s) {
     const bool box = A.L.vrow_off == nullptr;
     if (box && pre)
-        launch_w<MODE, EPI, ISO, RHO, true, true>(A, grid, smem, s);
+        launch_w<MODE, EPI, ISO, RHO, true, true, MIE>(A, grid, smem, s);
     else if (box)
-        launch_w<MODE, EPI, ISO, RHO, true, false>(A, grid, smem, s);
+        launch_w<MODE, EPI, ISO, RHO, true, false, MIE>(A, grid, smem, s);
     else if (pre)
-        launch_w<MODE, EPI, ISO, RHO, false, true>(A, grid, smem, s);
+        launch_w<MODE, EPI, ISO, RHO, false, true, MIE>(A, grid, smem, s);
     else
-        launch_w<MODE, EPI, ISO, RHO, false, false>(A, grid, smem, s);
+        launch_w<MODE, EPI, ISO, RHO, false, false, MIE>(A, grid, smem, s);
 }
 
 template <int MODE, int EPI>
@@ -52,10 +52,13 @@ int launch2d(const OpArgs& A0, bool iso, cudaStream_t s) {
     A.nseg = nseg;
     const int64_t warps = (int64_t)nseg * ((rows + per - 1) / per);
     dim3 grid((unsigned)((warps + NW2D - 1) / NW2D));
-    const size_t smem = NW2D * (sizeof(double) * 4 * MI::NF * 32 + 4 * 48 + 4 * sizeof(int));
+    const int nf = A.split ? ModeInfo<2, MODE, true>::NF : MI::NF;
+    const size_t smem = NW2D * (sizeof(double) * 4 * nf * 32 + 4 * 48 + 4 * sizeof(int));
     const bool rho = A.rho != nullptr;
     const bool pre = A.premasked != 0;
-    if (iso && rho)
+    if (A.split)   // Miehe split: general-cell kernel, modulus field resolved in-kernel
+        launch_box<MODE, EPI, false, false, true>(A, pre, grid, smem, s);
+    else if (iso && rho)
         launch_box<MODE, EPI, true, true>(A, pre, grid, smem, s);
     else if (iso)
         launch_box<MODE, EPI, true, false>(A, pre, grid, smem, s);

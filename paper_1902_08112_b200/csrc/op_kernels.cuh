@@ -13,6 +13,7 @@
 #include <cmath>
 
 #include "cellops_iso.cuh"
+#include "cellops_miehe.cuh"
 
 namespace pffmg {
 
@@ -39,6 +40,7 @@ struct OpArgs {
     int planes_per_cta;
     int nseg;                          // 2D warp kernel: 30-column segments per row
     int premasked;                     // PFFMG_HINT_PREMASKED
+    int split;                         // 0 NoSplit, 1 Miehe spectral split (2D)
 };
 
 // ------------------------------------------------------------ epilogue
@@ -264,17 +266,17 @@ struct RowAddr {
     }
 };
 
-template <int MODE, int EPI, int NW, bool ISO, bool RHO, bool BOX, bool PRE>
+template <int MODE, int EPI, int NW, bool ISO, bool RHO, bool BOX, bool PRE, bool MIE = false>
 #ifndef PFFMG_MINB_FULL
 #define PFFMG_MINB_FULL 4
 #endif
 #ifndef PFFMG_MINB_BLK
 #define PFFMG_MINB_BLK 8
 #endif
-__global__ void __launch_bounds__(32 * NW, MODE == M_FULL ? PFFMG_MINB_FULL : PFFMG_MINB_BLK)
+__global__ void __launch_bounds__(32 * NW, MIE ? 2 : (MODE == M_FULL ? PFFMG_MINB_FULL : PFFMG_MINB_BLK))
 op2dw_kernel(const OpArgs A) {
     constexpr int D = 2, NP = 4;
-    using MI = ModeInfo<D, MODE>;
+    using MI = ModeInfo<D, MODE, MIE>;
     constexpr int NF = MI::NF, NCO = MI::NCO, NV = MI::NV;
     constexpr int RING = 4, W = 32, SLOT = NF * W;
     constexpr int FB = 48;                      // flag bytes per slot (9 words + pad)
@@ -385,10 +387,15 @@ op2dw_kernel(const OpArgs A) {
                 cv[i][3] = r1[i * W + lane + 1];
             }
             const double* rq = RHO ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * NP : nullptr;
-            if (ISO)
-                cell_kernel_iso<D, MODE, RHO>(cv, rq, A.K, A.I, o);
-            else
-                cell_kernel<D, MODE>(cv, rq, A.K, o);
+            if constexpr (MIE) {   // spectral split: modulus field resolved at run time
+                cell_kernel_miehe2<MODE>(cv, A.rho ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * NP : nullptr,
+                                         A.K, o);
+            } else {
+                if (ISO)
+                    cell_kernel_iso<D, MODE, RHO>(cv, rq, A.K, A.I, o);
+                else
+                    cell_kernel<D, MODE>(cv, rq, A.K, o);
+            }
         } else {
 #pragma unroll
             for (int k = 0; k < NCO; ++k)

@@ -147,9 +147,8 @@ class PhaseFieldOperator:
         V = self.lat.n_vertices
         self.V = V
         code = _split_code(split)
-        if code != 0:
-            raise NotImplementedError("the CUDA operator implements SplitKind.NOSPLIT only "
-                                      "(Miehe split: SURVEY §8f row 3, not built yet)")
+        if code == 1 and self.dim != 2:
+            raise NotImplementedError("the CUDA Miehe split is implemented for 2D levels only")
         self._U = dev(state.U)
         self._pt = dev(state.phi_tilde)
         if self._U.numel() != self.nc * V or self._pt.numel() != V:
@@ -162,6 +161,7 @@ class PhaseFieldOperator:
         st.kappa, st.eps = float(params.kappa), float(params.eps)
         st.pressure = float(params.pressure(state.t))
         st.split = code
+        st.split_band = float(getattr(params, "split_band", 0.0) or 0.0)
         st.U = self._U.data_ptr()
         st.phi_tilde = self._pt.data_ptr()
         st.rho = self._rho.data_ptr() if self._rho is not None else None

@@ -96,6 +96,41 @@ def gen_operator():
     save("operator", **out)
 
 
+def gen_operator_band():
+    """Miehe split with the C^1 blend (MaterialParams.split_band > 0): band
+    0.05 is about half the typical principal strain of random_state, so many
+    quadrature points sit inside the blend (model.py:65-86)."""
+    out = {}
+    rng = np.random.default_rng(20261020)
+    for name, spec in MESHES.items():
+        disc = Discretization(ref_hierarchy(spec))
+        space = disc.finest
+        n = space.dofmap.n_dofs
+        for variant in ("plain", "masked"):
+            tag = f"{name}/miehe_band/{variant}"
+            params = params_for(space, None)
+            params.split_band = 0.05
+            state = selfcheck.random_state(space, rng, t=0.1)
+            flags = (rng.random(n) < 0.15) if variant == "masked" else np.zeros(n, bool)
+            mask = ConstraintMask(flags, np.zeros(n))
+            v = rng.standard_normal(n)
+            split = SplitKind.MIEHE
+            op = model.PhaseFieldOperator(space, state, mask, params, split)
+            d = space.dim * space.dofmap.n_vertices
+            out[f"{tag}/band"] = np.array(params.split_band)
+            out[f"{tag}/U"] = state.U
+            out[f"{tag}/phi_tilde"] = state.phi_tilde
+            out[f"{tag}/t"] = np.array(state.t)
+            out[f"{tag}/flags"] = flags
+            out[f"{tag}/v"] = v
+            out[f"{tag}/apply"] = op.apply(v)
+            out[f"{tag}/apply_u"] = op.apply_block(0, v[:d])
+            out[f"{tag}/apply_phi"] = op.apply_block(1, v[d:])
+            out[f"{tag}/diagonal"] = op.diagonal()
+            out[f"{tag}/residual"] = model.residual(space, state, mask, params, split)
+    save("operator_band", **out)
+
+
 def gen_transfers():
     out = {}
     rng = np.random.default_rng(99)
@@ -272,7 +307,7 @@ def gen_krylov():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["meshes", "operator", "transfers", "multigrid", "configs", "krylov"]
+    which = sys.argv[1:] or ["meshes", "operator", "operator_band", "transfers", "multigrid", "configs", "krylov"]
     for w in which:
         print(w)
         globals()[f"gen_{w}"]()

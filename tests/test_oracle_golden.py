@@ -58,6 +58,34 @@ def test_operator_oracle_vs_reference(golden, name, variant, split):
     assert rel_err(res, g[f"{tag}/residual"]) <= 1e-12
 
 
+@pytest.mark.parametrize("name", list(MESHES))
+@pytest.mark.parametrize("variant", ["plain", "masked"])
+def test_operator_band_oracle_vs_reference(golden, name, variant):
+    """Miehe split with the C^1 blend (split_band > 0, model.py:65-86)."""
+    g = golden["operator_band"]
+    tag = f"{name}/miehe_band/{variant}"
+    _, tables, _ = oracle_stack(name)
+    T = tables[-1]
+    mat = oracle_material(T)
+    mat.split_band = float(g[f"{tag}/band"])
+    st = oracle_state(g[f"{tag}/U"], g[f"{tag}/phi_tilde"], g[f"{tag}/t"])
+    op = jacobian.JacobianOperator(T, st, g[f"{tag}/flags"], mat, "miehe")
+    v = g[f"{tag}/v"]
+    d = T.dim * T.n_vertices
+    assert rel_err(op.apply(v), g[f"{tag}/apply"]) <= 1e-12
+    assert rel_err(op.apply_block(0, v[:d]), g[f"{tag}/apply_u"]) <= 1e-12
+    assert rel_err(op.apply_block(1, v[d:]), g[f"{tag}/apply_phi"]) <= 1e-12
+    assert rel_err(op.diagonal(), g[f"{tag}/diagonal"]) <= 1e-12
+    res = jacobian.residual(T, st, g[f"{tag}/flags"], mat, "miehe")
+    assert rel_err(res, g[f"{tag}/residual"]) <= 1e-12
+    # the blend region is populated (otherwise this case pins nothing new)
+    sp_ = T
+    loc = sp_.gather(g[f"{tag}/U"])
+    gu = sp_.vec_grad_at_qp(loc[:, :T.dim])
+    w = np.linalg.eigvalsh(0.5 * (gu + np.swapaxes(gu, -1, -2)))
+    assert np.mean(np.abs(w) < mat.split_band) > 0.05
+
+
 def test_operator_threads_bitwise(golden):
     g = golden["operator"]
     tag = "cfg1/none/masked"
