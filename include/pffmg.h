@@ -74,7 +74,7 @@ typedef struct {
 typedef struct {
     double mu, lam, g_c, kappa, eps;
     double pressure;            /* MaterialParams.pressure(state.t) */
-    int32_t split;              /* 0 = NOSPLIT; 1 = MIEHE (2D; 3D returns PFFMG_ERR_UNSUPPORTED) */
+    int32_t split;              /* 0 = NOSPLIT; 1 = MIEHE spectral split */
     int32_t hints;              /* bit 0 (PFFMG_HINT_PREMASKED): every input vector of the
                                    call is already zero at constrained dofs, so the masked
                                    gather (fem.py:205-206) can be skipped.  Results are
@@ -88,8 +88,8 @@ typedef struct {
     /* flags: V packed constraint bits: bit c <=> dof c*V+v constrained; the
      * buffer must stay readable (any content) up to 4*ceil(V/4) + 40 bytes:
      * kernels read aligned 32-bit words.
-     * split = 1 (Miehe spectral split, model.py:174-219) is implemented for 2D
-     * levels; 3D returns PFFMG_ERR_UNSUPPORTED. */
+     * split = 1 (Miehe spectral split, model.py:174-219): per-QP closed-form
+     * (2D) or Jacobi (3D) eigen-solve, tangent applied without forming it. */
 } pffmg_state;
 
 const char* pffmg_last_error(void);

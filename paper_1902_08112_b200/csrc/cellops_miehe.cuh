@@ -293,4 +293,318 @@ __device__ __forceinline__ void cell_kernel_miehe2(const double (&cv)[ModeInfo<2
     }
 }
 
+
+// ====================================================================== 3D
+// Symmetric 3x3 eigen-decomposition by cyclic Jacobi rotations: high absolute
+// accuracy (|dw| ~ eps ||e||) like LAPACK's eigh.  Eigenvalue order does not
+// matter below: every split quantity is symmetric in the eigen-pairs (the
+// divided differences dd_ab = dd_ba), so no sort is needed.
+struct Spec3 {
+    double w[3];
+    double n[3][3];          // n[a][i]: component i of eigenvector a
+    double tr, Ep;
+    double sp[6], sm[6];     // sigma+ / sigma- as (00, 11, 22, 01, 02, 12)
+    double H[3], Htr, dd[3]; // dd for pairs (0,1), (0,2), (1,2)
+};
+
+template <int P, int Q, int R>
+__device__ __forceinline__ void jacobi_rot(double (&a)[3][3], double (&v)[3][3]) {
+    const double apq = a[P][Q];
+    if (apq == 0.0) return;
+    const double theta = 0.5 * (a[Q][Q] - a[P][P]) / apq;
+    double t = 1.0 / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
+    if (theta < 0.0) t = -t;
+    const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = t * c;
+    a[P][P] -= t * apq;
+    a[Q][Q] += t * apq;
+    a[P][Q] = a[Q][P] = 0.0;
+    const double arp = a[R][P], arq = a[R][Q];
+    a[R][P] = a[P][R] = c * arp - s * arq;
+    a[R][Q] = a[Q][R] = s * arp + c * arq;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double vp = v[k][P], vq = v[k][Q];
+        v[k][P] = c * vp - s * vq;
+        v[k][Q] = s * vp + c * vq;
+    }
+}
+
+__device__ __forceinline__ void spectral3(const double (&e)[6], const Consts& K, Spec3& S) {
+    const double band = K.band;
+    double a[3][3] = {{e[0], e[3], e[4]}, {e[3], e[1], e[5]}, {e[4], e[5], e[2]}};
+    double v[3][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}};
+    const double fro2 = e[0] * e[0] + e[1] * e[1] + e[2] * e[2] + 2.0 * (e[3] * e[3] + e[4] * e[4] + e[5] * e[5]);
+#pragma unroll 1
+    for (int sweep = 0; sweep < 12; ++sweep) {
+        const double off = a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2];
+        if (off <= 1e-40 * fro2) break;
+        jacobi_rot<0, 1, 2>(a, v);
+        jacobi_rot<0, 2, 1>(a, v);
+        jacobi_rot<1, 2, 0>(a, v);
+    }
+    double wp[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        S.w[k] = a[k][k];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) S.n[k][i] = v[i][k];
+        wp[k] = blend_pos(S.w[k], band);
+        S.H[k] = blend_pos_prime(S.w[k], band);
+    }
+    const double tr = e[0] + e[1] + e[2];
+    S.tr = tr;
+    const double trp = blend_pos(tr, band);
+    const double Es = 0.5 * K.lam * tr * tr + K.mu * (S.w[0] * S.w[0] + S.w[1] * S.w[1] + S.w[2] * S.w[2]);
+    S.Ep = 0.5 * K.lam * blend_pos_sq(tr, band) +
+           K.mu * (blend_pos_sq(S.w[0], band) + blend_pos_sq(S.w[1], band) + blend_pos_sq(S.w[2], band));
+    (void)Es;
+    constexpr int II[6] = {0, 1, 2, 0, 0, 1}, JJ[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+        double ep = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) ep = fma(wp[k] * S.n[k][II[m]], S.n[k][JJ[m]], ep);
+        S.sp[m] = 2.0 * K.mu * ep + (m < 3 ? K.lam * trp : 0.0);
+        S.sm[m] = 2.0 * K.mu * e[m] + (m < 3 ? K.lam * tr : 0.0) - S.sp[m];
+    }
+    S.Htr = blend_pos_prime(tr, band);
+    const double scale = sqrt(fro2);
+    constexpr int PA[3] = {0, 0, 1}, PB[3] = {1, 2, 2};
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+        const double gap = S.w[PA[m]] - S.w[PB[m]];
+        const bool degenerate = fabs(gap) < 1e-8 * fmax(scale, 1e-300);   // model.py:203-209
+        S.dd[m] = degenerate ? 0.5 * (S.H[PA[m]] + S.H[PB[m]]) : (wp[PA[m]] - wp[PB[m]]) / gap;
+    }
+}
+
+// out = dsig+ : eps (both as (00, 11, 22, 01, 02, 12))
+__device__ __forceinline__ void tangent_action3(const Spec3& S, const Consts& K, const double (&ep)[6],
+                                                double (&out)[6]) {
+    constexpr int II[6] = {0, 1, 2, 0, 0, 1}, JJ[6] = {0, 1, 2, 1, 2, 2};
+    double en[3][3];   // en[b] = eps n_b
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        en[b][0] = ep[0] * S.n[b][0] + ep[3] * S.n[b][1] + ep[4] * S.n[b][2];
+        en[b][1] = ep[3] * S.n[b][0] + ep[1] * S.n[b][1] + ep[5] * S.n[b][2];
+        en[b][2] = ep[4] * S.n[b][0] + ep[5] * S.n[b][1] + ep[2] * S.n[b][2];
+    }
+    double c[3], cp[3];
+    constexpr int PA[3] = {0, 0, 1}, PB[3] = {1, 2, 2};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        c[a] = S.H[a] * (S.n[a][0] * en[a][0] + S.n[a][1] * en[a][1] + S.n[a][2] * en[a][2]);
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+        const int a = PA[m], b = PB[m];
+        cp[m] = 2.0 * S.dd[m] * (S.n[a][0] * en[b][0] + S.n[a][1] * en[b][1] + S.n[a][2] * en[b][2]);
+    }
+    const double l = K.lam * S.Htr * (ep[0] + ep[1] + ep[2]);
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+        const int i = II[m], j = JJ[m];
+        double t = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) t = fma(c[a] * S.n[a][i], S.n[a][j], t);
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            const int a = PA[p], b = PB[p];
+            t = fma(cp[p], 0.5 * (S.n[a][i] * S.n[b][j] + S.n[b][i] * S.n[a][j]), t);
+        }
+        out[m] = 2.0 * K.mu * t + (m < 3 ? l : 0.0);
+    }
+}
+
+// Value and physical gradient of one Q1 field at a single QP (b[a][k]: 1D
+// basis weight of corner bit k along axis a at this QP).
+__device__ __forceinline__ void qp_eval3(const double (&c)[8], const double (&b)[3][2], const Consts& K,
+                                         double& val, double (&g)[3]) {
+    double vx[4], dx[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        vx[r] = b[0][0] * c[2 * r] + b[0][1] * c[2 * r + 1];
+        dx[r] = c[2 * r + 1] - c[2 * r];
+    }
+    double vxy[2], dxy[2], dy[2];
+#pragma unroll
+    for (int z = 0; z < 2; ++z) {
+        vxy[z] = b[1][0] * vx[2 * z] + b[1][1] * vx[2 * z + 1];
+        dxy[z] = b[1][0] * dx[2 * z] + b[1][1] * dx[2 * z + 1];
+        dy[z] = vx[2 * z + 1] - vx[2 * z];
+    }
+    val = b[2][0] * vxy[0] + b[2][1] * vxy[1];
+    g[0] = (b[2][0] * dxy[0] + b[2][1] * dxy[1]) * K.ih[0];
+    g[1] = (b[2][0] * dy[0] + b[2][1] * dy[1]) * K.ih[1];
+    g[2] = (vxy[1] - vxy[0]) * K.ih[2];
+}
+
+// Adjoint of qp_eval3: o[n] += f N_n(q) + sum_a g[a] dN_n/dx_a(q)
+__device__ __forceinline__ void qp_scatter3(double f, const double (&gin)[3], const double (&b)[3][2],
+                                            const Consts& K, double (&o)[8]) {
+    const double gx = gin[0] * K.ih[0], gy = gin[1] * K.ih[1], gz = gin[2] * K.ih[2];
+    double Avxy[2], Adxy[2], Ady[2];
+#pragma unroll
+    for (int z = 0; z < 2; ++z) {
+        Avxy[z] = b[2][z] * f + (z ? gz : -gz);
+        Adxy[z] = b[2][z] * gx;
+        Ady[z] = b[2][z] * gy;
+    }
+    double Avx[4], Adx[4];
+#pragma unroll
+    for (int z = 0; z < 2; ++z)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) {
+            Avx[2 * z + y] = b[1][y] * Avxy[z] + (y ? Ady[z] : -Ady[z]);
+            Adx[2 * z + y] = b[1][y] * Adxy[z];
+        }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int x = 0; x < 2; ++x) o[2 * r + x] += b[0][x] * Avx[r] + (x ? Adx[r] : -Adx[r]);
+}
+
+template <int MODE>
+__device__ __forceinline__ void cell_kernel_miehe3(const double (&cv)[ModeInfo<3, MODE, true>::NF][8],
+                                                   const double* __restrict__ rho_q, const Consts& K,
+                                                   double (&o)[ModeInfo<3, MODE, true>::NCO][8]) {
+    constexpr int D = 3, NP = 8;
+    using MI = ModeInfo<D, MODE, true>;
+#pragma unroll
+    for (int k = 0; k < MI::NCO; ++k)
+#pragma unroll
+        for (int n = 0; n < NP; ++n) o[k][n] = 0.0;
+    const double p = 0.5 * K.two_p;
+#pragma unroll 1
+    for (int q = 0; q < NP; ++q) {
+        double b[3][2];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int qb = (q >> a) & 1;
+            b[a][0] = qb ? K.omg1 : K.omg0;
+            b[a][1] = qb ? K.g1 : K.g0;
+        }
+        const double rho = rho_q ? __ldg(rho_q + q) : 1.0;
+        // strain of the linearisation state
+        double gu[3][3], val;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) qp_eval3(cv[MI::F_U + i], b, K, val, gu[i]);
+        double e[6] = {gu[0][0], gu[1][1], gu[2][2], 0.5 * (gu[0][1] + gu[1][0]), 0.5 * (gu[0][2] + gu[2][0]),
+                       0.5 * (gu[1][2] + gu[2][1])};
+        Spec3 S;
+        spectral3(e, K, S);
+        double gk = 0.0, ptq = 0.0;
+        if (MI::PT) {
+            double gd[3];
+            qp_eval3(cv[MI::F_PT], b, K, ptq, gd);
+            gk = K.omk * (ptq * ptq) + K.kappa;
+        }
+        constexpr int II[6] = {0, 1, 2, 0, 0, 1}, JJ[6] = {0, 1, 2, 1, 2, 2};
+        auto sym = [](const double (&s)[6], int i, int j) -> double {
+            return i == j ? s[i] : s[i + j + 2];   // (0,1)->3, (0,2)->4, (1,2)->5
+        };
+
+        if (MODE == M_DIAG) {
+            const double am = K.omk * rho * S.Ep + K.two_p * S.tr + K.gc_over_eps;
+            const double gm = (gk - 1.0) * rho;
+#pragma unroll
+            for (int n = 0; n < NP; ++n) {
+                double Nv = 1.0;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) Nv *= b[a][(n >> a) & 1];
+                double gN[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    double t = ((n >> a) & 1) ? K.ih[a] : -K.ih[a];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        if (c != a) t *= b[c][(n >> c) & 1];
+                    gN[a] = t;
+                }
+                const double gg = gN[0] * gN[0] + gN[1] * gN[1] + gN[2] * gN[2];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    double E[6];
+#pragma unroll
+                    for (int m = 0; m < 6; ++m) {
+                        const int a = II[m], c = JJ[m];
+                        E[m] = (a == c) ? (a == i ? gN[i] : 0.0)
+                                        : (a == i ? 0.5 * gN[c] : (c == i ? 0.5 * gN[a] : 0.0));
+                    }
+                    double T[6];
+                    tangent_action3(S, K, E, T);
+                    const double edde = T[0] * E[0] + T[1] * E[1] + T[2] * E[2] +
+                                        2.0 * (T[3] * E[3] + T[4] * E[4] + T[5] * E[5]);
+                    const double iso = K.mu * gg + (K.mu + K.lam) * (gN[i] * gN[i]);
+                    o[i][n] += K.jxw * (rho * iso + gm * edde);
+                }
+                o[D][n] += K.jxw * (am * (Nv * Nv)) + K.k_phi * (K.jxw * gg);
+            }
+            continue;
+        }
+        if (MODE == M_RES) {
+            double ph, gph[3];
+            qp_eval3(cv[MI::F_U + D], b, K, ph, gph);
+            const double pp = ptq * ptq * p;
+            double s6[6];
+#pragma unroll
+            for (int m = 0; m < 6; ++m) s6[m] = gk * rho * S.sp[m] + rho * S.sm[m] + (m < 3 ? pp : 0.0);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                double g[3];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) g[j] = K.jxw * sym(s6, i, j);
+                qp_scatter3(0.0, g, b, K, o[i]);
+            }
+            const double f = K.jxw * (K.omk * ph * rho * S.Ep + K.two_p * ph * S.tr - K.gc_over_eps * (1.0 - ph));
+            double g[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) g[j] = K.jxw * K.k_phi * gph[j];
+            qp_scatter3(f, g, b, K, o[D]);
+            continue;
+        }
+        constexpr bool HAS_U = MODE == M_FULL || MODE == M_UBLK;
+        constexpr bool HAS_P = MODE == M_FULL || MODE == M_PBLK;
+        double coup = 0.0;
+        if (HAS_U) {
+            double gv[3][3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) qp_eval3(cv[MI::F_V + i], b, K, val, gv[i]);
+            double ev[6] = {gv[0][0], gv[1][1], gv[2][2], 0.5 * (gv[0][1] + gv[1][0]),
+                            0.5 * (gv[0][2] + gv[2][0]), 0.5 * (gv[1][2] + gv[2][1])};
+            double T[6];
+            tangent_action3(S, K, ev, T);
+            const double tre = ev[0] + ev[1] + ev[2], gm = (gk - 1.0) * rho;   // model.py:321-323
+            double s6[6];
+#pragma unroll
+            for (int m = 0; m < 6; ++m) s6[m] = rho * (2.0 * K.mu * ev[m] + (m < 3 ? K.lam * tre : 0.0)) + gm * T[m];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                double g[3];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) g[j] = K.jxw * sym(s6, i, j);
+                qp_scatter3(0.0, g, b, K, o[i]);
+            }
+            if (MODE == M_FULL) {
+                double phq, gd[3];
+                qp_eval3(cv[MI::F_U + D], b, K, phq, gd);
+                const double cph = rho * K.omk * phq;
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        coup += (cph * sym(S.sp, i, j) + (i == j ? K.two_p * phq : 0.0)) * gv[i][j];
+            }
+        }
+        if (HAS_P) {
+            double vp, gvp[3];
+            qp_eval3(cv[MODE == M_FULL ? MI::F_V + D : MI::F_V], b, K, vp, gvp);
+            const double a = K.omk * rho * S.Ep + K.two_p * S.tr + K.gc_over_eps;   // model.py:304-308
+            double g[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) g[j] = K.jxw * K.k_phi * gvp[j];
+            qp_scatter3(K.jxw * (coup + a * vp), g, b, K, o[MODE == M_FULL ? D : 0]);
+        }
+    }
+}
+
 }  // namespace pffmg

@@ -11,11 +11,11 @@ namespace pffmg {
 constexpr int TY3D = 8;    // generic kernel
 constexpr int TY3T = 8;    // streaming kernel
 
-template <int MODE, int EPI, bool ISO>
+template <int MODE, int EPI, bool ISO, bool MIE = false>
 static void set_smem(size_t smem) {
     static size_t done = 0;
     if (done < smem) {
-        cudaFuncSetAttribute(op3d_kernel<MODE, EPI, TY3D, ISO>,
+        cudaFuncSetAttribute(op3d_kernel<MODE, EPI, TY3D, ISO, MIE>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         done = smem;
     }
@@ -69,13 +69,14 @@ static int launch_stream(const OpArgs& A0, cudaStream_t s) {
 
 template <int MODE, int EPI>
 int launch3d(const OpArgs& A0, bool iso, cudaStream_t s) {
-    if (iso && MODE != M_DIAG) return launch_stream<MODE, EPI>(A0, s);
+    if (iso && MODE != M_DIAG && !A0.split) return launch_stream<MODE, EPI>(A0, s);
     OpArgs A = A0;
     const Lat& L = A.L;
     const int sms = sm_count();
     using MI = ModeInfo<3, MODE>;
     constexpr int TV = 33 * (TY3D + 1);
-    const size_t smem = sizeof(double) * (2 * MI::NF * TV + TY3D * 2 * MI::NCO * 32) + 2 * TV;
+    const int nf = A.split ? ModeInfo<3, MODE, true>::NF : MI::NF;
+    const size_t smem = sizeof(double) * (2 * nf * TV + TY3D * 2 * MI::NCO * 32) + 2 * TV;
     const int gx = (L.nx + 1 + 30) / 31;
     const int gy = (L.ny + 1 + TY3D - 2) / (TY3D - 1);
     const int planes = L.own_hi - L.own_lo;
@@ -83,7 +84,10 @@ int launch3d(const OpArgs& A0, bool iso, cudaStream_t s) {
     per = per < 4 ? 4 : (per > 32 ? 32 : per);
     A.planes_per_cta = per;
     dim3 grid(gx, gy, (planes + per - 1) / per);
-    if (iso) {
+    if (A.split) {   // Miehe spectral split: general cells, per-QP Jacobi eigen-solve
+        set_smem<MODE, EPI, false, true>(smem);
+        op3d_kernel<MODE, EPI, TY3D, false, true><<<grid, 32 * TY3D, smem, s>>>(A);
+    } else if (iso) {
         set_smem<MODE, EPI, true>(smem);
         op3d_kernel<MODE, EPI, TY3D, true><<<grid, 32 * TY3D, smem, s>>>(A);
     } else {

@@ -82,10 +82,10 @@ __device__ __forceinline__ void epilogue(const OpArgs& A, int64_t vid, uint8_t f
 }
 
 // Load one staged vertex: all NF fields (raw) + flags.
-template <int D, int MODE>
+template <int D, int MODE, bool SPLIT = false>
 __device__ __forceinline__ void load_vertex(const OpArgs& A, int64_t vid,
-                                            double (&f)[ModeInfo<D, MODE>::NF], uint8_t& fl) {
-    using MI = ModeInfo<D, MODE>;
+                                            double (&f)[ModeInfo<D, MODE, SPLIT>::NF], uint8_t& fl) {
+    using MI = ModeInfo<D, MODE, SPLIT>;
     const int64_t V = A.L.V;
     if (vid < 0) {
 #pragma unroll
@@ -434,10 +434,10 @@ op2dw_kernel(const OpArgs A) {
 // CTA = TY warps; warp w <-> cell row cy0 + w, lane <-> cell column cx0 + lane.
 // Finalises vertices (cx0 + lane, cy0 + w) for lane >= 1, w >= 1; marches in z.
 
-template <int MODE, int EPI, int TY, bool ISO>
+template <int MODE, int EPI, int TY, bool ISO, bool MIE = false>
 __global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
     constexpr int D = 3, NP = 8;
-    using MI = ModeInfo<D, MODE>;
+    using MI = ModeInfo<D, MODE, MIE>;
     constexpr int NF = MI::NF, NCO = MI::NCO;
     constexpr int TXV = 33, TYV = TY + 1, TV = TXV * TYV;
     constexpr int NT = 32 * TY;
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
                 const int jx = j % TXV, jy = j / TXV;
                 double f[NF];
                 uint8_t fl;
-                load_vertex<D, MODE>(A, vertex_id(L, cx0 + jx, cy0 + jy, z), f, fl);
+                load_vertex<D, MODE, MIE>(A, vertex_id(L, cx0 + jx, cy0 + jy, z), f, fl);
 #pragma unroll
                 for (int i = 0; i < NF; ++i) SV(buf, i, j) = f[i];
                 sfl[buf * TV + j] = fl;
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
             for (int s = 0; s < SLOTS; ++s) {
                 const int j = tid + s * NT;
                 const int64_t vid = j < TV ? vertex_id(L, cx0 + j % TXV, cy0 + j / TXV, cz + 2) : -1;
-                load_vertex<D, MODE>(A, vid, pf[s], pfl[s]);
+                load_vertex<D, MODE, MIE>(A, vid, pf[s], pfl[s]);
             }
         }
 
@@ -513,9 +513,13 @@ __global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
             }
             const double* rq =
                 A.rho ? A.rho + ((int64_t)cx + (int64_t)L.nx * (cy + (int64_t)L.ny * cz)) * NP : nullptr;
-            if (ISO && rq) cell_kernel_iso<D, MODE, true>(cv, rq, A.K, A.I, o);
-            else if (ISO) cell_kernel_iso<D, MODE, false>(cv, rq, A.K, A.I, o);
-            else cell_kernel<D, MODE>(cv, rq, A.K, o);
+            if constexpr (MIE) {
+                cell_kernel_miehe3<MODE>(cv, rq, A.K, o);
+            } else {
+                if (ISO && rq) cell_kernel_iso<D, MODE, true>(cv, rq, A.K, A.I, o);
+                else if (ISO) cell_kernel_iso<D, MODE, false>(cv, rq, A.K, A.I, o);
+                else cell_kernel<D, MODE>(cv, rq, A.K, o);
+            }
         } else {
 #pragma unroll
             for (int k = 0; k < NCO; ++k)

@@ -32,10 +32,6 @@ static int fill_args(const pffmg_lattice* lat, const pffmg_state* st, OpArgs* A)
         set_error("unknown split kind %d (0 NoSplit, 1 Miehe)", st->split);
         return PFFMG_ERR_ARG;
     }
-    if (st->split == 1 && lat->dim != 2) {
-        set_error("Miehe split is implemented for 2D lattices only (got dim %d)", lat->dim);
-        return PFFMG_ERR_UNSUPPORTED;
-    }
     PFFMG_REQUIRE(st->split_band >= 0.0 && std::isfinite(st->split_band), "split_band must be finite and >= 0");
     A->split = st->split;
     PFFMG_REQUIRE(st->flags, "state.flags is NULL");

@@ -147,8 +147,6 @@ class PhaseFieldOperator:
         V = self.lat.n_vertices
         self.V = V
         code = _split_code(split)
-        if code == 1 and self.dim != 2:
-            raise NotImplementedError("the CUDA Miehe split is implemented for 2D levels only")
         self._U = dev(state.U)
         self._pt = dev(state.phi_tilde)
         if self._U.numel() != self.nc * V or self._pt.numel() != V:

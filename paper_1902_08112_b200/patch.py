@@ -24,8 +24,8 @@ KRYLOV = ["gmres", "estimate_spectrum"]
 def install(fracmg=None, operator=False):
     """Swap the GPU twins into `fracmg` (module or None to import it).
 
-    operator=True also replaces `fracmg.model.PhaseFieldOperator` (both
-    splits in 2D; a 3D Miehe-split operator raises NotImplementedError)."""
+    operator=True also replaces `fracmg.model.PhaseFieldOperator` (NoSplit
+    and the Miehe split, 2D and 3D)."""
     if fracmg is None:
         fracmg = importlib.import_module("fracmg")
     from . import krylov, mgsolve, model

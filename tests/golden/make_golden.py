@@ -231,6 +231,50 @@ def gen_multigrid():
     save("multigrid", **out)
 
 
+def gen_multigrid_miehe():
+    """Level contexts, V-cycle and one GMRES solve with the Miehe split
+    (lshape with the C^1 blend, lshape3d with the hard split)."""
+    out = {}
+    for name, band in (("lshape", 0.02), ("lshape3d", 0.0)):
+        t0 = time.time()
+        disc, state, params, dirichlet, active = _mg_setup(name, 6)
+        params.split_band = band
+        split = SplitKind.MIEHE
+        ctxs = mgsolve.build_level_contexts(disc, state, active, dirichlet, params, split)
+        n = disc.finest.dofmap.n_dofs
+        out[f"{name}/band"] = np.array(band)
+        out[f"{name}/U"] = state.U
+        out[f"{name}/U_prev1"] = state.U_prev1
+        out[f"{name}/U_prev2"] = state.U_prev2
+        out[f"{name}/phi_tilde"] = state.phi_tilde
+        out[f"{name}/times"] = np.array([state.t, state.t_prev1, state.t_prev2])
+        out[f"{name}/dirichlet"] = dirichlet.is_constrained
+        out[f"{name}/dirichlet_vals"] = dirichlet.inhomogeneity
+        out[f"{name}/active"] = active
+        for l, c in enumerate(ctxs):
+            out[f"{name}/{l}/diag"] = c.diag
+            out[f"{name}/{l}/constrained"] = c.constrained
+            out[f"{name}/{l}/spectra"] = np.array([[s.lambda_min_hat, s.lambda_max_hat, s.fallback]
+                                                   for s in c.spectra], dtype=float)
+        rng = np.random.default_rng(12)
+        r = rng.standard_normal(n)
+        out[f"{name}/r"] = r
+        out[f"{name}/vcycle_full"] = mgsolve.vcycle(ctxs, mgsolve.PreconditionerKind.FULL, r)
+        fine = ctxs[-1]
+        mask = fine.op.mask
+        R = -model.residual(disc.finest, state, dirichlet, params, split)
+        R[mask.is_constrained] = 0.0
+        ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+        x, its = krylov.gmres(fine.op.apply,
+                              lambda v: mgsolve.vcycle(ctxs, mgsolve.PreconditionerKind.FULL, v),
+                              R, ctl)
+        out[f"{name}/gmres_rhs"] = R
+        out[f"{name}/gmres_x"] = x
+        out[f"{name}/gmres_iters"] = np.array(its)
+        print(f"  {name} (miehe): gmres {its} iterations ({time.time() - t0:.1f}s)")
+    save("multigrid_miehe", **out)
+
+
 def _ref_problem(prob):
     hier = ref_hierarchy((prob.blocks, prob.n_levels, prob.dim))
     disc = Discretization(hier)
@@ -307,7 +351,7 @@ def gen_krylov():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["meshes", "operator", "operator_band", "transfers", "multigrid", "configs", "krylov"]
+    which = sys.argv[1:] or ["meshes", "operator", "operator_band", "transfers", "multigrid", "multigrid_miehe", "configs", "krylov"]
     for w in which:
         print(w)
         globals()[f"gen_{w}"]()

@@ -45,7 +45,7 @@ def test_transfer_adjointness(name):
         assert abs(lhs - rhs) <= 1e-13 * abs(lhs)
 
 
-def _contexts(g, name):
+def _contexts(g, name, miehe=False):
     from paper_1902_08112_b200 import mgsolve
     from paper_1902_08112_b200.model import ConstraintMask, SplitKind
     disc = product_disc(name)
@@ -54,9 +54,32 @@ def _contexts(g, name):
                        g[f"{name}/U_prev2"], t[1], t[2])
     dirichlet = ConstraintMask(g[f"{name}/dirichlet"], g[f"{name}/dirichlet_vals"])
     params = product_params(disc.finest)
+    if miehe:
+        params.split_band = float(g[f"{name}/band"])
     ctxs = mgsolve.build_level_contexts(disc, st, g[f"{name}/active"], dirichlet, params,
-                                        SplitKind.NOSPLIT)
+                                        SplitKind.MIEHE if miehe else SplitKind.NOSPLIT)
     return disc, ctxs
+
+
+@pytest.mark.parametrize("name", ["lshape", "lshape3d"])
+def test_miehe_contexts_vcycle_gmres(golden, name):
+    """Miehe split through the whole solve: level diagonals and spectra, the
+    V-cycle and the GMRES iteration count vs the reference."""
+    from paper_1902_08112_b200 import krylov, mgsolve
+    g = golden["multigrid_miehe"]
+    disc, ctxs = _contexts(g, name, miehe=True)
+    for l, c in enumerate(ctxs):
+        assert np.array_equal(c.constrained, g[f"{name}/{l}/constrained"])
+        assert rel_err(c.diag, g[f"{name}/{l}/diag"]) <= 1e-12
+        sp = np.array([[s.lambda_min_hat, s.lambda_max_hat, s.fallback] for s in c.spectra])
+        assert np.allclose(sp, g[f"{name}/{l}/spectra"], rtol=1e-10, atol=0), (l, sp)
+    FULL = mgsolve.PreconditionerKind.FULL
+    assert rel_err(mgsolve.vcycle(ctxs, FULL, g[f"{name}/r"]), g[f"{name}/vcycle_full"]) <= 1e-10
+    ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+    x, its = krylov.gmres(ctxs[-1].op.apply, mgsolve.VCyclePreconditioner(ctxs, FULL),
+                          g[f"{name}/gmres_rhs"], ctl)
+    assert abs(its - int(g[f"{name}/gmres_iters"])) <= 1
+    assert rel_err(x, g[f"{name}/gmres_x"]) <= 1e-6
 
 
 MG = ["square", "lshape", "lshape3d", "cfg1"]
