@@ -135,6 +135,18 @@ int pffmg_cheb_init(const pffmg_lattice* lat, const pffmg_state* st, int which,
                     const double* x, const double* b, double* r, double* d,
                     const double* invdiag, double theta, void* stream);
 
+/* Device-coefficient forms ("_dc") of the Chebyshev entry points: the
+ * recurrence scalars are read from device memory at kernel run time
+ * (coef[0] = c_dd, coef[1] = c_dr; theta[0] = theta), so a CUDA graph that
+ * captures a V-cycle stays valid when the spectra of the next Newton step
+ * change its coefficients.  Results are bit-identical to the scalar forms. */
+int pffmg_cheb_step_dc(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                       const double* d_in, double* d_out, double* r, double* x,
+                       const double* invdiag, const double* coef, int x_add_din, void* stream);
+int pffmg_cheb_init_dc(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                       const double* x, const double* b, double* r, double* d,
+                       const double* invdiag, const double* theta, void* stream);
+
 /* ---------------------------------------------------------------- transfers */
 /* fem.py:308-411 with the V-cycle masking of mgsolve.py:228-234.
  * `coarse`/`fine` are consecutive levels l and l+1; n_comp components. */
@@ -177,6 +189,11 @@ int pffmg_cheb_init_zero(const double* b, const double* invdiag, double theta,
 /* Degenerate-range update (mgsolve.py:99): x += (inv*r)/theta. */
 int pffmg_jacobi_update(const double* r, const double* invdiag, double theta,
                         double* x, int64_t n, void* stream);
+/* Device-coefficient forms (theta read from device memory, see pffmg_cheb_step_dc). */
+int pffmg_cheb_init_zero_dc(const double* b, const double* invdiag, const double* theta,
+                            double* r, double* d, double* x, int64_t n, void* stream);
+int pffmg_jacobi_update_dc(const double* r, const double* invdiag, const double* theta,
+                           double* x, int64_t n, void* stream);
 
 /* y = a*x + y ; x = a*x ; y = x - y etc. */
 int pffmg_axpy(double a, const double* x, double* y, int64_t n, void* stream);

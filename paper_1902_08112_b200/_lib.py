@@ -52,6 +52,11 @@ _SIGS = {
                         C.c_double, C.c_double, C.c_int, vp],
     "pffmg_cheb_init": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp,
                         C.c_double, vp],
+    "pffmg_cheb_step_dc": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, vp,
+                           C.c_int, vp],
+    "pffmg_cheb_init_dc": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, vp, vp],
+    "pffmg_cheb_init_zero_dc": [vp, vp, vp, vp, vp, vp, C.c_int64, vp],
+    "pffmg_jacobi_update_dc": [vp, vp, vp, vp, C.c_int64, vp],
     "pffmg_restrict": [C.POINTER(Lattice), C.POINTER(Lattice), C.c_int, C.c_int, vp, vp, vp, vp],
     "pffmg_prolongate": [C.POINTER(Lattice), C.POINTER(Lattice), C.c_int, C.c_int, vp, vp, vp,
                          C.c_int, vp],

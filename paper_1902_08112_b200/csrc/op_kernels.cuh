@@ -36,6 +36,7 @@ struct OpArgs {
     double* __restrict__ dout;
     const double* __restrict__ inv;
     double c1, c2;                     // CHEB: c_dd, c_dr   CHEB0: theta
+    const double* __restrict__ coef;   // if set, c1/c2 are read from device memory (coef[0], coef[1])
     int x_add_din;                     // CHEB: x = (x + d_in) + d_out instead of x += d_out
     int planes_per_cta;
     int nseg;                          // 2D warp kernel: 30-column segments per row
@@ -68,7 +69,8 @@ __device__ __forceinline__ void epilogue(const OpArgs& A, int64_t vid, uint8_t f
             A.out[g] = A.b[g] - Av;                              // mgsolve.py:227
         } else if (EPI == E_CHEB) {                              // mgsolve.py:108-111
             const double rr = A.r[g] - Av;
-            const double dn = A.c1 * vin[k] + A.c2 * (A.inv[g] * rr);
+            const double c1 = A.coef ? __ldg(A.coef) : A.c1, c2 = A.coef ? __ldg(A.coef + 1) : A.c2;
+            const double dn = c1 * vin[k] + c2 * (A.inv[g] * rr);
             A.r[g] = rr;
             A.dout[g] = dn;
             const double xo = A.x[g];
@@ -76,7 +78,7 @@ __device__ __forceinline__ void epilogue(const OpArgs& A, int64_t vid, uint8_t f
         } else {                                                 // E_CHEB0: mgsolve.py:95, 105
             const double rr = A.b[g] - Av;                       // (x += d deferred to the
             A.r[g] = rr;                                         //  next step, see pffmg.h)
-            A.dout[g] = (A.inv[g] * rr) / A.c1;
+            A.dout[g] = (A.inv[g] * rr) / (A.coef ? __ldg(A.coef) : A.c1);
         }
     }
 }

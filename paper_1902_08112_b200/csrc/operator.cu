@@ -129,6 +129,40 @@ extern "C" int pffmg_cheb_step(const pffmg_lattice* lat, const pffmg_state* st, 
     return dispatch_which<E_CHEB>(A, which, as_stream(stream), "pffmg_cheb_step");
 }
 
+extern "C" int pffmg_cheb_step_dc(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                                  const double* d_in, double* d_out, double* r, double* x,
+                                  const double* invdiag, const double* coef, int x_add_din, void* stream) {
+    OpArgs A;
+    int rc = fill_args(lat, st, &A);
+    if (rc) return rc;
+    PFFMG_REQUIRE(d_in && d_out && r && x && invdiag && coef && d_in != d_out && x != d_in,
+                  "pffmg_cheb_step_dc: bad pointers");
+    A.v = d_in;
+    A.dout = d_out;
+    A.r = r;
+    A.x = x;
+    A.inv = invdiag;
+    A.coef = coef;
+    A.x_add_din = x_add_din;
+    return dispatch_which<E_CHEB>(A, which, as_stream(stream), "pffmg_cheb_step_dc");
+}
+
+extern "C" int pffmg_cheb_init_dc(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                                  const double* x, const double* b, double* r, double* d,
+                                  const double* invdiag, const double* theta, void* stream) {
+    OpArgs A;
+    int rc = fill_args(lat, st, &A);
+    if (rc) return rc;
+    PFFMG_REQUIRE(x && b && r && d && invdiag && theta && d != x && r != x, "pffmg_cheb_init_dc: bad pointers");
+    A.v = x;
+    A.b = b;
+    A.r = r;
+    A.dout = d;
+    A.inv = invdiag;
+    A.coef = theta;
+    return dispatch_which<E_CHEB0>(A, which, as_stream(stream), "pffmg_cheb_init_dc");
+}
+
 extern "C" int pffmg_cheb_init(const pffmg_lattice* lat, const pffmg_state* st, int which,
                                const double* x, const double* b, double* r, double* d,
                                const double* invdiag, double theta, void* stream) {

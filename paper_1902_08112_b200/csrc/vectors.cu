@@ -304,8 +304,9 @@ __global__ void masked_copy_k(const uint8_t* f, int64_t V, int comp0, int nc, co
 __global__ void reciprocal_k(const double* d, double* o, int64_t n) {
     GRID_STRIDE(i, n) o[i] = 1.0 / d[i];
 }
-__global__ void cheb_init_zero_k(const double* b, const double* inv, double theta, double* r, double* d,
-                                 double* x, int64_t n) {
+__global__ void cheb_init_zero_k(const double* b, const double* inv, double theta_v, const double* theta_p,
+                                 double* r, double* d, double* x, int64_t n) {
+    const double theta = theta_p ? *theta_p : theta_v;
     GRID_STRIDE(i, n) {
         const double ri = b[i];
         const double di = (inv[i] * ri) / theta;   // mgsolve.py:105
@@ -314,7 +315,9 @@ __global__ void cheb_init_zero_k(const double* b, const double* inv, double thet
         x[i] = 0.0 + di;                           // x = zeros; x += d
     }
 }
-__global__ void jacobi_update_k(const double* r, const double* inv, double theta, double* x, int64_t n) {
+__global__ void jacobi_update_k(const double* r, const double* inv, double theta_v, const double* theta_p,
+                                double* x, int64_t n) {
+    const double theta = theta_p ? *theta_p : theta_v;
     GRID_STRIDE(i, n) x[i] += (inv[i] * r[i]) / theta;   // mgsolve.py:99
 }
 __global__ void axpby_k(double a, const double* x, double b, double* y, int64_t n, int mode) {
@@ -384,14 +387,26 @@ extern "C" int pffmg_reciprocal(const double* diag, double* out, int64_t n, void
 extern "C" int pffmg_cheb_init_zero(const double* b, const double* invdiag, double theta, double* r,
                                     double* d, double* x, int64_t n, void* stream) {
     PFFMG_REQUIRE(b && invdiag && r && d && x, "pffmg_cheb_init_zero: bad args");
-    cheb_init_zero_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(b, invdiag, theta, r, d, x, n);
+    cheb_init_zero_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(b, invdiag, theta, nullptr, r, d, x, n);
     VCHECK("pffmg_cheb_init_zero");
+}
+extern "C" int pffmg_cheb_init_zero_dc(const double* b, const double* invdiag, const double* theta, double* r,
+                                       double* d, double* x, int64_t n, void* stream) {
+    PFFMG_REQUIRE(b && invdiag && theta && r && d && x, "pffmg_cheb_init_zero_dc: bad args");
+    cheb_init_zero_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(b, invdiag, 0.0, theta, r, d, x, n);
+    VCHECK("pffmg_cheb_init_zero_dc");
 }
 extern "C" int pffmg_jacobi_update(const double* r, const double* invdiag, double theta, double* x,
                                    int64_t n, void* stream) {
     PFFMG_REQUIRE(r && invdiag && x, "pffmg_jacobi_update: bad args");
-    jacobi_update_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(r, invdiag, theta, x, n);
+    jacobi_update_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(r, invdiag, theta, nullptr, x, n);
     VCHECK("pffmg_jacobi_update");
+}
+extern "C" int pffmg_jacobi_update_dc(const double* r, const double* invdiag, const double* theta, double* x,
+                                      int64_t n, void* stream) {
+    PFFMG_REQUIRE(r && invdiag && theta && x, "pffmg_jacobi_update_dc: bad args");
+    jacobi_update_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(r, invdiag, 0.0, theta, x, n);
+    VCHECK("pffmg_jacobi_update_dc");
 }
 extern "C" int pffmg_axpy(double a, const double* x, double* y, int64_t n, void* stream) {
     PFFMG_REQUIRE(x && y, "pffmg_axpy: bad args");

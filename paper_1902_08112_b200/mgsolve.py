@@ -128,7 +128,7 @@ class LevelContext:
     """Per-level solver state (mgsolve.py:116-125).  `diag` / `constrained`
     are numpy views materialised lazily; `diag_dev` / `flags` stay on the GPU."""
 
-    def __init__(self, level, op, diag, spectra, constrained, disc, flags=None):
+    def __init__(self, level, op, diag, spectra, constrained, disc, flags=None, inv=None):
         self.level = level
         self.op = op
         self.spectra = spectra
@@ -137,7 +137,12 @@ class LevelContext:
         self._constrained = constrained
         self.flags = flags
         self.diag_dev = dev(diag) if diag is not None else None
-        self.inv_dev = torch.reciprocal(self.diag_dev) if diag is not None else None
+        if inv is not None:
+            self.inv_dev = inv
+        else:
+            self.inv_dev = torch.reciprocal(self.diag_dev) if diag is not None else None
+        self._session = None     # set by _Session.build: contexts of a reusable setup
+        self._gen = 0
 
     @property
     def diag(self):
@@ -207,24 +212,38 @@ def contexts_from_operators(disc, ops, eig_iters=10, seed=0):
     return contexts
 
 
+def _fine_mask(dirichlet_mask, active_mask):
+    """fine mask = Dirichlet | active, values = Dirichlet inhomogeneity (mgsolve.py:168-171)."""
+    dir_c = dirichlet_mask.is_constrained
+    if is_tensor(dir_c) or is_tensor(active_mask):
+        return dev(dir_c, torch.bool) | dev(active_mask, torch.bool), None
+    fine_bool = np.asarray(dir_c, dtype=bool) | np.asarray(active_mask, dtype=bool)
+    return fine_bool, np.where(dir_c, dirichlet_mask.inhomogeneity, 0.0)
+
+
+# Reuse of the device setup across Newton steps (see _Session); PFFMG_REUSE_SETUP=0
+# rebuilds every buffer and re-records every graph on each call instead.
+REUSE_SETUP = os.environ.get("PFFMG_REUSE_SETUP", "1") != "0"
+
+
 def build_level_contexts(disc, state, active_mask, dirichlet_mask, params, split,
                          eig_iters=10, seed=0, threads=1):
     """Phase-field level contexts from finest-level data (mgsolve.py:154-197), on the GPU."""
     _lib.require_cuda()
     D = Discretization.wrap(disc)
+    fine_bool, fine_vals = _fine_mask(dirichlet_mask, active_mask)
+    if REUSE_SETUP:
+        sess = _Session.get(D, params, split, state.t, eig_iters, seed, threads)
+        return sess.build(disc, state, fine_bool, fine_vals)
+    return _build_fresh(disc, D, state, fine_bool, fine_vals, params, split, eig_iters, seed, threads)
+
+
+def _build_fresh(disc, D, state, fine_bool, fine_vals, params, split, eig_iters, seed, threads):
     hier = D.hierarchy
     L = hier.n_levels
     dim = hier.dim
     nc = dim + 1
     Vs = [m.n_vertices for m in hier.levels]
-    # fine mask = Dirichlet | active, values = Dirichlet inhomogeneity (mgsolve.py:168-171)
-    dir_c = dirichlet_mask.is_constrained
-    if is_tensor(dir_c) or is_tensor(active_mask):
-        fine_bool = dev(dir_c, torch.bool) | dev(active_mask, torch.bool)
-        fine_vals = None
-    else:
-        fine_bool = np.asarray(dir_c, dtype=bool) | np.asarray(active_mask, dtype=bool)
-        fine_vals = np.where(dir_c, dirichlet_mask.inhomogeneity, 0.0)
     flags = [None] * L
     flags[-1] = pack_flags(fine_bool, nc, Vs[-1])
     U = [None] * L
@@ -261,6 +280,176 @@ def build_level_contexts(disc, state, active_mask, dirichlet_mask, params, split
         spectra = tuple(lanczos_extremes(scal_host[2 * l + k], eig_iters) for k in range(2))
         contexts.append(LevelContext(l, ops[l], diags[l], spectra, None, disc, flags[l]))
     return contexts
+
+
+class _Session:
+    """Device buffers, operators and recorded graphs of one hierarchy, reused by
+    every build_level_contexts call with the same hierarchy / material / split.
+
+    A Newton loop rebuilds its level contexts once per step; only the state
+    values change, never the shapes.  The session keeps the per-level state,
+    flag, diagonal and inverse-diagonal buffers, records the whole device
+    setup (injections, diagonals, CG-Lanczos of both blocks on every level)
+    as one CUDA graph, and keeps the V-cycle graphs whose Chebyshev scalars
+    are read from device memory (libpffmg *_dc entry points), so a step costs
+    graph replays plus one host sync for the spectra.
+
+    Contexts keep the reference's value semantics: when a new build starts
+    while contexts (or operators) of the previous build are still referenced,
+    those are first detached onto private copies of their buffers."""
+
+    _cache = {}
+    MAX = 2
+
+    @classmethod
+    def get(cls, D, params, split, t, eig_iters, seed, threads):
+        from .model import _split_code
+        mf = getattr(params, "modulus_field", None)
+        key = (id(D.hierarchy), _split_code(split), float(params.mu), float(params.lam),
+               float(params.g_c), float(params.kappa), float(params.eps), float(params.pressure(t)),
+               float(getattr(params, "split_band", 0.0) or 0.0), id(mf), int(eig_iters), int(seed))
+        sess = cls._cache.get(key)
+        if sess is not None and sess.hier is D.hierarchy and sess.modulus is mf:
+            cls._cache[key] = cls._cache.pop(key)          # most recently used last
+            return sess
+        while len(cls._cache) >= cls.MAX:
+            cls._cache.pop(next(iter(cls._cache)))
+        sess = cls(D, params, split, t, eig_iters, seed, threads)
+        cls._cache[key] = sess
+        return sess
+
+    def __init__(self, D, params, split, t, eig_iters, seed, threads):
+        self.D = D
+        self.hier = D.hierarchy
+        self.modulus = getattr(params, "modulus_field", None)
+        self.params, self.split, self.threads = params, split, threads
+        self.eig_iters, self.seed = int(eig_iters), int(seed)
+        L = self.L = self.hier.n_levels
+        self.dim = self.hier.dim
+        nc = self.nc = self.dim + 1
+        Vs = self.Vs = [m.n_vertices for m in self.hier.levels]
+        self.U = [zeros(nc * V) for V in Vs]
+        self.P1 = [zeros(nc * V) for V in Vs]
+        self.P2 = [zeros(nc * V) for V in Vs]
+        self.PT = [zeros(V) for V in Vs]
+        self.flags = [flags_buffer(V) for V in Vs]
+        self.diag = [zeros(nc * V) for V in Vs]
+        self.inv = [zeros(nc * V) for V in Vs]
+        self.ops = []
+        for l in range(L):
+            st = LinearizationState(U=self.U[l], U_prev1=self.P1[l], U_prev2=self.P2[l], t=t,
+                                    t_prev1=t, t_prev2=t, phi_tilde=self.PT[l])
+            self.ops.append(PhaseFieldOperator(D.spaces[l], st, DeviceMask(self.flags[l], nc, Vs[l]),
+                                               params, split, threads, _flags=self.flags[l]))
+        self.graph = None
+        self.scal = None
+        self.use_graph = os.environ.get("PFFMG_GRAPHS", "1") != "0"
+        self.gen = 0
+        self.spectra = None
+        self._prev = []
+        self._cycles = {}
+
+    # -- device work of one setup (recorded once, replayed per Newton step)
+    def _device_setup(self):
+        D, s = self.D, _lib.stream()
+        for l in range(self.L - 2, -1, -1):                # mgsolve.py:173-186
+            D.inject_flags_dev(self.flags[l + 1], self.flags[l], l)
+            D.inject_dev(self.U[l + 1], self.U[l], l, self.nc)
+            D.inject_dev(self.P1[l + 1], self.P1[l], l, self.nc)
+            D.inject_dev(self.P2[l + 1], self.P2[l], l, self.nc)
+            D.inject_dev(self.PT[l + 1], self.PT[l], l, 1)
+        scals = []
+        for l in range(self.L):
+            self.ops[l].diagonal_dev(self.diag[l])
+            _lib.call("pffmg_reciprocal", _lib.ptr(self.diag[l]), _lib.ptr(self.inv[l]),
+                      self.diag[l].numel(), s)
+            scals += _cg_native(self.ops[l], self.diag[l], self.eig_iters, self.seed)
+        return torch.stack(scals)
+
+    def _detach_previous(self):
+        """Give still-referenced contexts / operators of the last build private buffers."""
+        prev, self._prev = self._prev, []
+        for l, op_ref, ctx_ref in prev:
+            op, ctx = op_ref(), ctx_ref()
+            if op is None and ctx is None:
+                continue
+            fl = flags_buffer(self.Vs[l])
+            fl.copy_(self.flags[l])
+            if op is not None:
+                U, P1, P2, PT = (self.U[l].clone(), self.P1[l].clone(), self.P2[l].clone(),
+                                 self.PT[l].clone())
+                op._rebind(U, PT, fl)
+                op.state = LinearizationState(U=U, U_prev1=P1, U_prev2=P2, t=op.state.t,
+                                              t_prev1=op.state.t_prev1, t_prev2=op.state.t_prev2,
+                                              phi_tilde=PT)
+            if ctx is not None:
+                d = self.diag[l].clone()
+                if ctx._diag is ctx.diag_dev:
+                    ctx._diag = d
+                ctx.diag_dev = d
+                ctx.inv_dev = self.inv[l].clone()
+                ctx.flags = fl
+                ctx._session = None
+
+    def build(self, disc, state, fine_bool, fine_vals):
+        import weakref
+        self._detach_previous()
+        L, nc = self.L, self.nc
+        for buf, src in ((self.U[-1], state.U), (self.P1[-1], state.U_prev1),
+                         (self.P2[-1], state.U_prev2), (self.PT[-1], state.phi_tilde)):
+            buf.copy_(src if is_tensor(src) else torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64)))
+        m = dev(fine_bool, torch.uint8) if not is_tensor(fine_bool) else fine_bool.to(torch.uint8).contiguous()
+        _lib.call("pffmg_pack_flags", _lib.ptr(m), nc, self.Vs[-1], _lib.ptr(self.flags[-1]), _lib.stream())
+        if not self.use_graph:
+            scal = self._device_setup()
+        elif self.graph is None:
+            scal = self._device_setup()                    # eager run: this build's results
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.scal = self._device_setup()
+            self.graph = g
+        else:
+            self.graph.replay()
+            scal = self.scal
+        scal_host = host(scal)                             # one sync for all levels
+        ei = self.eig_iters
+        self.spectra = [tuple(lanczos_extremes(scal_host[2 * l + k], ei) for k in range(2))
+                        for l in range(L)]
+        self.gen += 1
+        contexts = []
+        for l in range(L):
+            st = LinearizationState(U=self.U[l], U_prev1=self.P1[l], U_prev2=self.P2[l], t=state.t,
+                                    t_prev1=state.t_prev1, t_prev2=state.t_prev2, phi_tilde=self.PT[l])
+            mask = DeviceMask(self.flags[l], nc, self.Vs[l], fine_vals if l == L - 1 else None)
+            if l == L - 1 and not is_tensor(fine_bool):
+                mask._host = fine_bool
+            op = PhaseFieldOperator(self.D.spaces[l], st, mask, self.params, self.split, self.threads,
+                                    _flags=self.flags[l], _rho=self.ops[l]._rho)
+            ctx = LevelContext(l, op, self.diag[l], self.spectra[l], None, disc, self.flags[l],
+                               inv=self.inv[l])
+            ctx._session, ctx._gen = self, self.gen
+            contexts.append(ctx)
+            self._prev.append((l, weakref.ref(op), weakref.ref(ctx)))
+        return contexts
+
+    def owns(self, contexts):
+        return (len(contexts) == self.L and
+                all(getattr(c, "_session", None) is self and c._gen == self.gen for c in contexts))
+
+    def cycle(self, degree, target, cap):
+        """The session's V-cycle, coefficients of the current build."""
+        key = (degree, target, cap)
+        cyc = self._cycles.get(key)
+        internal = [LevelContext(l, self.ops[l], self.diag[l], self.spectra[l], None, self.D,
+                                 self.flags[l], inv=self.inv[l]) for l in range(self.L)]
+        if cyc is None:
+            cyc = _NativeCycle(internal, degree, target, cap)
+            cyc.gen = self.gen
+            self._cycles[key] = cyc
+        elif cyc.gen != self.gen:
+            cyc.set_spectra(internal)
+            cyc.gen = self.gen
+        return cyc
 
 
 # ------------------------------------------------------------- V-cycle
@@ -397,6 +586,9 @@ class _NativeCycle:
 
     @classmethod
     def get(cls, contexts, degree, target, cap):
+        sess = getattr(contexts[-1], "_session", None)
+        if sess is not None and sess.owns(contexts):
+            return sess.cycle(degree, target, cap)
         key = (tuple(id(c) for c in contexts), degree, target, cap)
         hit = cls._cache.get(key)
         if hit is not None and all(a is b for a, b in zip(hit.contexts, contexts)):
@@ -412,24 +604,61 @@ class _NativeCycle:
         self.degree = degree
         self.levels = [_Level(c) for c in contexts]
         self.disc = Discretization.wrap(contexts[-1].disc) if len(contexts) > 1 else None
-        self.smooth_prm = [[smoother_params(c.spectra[k], degree) for k in range(2)] for c in contexts]
-        self.coarse_prm = [solver_params(contexts[0].spectra[k],
-                                         chebyshev_solver_degree(contexts[0].spectra[k], target, cap))
-                           for k in range(2)]
+        self.target, self.cap = target, cap
         self.use_graph = os.environ.get("PFFMG_GRAPHS", "1") != "0"
         self.graphs = {}
         self.r_in = None
         self.x_out = None
+        self.coef = None
+        self.struct = None
+        self.set_spectra(contexts)
+
+    def set_spectra(self, contexts):
+        """Chebyshev parameters of every (level, block) smoother and of the coarse
+        solver, laid out as one device table the kernels read at run time:
+        slot = [theta, c_dd_1, c_dr_1, c_dd_2, c_dr_2, ...] (mgsolve.py:97-113).
+        Recorded graphs stay valid while the structure (degrees, degenerate
+        branches) is unchanged; otherwise they are dropped and re-recorded."""
+        self.smooth_prm = [[smoother_params(c.spectra[k], self.degree) for k in range(2)]
+                           for c in contexts]
+        self.coarse_prm = [solver_params(contexts[0].spectra[k],
+                                         chebyshev_solver_degree(contexts[0].spectra[k], self.target,
+                                                                 self.cap))
+                           for k in range(2)]
+        table, struct, self.slot = [], [], {}
+        items = [(("s", l, k), self.smooth_prm[l][k]) for l in range(len(contexts)) for k in range(2)]
+        items += [(("c", 0, k), self.coarse_prm[k]) for k in range(2)]
+        for key, prm in items:
+            theta, delta, degenerate = _cheb_coeffs(prm)
+            self.slot[key] = (len(table), prm, degenerate)
+            struct.append((key, prm.degree, degenerate))
+            table.append(theta)
+            if not degenerate:
+                sigma = theta / delta
+                rho_old = 1.0 / sigma
+                for _ in range(prm.degree - 1):
+                    rho = 1.0 / (2.0 * sigma - rho_old)
+                    table += [rho * rho_old, 2.0 * rho / delta]
+                    rho_old = rho
+        table = torch.tensor(table, dtype=torch.float64)
+        if self.coef is None or tuple(struct) != self.struct:
+            self.coef = table.to("cuda")
+            self.struct = tuple(struct)
+            self.graphs = {}
+        else:
+            self.coef.copy_(table)
 
     # one Chebyshev sweep on block k of level L: x (zero or not) -> smoothed x
-    def _cheb(self, L, k, prm, x_is_zero, pre=True):
+    def _cheb(self, L, k, slot, x_is_zero, pre=True):
         op = L.op
         b = L.blk(k)
         x, r, rhs, inv = L.x[b], L.cr[b], L.r[b], L.inv[b]
         d_in, d_out = L.d0[b], L.d1[b]
         nb = x.numel()
         s = _lib.stream()
-        theta, delta, degenerate = _cheb_coeffs(prm)
+        off, prm, degenerate = self.slot[slot]
+        coef = self.coef
+        theta = coef[off:off + 1]
         if degenerate:                                     # mgsolve.py:97-101
             if x_is_zero:
                 x.zero_()
@@ -437,37 +666,34 @@ class _NativeCycle:
             else:
                 op.residual_dev(k, x, rhs, r, pre=pre)
             for _ in range(prm.degree):
-                _lib.call("pffmg_jacobi_update", _lib.ptr(r), _lib.ptr(inv), theta, _lib.ptr(x), nb, s)
+                _lib.call("pffmg_jacobi_update_dc", _lib.ptr(r), _lib.ptr(inv), _lib.ptr(theta),
+                          _lib.ptr(x), nb, s)
                 op.residual_dev(k, x, rhs, r, pre=pre)
             return
-        sigma = theta / delta
-        rho_old = 1.0 / sigma
         if x_is_zero:                                      # r = b; d = inv r / theta; x = d
-            _lib.call("pffmg_cheb_init_zero", _lib.ptr(rhs), _lib.ptr(inv), theta, _lib.ptr(r),
-                      _lib.ptr(d_in), _lib.ptr(x), nb, s)
+            _lib.call("pffmg_cheb_init_zero_dc", _lib.ptr(rhs), _lib.ptr(inv), _lib.ptr(theta),
+                      _lib.ptr(r), _lib.ptr(d_in), _lib.ptr(x), nb, s)
             pending = False
         else:                                              # r = b - A x; d = inv r / theta
-            op.cheb_init_dev(k, x, rhs, r, d_in, inv, theta, pre=pre)
+            op.cheb_init_dc(k, x, rhs, r, d_in, inv, theta, pre=pre)
             pending = True                                 # x += d folded into the next step
-        for _ in range(prm.degree - 1):
-            rho = 1.0 / (2.0 * sigma - rho_old)
-            op.cheb_step_dev(k, d_in, d_out, r, x, inv, rho * rho_old, 2.0 * rho / delta, pending,
-                             pre=pre)
+        for i in range(prm.degree - 1):
+            c = coef[off + 1 + 2 * i: off + 3 + 2 * i]
+            op.cheb_step_dc(k, d_in, d_out, r, x, inv, c, pending, pre=pre)
             pending = False
             d_in, d_out = d_out, d_in
-            rho_old = rho
         if pending:                                        # degree 1 from a non-zero x
             _lib.call("pffmg_axpy", 1.0, _lib.ptr(d_in), _lib.ptr(x), nb, s)
 
     def _smooth(self, l, x_is_zero):
         L = self.levels[l]
         for k in range(2):
-            self._cheb(L, k, self.smooth_prm[l][k], x_is_zero)
+            self._cheb(L, k, ("s", l, k), x_is_zero)
 
     def _coarse_into_x(self, pre=True):
         L = self.levels[0]
         for k in range(2):
-            self._cheb(L, k, self.coarse_prm[k], True, pre)
+            self._cheb(L, k, ("c", 0, k), True, pre)
 
     def _cycle(self, l):                                   # mgsolve.py:221-235
         if l == 0:
@@ -484,11 +710,11 @@ class _NativeCycle:
     def _block_cycle(self, k, l):                          # mgsolve.py:238-259
         L = self.levels[l]
         if l == 0:
-            self._cheb(L, k, self.coarse_prm[k], True)
+            self._cheb(L, k, ("c", 0, k), True)
             return
         Lc = self.levels[l - 1]
         b = L.blk(k)
-        self._cheb(L, k, self.smooth_prm[l][k], True)
+        self._cheb(L, k, ("s", l, k), True)
         L.op.residual_dev(k, L.x[b], L.r[b], L.res[b], pre=True)
         ncomp = L.dim if k == 0 else 1
         comp0 = 0 if k == 0 else L.dim
@@ -496,7 +722,7 @@ class _NativeCycle:
         self._block_cycle(k, l - 1)
         self.disc.prolongate_dev(Lc.x[Lc.blk(k)], L.x[b], l - 1, ncomp, comp0, L.flags,
                                  accumulate=True)
-        self._cheb(L, k, self.smooth_prm[l][k], False)
+        self._cheb(L, k, ("s", l, k), False)
 
     def _body(self, kind):
         top = self.levels[-1]
@@ -543,13 +769,19 @@ class VCyclePreconditioner:
                  coarse_cap=30):
         self.contexts = contexts
         self.kind = _kind_value(kind)
-        self.cycle = _NativeCycle.get(contexts, degree, coarse_target, coarse_cap)
+        self._args = (degree, coarse_target, coarse_cap)
+        self.cycle = _NativeCycle.get(contexts, *self._args)
+
+    def _cycle(self):
+        # re-resolved per call: a later build_level_contexts may have detached
+        # these contexts from the reusable session (see _Session)
+        return _NativeCycle.get(self.contexts, *self._args)
 
     def __call__(self, r):
         rd = dev(r)
         out = empty(rd.numel())
-        self.cycle.run(self.kind, rd, out)
+        self._cycle().run(self.kind, rd, out)
         return like(out, r)
 
     def _pffmg_into(self, src, dst):
-        self.cycle.run(self.kind, src, dst)
+        self._cycle().run(self.kind, src, dst)

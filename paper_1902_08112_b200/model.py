@@ -133,7 +133,7 @@ def _split_code(split):
 class PhaseFieldOperator:
     """Matrix-free constrained Jacobian of one level (reference model.py:242-413)."""
 
-    def __init__(self, space, state, mask, params, split, threads=1, *, _flags=None):
+    def __init__(self, space, state, mask, params, split, threads=1, *, _flags=None, _rho=None):
         _lib.require_cuda()
         self.space = space
         self.state = state
@@ -153,7 +153,10 @@ class PhaseFieldOperator:
             raise ValueError(f"state sizes {self._U.numel()}/{self._pt.numel()} do not match "
                              f"the level ({self.nc}x{V} dofs)")
         self._flags = _flags if _flags is not None else pack_flags(mask.is_constrained, self.nc, V)
-        self._rho = self._modulus_table() if params.modulus_field is not None else None
+        if _rho is not None:
+            self._rho = _rho
+        else:
+            self._rho = self._modulus_table() if params.modulus_field is not None else None
         st = _lib.State()
         st.mu, st.lam, st.g_c = float(params.mu), float(params.lam), float(params.g_c)
         st.kappa, st.eps = float(params.kappa), float(params.eps)
@@ -174,6 +177,17 @@ class PhaseFieldOperator:
         st_pre.hints = 1
         self._st_pre = st_pre
         self._stp_pre = ctypes.byref(st_pre)
+
+    def _rebind(self, U, phi_tilde, flags):
+        """Point the operator at other device buffers of the same sizes (used
+        to detach an earlier generation of solver contexts, mgsolve._Session)."""
+        self._U, self._pt, self._flags = U, phi_tilde, flags
+        for st in (self._st, self._st_pre):
+            st.U = U.data_ptr()
+            st.phi_tilde = phi_tilde.data_ptr()
+            st.flags = flags.data_ptr()
+        if isinstance(self.mask, DeviceMask):
+            self.mask.flags = flags
 
     # -- reference surface --------------------------------------------------
     @property
@@ -245,6 +259,16 @@ class PhaseFieldOperator:
     def cheb_init_dev(self, which, x, b, r, d, inv, theta, pre=False):
         _lib.call("pffmg_cheb_init", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
                   _lib.ptr(r), _lib.ptr(d), _lib.ptr(inv), theta, _lib.stream())
+
+    # device-coefficient forms: scalars read from `coef` (a CUDA tensor view) at run time
+    def cheb_step_dc(self, which, d_in, d_out, r, x, inv, coef, x_add_din=False, pre=False):
+        _lib.call("pffmg_cheb_step_dc", self.lat.ref, self._sp(pre), which, _lib.ptr(d_in),
+                  _lib.ptr(d_out), _lib.ptr(r), _lib.ptr(x), _lib.ptr(inv), _lib.ptr(coef),
+                  int(x_add_din), _lib.stream())
+
+    def cheb_init_dc(self, which, x, b, r, d, inv, theta, pre=False):
+        _lib.call("pffmg_cheb_init_dc", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
+                  _lib.ptr(r), _lib.ptr(d), _lib.ptr(inv), _lib.ptr(theta), _lib.stream())
 
     # -- helpers ---------------------------------------------------------------
     def _modulus_table(self):

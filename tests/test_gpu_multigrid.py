@@ -189,3 +189,54 @@ def test_generic_vcycle_on_model_problem(golden):
            + 0.5 * mgsolve.vcycle(ctxs, mgsolve.PreconditionerKind.FULL, r2))
     assert rel_err(lhs, rhs) <= 1e-12
     assert np.all(lhs[ctxs[-1].constrained] == 0.0)
+
+
+def test_setup_reuse_across_newton_steps(golden, monkeypatch):
+    """Reusable setup (mgsolve._Session): a second build on the same hierarchy
+    with a different state replays the recorded graphs and gives bit-identical
+    results to a from-scratch build; contexts of the first build stay valid
+    (detached onto private buffers) and keep giving their own results."""
+    from paper_1902_08112_b200 import krylov, mgsolve
+    from paper_1902_08112_b200.model import ConstraintMask, SplitKind
+    g = golden["multigrid"]
+    name = "cfg1"
+    disc = product_disc(name)
+    t = g[f"{name}/times"]
+    dirichlet = ConstraintMask(g[f"{name}/dirichlet"], g[f"{name}/dirichlet_vals"])
+    params = product_params(disc.finest)
+    rng = np.random.default_rng(4)
+    U2 = g[f"{name}/U"] + 1e-3 * rng.standard_normal(g[f"{name}/U"].size)
+    states = [product_state(U, g[f"{name}/phi_tilde"], t[0], g[f"{name}/U_prev1"],
+                            g[f"{name}/U_prev2"], t[1], t[2]) for U in (g[f"{name}/U"], U2)]
+    r = torch.as_tensor(g[f"{name}/r"], device="cuda")
+    FULL = mgsolve.PreconditionerKind.FULL
+
+    def build(st):
+        return mgsolve.build_level_contexts(disc, st, g[f"{name}/active"], dirichlet, params,
+                                            SplitKind.NOSPLIT)
+
+    monkeypatch.setattr(mgsolve, "REUSE_SETUP", False)
+    fresh = []
+    for st in states:
+        c = build(st)
+        fresh.append((mgsolve.vcycle(c, FULL, r), [cc.spectra for cc in c], c[-1].op.apply(r)))
+    monkeypatch.setattr(mgsolve, "REUSE_SETUP", True)
+    mgsolve._Session._cache.clear()
+    c1 = build(states[0])
+    v1 = mgsolve.vcycle(c1, FULL, r)
+    c2 = build(states[1])                     # same session: replay, c1 detached
+    assert c2[-1]._session is not None and c1[-1]._session is None
+    v2 = mgsolve.vcycle(c2, FULL, r)
+    assert torch.equal(v1, fresh[0][0]) and torch.equal(v2, fresh[1][0])
+    assert [cc.spectra for cc in c2] == fresh[1][1]
+    assert torch.equal(c2[-1].op.apply(r), fresh[1][2])
+    # detached first-build contexts still see the first state
+    assert torch.equal(mgsolve.vcycle(c1, FULL, r), fresh[0][0])
+    assert torch.equal(c1[-1].op.apply(r), fresh[0][2])
+    # a third build (back to state 0) replays again and matches
+    c3 = build(states[0])
+    assert torch.equal(mgsolve.vcycle(c3, FULL, r), fresh[0][0])
+    ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+    x, its = krylov.gmres(c3[-1].op.apply, mgsolve.VCyclePreconditioner(c3, FULL),
+                          g[f"{name}/gmres_rhs"], ctl)
+    assert abs(its - int(g[f"{name}/gmres_iters"])) <= 1
