@@ -42,7 +42,12 @@ int launch2d(const OpArgs& A0, bool iso, cudaStream_t s) {
     // strips of H vertex rows: aim for ~24 resident warps per SM in one wave,
     // H in [4, 64] (the first cell row of a strip is recomputed: overhead 1/H)
     int64_t per = ((int64_t)rows * nseg + 24LL * sms - 1) / (24LL * sms);
-    per = per < 4 ? 4 : (per > 64 ? 64 : per);
+    // (small levels: short strips -- their kernels are latency-, not work-bound)
+    static const int minrows = [] {
+        const char* e = getenv("PFFMG_2D_MINROWS");
+        return e ? atoi(e) : 1;
+    }();
+    per = per < minrows ? minrows : (per > 64 ? 64 : per);
     static const int forced = [] {
         const char* e = getenv("PFFMG_2D_ROWS");
         return e ? atoi(e) : 0;

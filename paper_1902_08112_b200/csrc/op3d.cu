@@ -43,7 +43,11 @@ static int launch_stream(const OpArgs& A0, cudaStream_t s) {
     const int planes = L.own_hi - L.own_lo;
     // ~2 CTAs of work per SM per wave, strips of 4..32 planes
     int64_t per = ((int64_t)planes * gx * gy + 2LL * sms - 1) / (2LL * sms);
-    per = per < 4 ? 4 : (per > 32 ? 32 : per);
+    static const int minp = [] {
+        const char* e = getenv("PFFMG_3D_MINPLANES");
+        return e ? atoi(e) : 1;
+    }();
+    per = per < minp ? minp : (per > 32 ? 32 : per);
     static const int forced = [] {
         const char* e = getenv("PFFMG_3D_PLANES");
         return e ? atoi(e) : 0;

@@ -57,20 +57,27 @@ __global__ void restrict_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const doub
         if (cid < 0) continue;
         const uint8_t fl = cflags ? cflags[cid] : 0;
         const int zlo = Lc.dim == 3 ? -1 : 0, zhi = Lc.dim == 3 ? 1 : 0;
-        for (int k = 0; k < ncomp; ++k) {
-            double acc = 0.0;
-            for (int c = zlo; c <= zhi; ++c)
-                for (int b = -1; b <= 1; ++b)
-                    for (int a = -1; a <= 1; ++a) {
-                        int fx, fy, fz;
-                        fine_of(Lc, Lf, x, y, z, a, b, c, fx, fy, fz);
-                        const int64_t fid = vertex_id(Lf, fx, fy, fz);
-                        if (fid < 0) continue;
-                        const double w = (a ? 0.5 : 1.0) * (b ? 0.5 : 1.0) * (c ? 0.5 : 1.0);
-                        acc += w * vf[(int64_t)k * Lf.V + fid];
-                    }
-            if ((fl >> (comp0 + k)) & 1) acc = 0.0;
-            vc[(int64_t)k * Lc.V + cid] = acc;
+        // fine neighbours in increasing id order (the CSR product order); each
+        // neighbour's id is looked up once for all components
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int c = zlo; c <= zhi; ++c)
+#pragma unroll
+            for (int b = -1; b <= 1; ++b)
+#pragma unroll
+                for (int a = -1; a <= 1; ++a) {
+                    int fx, fy, fz;
+                    fine_of(Lc, Lf, x, y, z, a, b, c, fx, fy, fz);
+                    const int64_t fid = vertex_id(Lf, fx, fy, fz);
+                    if (fid < 0) continue;
+                    const double w = (a ? 0.5 : 1.0) * (b ? 0.5 : 1.0) * (c ? 0.5 : 1.0);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (k < ncomp) acc[k] += w * __ldg(vf + (int64_t)k * Lf.V + fid);
+                }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k >= ncomp) break;
+            vc[(int64_t)k * Lc.V + cid] = ((fl >> (comp0 + k)) & 1) ? 0.0 : acc[k];
         }
     }
 }
