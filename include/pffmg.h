@@ -147,6 +147,17 @@ int pffmg_cheb_init_dc(const pffmg_lattice* lat, const pffmg_state* st, int whic
                        const double* x, const double* b, double* r, double* d,
                        const double* invdiag, const double* theta, void* stream);
 
+/* pffmg_apply with HOST v / out (pinned for overlap): the copies in, the
+ * stencil and the copies out are pipelined over n_strips strips of planes of
+ * the last axis on two internal copy streams.  d_v / d_out are device scratch
+ * vectors of the block's size.  When the call returns the work is enqueued on
+ * `stream`; synchronise it before reading h_out.  h_plane_off (n_planes + 1
+ * host entries: first vertex id of every plane, then V) is required for
+ * non-box lattices, NULL for boxes.  Whole (non-slab) lattices only. */
+int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                     const double* h_v, double* h_out, double* d_v, double* d_out,
+                     const int64_t* h_plane_off, int n_strips, void* stream);
+
 /* ---------------------------------------------------------------- transfers */
 /* fem.py:308-411 with the V-cycle masking of mgsolve.py:228-234.
  * `coarse`/`fine` are consecutive levels l and l+1; n_comp components. */

@@ -76,6 +76,100 @@ extern "C" int pffmg_apply(const pffmg_lattice* lat, const pffmg_state* st, int 
     return dispatch_which<E_STORE>(A, which, as_stream(stream), "pffmg_apply");
 }
 
+// Host-buffer form of pffmg_apply: the H2D copy of v, the stencil and the D2H
+// copy of the result are overlapped plane strip by plane strip (strip i's
+// kernel needs planes [P_i - 1, P_{i+1}] of v, so it waits for the copies of
+// strips i and i+1; its output strip goes back while strip i+1 computes).
+namespace pffmg {
+namespace {
+struct PipeRes {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev[2 * 64 + 2] = {};
+    bool ok = false;
+};
+PipeRes& pipe_res() {
+    static thread_local PipeRes R;
+    if (!R.ok) {
+        bool good = cudaStreamCreateWithFlags(&R.h2d, cudaStreamNonBlocking) == cudaSuccess &&
+                    cudaStreamCreateWithFlags(&R.d2h, cudaStreamNonBlocking) == cudaSuccess;
+        for (auto& e : R.ev) good = good && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+        R.ok = good;
+    }
+    return R;
+}
+}  // namespace
+}  // namespace pffmg
+
+extern "C" int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                                const double* h_v, double* h_out, double* d_v, double* d_out,
+                                const int64_t* h_plane_off, int n_strips, void* stream) {
+    PFFMG_REQUIRE(lat && st && h_v && h_out && d_v && d_out && d_v != d_out, "pffmg_apply_host: bad pointers");
+    PFFMG_REQUIRE(which == PFFMG_FULL || which == PFFMG_UBLOCK || which == PFFMG_PBLOCK,
+                  "pffmg_apply_host: bad which %d", which);
+    const int nplanes = (lat->dim == 3 ? lat->nz : lat->ny) + 1;
+    PFFMG_REQUIRE(lat->own_lo == 0 && (lat->own_hi == 0 || lat->own_hi == nplanes),
+                  "pffmg_apply_host: needs a whole (non-slab) lattice");
+    PFFMG_REQUIRE(lat->vrow_off == nullptr || h_plane_off != nullptr,
+                  "pffmg_apply_host: non-box lattices need host plane offsets");
+    if (n_strips == 0) {   // zero-copy: the stencil reads v from / writes out to mapped host memory
+        void *dv = nullptr, *dout = nullptr;
+        if (cudaHostGetDevicePointer(&dv, const_cast<double*>(h_v), 0) != cudaSuccess ||
+            cudaHostGetDevicePointer(&dout, h_out, 0) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("pffmg_apply_host: zero-copy needs page-locked (pinned) host buffers");
+            return PFFMG_ERR_ARG;
+        }
+        return pffmg_apply(lat, st, which, static_cast<const double*>(dv), static_cast<double*>(dout), stream);
+    }
+    int K = n_strips < 1 ? 1 : (n_strips > 64 ? 64 : n_strips);
+    if (K > nplanes) K = nplanes;
+    PipeRes& R = pipe_res();
+    if (!R.ok) {
+        set_error("pffmg_apply_host: could not create copy streams/events");
+        return PFFMG_ERR_CUDA;
+    }
+    const cudaStream_t s = as_stream(stream);
+    const int64_t V = lat->n_vertices;
+    const int nc = which == PFFMG_FULL ? lat->dim + 1 : (which == PFFMG_UBLOCK ? lat->dim : 1);
+    const int64_t per_plane = lat->dim == 3 ? (int64_t)(lat->nx + 1) * (lat->ny + 1) : (int64_t)(lat->nx + 1);
+    auto off = [&](int p) -> int64_t { return h_plane_off ? h_plane_off[p] : (int64_t)p * per_plane; };
+    auto bound = [&](int i) -> int { return (int)(((int64_t)nplanes * i) / K); };
+    const size_t pitch = (size_t)V * sizeof(double);
+    cudaEvent_t* ein = R.ev;          // [K]
+    cudaEvent_t* ek = R.ev + 64;      // [K]
+    cudaEvent_t e0 = R.ev[128], edone = R.ev[129];
+    cudaEventRecord(e0, s);           // d_v / d_out free once prior work on `stream` is done
+    cudaStreamWaitEvent(R.h2d, e0, 0);
+    cudaStreamWaitEvent(R.d2h, e0, 0);
+    // (copies of a few MiB: much smaller ones serialise the two directions on this link)
+    for (int i = 0; i < K; ++i) {
+        const int64_t a = off(bound(i)), b = off(bound(i + 1));
+        if (b > a)
+            cudaMemcpy2DAsync(d_v + a, pitch, h_v + a, pitch, (size_t)(b - a) * sizeof(double), nc,
+                              cudaMemcpyHostToDevice, R.h2d);
+        cudaEventRecord(ein[i], R.h2d);
+    }
+    pffmg_lattice sub = *lat;
+    for (int i = 0; i < K; ++i) {
+        cudaStreamWaitEvent(s, ein[i + 1 < K ? i + 1 : K - 1], 0);
+        sub.own_lo = bound(i);
+        sub.own_hi = bound(i + 1);
+        if (sub.own_hi > sub.own_lo) {
+            const int rc = pffmg_apply(&sub, st, which, d_v, d_out, stream);
+            if (rc) return rc;
+        }
+        cudaEventRecord(ek[i], s);
+        cudaStreamWaitEvent(R.d2h, ek[i], 0);
+        const int64_t a = off(bound(i)), b = off(bound(i + 1));
+        if (b > a)
+            cudaMemcpy2DAsync(h_out + a, pitch, d_out + a, pitch, (size_t)(b - a) * sizeof(double), nc,
+                              cudaMemcpyDeviceToHost, R.d2h);
+    }
+    cudaEventRecord(edone, R.d2h);
+    cudaStreamWaitEvent(s, edone, 0);  // the caller's stream orders after the last copy
+    return check_launch("pffmg_apply_host");
+}
+
 extern "C" int pffmg_residual(const pffmg_lattice* lat, const pffmg_state* st, int which,
                               const double* x, const double* b, double* out, void* stream) {
     OpArgs A;

@@ -289,6 +289,9 @@ class DeviceLattice:
         L.plane0 = int(getattr(info, "plane_lo", 0))
         self.struct = L
         self.ref = C.byref(L)
+        # host plane offsets for pffmg_apply_host (NULL = box numbering)
+        self.plane_off_host = (None if info.rows is None
+                               else np.ascontiguousarray(info.plane_offsets(), dtype=np.int64))
 
     @property
     def n_lattice_cells(self):

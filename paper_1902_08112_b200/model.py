@@ -205,7 +205,10 @@ class PhaseFieldOperator:
 
     def apply(self, v, out=None):
         """G~ v with constrained rows = identity (model.py:368-375).  `out`
-        (optional, not in the reference signature) receives the result."""
+        (optional, not in the reference signature) receives the result.
+        Pinned host tensors take the pipelined host path (pffmg_apply_host)."""
+        if _pinned_f64(v) and (out is None or _pinned_f64(out)) and self.lat.info.own == (0, 0):
+            return self._apply_host(v, out)
         x = dev(v)
         if x.numel() != self.n_dofs:
             raise ValueError(f"expected {self.n_dofs} dofs, got {x.numel()}")
@@ -214,6 +217,23 @@ class PhaseFieldOperator:
         if y is out:
             return out
         return like(y, v, out)
+
+    def _apply_host(self, v, out):
+        n = self.n_dofs
+        if v.numel() != n or (out is not None and out.numel() != n):
+            raise ValueError(f"expected {n} dofs, got {v.numel()}")
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        bufs = getattr(self, "_host_bufs", None)
+        if bufs is None:
+            bufs = self._host_bufs = (empty(n), empty(n))
+        po = self.lat.plane_off_host
+        strips = int(max(1, min(8, round(8 * n / (6 << 20)))))  # ~6 MiB per strip and direction
+        _lib.call("pffmg_apply_host", self.lat.ref, self._stp, _lib.FULL, C_ptr(v), C_ptr(out),
+                  _lib.ptr(bufs[0]), _lib.ptr(bufs[1]), None if po is None else po.ctypes.data,
+                  strips, _lib.stream())
+        torch.cuda.current_stream().synchronize()
+        return out
 
     def apply_block(self, which, v_block):
         """Diagonal block action, 0 = displacement, 1 = phase field (model.py:377-392)."""
@@ -286,6 +306,16 @@ class PhaseFieldOperator:
             coords = _lattice_qp_coords(space.mesh)
             table = np.asarray(self.params.modulus_field(coords), dtype=float).reshape(ncell_lat, Q)
         return dev(table.ravel())
+
+
+def _pinned_f64(t):
+    return (is_tensor(t) and not t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+            and t.is_pinned())
+
+
+def C_ptr(t):
+    import ctypes
+    return ctypes.c_void_p(t.data_ptr())
 
 
 def _lattice_qp_coords(mesh):

@@ -179,3 +179,27 @@ def test_semilinear_residual_matches_reference(golden, name, variant):
     assert isinstance(out, np.ndarray)
     assert rel_err(out, g[f"{tag}/residual"]) <= TOL
     assert np.all(out[flags] == 0.0)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "lshape", "lprism", "cube"])
+def test_pinned_host_apply_pipeline_is_exact(golden, name):
+    """pffmg_apply_host (H2D / stencil / D2H overlapped by plane strips) gives
+    bit-identical results to the device apply for any strip count."""
+    import ctypes
+    from paper_1902_08112_b200 import _lib
+    g = golden["operator"]
+    op, tag = _op(g, name, "masked")
+    v = torch.as_tensor(g[f"{tag}/v"]).pin_memory()
+    ref = op.apply(v.cuda()).cpu()
+    assert torch.equal(op.apply(v), ref)                          # public path
+    out = torch.empty_like(v).pin_memory()
+    assert op.apply(v, out=out) is out and torch.equal(out, ref)
+    d_in, d_out = torch.empty_like(ref).cuda(), torch.empty_like(ref).cuda()
+    po = op.lat.plane_off_host
+    for strips in (1, 2, 3, 7, 64):
+        out.zero_()
+        _lib.call("pffmg_apply_host", op.lat.ref, op._stp, _lib.FULL, ctypes.c_void_p(v.data_ptr()),
+                  ctypes.c_void_p(out.data_ptr()), _lib.ptr(d_in), _lib.ptr(d_out),
+                  None if po is None else po.ctypes.data, strips, _lib.stream())
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), strips
