@@ -158,6 +158,13 @@ int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st, int which,
                      const double* h_v, double* h_out, double* d_v, double* d_out,
                      const int64_t* h_plane_off, int n_strips, void* stream);
 
+/* Quantities of interest (model.py:472-506) as one deterministic cell-integral
+ * reduction into the device scalar *result: kind 0 = crack_energy (uses eps,
+ * g_c), 1 = bulk_energy (split, band, modulus field, pressure; U's own phi
+ * degrades), 2 = fracture_volume.  st->U is the full (dim+1)*V state. */
+int pffmg_qoi(const pffmg_lattice* lat, const pffmg_state* st, int kind, double* result,
+              void* stream);
+
 /* ---------------------------------------------------------------- transfers */
 /* fem.py:308-411 with the V-cycle masking of mgsolve.py:228-234.
  * `coarse`/`fine` are consecutive levels l and l+1; n_comp components. */

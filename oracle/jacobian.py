@@ -8,6 +8,7 @@ Restates reference model.py:
     block and full local kernels (325-355), chunked threading (237-239, 357-364),
     apply / apply_block / diagonal (368-413)
   * residual (model.py:420-460) -- the Newton right-hand side
+  * quantities of interest crack_energy, bulk_energy, fracture_volume (model.py:472-504)
 """
 from __future__ import annotations
 
@@ -291,3 +292,34 @@ def residual(tables, state, constrained, material, split=NOSPLIT):
     out = sp_.scatter(np.concatenate([out_u, out_phi[:, None, :]], axis=1))
     out[np.asarray(constrained, dtype=bool)] = 0.0
     return out
+
+
+def crack_energy(tables, U, material):
+    """model.py:472-480."""
+    loc_phi = tables.gather(U)[:, tables.dim]
+    phi_q = tables.at_qp(loc_phi)
+    g = tables.grad_at_qp(loc_phi)
+    dens = np.square(1.0 - phi_q) / material.eps + material.eps * np.einsum("cqj,cqj->cq", g, g)
+    return 0.5 * material.g_c * float(np.einsum("q,cq->", tables.JxW, dens))
+
+
+def bulk_energy(tables, state, material, split=NOSPLIT):
+    """model.py:483-497 (U's own phase field degrades)."""
+    dim = tables.dim
+    loc = tables.gather(state.U)
+    gu = tables.vec_grad_at_qp(loc[:, :dim])
+    e = 0.5 * (gu + np.swapaxes(gu, -1, -2))
+    div = np.trace(gu, axis1=-2, axis2=-1)
+    phi_q = tables.at_qp(loc[:, dim])
+    rho = (np.asarray(material.modulus_field(tables.qp_coords), dtype=float)
+           if material.modulus_field is not None else np.ones_like(phi_q))
+    Ep, Em, _, _, _ = split_quantities(e, split, material.lam, material.mu, band=material.split_band)
+    dens = (degradation(phi_q, material.kappa) * rho * Ep + rho * Em
+            + np.square(phi_q) * material.pressure(state.t) * div)
+    return float(np.einsum("q,cq->", tables.JxW, dens))
+
+
+def fracture_volume(tables, U):
+    """model.py:500-504."""
+    phi_q = tables.at_qp(tables.gather(U)[:, tables.dim])
+    return float(np.einsum("q,cq->", tables.JxW, 1.0 - phi_q))

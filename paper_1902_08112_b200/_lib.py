@@ -53,6 +53,7 @@ _SIGS = {
     "pffmg_cheb_init": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp,
                         C.c_double, vp],
     "pffmg_apply_host": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, C.c_int, vp],
+    "pffmg_qoi": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp],
     "pffmg_cheb_step_dc": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, vp,
                            C.c_int, vp],
     "pffmg_cheb_init_dc": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, vp, vp],

@@ -102,6 +102,7 @@ int make_consts(const pffmg_lattice* lat, const pffmg_state* st, Consts* K) {
     K->gc_over_eps = st->g_c / st->eps;
     K->k_phi = st->g_c * st->eps;
     K->band = st->split_band;
+    K->eps = st->eps;
     return PFFMG_OK;
 }
 

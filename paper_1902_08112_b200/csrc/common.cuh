@@ -78,6 +78,7 @@ struct Consts {
     double jxw;           // quadrature weight * cell volume (identical for all QPs)
     double mu, lam, kappa, omk, two_p, gc_over_eps, k_phi;
     double band;          // C^1 blend half-width of the spectral split (0 = hard)
+    double eps;           // regularisation length (QoIs)
 };
 
 int make_consts(const pffmg_lattice* lat, const pffmg_state* st, Consts* K);

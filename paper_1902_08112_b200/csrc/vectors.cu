@@ -10,7 +10,7 @@
 // flags) stay in device memory so no host round trip is needed between steps.
 #include <cmath>
 
-#include "common.cuh"
+#include "cellops_miehe.cuh"
 
 namespace pffmg {
 
@@ -433,6 +433,142 @@ extern "C" int pffmg_sub(const double* x, const double* y, double* out, int64_t 
     sub_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(x, y, out, n);
     VCHECK("pffmg_sub");
 }
+// ------------------------------------------------------------ QoIs
+// Cell integrals of reference model.py:472-506 (crack_energy, bulk_energy,
+// fracture_volume): one thread per lattice cell, 2^D Gauss points, the same
+// deterministic block/last-block reduction as the dots.
+
+// value and physical gradient of a Q1 field at QP q
+template <int D>
+__device__ __forceinline__ void q1_eval(const double (&c)[1 << D], int q, const Consts& K, double& val,
+                                        double (&g)[D]) {
+    val = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) g[a] = 0.0;
+#pragma unroll
+    for (int n = 0; n < (1 << D); ++n) {
+        double B[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) B[a] = q1_shape(K, n, q, a);
+        double N = 1.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) N *= B[a];
+        val = fma(N, c[n], val);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            double t = ((n >> a) & 1) ? K.ih[a] : -K.ih[a];
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+                if (b != a) t *= B[b];
+            g[a] = fma(t, c[n], g[a]);
+        }
+    }
+}
+
+template <int D>
+struct QoiOp {
+    static constexpr bool REDUCES = true;
+    Lat L;
+    Consts K;
+    const double* U;
+    const double* rho;
+    int kind;      // 0 crack energy, 1 bulk energy, 2 fracture volume
+    int split;
+    double scale;
+    double* result;
+    __device__ bool skip() const { return false; }
+    __device__ void prepare() {}
+    __device__ void elem(int64_t i, double& a0, double&) const {
+        constexpr int NP = 1 << D;
+        const int cx = (int)(i % L.nx);
+        const int64_t t = i / L.nx;
+        const int cy = D == 3 ? (int)(t % L.ny) : (int)t;
+        const int cz = D == 3 ? (int)(t / L.ny) : 0;
+        if (!cell_exists<D>(L, cx, cy, cz)) return;
+        double c[D + 1][NP];
+#pragma unroll
+        for (int n = 0; n < NP; ++n) {
+            const int64_t vid = vertex_id(L, cx + (n & 1), cy + ((n >> 1) & 1), D == 3 ? cz + ((n >> 2) & 1) : 0);
+#pragma unroll
+            for (int k = 0; k <= D; ++k) c[k][n] = U[(int64_t)k * L.V + vid];
+        }
+        double sum = 0.0;
+        for (int q = 0; q < NP; ++q) {
+            double phi, gphi[D];
+            q1_eval<D>(c[D], q, K, phi, gphi);
+            double dens;
+            if (kind == 2) {                                    // model.py:500-504
+                dens = 1.0 - phi;
+            } else if (kind == 0) {                             // model.py:472-480
+                double gg = 0.0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) gg = fma(gphi[a], gphi[a], gg);
+                dens = (1.0 - phi) * (1.0 - phi) / K.eps + K.eps * gg;
+            } else {                                            // model.py:483-497
+                double gu[D][D], v;
+#pragma unroll
+                for (int k = 0; k < D; ++k) q1_eval<D>(c[k], q, K, v, gu[k]);
+                double div = 0.0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) div += gu[a][a];
+                double Ep, Em;
+                if (split == 0) {
+                    double ee = 0.0;
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int b = 0; b < D; ++b) {
+                            const double e = 0.5 * (gu[a][b] + gu[b][a]);
+                            ee = fma(e, e, ee);
+                        }
+                    Ep = 0.5 * K.lam * div * div + K.mu * ee;
+                    Em = 0.0;
+                } else if (D == 2) {
+                    Spec2 S;
+                    spectral2(gu[0][0], 0.5 * (gu[0][1] + gu[1][0]), gu[D - 1][D - 1], K, S);
+                    Ep = S.Ep;
+                    Em = S.Em;
+                } else {
+                    const double e6[6] = {gu[0][0], gu[1 % D][1 % D], gu[D - 1][D - 1],
+                                          0.5 * (gu[0][1 % D] + gu[1 % D][0]),
+                                          0.5 * (gu[0][D - 1] + gu[D - 1][0]),
+                                          0.5 * (gu[1 % D][D - 1] + gu[D - 1][1 % D])};
+                    Spec3 S;
+                    spectral3(e6, K, S);
+                    const double Es = 0.5 * K.lam * S.tr * S.tr +
+                                      K.mu * (S.w[0] * S.w[0] + S.w[1] * S.w[1] + S.w[2] * S.w[2]);
+                    Ep = S.Ep;
+                    Em = Es - S.Ep;
+                }
+                const double r = rho ? rho[i * NP + q] : 1.0;
+                const double g = K.omk * (phi * phi) + K.kappa;
+                dens = g * r * Ep + r * Em + phi * phi * (0.5 * K.two_p) * div;
+            }
+            sum = fma(K.jxw, dens, sum);
+        }
+        a0 += sum;
+    }
+    __device__ void finish(double s0, double) const { *result = scale * s0; }
+};
+
+extern "C" int pffmg_qoi(const pffmg_lattice* lat, const pffmg_state* st, int kind, double* result,
+                         void* stream) {
+    PFFMG_REQUIRE(lat && st && st->U && result && kind >= 0 && kind <= 2, "pffmg_qoi: bad args");
+    PFFMG_REQUIRE(st->split == 0 || st->split == 1, "pffmg_qoi: unknown split %d", st->split);
+    Lat L;
+    Consts K;
+    int rc = make_lat(lat, &L);
+    if (rc) return rc;
+    rc = make_consts(lat, st, &K);
+    if (rc) return rc;
+    const int64_t ncell = (int64_t)L.nx * L.ny * (L.dim == 3 ? L.nz : 1);
+    const double scale = kind == 0 ? 0.5 * st->g_c : 1.0;
+    const cudaStream_t s = as_stream(stream);
+    if (L.dim == 2)
+        return run_fused(QoiOp<2>{L, K, st->U, st->rho, kind, st->split, scale, result}, ncell, s, "pffmg_qoi");
+    return run_fused(QoiOp<3>{L, K, st->U, st->rho, kind, st->split, scale, result}, ncell, s, "pffmg_qoi");
+}
+
 extern "C" int pffmg_dot(const double* x, const double* y, int64_t n, double* result, void* stream) {
     PFFMG_REQUIRE(x && y && result && n >= 0, "pffmg_dot: bad args");
     return run_fused(DotOp{x, y, nullptr, result}, n, as_stream(stream), "pffmg_dot");

@@ -28,7 +28,8 @@ from .arrays import dev, empty, host, is_tensor, like, pack_flags, unpack_flags
 from .lattice import LatticeMesh, device_lattice
 
 __all__ = ["SplitKind", "MaterialParams", "LinearizationState", "ConstraintMask", "residual",
-           "PhaseFieldOperator", "extrapolate", "degradation", "jacobian_vmult", "diagonal"]
+           "PhaseFieldOperator", "extrapolate", "degradation", "jacobian_vmult", "diagonal",
+           "crack_energy", "bulk_energy", "fracture_volume"]
 
 
 class SplitKind(Enum):
@@ -292,20 +293,23 @@ class PhaseFieldOperator:
 
     # -- helpers ---------------------------------------------------------------
     def _modulus_table(self):
-        """rho(x_q) per lattice cell and QP (model.py:284-287)."""
-        info = self.lat.info
-        Q = 2 ** self.dim
-        ncell_lat = int(np.prod(info.ncell))
-        table = np.ones((ncell_lat, Q))
-        space = self.space
-        coords = getattr(space, "qp_coords", None)
-        if coords is not None and info.cell_perm is not None:
-            rho = np.asarray(self.params.modulus_field(coords), dtype=float)
-            table[info.cell_perm] = rho
-        else:
-            coords = _lattice_qp_coords(space.mesh)
-            table = np.asarray(self.params.modulus_field(coords), dtype=float).reshape(ncell_lat, Q)
-        return dev(table.ravel())
+        return _modulus_table(self.space, self.lat, self.params)
+
+
+def _modulus_table(space, lat, params):
+    """rho(x_q) per lattice cell and QP (model.py:284-287)."""
+    info = lat.info
+    Q = 2 ** lat.dim
+    ncell_lat = int(np.prod(info.ncell))
+    table = np.ones((ncell_lat, Q))
+    coords = getattr(space, "qp_coords", None)
+    if coords is not None and info.cell_perm is not None:
+        rho = np.asarray(params.modulus_field(coords), dtype=float)
+        table[info.cell_perm] = rho
+    else:
+        coords = _lattice_qp_coords(space.mesh)
+        table = np.asarray(params.modulus_field(coords), dtype=float).reshape(ncell_lat, Q)
+    return dev(table.ravel())
 
 
 def _pinned_f64(t):
@@ -345,3 +349,45 @@ def jacobian_vmult(space, state, mask, params, split, v, threads=1):
 
 def diagonal(space, state, mask, params, split, threads=1):
     return PhaseFieldOperator(space, state, mask, params, split, threads).diagonal()
+
+
+# ------------------------------------------------------------------ QoIs
+
+def _qoi(space, U, params, split, t, kind):
+    """One deterministic device reduction (libpffmg pffmg_qoi) -> float."""
+    import ctypes
+    _lib.require_cuda()
+    lat = device_lattice(space.mesh)
+    Ud = dev(U)
+    if Ud.numel() != (lat.dim + 1) * lat.n_vertices:
+        raise ValueError(f"U has {Ud.numel()} entries, expected {(lat.dim + 1) * lat.n_vertices}")
+    st = _lib.State()
+    st.mu, st.lam, st.g_c = float(params.mu), float(params.lam), float(params.g_c)
+    st.kappa, st.eps = float(params.kappa), float(params.eps)
+    st.pressure = float(params.pressure(t)) if t is not None else 0.0
+    st.split = _split_code(split)
+    st.split_band = float(getattr(params, "split_band", 0.0) or 0.0)
+    st.U = Ud.data_ptr()
+    rho = None
+    if kind == 1 and getattr(params, "modulus_field", None) is not None:
+        rho = _modulus_table(space, lat, params)
+        st.rho = rho.data_ptr()
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    _lib.call("pffmg_qoi", lat.ref, ctypes.byref(st), int(kind), _lib.ptr(out), _lib.stream())
+    return float(out.item())
+
+
+def crack_energy(space, state, params):
+    """Regularised surface energy (reference model.py:472-480)."""
+    return _qoi(space, state.U, params, SplitKind.NOSPLIT, None, 0)
+
+
+def bulk_energy(space, state, params, split):
+    """Degraded tensile + compressive elastic energy + pressure work (model.py:483-497)."""
+    return _qoi(space, state.U, params, split, state.t, 1)
+
+
+def fracture_volume(space, U):
+    """Integral of (1 - phi) (model.py:500-504)."""
+    p = MaterialParams(mu=0.0, lam=0.0, g_c=0.0, eps=1.0)
+    return _qoi(space, U, p, SplitKind.NOSPLIT, None, 2)

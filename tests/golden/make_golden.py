@@ -131,6 +131,30 @@ def gen_operator_band():
     save("operator_band", **out)
 
 
+def gen_qoi():
+    """crack_energy / bulk_energy / fracture_volume (model.py:472-504) on every
+    mesh, both splits (blended Miehe too), with and without a modulus field."""
+    out = {}
+    rng = np.random.default_rng(20261021)
+    for name, spec in MESHES.items():
+        disc = Discretization(ref_hierarchy(spec))
+        space = disc.finest
+        state = selfcheck.random_state(space, rng, t=0.1)
+        out[f"{name}/U"] = state.U
+        out[f"{name}/t"] = np.array(state.t)
+        for variant in ("plain", "modulus"):
+            params = params_for(space, modulus if variant == "modulus" else None)
+            out[f"{name}/{variant}/crack_energy"] = np.array(model.crack_energy(space, state, params))
+            out[f"{name}/{variant}/fracture_volume"] = np.array(model.fracture_volume(space, state.U))
+            for split in (SplitKind.NOSPLIT, SplitKind.MIEHE):
+                out[f"{name}/{variant}/{split.value}/bulk_energy"] = np.array(
+                    model.bulk_energy(space, state, params, split))
+            params.split_band = 0.05
+            out[f"{name}/{variant}/miehe_band/bulk_energy"] = np.array(
+                model.bulk_energy(space, state, params, SplitKind.MIEHE))
+    save("qoi", **out)
+
+
 def gen_transfers():
     out = {}
     rng = np.random.default_rng(99)
@@ -351,7 +375,7 @@ def gen_krylov():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["meshes", "operator", "operator_band", "transfers", "multigrid", "multigrid_miehe", "configs", "krylov"]
+    which = sys.argv[1:] or ["meshes", "operator", "operator_band", "transfers", "multigrid", "multigrid_miehe", "qoi", "configs", "krylov"]
     for w in which:
         print(w)
         globals()[f"gen_{w}"]()

@@ -160,3 +160,25 @@ def test_krylov_oracle_vs_reference(golden):
     est = np.array([[e.lambda_min_hat, e.lambda_max_hat] for e in
                     (solvers.estimate_spectrum(lambda v: A @ v, np.diag(A), 10, s) for s in range(5))])
     assert np.allclose(est, g["lap1d_est"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+def test_qoi_oracle_vs_reference(golden, name):
+    """crack_energy / bulk_energy / fracture_volume (model.py:472-504)."""
+    g = golden["qoi"]
+    _, tables, _ = oracle_stack(name)
+    T = tables[-1]
+    U = g[f"{name}/U"]
+    st = oracle_state(U, U[T.phi_slice], g[f"{name}/t"])
+    for variant in ("plain", "modulus"):
+        mat = oracle_material(T, variant == "modulus")
+        assert abs(jacobian.crack_energy(T, U, mat) - g[f"{name}/{variant}/crack_energy"]) <= \
+            1e-12 * abs(g[f"{name}/{variant}/crack_energy"])
+        assert abs(jacobian.fracture_volume(T, U) - g[f"{name}/{variant}/fracture_volume"]) <= \
+            1e-12 * abs(g[f"{name}/{variant}/fracture_volume"])
+        for split in ("none", "miehe"):
+            ref = g[f"{name}/{variant}/{split}/bulk_energy"]
+            assert abs(jacobian.bulk_energy(T, st, mat, split) - ref) <= 1e-12 * abs(ref)
+        mat.split_band = 0.05
+        ref = g[f"{name}/{variant}/miehe_band/bulk_energy"]
+        assert abs(jacobian.bulk_energy(T, st, mat, "miehe") - ref) <= 1e-12 * abs(ref)
