@@ -21,11 +21,19 @@ MGSOLVE = ["build_level_contexts", "contexts_from_operators", "vcycle", "coarse_
 KRYLOV = ["gmres", "estimate_spectrum"]
 
 
-def install(fracmg=None, operator=False):
+MODEL_PHYSICS = ["residual", "crack_energy", "bulk_energy", "fracture_volume"]
+NONLINEAR = ["compute_active_set"]
+
+
+def install(fracmg=None, operator=False, physics=False):
     """Swap the GPU twins into `fracmg` (module or None to import it).
 
     operator=True also replaces `fracmg.model.PhaseFieldOperator` (NoSplit
-    and the Miehe split, 2D and 3D)."""
+    and the Miehe split, 2D and 3D).  physics=True also replaces the Newton
+    right-hand side `model.residual`, the QoIs `model.crack_energy /
+    bulk_energy / fracture_volume` and `nonlinear.compute_active_set`, which
+    the reference's ActiveSetSolver and scenarios.run look up at call time
+    (nonlinear.py:146-150, 195; scenarios.py:411-415)."""
     if fracmg is None:
         fracmg = importlib.import_module("fracmg")
     from . import krylov, mgsolve, model
@@ -43,6 +51,15 @@ def install(fracmg=None, operator=False):
     if operator:
         _SAVED.setdefault((ref_model, "PhaseFieldOperator"), ref_model.PhaseFieldOperator)
         ref_model.PhaseFieldOperator = model.PhaseFieldOperator
+    if physics:
+        from . import nonlinear
+        ref_nl = importlib.import_module(fracmg.__name__ + ".nonlinear")
+        for name in MODEL_PHYSICS:
+            _SAVED.setdefault((ref_model, name), getattr(ref_model, name))
+            setattr(ref_model, name, getattr(model, name))
+        for name in NONLINEAR:
+            _SAVED.setdefault((ref_nl, name), getattr(ref_nl, name))
+            setattr(ref_nl, name, getattr(nonlinear, name))
     return fracmg
 
 

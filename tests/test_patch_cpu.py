@@ -31,3 +31,17 @@ def test_install_and_uninstall(fracmg):
         patch.uninstall()
     assert fracmg.mgsolve.vcycle is orig
     assert krylov._NO_CONVERGENCE[0] is krylov.NoConvergence
+
+
+def test_install_physics(fracmg):
+    from paper_1902_08112_b200 import model, nonlinear, patch
+    orig = fracmg.model.residual
+    patch.install(fracmg, operator=True, physics=True)
+    try:
+        assert fracmg.model.residual is model.residual
+        assert fracmg.model.bulk_energy is model.bulk_energy
+        assert fracmg.model.PhaseFieldOperator is model.PhaseFieldOperator
+        assert fracmg.nonlinear.compute_active_set is nonlinear.compute_active_set
+    finally:
+        patch.uninstall()
+    assert fracmg.model.residual is orig
