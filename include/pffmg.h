@@ -32,6 +32,8 @@ extern "C" {
 #define PFFMG_FULL (-1)     /* PhaseFieldOperator.apply          model.py:368-375 */
 #define PFFMG_UBLOCK 0      /* apply_block(0, .) displacement    model.py:377-392 */
 #define PFFMG_PBLOCK 1      /* apply_block(1, .) phase field     model.py:377-392 */
+#define PFFMG_BLOCKDIAG 2   /* both diagonal blocks at once on a full vector (u rows = apply_block(0),
+                               phi row = apply_block(1)): the operator of the block smoother */
 
 #define PFFMG_HINT_PREMASKED 1
 
@@ -164,6 +166,21 @@ int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st, int which,
  * degrades), 2 = fracture_volume.  st->U is the full (dim+1)*V state. */
 int pffmg_qoi(const pffmg_lattice* lat, const pffmg_state* st, int kind, double* result,
               void* stream);
+
+/* Block-diagonal ("_bd") forms: one kernel runs the Chebyshev recurrences of
+ * both diagonal blocks on full vectors (the blocks are independent in
+ * _smooth_blockwise, mgsolve.py:200-206), with per-block scalars read from
+ * device memory: coef_u/theta_u for the displacement components, coef_p /
+ * theta_p for the phase field.  n_u = dim*V in pffmg_cheb_init_zero_bd. */
+int pffmg_cheb_step_bd(const pffmg_lattice* lat, const pffmg_state* st, const double* d_in, double* d_out,
+                       double* r, double* x, const double* invdiag, const double* coef_u,
+                       const double* coef_p, int x_add_din, void* stream);
+int pffmg_cheb_init_bd(const pffmg_lattice* lat, const pffmg_state* st, const double* x, const double* b,
+                       double* r, double* d, const double* invdiag, const double* theta_u,
+                       const double* theta_p, void* stream);
+int pffmg_cheb_init_zero_bd(const double* b, const double* invdiag, const double* theta_u,
+                            const double* theta_p, int64_t n_u, double* r, double* d, double* x,
+                            int64_t n, void* stream);
 
 /* ---------------------------------------------------------------- transfers */
 /* fem.py:308-411 with the V-cycle masking of mgsolve.py:228-234.

@@ -14,7 +14,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpffmg.so")
 
-FULL, UBLOCK, PBLOCK = -1, 0, 1
+FULL, UBLOCK, PBLOCK, BLOCKDIAG = -1, 0, 1, 2
 
 c_double_p = C.POINTER(C.c_double)
 vp = C.c_void_p
@@ -54,6 +54,9 @@ _SIGS = {
                         C.c_double, vp],
     "pffmg_apply_host": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, C.c_int, vp],
     "pffmg_qoi": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp],
+    "pffmg_cheb_step_bd": [C.POINTER(Lattice), C.POINTER(State), vp, vp, vp, vp, vp, vp, vp, C.c_int, vp],
+    "pffmg_cheb_init_bd": [C.POINTER(Lattice), C.POINTER(State), vp, vp, vp, vp, vp, vp, vp, vp],
+    "pffmg_cheb_init_zero_bd": [vp, vp, vp, vp, C.c_int64, vp, vp, vp, C.c_int64, vp],
     "pffmg_cheb_step_dc": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, vp,
                            C.c_int, vp],
     "pffmg_cheb_init_dc": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, vp, vp],

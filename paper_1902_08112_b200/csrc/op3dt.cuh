@@ -111,6 +111,10 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
     int it = 0;
     for (int cz = vz0 - 1; cz < vz1; ++cz, ++it) {
         const int s0 = it & 3, s1 = (it + 1) & 3;
+        // vertex finalised this iteration and its epilogue operands (loaded early)
+        const int vid_f = (w >= 1 && cz >= vz0 && lane >= 1 && lane <= 30) ? vid_of(cx, cy, cz) : -1;
+        EpiIn<NCO, EPI> ein;
+        if (vid_f >= 0) epi_load<NCO, EPI>(A, vid_f, ein);
         if (cz + 2 <= vz1)
             issue(cz + 2, (it + 2) & 3);
         else
@@ -129,14 +133,16 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
             const double* p0;
             const double* p1;
             int lane, w;
+            bool zphi;                           // block-diagonal operator: phi(U) reads 0 (no G_phiu)
             __device__ __forceinline__ void load(int f, double (&c)[8]) const {
 #pragma unroll
                 for (int n = 0; n < 8; ++n) {
                     const double* p = (n >> 2) ? p1 : p0;
                     c[n] = p[(f * ROWS + w + ((n >> 1) & 1)) * W + lane + (n & 1)];
+                    if (MODE == M_FULL && f == MI::F_U + 3 && zphi) c[n] = 0.0;
                 }
             }
-        } C{p0, p1, lane < 31 ? lane : 30, w};
+        } C{p0, p1, lane < 31 ? lane : 30, w, A.nocoup != 0};
 
         const bool cell = lane_cell && (BOX ? ((unsigned)cx < (unsigned)L.nx && (unsigned)cy < (unsigned)L.ny &&
                                                (unsigned)cz < (unsigned)L.nz)
@@ -169,20 +175,18 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
                 acc[k] = carry[k] + (vp[k][0] + sy[(((w - 1) * NCO + k) * 2 + 0) * W + lane]);
                 top[k] = vp[k][1] + sy[(((w - 1) * NCO + k) * 2 + 1) * W + lane];
             }
-            if (cz >= vz0 && lane >= 1 && lane <= 30) {
-                const int vid = vid_of(cx, cy, cz);
-                if (vid >= 0) {
-                    const unsigned fl = flag(s0, w, lane);
-                    double vin[NCO];
+            if (vid_f >= 0) {
+                const int vid = vid_f;
+                const unsigned fl = flag(s0, w, lane);
+                double vin[NCO];
 #pragma unroll
-                    for (int k = 0; k < NCO; ++k) {
-                        // raw v (for identity rows): the staged copy was masked unless PRE
-                        vin[k] = PRE ? p0[((MI::F_V + k) * ROWS + w) * W + lane]
-                                     : (((fl >> (MI::COMP0 + k)) & 1) ? A.v[(int64_t)k * V + vid]
-                                                                      : p0[((MI::F_V + k) * ROWS + w) * W + lane]);
-                    }
-                    epilogue<NCO, MI::COMP0, EPI>(A, vid, (uint8_t)fl, acc, vin);
+                for (int k = 0; k < NCO; ++k) {
+                    // raw v (for identity rows): the staged copy was masked unless PRE
+                    vin[k] = PRE ? p0[((MI::F_V + k) * ROWS + w) * W + lane]
+                                 : (((fl >> (MI::COMP0 + k)) & 1) ? A.v[(int64_t)k * V + vid]
+                                                                  : p0[((MI::F_V + k) * ROWS + w) * W + lane]);
                 }
+                epilogue_pre<NCO, MI::COMP0, EPI>(A, vid, (uint8_t)fl, acc, vin, ein);
             }
 #pragma unroll
             for (int k = 0; k < NCO; ++k) carry[k] = top[k];

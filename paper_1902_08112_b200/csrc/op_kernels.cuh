@@ -37,6 +37,8 @@ struct OpArgs {
     const double* __restrict__ inv;
     double c1, c2;                     // CHEB: c_dd, c_dr   CHEB0: theta
     const double* __restrict__ coef;   // if set, c1/c2 are read from device memory (coef[0], coef[1])
+    const double* __restrict__ coef2;  // block-diagonal mode: the phase-field component's coefficients
+    int nocoup;                        // FULL mode without the G_phiu coupling (block-diagonal operator)
     int x_add_din;                     // CHEB: x = (x + d_in) + d_out instead of x += d_out
     int planes_per_cta;
     int nseg;                          // 2D warp kernel: 30-column segments per row
@@ -69,7 +71,8 @@ __device__ __forceinline__ void epilogue(const OpArgs& A, int64_t vid, uint8_t f
             A.out[g] = A.b[g] - Av;                              // mgsolve.py:227
         } else if (EPI == E_CHEB) {                              // mgsolve.py:108-111
             const double rr = A.r[g] - Av;
-            const double c1 = A.coef ? __ldg(A.coef) : A.c1, c2 = A.coef ? __ldg(A.coef + 1) : A.c2;
+            const double* cf = (A.coef2 && COMP0 + k == A.L.dim) ? A.coef2 : A.coef;
+            const double c1 = cf ? __ldg(cf) : A.c1, c2 = cf ? __ldg(cf + 1) : A.c2;
             const double dn = c1 * vin[k] + c2 * (A.inv[g] * rr);
             A.r[g] = rr;
             A.dout[g] = dn;
@@ -78,7 +81,75 @@ __device__ __forceinline__ void epilogue(const OpArgs& A, int64_t vid, uint8_t f
         } else {                                                 // E_CHEB0: mgsolve.py:95, 105
             const double rr = A.b[g] - Av;                       // (x += d deferred to the
             A.r[g] = rr;                                         //  next step, see pffmg.h)
-            A.dout[g] = (A.inv[g] * rr) / (A.coef ? __ldg(A.coef) : A.c1);
+            const double* cf = (A.coef2 && COMP0 + k == A.L.dim) ? A.coef2 : A.coef;
+            A.dout[g] = (A.inv[g] * rr) / (cf ? __ldg(cf) : A.c1);
+        }
+    }
+}
+
+// Epilogue operands loaded ahead of the cell work (their DRAM latency then
+// overlaps the stencil arithmetic instead of stalling the epilogue).
+template <int NCO, int EPI>
+struct EpiIn {
+    static constexpr int NL = EPI == E_CHEB ? 3 : (EPI == E_CHEB0 ? 2 : (EPI == E_RESID ? 1 : 0));
+    double a[NL > 0 ? NL : 1][NCO];
+};
+
+template <int NCO, int EPI>
+__device__ __forceinline__ void epi_load(const OpArgs& A, int64_t vid, EpiIn<NCO, EPI>& e) {
+    const int64_t V = A.L.V;
+#pragma unroll
+    for (int k = 0; k < NCO; ++k) {
+        const int64_t g = (int64_t)k * V + vid;
+        if (EPI == E_CHEB) {
+            e.a[0][k] = A.r[g];
+            e.a[1][k] = __ldg(A.inv + g);
+            e.a[2][k] = A.x[g];
+        } else if (EPI == E_CHEB0) {
+            e.a[0][k] = __ldg(A.b + g);
+            e.a[1][k] = __ldg(A.inv + g);
+        } else if (EPI == E_RESID) {
+            e.a[0][k] = __ldg(A.b + g);
+        }
+    }
+}
+
+// epilogue() with the operands from epi_load
+template <int NCO, int COMP0, int EPI>
+__device__ __forceinline__ void epilogue_pre(const OpArgs& A, int64_t vid, uint8_t fl, const double (&acc)[NCO],
+                                             const double (&vin)[NCO], const EpiIn<NCO, EPI>& e) {
+    const int64_t V = A.L.V;
+#pragma unroll
+    for (int k = 0; k < NCO; ++k) {
+        const bool con = (fl >> (COMP0 + k)) & 1;
+        const int64_t g = (int64_t)k * V + vid;
+        if (EPI == E_DIAG) {
+            A.out[g] = con ? 1.0 : acc[k];                       // model.py:412
+            continue;
+        }
+        if (EPI == E_RESZ) {
+            A.out[g] = con ? 0.0 : acc[k];                       // model.py:459
+            continue;
+        }
+        const double Av = con ? vin[k] : acc[k];                 // model.py:373-374, 390-391
+        if (EPI == E_STORE) {
+            A.out[g] = Av;
+        } else if (EPI == E_RESID) {
+            A.out[g] = e.a[0][k] - Av;                           // mgsolve.py:227
+        } else if (EPI == E_CHEB) {                              // mgsolve.py:108-111
+            const double rr = e.a[0][k] - Av;
+            const double* cf = (A.coef2 && COMP0 + k == A.L.dim) ? A.coef2 : A.coef;
+            const double c1 = cf ? __ldg(cf) : A.c1, c2 = cf ? __ldg(cf + 1) : A.c2;
+            const double dn = c1 * vin[k] + c2 * (e.a[1][k] * rr);
+            A.r[g] = rr;
+            A.dout[g] = dn;
+            const double xo = e.a[2][k];
+            A.x[g] = A.x_add_din ? (xo + vin[k]) + dn : xo + dn;
+        } else {                                                 // E_CHEB0: mgsolve.py:95, 105
+            const double rr = e.a[0][k] - Av;
+            A.r[g] = rr;
+            const double* cf = (A.coef2 && COMP0 + k == A.L.dim) ? A.coef2 : A.coef;
+            A.dout[g] = (e.a[1][k] * rr) / (cf ? __ldg(cf) : A.c1);
         }
     }
 }
@@ -359,6 +430,10 @@ op2dw_kernel(const OpArgs A) {
     int it = 0;
     for (int cy = vy0 - 1; cy < vy1; ++cy, ++it) {
         const int s0 = it & 3, s1 = (it + 1) & 3;
+        // vertex finalised this iteration and its epilogue operands (loaded early)
+        const int vid_f = (cy >= vy0 && col_fin) ? RowAddr<BOX>::id(L, cx, cy) : -1;
+        EpiIn<NCO, EPI> ein;
+        if (vid_f >= 0) epi_load<NCO, EPI>(A, vid_f, ein);
         if (it > 0) {                            // row cy+1 becomes the top row
             cp_async_wait<1>();
             __syncwarp();
@@ -388,6 +463,12 @@ op2dw_kernel(const OpArgs A) {
                 cv[i][2] = r1[i * W + lane];
                 cv[i][3] = r1[i * W + lane + 1];
             }
+            if constexpr (MODE == M_FULL) {      // block-diagonal operator: no G_phiu coupling
+                if (A.nocoup) {                  // (T_phiu = 0 when phi(U) reads 0, model.py:299-303)
+#pragma unroll
+                    for (int n = 0; n < NP; ++n) cv[MI::F_U + D][n] = 0.0;
+                }
+            }
             const double* rq = RHO ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * NP : nullptr;
             if constexpr (MIE) {   // spectral split: modulus field resolved at run time
                 cell_kernel_miehe2<MODE>(cv, A.rho ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * NP : nullptr,
@@ -413,17 +494,14 @@ op2dw_kernel(const OpArgs A) {
             bot[k] = o[k][0] + q0;
             top[k] = o[k][2] + q1;
         }
-        if (cy >= vy0 && col_fin) {
-            const int vid = RowAddr<BOX>::id(L, cx, cy);
-            if (vid >= 0) {
-                double acc[NCO], vin[NCO];
+        if (vid_f >= 0) {
+            double acc[NCO], vin[NCO];
 #pragma unroll
-                for (int k = 0; k < NCO; ++k) {
-                    acc[k] = carry[k] + bot[k];
-                    vin[k] = (MODE == M_DIAG) ? 0.0 : raw_bot[k < NV ? k : 0];
-                }
-                epilogue<NCO, MI::COMP0, EPI>(A, vid, (uint8_t)flag(s0), acc, vin);
+            for (int k = 0; k < NCO; ++k) {
+                acc[k] = carry[k] + bot[k];
+                vin[k] = (MODE == M_DIAG) ? 0.0 : raw_bot[k < NV ? k : 0];
             }
+            epilogue_pre<NCO, MI::COMP0, EPI>(A, vid_f, (uint8_t)flag(s0), acc, vin, ein);
         }
 #pragma unroll
         for (int k = 0; k < NCO; ++k) carry[k] = top[k];
@@ -486,6 +564,9 @@ __global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
     int b0 = 0;
     for (int cz = vz0 - 1; cz < vz1; ++cz) {
         const int b1 = b0 ^ 1;
+        const int64_t vid_f = (w >= 1 && cz >= vz0 && lane >= 1) ? vertex_id(L, cx, cy, cz) : -1;
+        EpiIn<NCO, EPI> ein;
+        if (vid_f >= 0) epi_load<NCO, EPI>(A, vid_f, ein);
         double pf[SLOTS][NF];
         uint8_t pfl[SLOTS];
         const bool need_next = (cz + 2 <= vz1);
@@ -511,6 +592,12 @@ __global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
                     double val = SV(bb, i, j);
                     if (i < MI::NV && ((fl >> (MI::COMP0 + i)) & 1)) val = 0.0;
                     cv[i][n] = val;
+                }
+            }
+            if constexpr (MODE == M_FULL) {      // block-diagonal operator: no G_phiu coupling
+                if (A.nocoup) {
+#pragma unroll
+                    for (int n = 0; n < NP; ++n) cv[MI::F_U + D][n] = 0.0;
                 }
             }
             const double* rq =
@@ -554,19 +641,16 @@ __global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
 #pragma unroll
                 for (int k = 0; k < NCO; ++k)
                     vp[zb][k] = part[0][zb][k] + sy[(((w - 1) * 2 + zb) * NCO + k) * 32 + lane];
-            if (cz >= vz0 && lane >= 1) {
-                const int64_t vid = vertex_id(L, cx, cy, cz);
-                if (vid >= 0) {
-                    const int j = lane + TXV * w;
-                    const uint8_t fl = sfl[b0 * TV + j];
-                    double acc[NCO], vin[NCO];
+            if (vid_f >= 0) {
+                const int j = lane + TXV * w;
+                const uint8_t fl = sfl[b0 * TV + j];
+                double acc[NCO], vin[NCO];
 #pragma unroll
-                    for (int k = 0; k < NCO; ++k) {
-                        acc[k] = carry[k] + vp[0][k];
-                        vin[k] = (MODE == M_DIAG) ? 0.0 : SV(b0, MI::F_V + k, j);
-                    }
-                    epilogue<NCO, MI::COMP0, EPI>(A, vid, fl, acc, vin);
+                for (int k = 0; k < NCO; ++k) {
+                    acc[k] = carry[k] + vp[0][k];
+                    vin[k] = (MODE == M_DIAG) ? 0.0 : SV(b0, MI::F_V + k, j);
                 }
+                epilogue_pre<NCO, MI::COMP0, EPI>(A, vid_f, fl, acc, vin, ein);
             }
 #pragma unroll
             for (int k = 0; k < NCO; ++k) carry[k] = vp[1][k];

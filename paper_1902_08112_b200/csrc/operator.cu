@@ -57,7 +57,13 @@ static int dispatch_which(const OpArgs& A, int which, cudaStream_t s, const char
         PFFMG_REQUIRE(A.U, "%s: phi block needs U", what);
         return launch<M_PBLK, EPI>(A, s, what);
     }
-    set_error("%s: which must be -1, 0 or 1 (got %d)", what, which);
+    if (which == PFFMG_BLOCKDIAG) {
+        PFFMG_REQUIRE(A.U && A.pt, "%s: block-diagonal operator needs U and phi_tilde", what);
+        OpArgs B = A;
+        B.nocoup = 1;
+        return launch<M_FULL, EPI>(B, s, what);
+    }
+    set_error("%s: which must be -1, 0, 1 or 2 (got %d)", what, which);
     return PFFMG_ERR_ARG;
 }
 
@@ -255,6 +261,43 @@ extern "C" int pffmg_cheb_init_dc(const pffmg_lattice* lat, const pffmg_state* s
     A.inv = invdiag;
     A.coef = theta;
     return dispatch_which<E_CHEB0>(A, which, as_stream(stream), "pffmg_cheb_init_dc");
+}
+
+extern "C" int pffmg_cheb_step_bd(const pffmg_lattice* lat, const pffmg_state* st, const double* d_in,
+                                  double* d_out, double* r, double* x, const double* invdiag,
+                                  const double* coef_u, const double* coef_p, int x_add_din, void* stream) {
+    OpArgs A;
+    int rc = fill_args(lat, st, &A);
+    if (rc) return rc;
+    PFFMG_REQUIRE(d_in && d_out && r && x && invdiag && coef_u && coef_p && d_in != d_out && x != d_in,
+                  "pffmg_cheb_step_bd: bad pointers");
+    A.v = d_in;
+    A.dout = d_out;
+    A.r = r;
+    A.x = x;
+    A.inv = invdiag;
+    A.coef = coef_u;
+    A.coef2 = coef_p;
+    A.x_add_din = x_add_din;
+    return dispatch_which<E_CHEB>(A, PFFMG_BLOCKDIAG, as_stream(stream), "pffmg_cheb_step_bd");
+}
+
+extern "C" int pffmg_cheb_init_bd(const pffmg_lattice* lat, const pffmg_state* st, const double* x,
+                                  const double* b, double* r, double* d, const double* invdiag,
+                                  const double* theta_u, const double* theta_p, void* stream) {
+    OpArgs A;
+    int rc = fill_args(lat, st, &A);
+    if (rc) return rc;
+    PFFMG_REQUIRE(x && b && r && d && invdiag && theta_u && theta_p && d != x && r != x,
+                  "pffmg_cheb_init_bd: bad pointers");
+    A.v = x;
+    A.b = b;
+    A.r = r;
+    A.dout = d;
+    A.inv = invdiag;
+    A.coef = theta_u;
+    A.coef2 = theta_p;
+    return dispatch_which<E_CHEB0>(A, PFFMG_BLOCKDIAG, as_stream(stream), "pffmg_cheb_init_bd");
 }
 
 extern "C" int pffmg_cheb_init(const pffmg_lattice* lat, const pffmg_state* st, int which,

@@ -396,6 +396,25 @@ extern "C" int pffmg_cheb_init_zero_dc(const double* b, const double* invdiag, c
     cheb_init_zero_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(b, invdiag, 0.0, theta, r, d, x, n);
     VCHECK("pffmg_cheb_init_zero_dc");
 }
+__global__ void cheb_init_zero_bd_k(const double* b, const double* inv, const double* tu, const double* tp,
+                                    int64_t n_u, double* r, double* d, double* x, int64_t n) {
+    const double thu = *tu, thp = *tp;
+    GRID_STRIDE(i, n) {
+        const double ri = b[i];
+        const double di = (inv[i] * ri) / (i < n_u ? thu : thp);
+        r[i] = ri;
+        d[i] = di;
+        x[i] = 0.0 + di;
+    }
+}
+extern "C" int pffmg_cheb_init_zero_bd(const double* b, const double* invdiag, const double* theta_u,
+                                       const double* theta_p, int64_t n_u, double* r, double* d, double* x,
+                                       int64_t n, void* stream) {
+    PFFMG_REQUIRE(b && invdiag && theta_u && theta_p && r && d && x && n_u >= 0 && n_u <= n,
+                  "pffmg_cheb_init_zero_bd: bad args");
+    cheb_init_zero_bd_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(b, invdiag, theta_u, theta_p, n_u, r, d, x, n);
+    VCHECK("pffmg_cheb_init_zero_bd");
+}
 extern "C" int pffmg_jacobi_update(const double* r, const double* invdiag, double theta, double* x,
                                    int64_t n, void* stream) {
     PFFMG_REQUIRE(r && invdiag && x, "pffmg_jacobi_update: bad args");

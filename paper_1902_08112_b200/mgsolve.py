@@ -224,6 +224,9 @@ def _fine_mask(dirichlet_mask, active_mask):
 # Reuse of the device setup across Newton steps (see _Session); PFFMG_REUSE_SETUP=0
 # rebuilds every buffer and re-records every graph on each call instead.
 REUSE_SETUP = os.environ.get("PFFMG_REUSE_SETUP", "1") != "0"
+# Smooth both diagonal blocks with one block-diagonal kernel per Chebyshev step
+# (PFFMG_BLOCKDIAG_SMOOTH=0: one kernel per block and step, the reference's order).
+BLOCKDIAG_SMOOTH = os.environ.get("PFFMG_BLOCKDIAG_SMOOTH", "1") != "0"
 
 
 def build_level_contexts(disc, state, active_mask, dirichlet_mask, params, split,
@@ -574,6 +577,10 @@ class _Level:
         self.cr = zeros(n)      # Chebyshev residual
         self.d0 = zeros(n)
         self.d1 = zeros(n)
+        # one block-diagonal kernel per Chebyshev step pays in 2D and on small
+        # (launch-latency-bound) 3D levels; large 3D levels are FP64-bound and
+        # run faster as two block kernels (measured, cfg4)
+        self.bd_ok = self.dim == 2 or self.V < (1 << 17)
 
     def blk(self, k):
         return slice(0, self.dim * self.V) if k == 0 else slice(self.dim * self.V, self.n)
@@ -685,15 +692,47 @@ class _NativeCycle:
         if pending:                                        # degree 1 from a non-zero x
             _lib.call("pffmg_axpy", 1.0, _lib.ptr(d_in), _lib.ptr(x), nb, s)
 
+    def _cheb_pair(self, L, su, sp, x_is_zero, pre=True):
+        """Chebyshev on both diagonal blocks (independent, mgsolve.py:200-206) with
+        one block-diagonal kernel per step while both recurrences run."""
+        ou, pu, degu = self.slot[su]
+        op_, pp, degp = self.slot[sp]
+        if (not BLOCKDIAG_SMOOTH or not L.bd_ok or degu or degp or
+                (pu.degree != pp.degree and not x_is_zero)):
+            self._cheb(L, 0, su, x_is_zero, pre)
+            self._cheb(L, 1, sp, x_is_zero, pre)
+            return
+        op, coef, s = L.op, self.coef, _lib.stream()
+        x, r, rhs, inv, d_in, d_out = L.x, L.cr, L.r, L.inv, L.d0, L.d1
+        tu, tp = coef[ou:ou + 1], coef[op_:op_ + 1]
+        if x_is_zero:
+            _lib.call("pffmg_cheb_init_zero_bd", _lib.ptr(rhs), _lib.ptr(inv), _lib.ptr(tu), _lib.ptr(tp),
+                      L.dim * L.V, _lib.ptr(r), _lib.ptr(d_in), _lib.ptr(x), L.n, s)
+            pending = False
+        else:
+            op.cheb_init_bd(x, rhs, r, d_in, inv, tu, tp, pre=pre)
+            pending = True
+        common = min(pu.degree, pp.degree) - 1
+        for i in range(common):
+            op.cheb_step_bd(d_in, d_out, r, x, inv, coef[ou + 1 + 2 * i: ou + 3 + 2 * i],
+                            coef[op_ + 1 + 2 * i: op_ + 3 + 2 * i], pending, pre=pre)
+            pending = False
+            d_in, d_out = d_out, d_in
+        if pending:                                        # degree 1 from a non-zero x
+            _lib.call("pffmg_axpy", 1.0, _lib.ptr(d_in), _lib.ptr(x), L.n, s)
+        for k, (o, prm) in enumerate(((ou, pu), (op_, pp))):   # the longer recurrence goes on alone
+            b = L.blk(k)
+            di, do = d_in[b], d_out[b]
+            for i in range(common, prm.degree - 1):
+                op.cheb_step_dc(k, di, do, r[b], x[b], inv[b], coef[o + 1 + 2 * i: o + 3 + 2 * i],
+                                False, pre=pre)
+                di, do = do, di
+
     def _smooth(self, l, x_is_zero):
-        L = self.levels[l]
-        for k in range(2):
-            self._cheb(L, k, ("s", l, k), x_is_zero)
+        self._cheb_pair(self.levels[l], ("s", l, 0), ("s", l, 1), x_is_zero)
 
     def _coarse_into_x(self, pre=True):
-        L = self.levels[0]
-        for k in range(2):
-            self._cheb(L, k, ("c", 0, k), True, pre)
+        self._cheb_pair(self.levels[0], ("c", 0, 0), ("c", 0, 1), True, pre)
 
     def _cycle(self, l):                                   # mgsolve.py:221-235
         if l == 0:

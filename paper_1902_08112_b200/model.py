@@ -287,6 +287,16 @@ class PhaseFieldOperator:
                   _lib.ptr(d_out), _lib.ptr(r), _lib.ptr(x), _lib.ptr(inv), _lib.ptr(coef),
                   int(x_add_din), _lib.stream())
 
+    def cheb_step_bd(self, d_in, d_out, r, x, inv, coef_u, coef_p, x_add_din=False, pre=False):
+        """Both diagonal blocks' Chebyshev steps in one kernel (full-length vectors)."""
+        _lib.call("pffmg_cheb_step_bd", self.lat.ref, self._sp(pre), _lib.ptr(d_in), _lib.ptr(d_out),
+                  _lib.ptr(r), _lib.ptr(x), _lib.ptr(inv), _lib.ptr(coef_u), _lib.ptr(coef_p),
+                  int(x_add_din), _lib.stream())
+
+    def cheb_init_bd(self, x, b, r, d, inv, theta_u, theta_p, pre=False):
+        _lib.call("pffmg_cheb_init_bd", self.lat.ref, self._sp(pre), _lib.ptr(x), _lib.ptr(b), _lib.ptr(r),
+                  _lib.ptr(d), _lib.ptr(inv), _lib.ptr(theta_u), _lib.ptr(theta_p), _lib.stream())
+
     def cheb_init_dc(self, which, x, b, r, d, inv, theta, pre=False):
         _lib.call("pffmg_cheb_init_dc", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
                   _lib.ptr(r), _lib.ptr(d), _lib.ptr(inv), _lib.ptr(theta), _lib.stream())

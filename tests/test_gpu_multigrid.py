@@ -240,3 +240,19 @@ def test_setup_reuse_across_newton_steps(golden, monkeypatch):
     x, its = krylov.gmres(c3[-1].op.apply, mgsolve.VCyclePreconditioner(c3, FULL),
                           g[f"{name}/gmres_rhs"], ctl)
     assert abs(its - int(g[f"{name}/gmres_iters"])) <= 1
+
+
+@pytest.mark.parametrize("name", MG)
+def test_blockdiag_smoothing_matches_per_block(golden, name, monkeypatch):
+    """One block-diagonal kernel per Chebyshev step == the per-block kernels."""
+    from paper_1902_08112_b200 import mgsolve
+    g = golden["multigrid"]
+    r = torch.as_tensor(g[f"{name}/r"], device="cuda")
+    FULL = mgsolve.PreconditionerKind.FULL
+    out = []
+    for flag in (True, False):
+        monkeypatch.setattr(mgsolve, "BLOCKDIAG_SMOOTH", flag)
+        mgsolve._Session._cache.clear()
+        disc, ctxs = _contexts(g, name)
+        out.append(mgsolve.vcycle(ctxs, FULL, r).cpu().numpy())
+    assert rel_err(out[0], out[1]) <= 1e-12

@@ -203,3 +203,27 @@ def test_pinned_host_apply_pipeline_is_exact(golden, name):
                   None if po is None else po.ctypes.data, strips, _lib.stream())
         torch.cuda.synchronize()
         assert torch.equal(out, ref), strips
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+@pytest.mark.parametrize("split", ["none", "miehe"])
+def test_blockdiag_operator_equals_blocks(golden, name, split):
+    """PFFMG_BLOCKDIAG (both diagonal blocks in one kernel, the block smoother's
+    operator) == [apply_block(0); apply_block(1)]."""
+    from paper_1902_08112_b200 import _lib
+    from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, SplitKind
+    g = golden["operator"]
+    tag = f"{name}/{split}/masked"
+    space = product_disc(name).finest
+    st = product_state(g[f"{tag}/U"], g[f"{tag}/phi_tilde"], g[f"{tag}/t"])
+    flags = g[f"{tag}/flags"]
+    op = PhaseFieldOperator(space, st, ConstraintMask(flags, np.zeros(flags.size)), product_params(space),
+                            SplitKind.MIEHE if split == "miehe" else SplitKind.NOSPLIT)
+    v = torch.as_tensor(g[f"{tag}/v"], device="cuda")
+    d = op.dim * op.V
+    out = torch.empty_like(v)
+    op.apply_dev(_lib.BLOCKDIAG, v, out)
+    ref = torch.cat([op.apply_block(0, v[:d]), op.apply_block(1, v[d:])])
+    assert rel_err(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-14
+    assert rel_err(out[:d].cpu().numpy(), ref[:d].cpu().numpy()) <= 1e-14
+    assert rel_err(out[d:].cpu().numpy(), ref[d:].cpu().numpy()) <= 1e-14
