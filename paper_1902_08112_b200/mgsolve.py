@@ -213,12 +213,21 @@ def contexts_from_operators(disc, ops, eig_iters=10, seed=0):
 
 
 def _fine_mask(dirichlet_mask, active_mask):
-    """fine mask = Dirichlet | active, values = Dirichlet inhomogeneity (mgsolve.py:168-171)."""
+    """fine mask = Dirichlet | active, values = Dirichlet inhomogeneity (mgsolve.py:168-171).
+    The union is formed on the device; the host views (numpy inputs only) are
+    lazily evaluated callables -- the solve never needs them."""
     dir_c = dirichlet_mask.is_constrained
+    fine_dev = dev(dir_c, torch.bool) | dev(active_mask, torch.bool)
     if is_tensor(dir_c) or is_tensor(active_mask):
-        return dev(dir_c, torch.bool) | dev(active_mask, torch.bool), None
-    fine_bool = np.asarray(dir_c, dtype=bool) | np.asarray(active_mask, dtype=bool)
-    return fine_bool, np.where(dir_c, dirichlet_mask.inhomogeneity, 0.0)
+        return fine_dev, None, None
+    inh = dirichlet_mask.inhomogeneity
+
+    def vals():
+        return np.where(np.asarray(dir_c, dtype=bool), inh, 0.0)
+
+    def union():
+        return np.asarray(dir_c, dtype=bool) | np.asarray(active_mask, dtype=bool)
+    return fine_dev, vals, union
 
 
 # Reuse of the device setup across Newton steps (see _Session); PFFMG_REUSE_SETUP=0
@@ -234,14 +243,15 @@ def build_level_contexts(disc, state, active_mask, dirichlet_mask, params, split
     """Phase-field level contexts from finest-level data (mgsolve.py:154-197), on the GPU."""
     _lib.require_cuda()
     D = Discretization.wrap(disc)
-    fine_bool, fine_vals = _fine_mask(dirichlet_mask, active_mask)
+    fine_bool, fine_vals, fine_host = _fine_mask(dirichlet_mask, active_mask)
     if REUSE_SETUP:
         sess = _Session.get(D, params, split, state.t, eig_iters, seed, threads)
-        return sess.build(disc, state, fine_bool, fine_vals)
-    return _build_fresh(disc, D, state, fine_bool, fine_vals, params, split, eig_iters, seed, threads)
+        return sess.build(disc, state, fine_bool, fine_vals, fine_host)
+    return _build_fresh(disc, D, state, fine_bool, fine_vals, fine_host, params, split, eig_iters, seed,
+                        threads)
 
 
-def _build_fresh(disc, D, state, fine_bool, fine_vals, params, split, eig_iters, seed, threads):
+def _build_fresh(disc, D, state, fine_bool, fine_vals, fine_host, params, split, eig_iters, seed, threads):
     hier = D.hierarchy
     L = hier.n_levels
     dim = hier.dim
@@ -269,8 +279,8 @@ def _build_fresh(disc, D, state, fine_bool, fine_vals, params, split, eig_iters,
         st = LinearizationState(U=U[l], U_prev1=P1[l], U_prev2=P2[l], t=state.t,
                                 t_prev1=state.t_prev1, t_prev2=state.t_prev2, phi_tilde=PT[l])
         mask = DeviceMask(flags[l], nc, Vs[l], fine_vals if l == L - 1 else None)
-        if l == L - 1 and not is_tensor(fine_bool):
-            mask._host = fine_bool
+        if l == L - 1:
+            mask._host_fn = fine_host
         op = PhaseFieldOperator(D.spaces[l], st, mask, params, split, threads, _flags=flags[l])
         diag = empty(op.n_dofs)
         op.diagonal_dev(diag)
@@ -394,7 +404,7 @@ class _Session:
                 ctx.flags = fl
                 ctx._session = None
 
-    def build(self, disc, state, fine_bool, fine_vals):
+    def build(self, disc, state, fine_bool, fine_vals, fine_host=None):
         import weakref
         self._detach_previous()
         L, nc = self.L, self.nc
@@ -424,8 +434,8 @@ class _Session:
             st = LinearizationState(U=self.U[l], U_prev1=self.P1[l], U_prev2=self.P2[l], t=state.t,
                                     t_prev1=state.t_prev1, t_prev2=state.t_prev2, phi_tilde=self.PT[l])
             mask = DeviceMask(self.flags[l], nc, self.Vs[l], fine_vals if l == L - 1 else None)
-            if l == L - 1 and not is_tensor(fine_bool):
-                mask._host = fine_bool
+            if l == L - 1:
+                mask._host_fn = fine_host
             op = PhaseFieldOperator(self.D.spaces[l], st, mask, self.params, self.split, self.threads,
                                     _flags=self.flags[l], _rho=self.ops[l]._rho)
             ctx = LevelContext(l, op, self.diag[l], self.spectra[l], None, disc, self.flags[l],

@@ -93,18 +93,22 @@ class DeviceMask:
         self.n_comp = n_comp
         self.V = V
         self._host = None
-        self._inh = inhomogeneity
+        self._host_fn = None          # optional lazy host view (e.g. the caller's own arrays)
+        self._inh = inhomogeneity     # array, callable (lazy) or None (zeros)
 
     @property
     def is_constrained(self):
         if self._host is None:
-            self._host = host(unpack_flags(self.flags, self.n_comp, self.V))
+            self._host = (self._host_fn() if self._host_fn is not None
+                          else host(unpack_flags(self.flags, self.n_comp, self.V)))
         return self._host
 
     @property
     def inhomogeneity(self):
         if self._inh is None:
             self._inh = np.zeros(self.n_comp * self.V)
+        elif callable(self._inh):
+            self._inh = self._inh()
         return self._inh
 
 

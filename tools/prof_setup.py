@@ -46,3 +46,20 @@ for _ in range(10):
     pc._pffmg_into(rhs, x)
 torch.cuda.synchronize()
 print("vcycle", (time.perf_counter() - t0) / 10)
+# device time of one setup-graph replay
+sess = ctxs[-1]._session
+if sess is not None and sess.graph is not None:
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(10):
+        e0.record()
+        sess.graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    print("setup graph replay ms", sorted(ts)[5])
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        sess.graph.replay()
+        torch.cuda.synchronize()
+    print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=14))
