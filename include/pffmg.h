@@ -64,7 +64,11 @@ typedef struct {
     /* Global index of local plane 0 along the cut axis (0 unless this is a
      * slab of a larger level); transfers use it to pair coarse and fine slabs. */
     int32_t plane0;
-    int32_t pad_;
+    /* Element order: 0 or 1 = trilinear/bilinear Q1 (the reference's element,
+     * fem.py:1-8); 2 = biquadratic Q2 (2D box lattices, whole lattice only):
+     * dofs live on the nodes of the half-spacing lattice, (2nx+1)(2ny+1) of
+     * them, x fastest; 3x3 Gauss points (BASELINE configs[2]). */
+    int32_t order;
 } pffmg_lattice;
 
 /*

@@ -28,7 +28,7 @@ class Lattice(C.Structure):
                 ("vrow_off", vp), ("vrow_lo", vp), ("vrow_hi", vp),
                 ("crow_lo", vp), ("crow_hi", vp),
                 ("own_lo", C.c_int32), ("own_hi", C.c_int32),
-                ("plane0", C.c_int32), ("pad_", C.c_int32)]
+                ("plane0", C.c_int32), ("order", C.c_int32)]
 
 
 class State(C.Structure):

@@ -44,11 +44,21 @@ int make_lat(const pffmg_lattice* in, Lat* out) {
     PFFMG_REQUIRE(in->nx >= 1 && in->ny >= 1 && (in->dim == 2 ? in->nz == 0 : in->nz >= 1),
                   "bad lattice extents %d x %d x %d", in->nx, in->ny, in->nz);
     PFFMG_REQUIRE(in->n_vertices > 0, "n_vertices must be positive");
+    const int order = in->order <= 1 ? 1 : in->order;
+    PFFMG_REQUIRE(order == 1 || order == 2, "lattice order must be 1 (Q1) or 2 (Q2), got %d", in->order);
+    if (order == 2) {
+        PFFMG_REQUIRE(in->dim == 2 && in->vrow_off == nullptr, "Q2 lattices must be 2D boxes");
+        PFFMG_REQUIRE((int64_t)(2 * in->nx + 1) * (2 * in->ny + 1) == in->n_vertices,
+                      "Q2 box has %lld nodes, n_vertices=%lld",
+                      (long long)(2 * in->nx + 1) * (2 * in->ny + 1), (long long)in->n_vertices);
+        PFFMG_REQUIRE(in->own_lo == 0 && (in->own_hi == 0 || in->own_hi == 2 * in->ny + 1) && in->plane0 == 0,
+                      "Q2 lattices are whole (no slabs)");
+    }
     const bool has_rows = in->vrow_off != nullptr;
     PFFMG_REQUIRE(has_rows == (in->vrow_lo != nullptr) && has_rows == (in->vrow_hi != nullptr) &&
                       has_rows == (in->crow_lo != nullptr) && has_rows == (in->crow_hi != nullptr),
                   "row tables must be all NULL (box) or all set");
-    if (!has_rows) {
+    if (!has_rows && order == 1) {
         const int64_t Vbox = (int64_t)(in->nx + 1) * (in->ny + 1) * (in->dim == 3 ? in->nz + 1 : 1);
         PFFMG_REQUIRE(Vbox == in->n_vertices, "box lattice has %lld vertices, n_vertices=%lld",
                       (long long)Vbox, (long long)in->n_vertices);
@@ -67,7 +77,8 @@ int make_lat(const pffmg_lattice* in, Lat* out) {
     out->crow_lo = in->crow_lo;
     out->crow_hi = in->crow_hi;
     out->plane0 = in->plane0;
-    const int nplanes = (in->dim == 3 ? in->nz : in->ny) + 1;
+    out->order = order;
+    const int nplanes = order == 2 ? 2 * in->ny + 1 : (in->dim == 3 ? in->nz : in->ny) + 1;
     if (in->own_lo == 0 && in->own_hi == 0) {
         out->own_lo = 0;
         out->own_hi = nplanes;

@@ -41,6 +41,7 @@ struct Lat {
     const int32_t* __restrict__ crow_hi;
     int own_lo, own_hi;    // finalised vertex planes of the last axis (always set by make_lat)
     int plane0;            // global index of local plane 0 along the last axis
+    int order;             // 1 = Q1, 2 = Q2 (2D box, nodes on the half-spacing lattice)
 };
 
 int make_lat(const pffmg_lattice* in, Lat* out);

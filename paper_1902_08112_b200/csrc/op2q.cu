@@ -1,0 +1,136 @@
+// Q2 (9-node) 2D fused operator kernels (BASELINE configs[2]).
+//
+// One thread = one Q2 cell; a warp = 32 consecutive cells of a cell row
+// (lane 0 is the halo cell of the previous segment: it only feeds its right
+// node column to lane 1) marching up a strip of cell rows.  A cell row cy
+// owns node rows 2cy (finished with the carry of the row below) and 2cy+1
+// (interior to the row); node row 2cy+2 is carried.  Node columns likewise:
+// column 2cx gets the left neighbour's right column by one shuffle, column
+// 2cx+1 is interior.  Every node is summed in a fixed order -- deterministic,
+// no atomics.  Epilogues are the ones of the Q1 kernels (op_kernels.cuh).
+#include <cstdlib>
+
+#include "cell_q2.cuh"
+#include "op_launch.cuh"
+
+namespace pffmg {
+
+template <int MODE, int EPI, bool MIE>
+__global__ void __launch_bounds__(128) op2q_kernel(const OpArgs A, const Q2Tab T) {
+    using MI = ModeInfo<2, MODE, MIE>;
+    constexpr int NF = MI::NF, NCO = MI::NCO, NV = MI::NV;
+    const Lat& L = A.L;
+    const int lane = threadIdx.x & 31;
+    const int gw = (int)blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int seg = gw % A.nseg, strip = gw / A.nseg;
+    const int cy0 = strip * A.planes_per_cta;
+    if (cy0 > L.ny) return;
+    const int cy1 = min(cy0 + A.planes_per_cta, L.ny + 1);   // cell rows whose node rows are finalised
+    const int cx = 31 * seg - 1 + lane;
+    const int nxn = 2 * L.nx + 1;
+    const int64_t V = L.V;
+
+    const double* fsrc[NF];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) fsrc[MI::F_V + i] = A.v + (int64_t)i * V;
+#pragma unroll
+    for (int i = 0; i < MI::NU; ++i) fsrc[MI::F_U + i] = A.U + (int64_t)i * V;
+    if (MI::PT) fsrc[MI::F_PT] = A.pt;
+
+    double carry_s[NCO], carry_m[NCO];     // node row 2cy from the row below: columns 2cx, 2cx+1
+#pragma unroll
+    for (int k = 0; k < NCO; ++k) carry_s[k] = carry_m[k] = 0.0;
+
+    for (int cy = cy0 - 1; cy < cy1; ++cy) {
+        double o[NCO][9];
+        const bool cell = cx >= 0 && cx < L.nx && cy >= 0 && cy < L.ny;
+        if (cell) {
+            double cv[NF][9];
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const int64_t id = (int64_t)(2 * cy + b) * nxn + 2 * cx + a;
+                    const unsigned fl = (NV > 0 && !A.premasked) ? __ldg(A.flags + id) : 0u;
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) {
+                        double x = __ldg(fsrc[f] + id);
+                        if (f < NV && ((fl >> (MI::COMP0 + f)) & 1)) x = 0.0;   // fem.py:205-206
+                        cv[f][3 * b + a] = x;
+                    }
+                }
+            if constexpr (MODE == M_FULL) {
+                if (A.nocoup) {                  // block-diagonal operator: phi(U) reads 0
+#pragma unroll
+                    for (int n = 0; n < 9; ++n) cv[MI::F_U + 2][n] = 0.0;
+                }
+            }
+            const double* rq = A.rho ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * 9 : nullptr;
+            cell_q2<MODE, MIE>(cv, rq, A.K, T, o);
+        } else {
+#pragma unroll
+            for (int k = 0; k < NCO; ++k)
+#pragma unroll
+                for (int n = 0; n < 9; ++n) o[k][n] = 0.0;
+        }
+        // node column 2cx: own left column + the left neighbour's right column
+        double s[NCO][3], m[NCO][3];
+#pragma unroll
+        for (int k = 0; k < NCO; ++k)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                s[k][b] = o[k][3 * b] + __shfl_up_sync(0xffffffffu, o[k][3 * b + 2], 1);
+                m[k][b] = o[k][3 * b + 1];
+            }
+        if (cy >= cy0 && lane >= 1 && cx >= 0 && cx <= L.nx) {
+            // (column offset, row offset, value source) of the up to four nodes
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int dx = t & 1, dy = t >> 1;
+                if (dx == 1 && cx >= L.nx) continue;
+                if (dy == 1 && cy >= L.ny) continue;
+                const int64_t id = (int64_t)(2 * cy + dy) * nxn + 2 * cx + dx;
+                double acc[NCO], vin[NCO];
+#pragma unroll
+                for (int k = 0; k < NCO; ++k) {
+                    acc[k] = dy == 0 ? (dx == 0 ? carry_s[k] + s[k][0] : carry_m[k] + m[k][0])
+                                     : (dx == 0 ? s[k][1] : m[k][1]);
+                    vin[k] = (MODE == M_DIAG || MODE == M_RES) ? 0.0 : __ldg(A.v + (int64_t)k * V + id);
+                }
+                EpiIn<NCO, EPI> ein;
+                epi_load<NCO, EPI>(A, id, ein);
+                epilogue_pre<NCO, MI::COMP0, EPI>(A, id, __ldg(A.flags + id), acc, vin, ein);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NCO; ++k) {
+            carry_s[k] = s[k][2];
+            carry_m[k] = m[k][2];
+        }
+    }
+}
+
+template <int MODE, int EPI>
+int launch2q(const OpArgs& A0, cudaStream_t s) {
+    OpArgs A = A0;
+    const Lat& L = A.L;
+    const int sms = sm_count();
+    const int nseg = (L.nx + 1 + 30) / 31;
+    const int rows = L.ny + 1;
+    int64_t per = ((int64_t)rows * nseg + 16LL * sms - 1) / (16LL * sms);
+    per = per < 1 ? 1 : (per > 32 ? 32 : per);
+    A.planes_per_cta = (int)per;
+    A.nseg = nseg;
+    const int64_t warps = (int64_t)nseg * ((rows + per - 1) / per);
+    const dim3 grid((unsigned)((warps + 3) / 4));
+    const Q2Tab T = make_q2_host(L.hx, L.hy);
+    if (A.split)
+        op2q_kernel<MODE, EPI, true><<<grid, 128, 0, s>>>(A, T);
+    else
+        op2q_kernel<MODE, EPI, false><<<grid, 128, 0, s>>>(A, T);
+    return PFFMG_OK;
+}
+
+PFFMG_INSTANTIATE_LAUNCH2(launch2q)
+
+}  // namespace pffmg

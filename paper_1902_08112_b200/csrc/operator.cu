@@ -12,7 +12,9 @@ template <int MODE, int EPI>
 static int launch(const OpArgs& A, cudaStream_t s, const char* what) {
     const Lat& L = A.L;
     const bool iso = L.hx == L.hy && (L.dim == 2 || L.hz == L.hx);
-    if (L.dim == 2)
+    if (L.order == 2)
+        launch2q<MODE, EPI>(A, s);
+    else if (L.dim == 2)
         launch2d<MODE, EPI>(A, iso, s);
     else
         launch3d<MODE, EPI>(A, iso, s);
@@ -112,7 +114,8 @@ extern "C" int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st,
     PFFMG_REQUIRE(lat && st && h_v && h_out && d_v && d_out && d_v != d_out, "pffmg_apply_host: bad pointers");
     PFFMG_REQUIRE(which == PFFMG_FULL || which == PFFMG_UBLOCK || which == PFFMG_PBLOCK,
                   "pffmg_apply_host: bad which %d", which);
-    const int nplanes = (lat->dim == 3 ? lat->nz : lat->ny) + 1;
+    const bool q2 = lat->order == 2;
+    const int nplanes = q2 ? 2 * lat->ny + 1 : (lat->dim == 3 ? lat->nz : lat->ny) + 1;
     PFFMG_REQUIRE(lat->own_lo == 0 && (lat->own_hi == 0 || lat->own_hi == nplanes),
                   "pffmg_apply_host: needs a whole (non-slab) lattice");
     PFFMG_REQUIRE(lat->vrow_off == nullptr || h_plane_off != nullptr,
@@ -129,6 +132,7 @@ extern "C" int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st,
     }
     int K = n_strips < 1 ? 1 : (n_strips > 64 ? 64 : n_strips);
     if (K > nplanes) K = nplanes;
+    if (lat->order == 2) K = 1;       // Q2: one strip (the kernel does not take node-row ranges)
     PipeRes& R = pipe_res();
     if (!R.ok) {
         set_error("pffmg_apply_host: could not create copy streams/events");
@@ -137,7 +141,8 @@ extern "C" int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st,
     const cudaStream_t s = as_stream(stream);
     const int64_t V = lat->n_vertices;
     const int nc = which == PFFMG_FULL ? lat->dim + 1 : (which == PFFMG_UBLOCK ? lat->dim : 1);
-    const int64_t per_plane = lat->dim == 3 ? (int64_t)(lat->nx + 1) * (lat->ny + 1) : (int64_t)(lat->nx + 1);
+    const int64_t per_plane = q2 ? (int64_t)(2 * lat->nx + 1)
+                                 : (lat->dim == 3 ? (int64_t)(lat->nx + 1) * (lat->ny + 1) : (int64_t)(lat->nx + 1));
     auto off = [&](int p) -> int64_t { return h_plane_off ? h_plane_off[p] : (int64_t)p * per_plane; };
     auto bound = [&](int i) -> int { return (int)(((int64_t)nplanes * i) / K); };
     const size_t pitch = (size_t)V * sizeof(double);
@@ -158,9 +163,11 @@ extern "C" int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st,
     pffmg_lattice sub = *lat;
     for (int i = 0; i < K; ++i) {
         cudaStreamWaitEvent(s, ein[i + 1 < K ? i + 1 : K - 1], 0);
-        sub.own_lo = bound(i);
-        sub.own_hi = bound(i + 1);
-        if (sub.own_hi > sub.own_lo) {
+        if (lat->order != 2) {
+            sub.own_lo = bound(i);
+            sub.own_hi = bound(i + 1);
+        }
+        if (q2 || sub.own_hi > sub.own_lo) {
             const int rc = pffmg_apply(&sub, st, which, d_v, d_out, stream);
             if (rc) return rc;
         }

@@ -129,6 +129,99 @@ __global__ void prolongate_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const do
     }
 }
 
+// ---- Q2 levels (2D boxes; node lattices, see oracle/q2.py) ----------------
+// 1D Q2 interpolation of a coarse function at the fine nodes: fine node j
+// even -> coarse node j/2; j = 4c+1 / 4c+3 -> coarse nodes 2c, 2c+1, 2c+2 with
+// weights (3/8, 3/4, -1/8) / (-1/8, 3/4, 3/8).  Restriction = its transpose:
+// coarse node i even gathers fine 2i + {-3,-1,0,1,3} with (-1/8, 3/8, 1, 3/8,
+// -1/8); i odd gathers 2i + {-1,0,1} with (3/4, 1, 3/4).
+__device__ __forceinline__ int q2_restrict_taps(int i, int (&off)[5], double (&w)[5]) {
+    if ((i & 1) == 0) {
+        off[0] = -3; off[1] = -1; off[2] = 0; off[3] = 1; off[4] = 3;
+        w[0] = -0.125; w[1] = 0.375; w[2] = 1.0; w[3] = 0.375; w[4] = -0.125;
+        return 5;
+    }
+    off[0] = -1; off[1] = 0; off[2] = 1;
+    w[0] = 0.75; w[1] = 1.0; w[2] = 0.75;
+    return 3;
+}
+
+__device__ __forceinline__ int q2_prolong_taps(int j, int (&idx)[3], double (&w)[3]) {
+    if ((j & 1) == 0) {
+        idx[0] = j >> 1;
+        w[0] = 1.0;
+        return 1;
+    }
+    const int c = j >> 2;
+    const bool first = (j & 3) == 1;
+    idx[0] = 2 * c; idx[1] = 2 * c + 1; idx[2] = 2 * c + 2;
+    w[0] = first ? 0.375 : -0.125;
+    w[1] = 0.75;
+    w[2] = first ? -0.125 : 0.375;
+    return 3;
+}
+
+// Lc / Lf are the NODE lattices (nx = 2 * cells): nxn = nx + 1 nodes per row
+__global__ void restrict_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vf,
+                                   double* __restrict__ vc, const uint8_t* __restrict__ cflags) {
+    const int nxc = Lc.nx + 1, nyc = Lc.ny + 1, nxf = Lf.nx + 1, nyf = Lf.ny + 1;
+    const int64_t npts = (int64_t)nxc * nyc;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nxc), y = (int)(i / nxc);
+        int ox[5], oy[5];
+        double wx[5], wy[5];
+        const int nx5 = q2_restrict_taps(x, ox, wx), ny5 = q2_restrict_taps(y, oy, wy);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int b = 0; b < ny5; ++b) {                    // increasing fine id (CSR order)
+            const int fy = 2 * y + oy[b];
+            if (fy < 0 || fy >= nyf) continue;
+            for (int a = 0; a < nx5; ++a) {
+                const int fx = 2 * x + ox[a];
+                if (fx < 0 || fx >= nxf) continue;
+                const int64_t fid = (int64_t)fy * nxf + fx;
+                const double w = wx[a] * wy[b];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < ncomp) acc[k] += w * __ldg(vf + (int64_t)k * Lf.V + fid);
+            }
+        }
+        const uint8_t fl = cflags ? cflags[i] : 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k >= ncomp) break;
+            vc[(int64_t)k * Lc.V + i] = ((fl >> (comp0 + k)) & 1) ? 0.0 : acc[k];
+        }
+    }
+}
+
+__global__ void prolongate_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vc,
+                                     double* __restrict__ vf, const uint8_t* __restrict__ fflags,
+                                     int accumulate) {
+    const int nxc = Lc.nx + 1, nxf = Lf.nx + 1, nyf = Lf.ny + 1;
+    const int64_t npts = (int64_t)nxf * nyf;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int X = (int)(i % nxf), Y = (int)(i / nxf);
+        int ix[3], iy[3];
+        double wx[3], wy[3];
+        const int nx3 = q2_prolong_taps(X, ix, wx), ny3 = q2_prolong_taps(Y, iy, wy);
+        const uint8_t fl = fflags ? fflags[i] : 0;
+        for (int k = 0; k < ncomp; ++k) {
+            double acc = 0.0;
+            for (int b = 0; b < ny3; ++b)
+                for (int a = 0; a < nx3; ++a)
+                    acc += (wx[a] * wy[b]) * vc[(int64_t)k * Lc.V + (int64_t)iy[b] * nxc + ix[a]];
+            const int64_t g = (int64_t)k * Lf.V + i;
+            if ((fl >> (comp0 + k)) & 1) acc = 0.0;
+            if (accumulate)
+                vf[g] += acc;
+            else
+                vf[g] = acc;
+        }
+    }
+}
+
 __global__ void inject_f64_kernel(Lat Lc, Lat Lf, int ncomp, const double* __restrict__ vf,
                                   double* __restrict__ vc) {
     const int64_t npts = owned_points(Lc);
@@ -162,11 +255,26 @@ __global__ void inject_u8_kernel(Lat Lc, Lat Lf, const uint8_t* __restrict__ ff,
     }
 }
 
-static int check_pair(const pffmg_lattice* c, const pffmg_lattice* f, Lat* Lc, Lat* Lf) {
+// Q2 levels are handled on their node lattices (a Q1-shaped lattice of twice
+// the cells): injection is then the Q1 vertex injection.
+static void to_node_lattice(Lat* L) {
+    if (L->order != 2) return;
+    L->nx *= 2;
+    L->ny *= 2;
+    L->hx *= 0.5;
+    L->hy *= 0.5;
+    L->order = 1;
+}
+
+static int check_pair(const pffmg_lattice* c, const pffmg_lattice* f, Lat* Lc, Lat* Lf, bool* q2 = nullptr) {
     int rc = make_lat(c, Lc);
     if (rc) return rc;
     rc = make_lat(f, Lf);
     if (rc) return rc;
+    PFFMG_REQUIRE(Lc->order == Lf->order, "levels of different element order");
+    if (q2) *q2 = Lc->order == 2;
+    to_node_lattice(Lc);
+    to_node_lattice(Lf);
     // the cut axis (last) may be a slab of the level: only the others must nest
     PFFMG_REQUIRE(Lc->dim == Lf->dim && Lf->nx == 2 * Lc->nx && (Lc->dim == 2 || Lf->ny == 2 * Lc->ny),
                   "levels are not nested lattices (coarse %dx%dx%d, fine %dx%dx%d)", Lc->nx, Lc->ny,
@@ -192,10 +300,16 @@ extern "C" int pffmg_restrict(const pffmg_lattice* coarse, const pffmg_lattice* 
                               int comp0, const double* vf, double* vc, const uint8_t* coarse_flags,
                               void* stream) {
     Lat Lc, Lf;
-    int rc = check_pair(coarse, fine, &Lc, &Lf);
+    bool q2 = false;
+    int rc = check_pair(coarse, fine, &Lc, &Lf, &q2);
     if (rc) return rc;
     PFFMG_REQUIRE(vf && vc && n_comp >= 1 && comp0 >= 0 && comp0 + n_comp <= Lc.dim + 1,
                   "pffmg_restrict: bad arguments");
+    if (q2) {
+        restrict_q2_kernel<<<grid_for((int64_t)(Lc.nx + 1) * (Lc.ny + 1)), 256, 0, as_stream(stream)>>>(
+            Lc, Lf, n_comp, comp0, vf, vc, coarse_flags);
+        return check_launch("pffmg_restrict");
+    }
     restrict_kernel<<<grid_for(box_points_host(Lc)), 256, 0, as_stream(stream)>>>(Lc, Lf, n_comp, comp0, vf,
                                                                                 vc, coarse_flags);
     return check_launch("pffmg_restrict");
@@ -205,10 +319,16 @@ extern "C" int pffmg_prolongate(const pffmg_lattice* coarse, const pffmg_lattice
                                 int comp0, const double* vc, double* vf, const uint8_t* fine_flags,
                                 int accumulate, void* stream) {
     Lat Lc, Lf;
-    int rc = check_pair(coarse, fine, &Lc, &Lf);
+    bool q2 = false;
+    int rc = check_pair(coarse, fine, &Lc, &Lf, &q2);
     if (rc) return rc;
     PFFMG_REQUIRE(vf && vc && n_comp >= 1 && comp0 >= 0 && comp0 + n_comp <= Lc.dim + 1,
                   "pffmg_prolongate: bad arguments");
+    if (q2) {
+        prolongate_q2_kernel<<<grid_for((int64_t)(Lf.nx + 1) * (Lf.ny + 1)), 256, 0, as_stream(stream)>>>(
+            Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
+        return check_launch("pffmg_prolongate");
+    }
     prolongate_kernel<<<grid_for(box_points_host(Lf)), 256, 0, as_stream(stream)>>>(
         Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
     return check_launch("pffmg_prolongate");

@@ -20,7 +20,7 @@ from . import _lib
 from .arrays import dev, empty, host, like
 from .lattice import LatticeMesh, build_hierarchy as _build_levels, device_lattice
 
-__all__ = ["DofMap", "LevelSpace", "Hierarchy", "Discretization", "build_hierarchy"]
+__all__ = ["DofMap", "LevelSpace", "Hierarchy", "Discretization", "build_hierarchy", "build_q2_hierarchy"]
 
 
 class DofMap:
@@ -89,6 +89,12 @@ class Hierarchy:
 
 def build_hierarchy(blocks, n_levels, dim):
     return Hierarchy(dim, _build_levels(blocks, n_levels, dim))
+
+
+def build_q2_hierarchy(lo, hi, n_coarse, n_levels):
+    """Biquadratic (Q2) box hierarchy (BASELINE configs[2]; no reference counterpart)."""
+    from .lattice import build_q2_hierarchy as _q2
+    return Hierarchy(2, _q2(lo, hi, n_coarse, n_levels))
 
 
 class Discretization:

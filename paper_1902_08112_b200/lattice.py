@@ -149,6 +149,71 @@ def build_hierarchy(blocks, n_levels, dim):
     return [LatticeMesh(blocks, l, dim) for l in range(n_levels)]
 
 
+class Q2LatticeMesh:
+    """A 2D box of nx x ny biquadratic (Q2, 9-node) cells (BASELINE configs[2]).
+
+    The reference has Q1 elements only; Q2 dofs live on the nodes of the
+    half-spacing lattice, numbered x fastest like the Q1 vertices
+    (oracle/q2.py holds the matching CPU definitions).  `n_vertices` is the
+    node count (the component stride of every dof vector)."""
+
+    order = 2
+    dim = 2
+    is_box = True
+
+    def __init__(self, lo, hi, ncell):
+        self.lo = np.asarray(lo, dtype=float) * np.ones(2)
+        hi = np.asarray(hi, dtype=float) * np.ones(2)
+        self.ncell = np.asarray(ncell, dtype=np.int64) * np.ones(2, dtype=np.int64)
+        self.cell_size = (hi - self.lo) / self.ncell
+        info = LatticeInfo(2, self.ncell, self.cell_size, self.n_vertices, True)
+        info.order = 2
+        self.lattice_info = info
+
+    @property
+    def n_node_axis(self):
+        return 2 * self.ncell + 1
+
+    @property
+    def n_vertices(self):
+        return int(np.prod(self.n_node_axis))
+
+    @property
+    def n_cells(self):
+        return int(np.prod(self.ncell))
+
+    @property
+    def cell_volume(self):
+        return float(np.prod(self.cell_size))
+
+    @property
+    def diameter(self):
+        return float(np.linalg.norm(self.cell_size))
+
+    @cached_property
+    def vertices(self):
+        """Node coordinates (V, 2), x fastest."""
+        nxn, nyn = self.n_node_axis
+        y, x = np.meshgrid(np.arange(nyn), np.arange(nxn), indexing="ij")
+        return self.lo[None, :] + np.stack([x.ravel(), y.ravel()], axis=1) * (0.5 * self.cell_size)
+
+    @cached_property
+    def cells(self):
+        """(C, 9) node ids, cells x fastest, local nodes a + 3 b."""
+        nx, ny = (int(v) for v in self.ncell)
+        nxn = 2 * nx + 1
+        cy, cx = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+        base = 2 * cx.ravel() + nxn * 2 * cy.ravel()
+        a = np.array([0, 1, 2] * 3)
+        b = np.repeat([0, 1, 2], 3)
+        return base[:, None] + a[None, :] + nxn * b[None, :]
+
+
+def build_q2_hierarchy(lo, hi, n_coarse, n_levels):
+    """Q2 levels 0 (n_coarse^2 cells) .. n_levels-1 of the box [lo, hi]^2."""
+    return [Q2LatticeMesh(lo, hi, n_coarse * 2 ** l) for l in range(n_levels)]
+
+
 # --------------------------------------------------------------- descriptors
 
 class LatticeInfo:
@@ -163,6 +228,7 @@ class LatticeInfo:
         self.rows = rows                 # (vrow_off, vrow_lo, vrow_hi, crow_lo, crow_hi) or None
         self.cell_perm = cell_perm       # mesh cell index -> lattice cell index (for rho)
         self.own = (0, 0)                # finalised planes of the last axis; (0, 0) = all
+        self.order = 1                   # element order (2: Q2 node lattice)
 
     @property
     def n_planes(self):
@@ -170,6 +236,9 @@ class LatticeInfo:
 
     def plane_offsets(self):
         """Vertex id of the first vertex of every plane of the last axis (+ V)."""
+        if getattr(self, "order", 1) == 2:
+            nxn, nyn = 2 * self.ncell + 1
+            return np.arange(nyn + 1, dtype=np.int64) * nxn
         if self.rows is None:
             per = int(np.prod(self.ncell[:-1] + 1))
             return np.arange(self.n_planes + 1, dtype=np.int64) * per
@@ -287,6 +356,7 @@ class DeviceLattice:
             L.vrow_off, L.vrow_lo, L.vrow_hi, L.crow_lo, L.crow_hi = [t.data_ptr() for t in ts]
         L.own_lo, L.own_hi = int(info.own[0]), int(info.own[1])
         L.plane0 = int(getattr(info, "plane_lo", 0))
+        L.order = int(getattr(info, "order", 1))
         self.struct = L
         self.ref = C.byref(L)
         # host plane offsets for pffmg_apply_host (NULL = box numbering)

@@ -313,7 +313,7 @@ class PhaseFieldOperator:
 def _modulus_table(space, lat, params):
     """rho(x_q) per lattice cell and QP (model.py:284-287)."""
     info = lat.info
-    Q = 2 ** lat.dim
+    Q = 9 if getattr(info, "order", 1) == 2 else 2 ** lat.dim
     ncell_lat = int(np.prod(info.ncell))
     table = np.ones((ncell_lat, Q))
     coords = getattr(space, "qp_coords", None)
@@ -338,6 +338,13 @@ def C_ptr(t):
 
 def _lattice_qp_coords(mesh):
     """QP coordinates of every lattice cell (lattice order), fem.py:181-182."""
+    if getattr(mesh, "order", 1) == 2:                    # Q2: 3x3 Gauss, qx + 3 qy
+        g = np.array([0.5 - 0.5 * np.sqrt(0.6), 0.5, 0.5 + 0.5 * np.sqrt(0.6)])
+        pts = np.stack([np.tile(g, 3), np.repeat(g, 3)], axis=1)
+        nx, ny = (int(v) for v in mesh.ncell)
+        cy, cx = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+        lo = mesh.lo[None, :] + np.stack([cx.ravel(), cy.ravel()], axis=1) * mesh.cell_size
+        return lo[:, None, :] + pts[None, :, :] * mesh.cell_size
     dim = mesh.dim
     g = np.array([0.5 - 0.5 / np.sqrt(3.0), 0.5 + 0.5 / np.sqrt(3.0)])
     idx = np.arange(2 ** dim)

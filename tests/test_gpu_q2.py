@@ -1,0 +1,136 @@
+"""Biquadratic (Q2) path -- BASELINE configs[2] -- vs the Q2 oracle
+(oracle/q2.py, itself pinned by known-answer tests; the reference has no Q2
+elements, so parity is against our CPU definitions: PARITY UNPINNED w.r.t.
+the reference).  Same bars as Q1: operator <= 1e-12, transfers <= 1e-14,
+injection exact, V-cycle <= 1e-10, GMRES iterations +-1."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import jacobian, q2, solvers
+from tests.conftest import rel_err
+from tests.golden.specs import modulus, params_for
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+GEOM = (0.0, 2.0, 2, 3)         # box [0,2]^2, 2x2 coarse cells, 3 levels (finest 8x8 Q2 cells)
+
+
+def _product(geom=GEOM):
+    from paper_1902_08112_b200.fem import Discretization, build_q2_hierarchy
+    return Discretization(build_q2_hierarchy(*geom))
+
+
+def _oracle(geom=GEOM):
+    levels = q2.q2_hierarchy(*geom)
+    return levels, [q2.Q2Tables(lev, l) for l, lev in enumerate(levels)], q2.Q2Transfers(levels)
+
+
+def _state(T, seed):
+    rng = np.random.default_rng(seed)
+    n = T.n_dofs
+    h = float(T.mesh.cell_size[0])
+    U = 0.1 * h * rng.standard_normal(n)
+    U[T.phi_slice] = np.clip(0.6 + 0.4 * rng.standard_normal(T.n_vertices), 0, 1)
+    pt = np.clip(U[T.phi_slice] + 0.05 * rng.standard_normal(T.n_vertices), 0, 1)
+    return U, pt, rng
+
+
+@pytest.mark.parametrize("split,band,mod", [("none", 0.0, False), ("none", 0.0, True),
+                                            ("miehe", 0.0, False), ("miehe", 0.02, True)])
+def test_q2_operator_matches_oracle(split, band, mod):
+    from paper_1902_08112_b200 import model as M
+    _, tables, _ = _oracle()
+    T = tables[-1]
+    U, pt, rng = _state(T, 3)
+    n = T.n_dofs
+    flags = rng.random(n) < 0.15
+    v = rng.standard_normal(n)
+    mat = params_for(T, modulus if mod else None, cls=jacobian.Material)
+    mat.split_band = band
+    st_o = jacobian.State(U=U, U_prev1=U, U_prev2=U, t=0.1, t_prev1=0.0, t_prev2=0.0, phi_tilde=pt)
+    ref = jacobian.JacobianOperator(T, st_o, flags, mat, split)
+    disc = _product()
+    space = disc.finest
+    params = params_for(space, modulus if mod else None, cls=M.MaterialParams)
+    params.split_band = band
+    st = M.LinearizationState(U=U, U_prev1=U, U_prev2=U, t=0.1, t_prev1=0.0, t_prev2=0.0, phi_tilde=pt)
+    mask = M.ConstraintMask(flags, np.zeros(n))
+    sk = M.SplitKind.MIEHE if split == "miehe" else M.SplitKind.NOSPLIT
+    op = M.PhaseFieldOperator(space, st, mask, params, sk)
+    d = T.dim * T.n_vertices
+    out = op.apply(v)
+    assert rel_err(out, ref.apply(v)) <= TOL
+    assert np.array_equal(out[flags], v[flags])
+    assert rel_err(op.apply_block(0, v[:d]), ref.apply_block(0, v[:d])) <= TOL
+    assert rel_err(op.apply_block(1, v[d:]), ref.apply_block(1, v[d:])) <= TOL
+    diag = op.diagonal()
+    assert rel_err(diag, ref.diagonal()) <= TOL and np.all(diag[flags] == 1.0)
+    res = M.residual(space, st, mask, params, sk)
+    assert rel_err(res, jacobian.residual(T, st_o, flags, mat, split)) <= TOL
+    # block-diagonal kernel == the two blocks
+    from paper_1902_08112_b200 import _lib
+    vd = torch.as_tensor(v, device="cuda")
+    bd = torch.empty_like(vd)
+    op.apply_dev(_lib.BLOCKDIAG, vd, bd)
+    assert rel_err(bd.cpu().numpy(), np.concatenate([ref.apply_block(0, v[:d]), ref.apply_block(1, v[d:])])) <= TOL
+    # pinned host path
+    vh = torch.as_tensor(v).pin_memory()
+    assert rel_err(op.apply(vh).numpy(), ref.apply(v)) <= TOL
+
+
+def test_q2_transfers_match_oracle():
+    _, _, tr = _oracle()
+    disc = _product()
+    rng = np.random.default_rng(5)
+    for l in range(2):
+        Vc, Vf = tr.levels[l].n_vertices, tr.levels[l + 1].n_vertices
+        vf, vc = rng.standard_normal(3 * Vf), rng.standard_normal(3 * Vc)
+        assert np.array_equal(disc.injection(l), tr.inj[l])
+        assert rel_err(disc.restrict(vf, l), tr.restrict(vf, l)) <= 1e-14
+        assert rel_err(disc.prolongate(vc, l), tr.prolongate(vc, l)) <= 1e-14
+        assert np.array_equal(disc.restrict_nodal(vf, l), tr.restrict_nodal(vf, l))
+
+
+def test_q2_vcycle_and_gmres_match_oracle():
+    from paper_1902_08112_b200 import krylov, mgsolve
+    from paper_1902_08112_b200 import model as M
+    levels, tables, tr = _oracle()
+    T = tables[-1]
+    U, pt, rng = _state(T, 7)
+    n = T.n_dofs
+    X = levels[-1].nodes
+    bd = np.isclose(X[:, 0], 0.0) | np.isclose(X[:, 0], 2.0) | np.isclose(X[:, 1], 0.0) | np.isclose(X[:, 1], 2.0)
+    V = T.n_vertices
+    dirichlet = np.zeros(n, bool)
+    dirichlet[np.flatnonzero(bd)] = True
+    dirichlet[V + np.flatnonzero(bd)] = True
+    active = np.zeros(n, bool)
+    active[2 * V + np.flatnonzero(rng.random(V) < 0.1)] = True
+    mat = params_for(T, None, cls=jacobian.Material)
+    st_o = jacobian.State(U=U, U_prev1=U, U_prev2=U, t=0.1, t_prev1=0.0, t_prev2=0.0, phi_tilde=pt)
+    olev = solvers.build_levels(tr, tables, st_o, active, dirichlet, mat, "none")
+    r = rng.standard_normal(n)
+    ref_v = solvers.vcycle(olev, r, "full", degree=4)
+    disc = _product()
+    params = params_for(disc.finest, None, cls=M.MaterialParams)
+    st = M.LinearizationState(U=U, U_prev1=U, U_prev2=U, t=0.1, t_prev1=0.0, t_prev2=0.0, phi_tilde=pt)
+    ctxs = mgsolve.build_level_contexts(disc, st, active, M.ConstraintMask(dirichlet, np.zeros(n)), params,
+                                        M.SplitKind.NOSPLIT)
+    for c, o in zip(ctxs, olev):
+        assert np.array_equal(c.constrained, o.constrained)
+        assert rel_err(c.diag, o.diag) <= TOL
+        sp = [(s.lambda_min_hat, s.lambda_max_hat) for s in c.spectra]
+        osp = [(s.lambda_min_hat, s.lambda_max_hat) for s in o.spectra]
+        assert np.allclose(sp, osp, rtol=1e-10, atol=0)
+    out = mgsolve.vcycle(ctxs, mgsolve.PreconditionerKind.FULL, r)
+    assert rel_err(out, ref_v) <= 1e-10
+    b = rng.standard_normal(n)
+    b[ctxs[-1].constrained] = 0.0
+    ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+    x, its = krylov.gmres(ctxs[-1].op.apply, mgsolve.VCyclePreconditioner(ctxs), b, ctl)
+    xo, its_o = solvers.gmres(olev[-1].op.apply, lambda v: solvers.vcycle(olev, v, "full", degree=4), b,
+                              solvers.Control(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000))
+    assert abs(its - its_o) <= 1
+    assert rel_err(x, xo) <= 1e-6
