@@ -49,9 +49,10 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def algorithmic_bytes(dim, V, C):
-    """B_C (cached tables, the reference algorithm) and B_F (recompute)."""
-    nc, Q = dim + 1, 2 ** dim
+def algorithmic_bytes(dim, V, C, Q=None):
+    """SURVEY §8d: B_C (cached tables, the reference algorithm) and B_F (recompute);
+    Q = quadrature points per cell (2^dim for Q1, 9 for the Q2 cfg3)."""
+    nc, Q = dim + 1, (Q or 2 ** dim)
     b_c = 16 * nc * V + 8 * Q * (2 + dim * (dim + 1) // 2) * C + nc * V
     b_f = 8 * (3 * nc + 1) * V + nc * V
     return b_c, b_f
@@ -357,7 +358,8 @@ def run_gpu(args):
         return 0
 
     hbm, peak_kind = peaks()
-    b_c, b_f = algorithmic_bytes(prob.dim, mesh.n_vertices, mesh.n_cells)
+    b_c, b_f = algorithmic_bytes(prob.dim, mesh.n_vertices, mesh.n_cells,
+                                 9 if getattr(mesh, "order", 1) == 2 else None)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_vmult_cfg2.json")
     if os.path.exists(prof) and args.config == "cfg2":
@@ -370,7 +372,11 @@ def run_gpu(args):
     peak_all = hbm * ws                           # aggregate over the ranks
     workload = (f"{args.config}: 2D notched square 1024^2 Q1 NoSplit vmult" if ws == 1 else
                 f"{args.config} x{ws}: {ws} stacked 1024^2 notched squares (1024 x {1024 * ws} Q1), "
-                f"y-slab per GPU, {args.backend} halo exchange + fused vmult") if args.config == "cfg2" else args.config
+                f"y-slab per GPU, {args.backend} halo exchange + fused vmult") if args.config == "cfg2" else \
+        {"cfg1": "cfg1: 2D notched square 64^2 Q1 NoSplit vmult",
+         "cfg3": "cfg3: 2D pressurised cracks 512^2 Q2 (3x3 Gauss) NoSplit vmult, p = 1e-3",
+         "cfg4": "cfg4: 3D L-prism 786k Q1 hexes NoSplit vmult",
+         "cfg5": "cfg5: 3D cube 384^3 Q1 hexes NoSplit vmult"}.get(args.config, args.config)
     line = {
         "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
@@ -416,7 +422,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="pffmg", choices=["pffmg", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg4", "cfg5"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],

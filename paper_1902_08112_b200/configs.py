@@ -10,7 +10,8 @@ Choices BASELINE.json leaves open follow SURVEY Appendix A.
   cfg2  same, 8 levels (1024^2), Cheb deg 3
   cfg4  3D L-prism [0,1]^2\\[0.5,1]^2 x [0,0.5], 0.25 blocks, 6 levels (128/unit)
   cfg5  3D unit cube, 3^3 blocks, 8 levels (384^3), penny crack r = 0.2
-(cfg3 needs Q2 elements, which the reference does not implement -- not built.)
+  cfg3  2D pressurised cracks on [-20,20]^2, 512^2 biquadratic (Q2) cells, 7 levels
+        (the reference has no Q2 elements: our own Q2 definitions, oracle/q2.py)
 """
 from __future__ import annotations
 
@@ -18,7 +19,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .fem import Discretization, build_hierarchy
+from .fem import Discretization, build_hierarchy, build_q2_hierarchy
 from .model import ConstraintMask, LinearizationState, MaterialParams
 
 
@@ -173,17 +174,64 @@ def penny_cube(n_levels=8, degree=4, name="cfg5"):
                    ConstraintMask(flags, vals), active, v, degree, disc)
 
 
+def _segment_distance(P, c, ang, half):
+    d = np.array([np.cos(ang), np.sin(ang)])
+    rel = P - c[None, :]
+    t = np.clip(rel @ d, -half, half)
+    return np.linalg.norm(rel - t[:, None] * d[None, :], axis=1)
+
+
+def pressurized_cracks(n_levels=7, degree=4, name="cfg3", n_coarse=8):
+    """cfg3 (BASELINE configs[2]): three straight phi = 0 cracks of
+    length 4 with seeded centres ~ U([-15,15]^2) and angles ~ U[0, pi) in
+    [-20,20]^2, biquadratic cells, p = 1e-3, u = 0 on the whole boundary,
+    active set = crack nodes, u ~ N(0, 1e-4).  Material: the reference's
+    fracture values (scenarios.py:223-227)."""
+    disc = Discretization(build_q2_hierarchy(-20.0, 20.0, n_coarse, n_levels))
+    mesh = disc.hierarchy.finest
+    V = mesh.n_vertices
+    h = float(mesh.cell_size[0])
+    X = mesh.vertices
+    rng = np.random.default_rng(0)
+    centres = rng.uniform(-15.0, 15.0, (3, 2))
+    angles = rng.uniform(0.0, np.pi, 3)
+    crack = np.zeros(V, dtype=bool)
+    for c, a in zip(centres, angles):
+        crack |= _segment_distance(X, c, a, 2.0) < h
+    phi = np.where(crack, 0.0, 1.0)
+    U = np.empty(3 * V)
+    U[:2 * V] = rng.normal(0.0, 1e-4, 2 * V)
+    U[2 * V:] = phi
+    bd = (np.isclose(X[:, 0], -20.0) | np.isclose(X[:, 0], 20.0) | np.isclose(X[:, 1], -20.0)
+          | np.isclose(X[:, 1], 20.0))
+    flags = np.zeros(3 * V, dtype=bool)
+    flags[np.flatnonzero(bd)] = True
+    flags[V + np.flatnonzero(bd)] = True
+    U[flags] = 0.0
+    active = np.zeros(3 * V, dtype=bool)
+    active[2 * V + np.flatnonzero(crack)] = True
+    params = MaterialParams(mu=4166.67, lam=2777.78, g_c=1.0, kappa=1e-10, eps=2.0 * h,
+                            pressure_fn=lambda t: 1e-3)
+    state = LinearizationState(U=U, U_prev1=U.copy(), U_prev2=U.copy(), t=0.0, t_prev1=0.0,
+                               t_prev2=0.0, phi_tilde=phi.copy())
+    v = np.random.default_rng(1).standard_normal(3 * V)
+    return Problem(name, 2, [[(-20.0, -20.0), (20.0, 20.0)]], n_levels, params, state,
+                   ConstraintMask(flags, np.zeros(3 * V)), active, v, degree, disc)
+
+
 def make(name, n_levels=None):
     """Problem by config name; `n_levels` shrinks the hierarchy for parity runs."""
     if name == "cfg1":
         return notched_square(n_levels or 4, 4, name)
     if name == "cfg2":
         return notched_square(n_levels or 8, 3, name)
+    if name == "cfg3":
+        return pressurized_cracks(n_levels or 7, 4, name)
     if name == "cfg4":
         return lprism(n_levels or 6, 4, name)
     if name == "cfg5":
         return penny_cube(n_levels or 8, 4, name)
-    raise KeyError(f"unknown config {name!r} (cfg3 needs Q2 elements: not available)")
+    raise KeyError(f"unknown config {name!r}")
 
 
 def fallback_rhs(problem):
