@@ -76,3 +76,37 @@ def test_newton_rhs_on_gpu_matches_reference(golden, name, levels, tag):
     R = -M.residual(prob.disc.finest, prob.state, prob.dirichlet, prob.params, M.SplitKind.NOSPLIT)
     R[mask.is_constrained] = 0.0
     assert rel_err(R, g[f"{tag}/gmres_rhs"]) <= 1e-12
+
+
+def test_cfg3_q2_newton_step_matches_oracle():
+    """cfg3 (Q2, pressure) at 4 levels (64^2 Q2 cells): Newton RHS, level
+    contexts, and the GMRES iteration count against the Q2 oracle."""
+    from oracle import jacobian, q2, solvers
+    from paper_1902_08112_b200 import krylov, mgsolve
+    from paper_1902_08112_b200 import model as M
+    prob, mask, op = _setup("cfg3", 4)
+    levels = q2.q2_hierarchy(-20.0, 20.0, 8, 4)
+    tables = [q2.Q2Tables(lev, l) for l, lev in enumerate(levels)]
+    tr = q2.Q2Transfers(levels)
+    p = prob.params
+    mat = jacobian.Material(mu=p.mu, lam=p.lam, g_c=p.g_c, kappa=p.kappa, eps=p.eps,
+                            pressure_fn=p.pressure_fn)
+    s = prob.state
+    st = jacobian.State(U=s.U, U_prev1=s.U_prev1, U_prev2=s.U_prev2, t=s.t, t_prev1=s.t_prev1,
+                        t_prev2=s.t_prev2, phi_tilde=s.phi_tilde)
+    R_ref = -jacobian.residual(tables[-1], st, prob.dirichlet.is_constrained, mat)
+    R_ref[mask.is_constrained] = 0.0
+    R = -M.residual(prob.disc.finest, s, prob.dirichlet, p, M.SplitKind.NOSPLIT)
+    R[mask.is_constrained] = 0.0
+    assert rel_err(R, R_ref) <= 1e-12
+    olev = solvers.build_levels(tr, tables, st, prob.active, prob.dirichlet.is_constrained, mat, "none")
+    ctxs = mgsolve.build_level_contexts(prob.disc, s, prob.active, prob.dirichlet, p, M.SplitKind.NOSPLIT)
+    for c, o in zip(ctxs, olev):
+        assert np.array_equal(c.constrained, o.constrained)
+        assert rel_err(c.diag, o.diag) <= 1e-12
+    ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+    x, its = krylov.gmres(ctxs[-1].op.apply, mgsolve.VCyclePreconditioner(ctxs, degree=prob.degree), R, ctl)
+    xo, its_o = solvers.gmres(olev[-1].op.apply, lambda v: solvers.vcycle(olev, v, "full", degree=prob.degree),
+                              R_ref, solvers.Control(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000))
+    assert abs(its - its_o) <= 1, (its, its_o)
+    assert rel_err(x, xo) <= 1e-6
