@@ -186,6 +186,16 @@ int pffmg_cheb_init_zero_bd(const double* b, const double* invdiag, const double
                             const double* theta_p, int64_t n_u, double* r, double* d, double* x,
                             int64_t n, void* stream);
 
+/* The whole coarse_solve of the V-cycle (mgsolve.py:209-218) in one launch for
+ * small whole levels (<= 256 lattice cells): both blocks' Chebyshev
+ * recurrences from x = 0 with degrees deg_u / deg_p and the coefficient
+ * tables coef_u / coef_p = [theta, c_dd_1, c_dr_1, ...] (device memory, as
+ * for the _dc entry points).  b, x, r, d, invdiag: full vectors of the level.
+ * Returns PFFMG_ERR_UNSUPPORTED for larger levels. */
+int pffmg_coarse_cheb(const pffmg_lattice* lat, const pffmg_state* st, const double* b, double* x,
+                      double* r, double* d, const double* invdiag, const double* coef_u, int deg_u,
+                      const double* coef_p, int deg_p, void* stream);
+
 /* ---------------------------------------------------------------- transfers */
 /* fem.py:308-411 with the V-cycle masking of mgsolve.py:228-234.
  * `coarse`/`fine` are consecutive levels l and l+1; n_comp components. */

@@ -236,6 +236,9 @@ REUSE_SETUP = os.environ.get("PFFMG_REUSE_SETUP", "1") != "0"
 # Smooth both diagonal blocks with one block-diagonal kernel per Chebyshev step
 # (PFFMG_BLOCKDIAG_SMOOTH=0: one kernel per block and step, the reference's order).
 BLOCKDIAG_SMOOTH = os.environ.get("PFFMG_BLOCKDIAG_SMOOTH", "1") != "0"
+# Coarsest-level solve in one kernel (pffmg_coarse_cheb) when the level is small;
+# PFFMG_COARSE_KERNEL=0: one kernel per Chebyshev step.
+COARSE_KERNEL = os.environ.get("PFFMG_COARSE_KERNEL", "1") != "0"
 
 
 def build_level_contexts(disc, state, active_mask, dirichlet_mask, params, split,
@@ -591,6 +594,8 @@ class _Level:
         # (launch-latency-bound) 3D levels; large 3D levels are FP64-bound and
         # run faster as two block kernels (measured, cfg4)
         self.bd_ok = self.dim == 2 or self.V < (1 << 17)
+        info = op.lat.info
+        self.coarse_ok = int(np.prod(info.ncell)) <= 256 and tuple(info.own) == (0, 0)
 
     def blk(self, k):
         return slice(0, self.dim * self.V) if k == 0 else slice(self.dim * self.V, self.n)
@@ -742,7 +747,17 @@ class _NativeCycle:
         self._cheb_pair(self.levels[l], ("s", l, 0), ("s", l, 1), x_is_zero)
 
     def _coarse_into_x(self, pre=True):
-        self._cheb_pair(self.levels[0], ("c", 0, 0), ("c", 0, 1), True, pre)
+        L = self.levels[0]
+        ou, pu, degu = self.slot[("c", 0, 0)]
+        op_, pp, degp = self.slot[("c", 0, 1)]
+        if COARSE_KERNEL and L.coarse_ok and not (degu or degp):
+            # the whole coarse_solve in one launch (libpffmg pffmg_coarse_cheb)
+            c = self.coef
+            _lib.call("pffmg_coarse_cheb", L.op.lat.ref, L.op._sp(pre), _lib.ptr(L.r), _lib.ptr(L.x),
+                      _lib.ptr(L.cr), _lib.ptr(L.d0), _lib.ptr(L.inv), _lib.ptr(c[ou:]), pu.degree,
+                      _lib.ptr(c[op_:]), pp.degree, _lib.stream())
+            return
+        self._cheb_pair(L, ("c", 0, 0), ("c", 0, 1), True, pre)
 
     def _cycle(self, l):                                   # mgsolve.py:221-235
         if l == 0:

@@ -256,3 +256,22 @@ def test_blockdiag_smoothing_matches_per_block(golden, name, monkeypatch):
         disc, ctxs = _contexts(g, name)
         out.append(mgsolve.vcycle(ctxs, FULL, r).cpu().numpy())
     assert rel_err(out[0], out[1]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", MG)
+def test_coarse_kernel_matches_per_step(golden, name, monkeypatch):
+    """Single-launch coarse solve (pffmg_coarse_cheb) == the per-step kernels."""
+    from paper_1902_08112_b200 import mgsolve
+    g = golden["multigrid"]
+    rc = g[f"{name}/coarse_r"]
+    r = torch.as_tensor(g[f"{name}/r"], device="cuda")
+    out = []
+    for flag in (True, False):
+        monkeypatch.setattr(mgsolve, "COARSE_KERNEL", flag)
+        mgsolve._Session._cache.clear()
+        disc, ctxs = _contexts(g, name)
+        out.append((mgsolve.vcycle(ctxs, mgsolve.PreconditionerKind.FULL, r).cpu().numpy(),
+                    mgsolve.coarse_solve(ctxs[0], rc)))
+    assert rel_err(out[0][0], out[1][0]) <= 1e-12
+    assert rel_err(out[0][1], out[1][1]) <= 1e-12
+    assert rel_err(out[0][1], g[f"{name}/coarse"]) <= 1e-10
