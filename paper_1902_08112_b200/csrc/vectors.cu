@@ -9,6 +9,8 @@
 // Scalars that steer later kernels (GMRES H entries, CG alpha/beta, stop
 // flags) stay in device memory so no host round trip is needed between steps.
 #include <cmath>
+#include <mutex>
+#include <unordered_map>
 
 #include "cellops_miehe.cuh"
 
@@ -22,18 +24,25 @@ struct Scratch {
     unsigned int counter;
 };
 
-static Scratch* g_scratch = nullptr;
-
-static int scratch(Scratch** out) {
-    if (!g_scratch) {
-        if (cudaMalloc(&g_scratch, sizeof(Scratch)) != cudaSuccess ||
-            cudaMemset(g_scratch, 0, sizeof(Scratch)) != cudaSuccess) {
-            g_scratch = nullptr;
-            set_error("cannot allocate reduction scratch");
-            return PFFMG_ERR_CUDA;
-        }
+// One scratch block per stream: reductions on different streams (e.g. the
+// concurrent per-level CG-Lanczos branches of the recorded setup graph) must
+// not share the partials / last-block counter.
+static int scratch(cudaStream_t stream, Scratch** out) {
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, Scratch*> table;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = table.find(stream);
+    if (it != table.end()) {
+        *out = it->second;
+        return PFFMG_OK;
     }
-    *out = g_scratch;
+    Scratch* S = nullptr;
+    if (cudaMalloc(&S, sizeof(Scratch)) != cudaSuccess || cudaMemset(S, 0, sizeof(Scratch)) != cudaSuccess) {
+        set_error("cannot allocate reduction scratch");
+        return PFFMG_ERR_CUDA;
+    }
+    table[stream] = S;
+    *out = S;
     return PFFMG_OK;
 }
 
@@ -102,7 +111,7 @@ __global__ void __launch_bounds__(RT) fused_kernel(Op op, int64_t n, Scratch* S)
 template <class Op>
 static int run_fused(const Op& op, int64_t n, cudaStream_t s, const char* what) {
     Scratch* S;
-    int rc = scratch(&S);
+    int rc = scratch(s, &S);
     if (rc) return rc;
     fused_kernel<Op><<<red_blocks(n), RT, 0, s>>>(op, n, S);
     return check_launch(what);

@@ -364,6 +364,7 @@ class _Session:
         self.spectra = None
         self._prev = []
         self._cycles = {}
+        self._streams = None
 
     # -- device work of one setup (recorded once, replayed per Newton step)
     def _device_setup(self):
@@ -374,13 +375,25 @@ class _Session:
             D.inject_dev(self.P1[l + 1], self.P1[l], l, self.nc)
             D.inject_dev(self.P2[l + 1], self.P2[l], l, self.nc)
             D.inject_dev(self.PT[l + 1], self.PT[l], l, 1)
-        scals = []
         for l in range(self.L):
             self.ops[l].diagonal_dev(self.diag[l])
             _lib.call("pffmg_reciprocal", _lib.ptr(self.diag[l]), _lib.ptr(self.inv[l]),
                       self.diag[l].numel(), s)
-            scals += _cg_native(self.ops[l], self.diag[l], self.eig_iters, self.seed)
-        return torch.stack(scals)
+        # the 2L block CG-Lanczos runs are independent: one stream per level, so the
+        # latency-bound coarse-level ones overlap the fine level's (each stream has
+        # its own reduction scratch in libpffmg)
+        main = torch.cuda.current_stream()
+        if self._streams is None:
+            self._streams = [torch.cuda.Stream() for _ in range(self.L)]
+        scals = [None] * self.L
+        for l in range(self.L - 1, -1, -1):
+            st = self._streams[l]
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
+                scals[l] = _cg_native(self.ops[l], self.diag[l], self.eig_iters, self.seed)
+        for st in self._streams:
+            main.wait_stream(st)
+        return torch.stack([t for pair in scals for t in pair])
 
     def _detach_previous(self):
         """Give still-referenced contexts / operators of the last build private buffers."""
