@@ -26,6 +26,8 @@ def step():
     R = M.residual(prob.disc.finest, st, prob.dirichlet, prob.params, M.SplitKind.NOSPLIT)
     R.neg_()
     R[cm] = 0
+    torch.cuda.synchronize()
+    print("  residual", time.perf_counter() - t0)
     ctxs = mgsolve.build_level_contexts(prob.disc, st, prob.active, prob.dirichlet, prob.params,
                                         M.SplitKind.NOSPLIT)
     torch.cuda.synchronize()
@@ -39,6 +41,12 @@ def step():
 
 step()
 print("wall", step())
+import cProfile, pstats
+pr = cProfile.Profile()
+pr.enable()
+step()
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(15)
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     res = step()
 print("profiled wall", res)
