@@ -3,6 +3,7 @@
 // op_kernels.cuh).  Replaces reference model.py:368-413 and the vector
 // updates of mgsolve.py:82-113 / 227 (fused epilogues).
 #include <cmath>
+#include <cstdlib>
 
 #include "op_launch.cuh"
 
@@ -144,7 +145,20 @@ extern "C" int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st,
     const int64_t per_plane = q2 ? (int64_t)(2 * lat->nx + 1)
                                  : (lat->dim == 3 ? (int64_t)(lat->nx + 1) * (lat->ny + 1) : (int64_t)(lat->nx + 1));
     auto off = [&](int p) -> int64_t { return h_plane_off ? h_plane_off[p] : (int64_t)p * per_plane; };
-    auto bound = [&](int i) -> int { return (int)(((int64_t)nplanes * i) / K); };
+    // Strip i's kernel waits for the copies of strips i and i+1, and the copy out
+    // of the last strip runs alone: small strips at both ends shorten the
+    // exposed head and tail (triangular weights 1, 2, .., 2, 1).
+    static const int tri = [] {
+        const char* e = getenv("PFFMG_PIPE_TRI");
+        return e ? atoi(e) : 1;
+    }();
+    int wsum = 0, wcum[65] = {0};
+    for (int i = 0; i < K; ++i) {
+        const int w = tri ? min(i + 1, K - i) : 1;
+        wsum += w;
+        wcum[i + 1] = wsum;
+    }
+    auto bound = [&](int i) -> int { return (int)(((int64_t)nplanes * wcum[i]) / wsum); };
     const size_t pitch = (size_t)V * sizeof(double);
     cudaEvent_t* ein = R.ev;          // [K]
     cudaEvent_t* ek = R.ev + 64;      // [K]

@@ -233,7 +233,7 @@ class PhaseFieldOperator:
         if bufs is None:
             bufs = self._host_bufs = (empty(n), empty(n))
         po = self.lat.plane_off_host
-        strips = int(max(1, min(8, round(8 * n / (6 << 20)))))  # ~6 MiB per strip and direction
+        strips = int(max(1, min(8, round(8 * n / (4 << 20)))))  # ~4 MiB per strip and direction
         _lib.call("pffmg_apply_host", self.lat.ref, self._stp, _lib.FULL, C_ptr(v), C_ptr(out),
                   _lib.ptr(bufs[0]), _lib.ptr(bufs[1]), None if po is None else po.ctypes.data,
                   strips, _lib.stream())
