@@ -156,8 +156,15 @@ class Halo:
 
         With NCCL the planes go device to device; with gloo (CPU tests, or
         ranks sharing one GPU in tests) CUDA planes are staged through host memory."""
+        self.finish(self.start(vec, n_comp))
+        return vec
+
+    def start(self, vec, n_comp):
+        """Post the exchange; returns a handle for finish().  Under NCCL the
+        transfers run on NCCL's stream, concurrently with work enqueued on the
+        current stream afterwards (which must not touch the ghost planes)."""
         if self.world == 1 or self.slab.replicated:
-            return vec
+            return None
         stage = vec.is_cuda and _backend(self.group) != "nccl"
         ops, back = [], []
         V = self.V
@@ -178,12 +185,18 @@ class Halo:
                 ops.append(dist.P2POp(dist.irecv, r, peer, self.group))
                 if stage:
                     back.append((vec[base + a:base + b], r))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        return reqs, back
+
+    @staticmethod
+    def finish(handle):
+        if handle is None:
+            return
+        reqs, back = handle
+        for req in reqs:
+            req.wait()
         for dst, src in back:
             dst.copy_(src)
-        return vec
 
 
 def _backend(group=None):
@@ -261,7 +274,21 @@ class DistributedOperator:
         return to_local(vec, self.n_comp, self.info_global, self.slab)
 
     def apply_local(self, v_loc, out_loc):
-        """out (owned rows) = G~ v, after refreshing v's ghost planes."""
+        """out (owned rows) = G~ v, after refreshing v's ghost planes.
+
+        The halo exchange overlaps the interior rows (their cells read owned
+        planes only; NCCL runs on its own stream, gloo stages through the host);
+        the two boundary rows run after it lands."""
+        lo, hi = self.info.own if self.info.own != (0, 0) else (0, self.info.n_planes)
+        if (hasattr(self.local, "apply_rows_dev") and v_loc.is_cuda and self.world > 1
+                and hi - lo >= 3 and not self.slab.replicated):
+            from . import _lib
+            h = self.halo.start(v_loc, self.n_comp)
+            self.local.apply_rows_dev(_lib.FULL, v_loc, out_loc, lo + 1, hi - 1)
+            self.halo.finish(h)
+            self.local.apply_rows_dev(_lib.FULL, v_loc, out_loc, lo, lo + 1)
+            self.local.apply_rows_dev(_lib.FULL, v_loc, out_loc, hi - 1, hi)
+            return out_loc
         self.halo.exchange(v_loc, self.n_comp)
         if hasattr(self.local, "apply_dev") and v_loc.is_cuda:
             from . import _lib

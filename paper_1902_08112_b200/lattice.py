@@ -359,9 +359,21 @@ class DeviceLattice:
         L.order = int(getattr(info, "order", 1))
         self.struct = L
         self.ref = C.byref(L)
+        self._rows = {}
         # host plane offsets for pffmg_apply_host (NULL = box numbering)
         self.plane_off_host = (None if info.rows is None
                                else np.ascontiguousarray(info.plane_offsets(), dtype=np.int64))
+
+    def rows(self, lo, hi):
+        """The same lattice finalising only planes [lo, hi) of the last axis."""
+        key = (int(lo), int(hi))
+        ref = self._rows.get(key)
+        if ref is None:
+            L = _lib.Lattice()
+            C.pointer(L)[0] = self.struct
+            L.own_lo, L.own_hi = key
+            ref = self._rows[key] = (L, C.byref(L))
+        return ref[1]
 
     @property
     def n_lattice_cells(self):

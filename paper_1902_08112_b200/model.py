@@ -265,6 +265,11 @@ class PhaseFieldOperator:
         _lib.call("pffmg_apply", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(out),
                   _lib.stream())
 
+    def apply_rows_dev(self, which, x, out, lo, hi, pre=False):
+        """apply_dev finalising only vertex planes [lo, hi) of the last axis."""
+        _lib.call("pffmg_apply", self.lat.rows(lo, hi), self._sp(pre), which, _lib.ptr(x), _lib.ptr(out),
+                  _lib.stream())
+
     def residual_dev(self, which, x, b, out, pre=False):
         _lib.call("pffmg_residual", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
                   _lib.ptr(out), _lib.stream())

@@ -48,6 +48,16 @@ def test_slab_operator_stitches(name, world):
         v_loc = torch.as_tensor(op.to_local(v), device="cuda")     # ghosts already true values
         out = torch.zeros(op.n_local, dtype=torch.float64, device="cuda")
         op.local.apply_dev(_lib.FULL, v_loc, out)
+        # the overlapped form of DistributedOperator.apply_local: interior rows,
+        # then the two boundary rows, must give the same owned values bitwise
+        lo, hi = op.info.own if op.info.own != (0, 0) else (0, op.info.n_planes)
+        if hi - lo >= 3:
+            out2 = torch.zeros_like(out)
+            op.local.apply_rows_dev(_lib.FULL, v_loc, out2, lo + 1, hi - 1)
+            op.local.apply_rows_dev(_lib.FULL, v_loc, out2, lo, lo + 1)
+            op.local.apply_rows_dev(_lib.FULL, v_loc, out2, hi - 1, hi)
+            for sl in op.owned:
+                assert torch.equal(out[sl], out2[sl])
         s = part.slab(L)
         a, b = int(offs[s.own_lo]), int(offs[s.own_hi])
         per = b - a
