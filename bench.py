@@ -38,6 +38,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "PFF Jacobian vmult GDoF/s and GMG-GMRES solve time/Newton step, % HBM roofline"
+FP64_PEAK_TFLOPS = 34.2     # B200 FP64 FMA throughput measured with tools/microbench.cu
 
 
 def peaks():
@@ -363,14 +364,16 @@ def run_gpu(args):
     hbm, peak_kind = peaks()
     b_c, b_f = algorithmic_bytes(prob.dim, mesh.n_vertices, mesh.n_cells,
                                  9 if getattr(mesh, "order", 1) == 2 else None)
-    traffic = None
+    traffic = flops = None
     prof = os.path.join(ROOT, "profiles", "ncu_vmult_cfg2.json")
     if os.path.exists(prof) and args.config == "cfg2":
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                pj = json.load(f)
+            traffic = pj.get("dram_bytes_per_launch")
+            flops = pj.get("fp64_flops_per_launch")
         except Exception:
-            traffic = None
+            traffic = flops = None
     achieved = b_c / per * 1e-9
     peak_all = hbm * ws                           # aggregate over the ranks
     workload = (f"{args.config}: 2D notched square 1024^2 Q1 NoSplit vmult" if ws == 1 else
@@ -395,7 +398,14 @@ def run_gpu(args):
                      "algorithmic_bytes_BC": b_c, "algorithmic_bytes_BF": b_f,
                      "frac_BF": b_f / per * 1e-9 / peak_all,
                      "frac_ncu": (traffic / per * 1e-9 / hbm) if (traffic and ws == 1) else None,
-                     "peak_kind": peak_kind + (f" x{ws} GPUs" if ws > 1 else "")},
+                     "peak_kind": peak_kind + (f" x{ws} GPUs" if ws > 1 else ""),
+                     # the kernel recomputes the coefficient tables: its own ceiling is FP64
+                     # issue; flops = SASS DFMA x2 + DADD + DMUL of the ncu capture
+                     "fp64": ({"achieved": flops / per * 1e-12, "peak": FP64_PEAK_TFLOPS * ws,
+                               "unit": "TFLOP/s", "frac": flops / per * 1e-12 / FP64_PEAK_TFLOPS,
+                               "flops_per_launch": flops,
+                               "peak_kind": "measured, tools/microbench.cu DFMA chains"}
+                              if (flops and ws == 1) else None)},
         "e2e": {"value": n / e2e_per * 1e-9, "unit": "GDoF/s", "h2d_bytes_per_step": e2e_bytes,
                 "d2h_bytes_per_step": e2e_bytes,
                 "path": ("PhaseFieldOperator.apply(pinned host tensor, out=pinned host tensor)" if ws == 1

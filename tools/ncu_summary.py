@@ -39,6 +39,26 @@ def raw(rep):
     return rows[0], rows[1], rows[2:]
 
 
+def opcode_counts(rep):
+    """Warp-level executed instructions per SASS opcode of the first captured kernel."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--print-metric-instances", "details",
+                          "--metrics", "sass__inst_executed_per_opcode"], capture_output=True, text=True).stdout
+    flat = " ".join(out.split())
+    i = flat.find("sass__inst_executed_per_opcode")
+    if i < 0 or "(" not in flat[i:]:
+        return {}
+    body = flat[flat.index("(", i) + 1:flat.index(")", i)]
+    counts = {}
+    for part in body.split(";"):
+        if ":" in part:
+            k, v = part.split(":", 1)
+            try:
+                counts[k.strip()] = float(v.strip().replace(",", ""))
+            except ValueError:
+                pass
+    return counts
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rep", required=True)
@@ -78,6 +98,12 @@ def main():
     wb = k0["dram_write_MB"] * scale.get(k0.get("dram_write_MB_unit", "Mbyte"), 1e6)
     summary = {"name": a.name, "source": os.path.basename(a.rep), "kernels": kernels,
                "dram_bytes_per_launch": rb + wb, "note": a.note}
+    ops = opcode_counts(a.rep)
+    if ops:
+        # FP64 flops per launch: DFMA = 2, DADD / DMUL = 1, per thread (32 per warp instruction)
+        summary["fp64_flops_per_launch"] = 32.0 * (2.0 * ops.get("DFMA", 0.0) + ops.get("DADD", 0.0)
+                                                   + ops.get("DMUL", 0.0))
+        summary["opcodes_top"] = dict(sorted(ops.items(), key=lambda kv: -kv[1])[:16])
     if a.launches:
         lines = [l for l in open(a.launches) if not l.startswith("==")]
         lr = list(csv.reader(lines))
@@ -106,6 +132,10 @@ def main():
         md.append(f"- stalls (warps per issue): {d['stalls_per_issue']}")
         md.append("")
     md.append(f"DRAM bytes per launch (read + write): {summary['dram_bytes_per_launch'] / 1e6:.2f} MB")
+    if "fp64_flops_per_launch" in summary:
+        md.append(f"FP64 flops per launch (SASS DFMA x2 + DADD + DMUL): "
+                  f"{summary['fp64_flops_per_launch'] / 1e6:.1f} MFLOP")
+        md.append(f"Top opcodes (warp instructions): {summary['opcodes_top']}")
     if "launch_list" in summary:
         md += ["", "## Launch list (ncu --metrics gpu__time_duration.sum, serialised, cold)", "",
                "| share | launches | mean us | kernel |", "|---|---|---|---|"]
