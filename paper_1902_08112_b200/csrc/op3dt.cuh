@@ -41,6 +41,21 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
     const int nwords = (V + 3) / 4 + 8;
     const bool lane_cell = lane <= 30;
 
+    if (!BOX) {
+        // tiles of the bounding lattice that hold no vertex (e.g. the missing
+        // quadrant of an L-shape) leave at once
+        int any = 0;
+        const int np = vz1 - vz0 + 2;
+        for (int e = tid; e < ROWS * np; e += 32 * TY) {
+            const int y = y0 + e % ROWS, z = vz0 - 1 + e / ROWS;
+            if ((unsigned)y > (unsigned)L.ny || (unsigned)z > (unsigned)L.nz) continue;
+            const int r = y + (L.ny + 1) * z;
+            const int lo = __ldg(L.vrow_lo + r), hi = __ldg(L.vrow_hi + r);
+            if (hi > lo && hi > x0 && lo <= x0 + 31) any = 1;
+        }
+        if (!__syncthreads_or(any)) return;
+    }
+
     const double* fsrc[NF];
 #pragma unroll
     for (int i = 0; i < NV; ++i) fsrc[MI::F_V + i] = A.v + (int64_t)i * V;
