@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(128) op2q_kernel(const OpArgs A, const Q2Tab T
                 }
                 EpiIn<NCO, EPI> ein;
                 epi_load<NCO, EPI>(A, id, ein);
-                epilogue_pre<NCO, MI::COMP0, EPI>(A, id, __ldg(A.flags + id), acc, vin, ein);
+                epilogue<NCO, MI::COMP0, EPI>(A, id, __ldg(A.flags + id), acc, vin, ein);
             }
         }
 #pragma unroll

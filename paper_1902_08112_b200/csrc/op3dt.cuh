@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
                                  : (((fl >> (MI::COMP0 + k)) & 1) ? A.v[(int64_t)k * V + vid]
                                                                   : p0[((MI::F_V + k) * ROWS + w) * W + lane]);
                 }
-                epilogue_pre<NCO, MI::COMP0, EPI>(A, vid, (uint8_t)fl, acc, vin, ein);
+                epilogue<NCO, MI::COMP0, EPI>(A, vid, (uint8_t)fl, acc, vin, ein);
             }
 #pragma unroll
             for (int k = 0; k < NCO; ++k) carry[k] = top[k];

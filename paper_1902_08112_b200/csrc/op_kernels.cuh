@@ -48,45 +48,6 @@ struct OpArgs {
 
 // ------------------------------------------------------------ epilogue
 
-template <int NCO, int COMP0, int EPI>
-__device__ __forceinline__ void epilogue(const OpArgs& A, int64_t vid, uint8_t fl,
-                                         const double (&acc)[NCO], const double (&vin)[NCO]) {
-    const int64_t V = A.L.V;
-#pragma unroll
-    for (int k = 0; k < NCO; ++k) {
-        const bool con = (fl >> (COMP0 + k)) & 1;
-        const int64_t g = (int64_t)k * V + vid;
-        if (EPI == E_DIAG) {
-            A.out[g] = con ? 1.0 : acc[k];                       // model.py:412
-            continue;
-        }
-        if (EPI == E_RESZ) {
-            A.out[g] = con ? 0.0 : acc[k];                       // model.py:459
-            continue;
-        }
-        const double Av = con ? vin[k] : acc[k];                 // model.py:373-374, 390-391
-        if (EPI == E_STORE) {
-            A.out[g] = Av;
-        } else if (EPI == E_RESID) {
-            A.out[g] = A.b[g] - Av;                              // mgsolve.py:227
-        } else if (EPI == E_CHEB) {                              // mgsolve.py:108-111
-            const double rr = A.r[g] - Av;
-            const double* cf = (A.coef2 && COMP0 + k == A.L.dim) ? A.coef2 : A.coef;
-            const double c1 = cf ? __ldg(cf) : A.c1, c2 = cf ? __ldg(cf + 1) : A.c2;
-            const double dn = c1 * vin[k] + c2 * (A.inv[g] * rr);
-            A.r[g] = rr;
-            A.dout[g] = dn;
-            const double xo = A.x[g];
-            A.x[g] = A.x_add_din ? (xo + vin[k]) + dn : xo + dn;
-        } else {                                                 // E_CHEB0: mgsolve.py:95, 105
-            const double rr = A.b[g] - Av;                       // (x += d deferred to the
-            A.r[g] = rr;                                         //  next step, see pffmg.h)
-            const double* cf = (A.coef2 && COMP0 + k == A.L.dim) ? A.coef2 : A.coef;
-            A.dout[g] = (A.inv[g] * rr) / (cf ? __ldg(cf) : A.c1);
-        }
-    }
-}
-
 // Epilogue operands loaded ahead of the cell work (their DRAM latency then
 // overlaps the stencil arithmetic instead of stalling the epilogue).
 template <int NCO, int EPI>
@@ -114,9 +75,10 @@ __device__ __forceinline__ void epi_load(const OpArgs& A, int64_t vid, EpiIn<NCO
     }
 }
 
-// epilogue() with the operands from epi_load
+// Vertex epilogue (model.py:373-374, 390-391, 412, 459; mgsolve.py:95-111, 227)
+// with the operands from epi_load.
 template <int NCO, int COMP0, int EPI>
-__device__ __forceinline__ void epilogue_pre(const OpArgs& A, int64_t vid, uint8_t fl, const double (&acc)[NCO],
+__device__ __forceinline__ void epilogue(const OpArgs& A, int64_t vid, uint8_t fl, const double (&acc)[NCO],
                                              const double (&vin)[NCO], const EpiIn<NCO, EPI>& e) {
     const int64_t V = A.L.V;
 #pragma unroll
@@ -172,138 +134,6 @@ __device__ __forceinline__ void load_vertex(const OpArgs& A, int64_t vid,
     for (int i = 0; i < MI::NU; ++i) f[MI::F_U + i] = __ldg(A.U + (int64_t)i * V + vid);
     if (MI::PT) f[MI::F_PT] = __ldg(A.pt + vid);
     fl = __ldg(A.flags + vid);
-}
-
-// ======================================================================= 2D
-// CTA = NW warps along x.  Warp w computes cells cx0 + 31 w + lane (lane 0 of
-// warp w and lane 31 of warp w-1 share a cell) and finalises the vertex
-// columns of lanes 1..31.  The CTA marches over a strip of vertex rows.
-
-template <int MODE, int EPI, int NW, bool ISO>
-__global__ void __launch_bounds__(32 * NW) op2d_kernel(const OpArgs A) {
-    constexpr int D = 2, NP = 4;
-    using MI = ModeInfo<D, MODE>;
-    constexpr int NF = MI::NF, NCO = MI::NCO;
-    constexpr int TW = 31 * NW + 2;            // staged vertices per row
-    constexpr int NT = 32 * NW;
-    constexpr int SLOTS = (TW + NT - 1) / NT;
-
-    __shared__ double sv[2][NF][TW];
-    __shared__ uint8_t sfl[2][TW];
-
-    const Lat& L = A.L;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int cx0 = -1 + (int)blockIdx.x * 31 * NW;
-    const int vy0 = (int)blockIdx.y * A.planes_per_cta;
-    const int vy1 = min(vy0 + A.planes_per_cta, L.ny + 1);
-    const int jc = 31 * w + lane;              // staged column of this thread's left corner
-    const int cx = cx0 + jc;
-
-    auto stage_now = [&](int y, int buf) {
-#pragma unroll
-        for (int s = 0; s < SLOTS; ++s) {
-            const int j = tid + s * NT;
-            if (j < TW) {
-                double f[NF];
-                uint8_t fl;
-                load_vertex<D, MODE>(A, vertex_id(L, cx0 + j, y, 0), f, fl);
-#pragma unroll
-                for (int i = 0; i < NF; ++i) sv[buf][i][j] = f[i];
-                sfl[buf][j] = fl;
-            }
-        }
-    };
-
-    stage_now(vy0 - 1, 0);
-    stage_now(vy0, 1);
-    __syncthreads();
-
-    double carry[NCO];
-#pragma unroll
-    for (int k = 0; k < NCO; ++k) carry[k] = 0.0;
-
-    int b0 = 0;
-    for (int cy = vy0 - 1; cy < vy1; ++cy) {
-        const int b1 = b0 ^ 1;
-        // prefetch row cy + 2 into registers
-        double pf[SLOTS][NF];
-        uint8_t pfl[SLOTS];
-        const bool need_next = (cy + 2 <= vy1);
-        if (need_next) {
-#pragma unroll
-            for (int s = 0; s < SLOTS; ++s) {
-                const int j = tid + s * NT;
-                load_vertex<D, MODE>(A, j < TW ? vertex_id(L, cx0 + j, cy + 2, 0) : -1, pf[s], pfl[s]);
-            }
-        }
-
-        // ---- cell (cx, cy)
-        double o[NCO][NP];
-        if (cell_exists<D>(L, cx, cy, 0)) {
-            double cv[NF][NP];
-#pragma unroll
-            for (int n = 0; n < NP; ++n) {
-                const int bb = (n >> 1) ? b1 : b0;
-                const int j = jc + (n & 1);
-                const uint8_t fl = sfl[bb][j];
-#pragma unroll
-                for (int i = 0; i < NF; ++i) {
-                    double val = sv[bb][i][j];
-                    if (i < MI::NV && ((fl >> (MI::COMP0 + i)) & 1)) val = 0.0;   // fem.py:205-206
-                    cv[i][n] = val;
-                }
-            }
-            const double* rq = A.rho ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * NP : nullptr;
-            if (ISO && rq) cell_kernel_iso<D, MODE, true>(cv, rq, A.K, A.I, o);
-            else if (ISO) cell_kernel_iso<D, MODE, false>(cv, rq, A.K, A.I, o);
-            else cell_kernel<D, MODE>(cv, rq, A.K, o);
-        } else {
-#pragma unroll
-            for (int k = 0; k < NCO; ++k)
-#pragma unroll
-                for (int n = 0; n < NP; ++n) o[k][n] = 0.0;
-        }
-
-        // ---- x-combine: vertex column cx gets own corners (x=0) + left cell's (x=1)
-        double bot[NCO], top[NCO];
-#pragma unroll
-        for (int k = 0; k < NCO; ++k) {
-            const double r0 = __shfl_up_sync(0xffffffffu, o[k][1], 1);
-            const double r1 = __shfl_up_sync(0xffffffffu, o[k][3], 1);
-            bot[k] = o[k][0] + r0;
-            top[k] = o[k][2] + r1;
-        }
-        if (cy >= vy0 && lane >= 1) {
-            const int64_t vid = vertex_id(L, cx, cy, 0);
-            if (vid >= 0) {
-                double acc[NCO], vin[NCO];
-                const uint8_t fl = sfl[b0][jc];
-#pragma unroll
-                for (int k = 0; k < NCO; ++k) {
-                    acc[k] = carry[k] + bot[k];
-                    vin[k] = (MODE == M_DIAG) ? 0.0 : sv[b0][MI::F_V + k][jc];
-                }
-                epilogue<NCO, MI::COMP0, EPI>(A, vid, fl, acc, vin);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < NCO; ++k) carry[k] = top[k];
-
-        __syncthreads();                      // all reads of buffer b0 done
-        if (need_next) {
-#pragma unroll
-            for (int s = 0; s < SLOTS; ++s) {
-                const int j = tid + s * NT;
-                if (j < TW) {
-#pragma unroll
-                    for (int i = 0; i < NF; ++i) sv[b0][i][j] = pf[s][i];
-                    sfl[b0][j] = pfl[s];
-                }
-            }
-        }
-        __syncthreads();
-        b0 = b1;
-    }
 }
 
 // ================================================================ 2D (warps)
@@ -501,7 +331,7 @@ op2dw_kernel(const OpArgs A) {
                 acc[k] = carry[k] + bot[k];
                 vin[k] = (MODE == M_DIAG) ? 0.0 : raw_bot[k < NV ? k : 0];
             }
-            epilogue_pre<NCO, MI::COMP0, EPI>(A, vid_f, (uint8_t)flag(s0), acc, vin, ein);
+            epilogue<NCO, MI::COMP0, EPI>(A, vid_f, (uint8_t)flag(s0), acc, vin, ein);
         }
 #pragma unroll
         for (int k = 0; k < NCO; ++k) carry[k] = top[k];
@@ -650,7 +480,7 @@ __global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
                     acc[k] = carry[k] + vp[0][k];
                     vin[k] = (MODE == M_DIAG) ? 0.0 : SV(b0, MI::F_V + k, j);
                 }
-                epilogue_pre<NCO, MI::COMP0, EPI>(A, vid_f, fl, acc, vin, ein);
+                epilogue<NCO, MI::COMP0, EPI>(A, vid_f, fl, acc, vin, ein);
             }
 #pragma unroll
             for (int k = 0; k < NCO; ++k) carry[k] = vp[1][k];
