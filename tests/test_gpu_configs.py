@@ -46,9 +46,12 @@ def test_config_vmult_and_solve_match_reference(golden, name, levels, tag):
 
 
 @pytest.mark.slow
-def test_cfg2_full_size_properties():
-    """1024^2: linearity, identity rows, symmetry of the u block, determinism."""
-    prob, mask, op = _setup("cfg2")
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5"])
+def test_full_size_properties(name):
+    """BASELINE sizes (cfg5: 228M DoFs, the largest): linearity, identity rows,
+    symmetry of the u block, determinism, and the residual's constrained rows."""
+    from paper_1902_08112_b200 import model as M
+    prob, mask, op = _setup(name)
     n, d = op.n_dofs, op.dim * op.V
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
@@ -65,6 +68,14 @@ def test_cfg2_full_size_properties():
     lhs = torch.dot(op.apply_block(0, xu), yu)
     rhs = torch.dot(xu, op.apply_block(0, yu))
     assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+    R = M.residual(prob.disc.finest, M.LinearizationState(
+        U=torch.as_tensor(prob.state.U, device="cuda"), U_prev1=None, U_prev2=None, t=prob.state.t,
+        t_prev1=prob.state.t_prev1, t_prev2=prob.state.t_prev2,
+        phi_tilde=torch.as_tensor(prob.state.phi_tilde, device="cuda")), prob.dirichlet, prob.params,
+        M.SplitKind.NOSPLIT)
+    assert torch.isfinite(R).all()
+    dc = torch.as_tensor(prob.dirichlet.is_constrained, device="cuda")
+    assert torch.all(R[dc] == 0.0)
 
 
 @pytest.mark.parametrize("name,levels,tag", [("cfg1", None, "cfg1"), ("cfg2", 6, "cfg2_l6")])
