@@ -28,7 +28,7 @@ from .distributed import (Halo, SlabMesh, SlabPartition, SlabSpace, allreduce_, 
                           to_local)
 from .krylov import NoConvergence, SolverControl, lanczos_extremes, probe_vector
 from .lattice import device_lattice, info_from_mesh
-from .mgsolve import (_cheb_coeffs, chebyshev_solver_degree, smoother_params, solver_params)
+
 from .model import DeviceMask, LinearizationState, PhaseFieldOperator
 
 
@@ -201,94 +201,45 @@ class DistGMG:
         return tuple(out)
 
     def _buffers(self):
-        for lev in self.L:
-            for name in ("r", "x", "res", "cr", "d0", "d1"):
-                setattr(lev, name, zeros(lev.n))
-        self.smooth_prm = [[smoother_params(s[k], self.degree) for k in range(2)] for s in self.spectra]
-        s0 = self.spectra[0]
-        self.coarse_prm = [solver_params(s0[k], chebyshev_solver_degree(s0[k], self.target, self.cap))
-                           for k in range(2)]
+        from .mgsolve import LevelContext, _NativeCycle
+        ctxs = [LevelContext(l, self.ops[l], lev.diag, self.spectra[l], None, None, lev.flags, inv=self.inv[l])
+                for l, lev in enumerate(self.L)]
+        # the single-GPU V-cycle (block-diagonal smoothing, device-resident
+        # Chebyshev coefficients, one-launch coarse solve) with this object as
+        # its communication layer (halo / restrict / prolongate below)
+        self.cycle = _NativeCycle(ctxs, self.degree, self.target, self.cap, comm=self)
+
+    # ------------------------------------------------- communication layer
+    def halo(self, l, vec, n_comp):
+        """Refresh the ghost planes of a level-l vector (no-op on replicated levels)."""
+        lev = self.L[l]
+        if lev.sharded:
+            lev.halo.exchange(vec, n_comp)
+
+    def restrict(self, l, fine, coarse, n_comp, comp0):
+        """coarse (level l) = masked P^T fine (level l+1); agglomerated into a replicated level."""
+        f, c = self.L[l + 1], self.L[l]
+        self.halo(l + 1, fine, n_comp)
+        clat = c.lat if (c.sharded or not f.sharded) else self.virt[l]
+        agglomerate = f.sharded and not c.sharded
+        if agglomerate:
+            coarse.zero_()
+        _lib.call("pffmg_restrict", clat.ref, f.lat.ref, n_comp, comp0, _lib.ptr(fine), _lib.ptr(coarse),
+                  _lib.ptr(c.flags), _lib.stream())
+        if agglomerate:
+            allreduce_(coarse, self.group)
+
+    def prolongate(self, l, coarse, fine, n_comp, comp0):
+        """fine (level l+1) += masked P coarse (level l)."""
+        f, c = self.L[l + 1], self.L[l]
+        self.halo(l, coarse, n_comp)
+        _lib.call("pffmg_prolongate", c.lat.ref, f.lat.ref, n_comp, comp0, _lib.ptr(coarse), _lib.ptr(fine),
+                  _lib.ptr(f.flags), 1, _lib.stream())
 
     # --------------------------------------------------------------- V-cycle
-    def _blk(self, lev, k):
-        return slice(0, lev.dim * lev.V) if k == 0 else slice(lev.dim * lev.V, lev.n)
-
-    def _cheb(self, l, k, prm, x_is_zero):
-        """chebyshev_apply (mgsolve.py:82-113) on block k with halos before every stencil."""
-        lev, op = self.L[l], self.ops[l]
-        b = self._blk(lev, k)
-        nk = lev.dim if k == 0 else 1
-        x, r, rhs, inv = lev.x[b], lev.cr[b], lev.r[b], self.inv[l][b]
-        d_in, d_out = lev.d0[b], lev.d1[b]
-        nb = x.numel()
-        s = _lib.stream()
-        theta, delta, degenerate = _cheb_coeffs(prm)
-        if degenerate:
-            if x_is_zero:
-                x.zero_()
-                r.copy_(rhs)
-            else:
-                lev.halo.exchange(x, nk)
-                op.residual_dev(k, x, rhs, r, pre=True)
-            for _ in range(prm.degree):
-                _lib.call("pffmg_jacobi_update", _lib.ptr(r), _lib.ptr(inv), theta, _lib.ptr(x), nb, s)
-                lev.halo.exchange(x, nk)
-                op.residual_dev(k, x, rhs, r, pre=True)
-            return
-        sigma = theta / delta
-        rho_old = 1.0 / sigma
-        if x_is_zero:
-            _lib.call("pffmg_cheb_init_zero", _lib.ptr(rhs), _lib.ptr(inv), theta, _lib.ptr(r),
-                      _lib.ptr(d_in), _lib.ptr(x), nb, s)
-            pending = False
-        else:
-            lev.halo.exchange(x, nk)
-            op.cheb_init_dev(k, x, rhs, r, d_in, inv, theta, pre=True)
-            pending = True
-        for _ in range(prm.degree - 1):
-            rho = 1.0 / (2.0 * sigma - rho_old)
-            lev.halo.exchange(d_in, nk)
-            op.cheb_step_dev(k, d_in, d_out, r, x, inv, rho * rho_old, 2.0 * rho / delta, pending, pre=True)
-            pending = False
-            d_in, d_out = d_out, d_in
-            rho_old = rho
-        if pending:
-            _lib.call("pffmg_axpy", 1.0, _lib.ptr(d_in), _lib.ptr(x), nb, s)
-
-    def _cycle(self, l):
-        lev = self.L[l]
-        if l == 0:
-            for k in range(2):
-                self._cheb(0, k, self.coarse_prm[k], True)
-            return
-        c = self.L[l - 1]
-        for k in range(2):
-            self._cheb(l, k, self.smooth_prm[l][k], True)
-        lev.halo.exchange(lev.x, lev.nc)
-        self.ops[l].residual_dev(_lib.FULL, lev.x, lev.r, lev.res, pre=True)
-        lev.halo.exchange(lev.res, lev.nc)
-        clat = c.lat if (c.sharded or not lev.sharded) else self.virt[l - 1]
-        if lev.sharded and not c.sharded:
-            c.r.zero_()
-        _lib.call("pffmg_restrict", clat.ref, lev.lat.ref, lev.nc, 0, _lib.ptr(lev.res), _lib.ptr(c.r),
-                  _lib.ptr(c.flags), _lib.stream())
-        if lev.sharded and not c.sharded:
-            allreduce_(c.r, self.group)                     # agglomerate the coarse residual
-        self._cycle(l - 1)
-        if c.sharded:
-            c.halo.exchange(c.x, c.nc)
-        _lib.call("pffmg_prolongate", c.lat.ref, lev.lat.ref, lev.nc, 0, _lib.ptr(c.x), _lib.ptr(lev.x),
-                  _lib.ptr(lev.flags), 1, _lib.stream())
-        for k in range(2):
-            self._cheb(l, k, self.smooth_prm[l][k], False)
-
     def vcycle(self, r, out):
         """V(1,1) on a local fine residual (mgsolve.py:262-283, FULL); owned rows of `out`."""
-        top = self.L[-1]
-        _lib.call("pffmg_masked_copy", _lib.ptr(top.flags), top.V, 0, top.nc, _lib.ptr(r), _lib.ptr(top.r),
-                  _lib.stream())
-        self._cycle(len(self.L) - 1)
-        out.copy_(top.x)
+        self.cycle.run("full", r, out)
         return out
 
     def apply(self, v, out):

@@ -606,6 +606,7 @@ class _Level:
         # one block-diagonal kernel per Chebyshev step pays in 2D and on small
         # (launch-latency-bound) 3D levels; large 3D levels are FP64-bound and
         # run faster as two block kernels (measured, cfg4)
+        self.index = ctx.level
         self.bd_ok = self.dim == 2 or self.V < (1 << 17)
         info = op.lat.info
         self.coarse_ok = int(np.prod(info.ncell)) <= 256 and tuple(info.own) == (0, 0)
@@ -634,13 +635,20 @@ class _NativeCycle:
         cls._cache[key] = cyc
         return cyc
 
-    def __init__(self, contexts, degree, target, cap):
+    def __init__(self, contexts, degree, target, cap, comm=None):
+        """`comm` (optional) makes the cycle slab-distributed: it provides
+        halo(l, vec, n_comp) -- refresh the ghost planes of a level-l vector
+        before a stencil reads it -- and restrict(l, fine, coarse, n_comp, comp0)
+        / prolongate(l, coarse, fine, n_comp, comp0) between levels l and l+1
+        (dist_solver.DistGMG).  Distributed cycles are not graph-recorded."""
         self.contexts = list(contexts)
         self.degree = degree
+        self.comm = comm
         self.levels = [_Level(c) for c in contexts]
-        self.disc = Discretization.wrap(contexts[-1].disc) if len(contexts) > 1 else None
+        self.disc = (Discretization.wrap(contexts[-1].disc) if len(contexts) > 1 and comm is None
+                     else None)
         self.target, self.cap = target, cap
-        self.use_graph = os.environ.get("PFFMG_GRAPHS", "1") != "0"
+        self.use_graph = comm is None and os.environ.get("PFFMG_GRAPHS", "1") != "0"
         self.graphs = {}
         self.r_in = None
         self.x_out = None
@@ -683,6 +691,22 @@ class _NativeCycle:
         else:
             self.coef.copy_(table)
 
+    def _halo(self, L, vec, n_comp):
+        if self.comm is not None:
+            self.comm.halo(L.index, vec, n_comp)
+
+    def _restrict(self, l, fine, coarse, n_comp, comp0, coarse_flags):
+        if self.comm is not None:
+            self.comm.restrict(l, fine, coarse, n_comp, comp0)
+        else:
+            self.disc.restrict_dev(fine, coarse, l, n_comp, comp0, coarse_flags)
+
+    def _prolongate(self, l, coarse, fine, n_comp, comp0, fine_flags):
+        if self.comm is not None:
+            self.comm.prolongate(l, coarse, fine, n_comp, comp0)
+        else:
+            self.disc.prolongate_dev(coarse, fine, l, n_comp, comp0, fine_flags, accumulate=True)
+
     # one Chebyshev sweep on block k of level L: x (zero or not) -> smoothed x
     def _cheb(self, L, k, slot, x_is_zero, pre=True):
         op = L.op
@@ -695,14 +719,17 @@ class _NativeCycle:
         coef = self.coef
         theta = coef[off:off + 1]
         if degenerate:                                     # mgsolve.py:97-101
+            nk = L.dim if k == 0 else 1
             if x_is_zero:
                 x.zero_()
                 r.copy_(rhs)
             else:
+                self._halo(L, x, nk)
                 op.residual_dev(k, x, rhs, r, pre=pre)
             for _ in range(prm.degree):
                 _lib.call("pffmg_jacobi_update_dc", _lib.ptr(r), _lib.ptr(inv), _lib.ptr(theta),
                           _lib.ptr(x), nb, s)
+                self._halo(L, x, nk)
                 op.residual_dev(k, x, rhs, r, pre=pre)
             return
         if x_is_zero:                                      # r = b; d = inv r / theta; x = d
@@ -710,10 +737,12 @@ class _NativeCycle:
                       _lib.ptr(r), _lib.ptr(d_in), _lib.ptr(x), nb, s)
             pending = False
         else:                                              # r = b - A x; d = inv r / theta
+            self._halo(L, x, L.dim if k == 0 else 1)
             op.cheb_init_dc(k, x, rhs, r, d_in, inv, theta, pre=pre)
             pending = True                                 # x += d folded into the next step
         for i in range(prm.degree - 1):
             c = coef[off + 1 + 2 * i: off + 3 + 2 * i]
+            self._halo(L, d_in, L.dim if k == 0 else 1)
             op.cheb_step_dc(k, d_in, d_out, r, x, inv, c, pending, pre=pre)
             pending = False
             d_in, d_out = d_out, d_in
@@ -738,10 +767,12 @@ class _NativeCycle:
                       L.dim * L.V, _lib.ptr(r), _lib.ptr(d_in), _lib.ptr(x), L.n, s)
             pending = False
         else:
+            self._halo(L, x, L.dim + 1)
             op.cheb_init_bd(x, rhs, r, d_in, inv, tu, tp, pre=pre)
             pending = True
         common = min(pu.degree, pp.degree) - 1
         for i in range(common):
+            self._halo(L, d_in, L.dim + 1)
             op.cheb_step_bd(d_in, d_out, r, x, inv, coef[ou + 1 + 2 * i: ou + 3 + 2 * i],
                             coef[op_ + 1 + 2 * i: op_ + 3 + 2 * i], pending, pre=pre)
             pending = False
@@ -752,6 +783,7 @@ class _NativeCycle:
             b = L.blk(k)
             di, do = d_in[b], d_out[b]
             for i in range(common, prm.degree - 1):
+                self._halo(L, di, L.dim if k == 0 else 1)
                 op.cheb_step_dc(k, di, do, r[b], x[b], inv[b], coef[o + 1 + 2 * i: o + 3 + 2 * i],
                                 False, pre=pre)
                 di, do = do, di
@@ -778,10 +810,11 @@ class _NativeCycle:
             return
         L, Lc = self.levels[l], self.levels[l - 1]
         self._smooth(l, True)
+        self._halo(L, L.x, L.dim + 1)
         L.op.residual_dev(_lib.FULL, L.x, L.r, L.res, pre=True)
-        self.disc.restrict_dev(L.res, Lc.r, l - 1, L.dim + 1, 0, Lc.flags)
+        self._restrict(l - 1, L.res, Lc.r, L.dim + 1, 0, Lc.flags)
         self._cycle(l - 1)
-        self.disc.prolongate_dev(Lc.x, L.x, l - 1, L.dim + 1, 0, L.flags, accumulate=True)
+        self._prolongate(l - 1, Lc.x, L.x, L.dim + 1, 0, L.flags)
         self._smooth(l, False)
 
     def _block_cycle(self, k, l):                          # mgsolve.py:238-259
@@ -792,13 +825,13 @@ class _NativeCycle:
         Lc = self.levels[l - 1]
         b = L.blk(k)
         self._cheb(L, k, ("s", l, k), True)
-        L.op.residual_dev(k, L.x[b], L.r[b], L.res[b], pre=True)
         ncomp = L.dim if k == 0 else 1
         comp0 = 0 if k == 0 else L.dim
-        self.disc.restrict_dev(L.res[b], Lc.r[Lc.blk(k)], l - 1, ncomp, comp0, Lc.flags)
+        self._halo(L, L.x[b], ncomp)
+        L.op.residual_dev(k, L.x[b], L.r[b], L.res[b], pre=True)
+        self._restrict(l - 1, L.res[b], Lc.r[Lc.blk(k)], ncomp, comp0, Lc.flags)
         self._block_cycle(k, l - 1)
-        self.disc.prolongate_dev(Lc.x[Lc.blk(k)], L.x[b], l - 1, ncomp, comp0, L.flags,
-                                 accumulate=True)
+        self._prolongate(l - 1, Lc.x[Lc.blk(k)], L.x[b], ncomp, comp0, L.flags)
         self._cheb(L, k, ("s", l, k), False)
 
     def _body(self, kind):
