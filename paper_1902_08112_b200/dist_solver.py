@@ -81,6 +81,15 @@ class DistGMG:
                 self.virt[l - 1] = device_lattice(SlabMesh(vi))
 
     # --------------------------------------------------------------- helpers
+    def dot_dev(self, lev, x, y):
+        """Owned-dof inner product as a 1-element CUDA tensor, all-reduced (no host sync)."""
+        t = torch.zeros(1, dtype=torch.float64, device=x.device)
+        for s in lev.owned:
+            t += torch.dot(x[s], y[s])
+        if lev.sharded:
+            allreduce_(t, self.group)
+        return t
+
     def dot(self, lev, x, y):
         t = torch.zeros(1, dtype=torch.float64, device=x.device)
         for s in lev.owned:
@@ -278,16 +287,30 @@ class DistGMG:
                 w = V[j + 1]
                 self.apply(Z[j], w)
                 total += 1
-                w0 = np.sqrt(self.dot(top, w, w))
+                # MGS (krylov.py:93-107) with the dots kept on the device: each
+                # pass all-reduces one scalar and subtracts without a host round
+                # trip; the host reads the Hessenberg column once per pass set
+                w0 = self.dot_dev(top, w, w)
+                hs = []
                 for i in range(j + 1):
-                    H[i, j] = self.dot(top, V[i], w)
-                    w -= H[i, j] * V[i]
-                if np.sqrt(self.dot(top, w, w)) < 1e-3 * w0:
+                    h = self.dot_dev(top, V[i], w)
+                    w.sub_(h * V[i])
+                    hs.append(h)
+                nrm = self.dot_dev(top, w, w)
+                vals = host(torch.cat(hs + [w0, nrm]))
+                H[:j + 1, j] = vals[:j + 1]
+                w0, nrm = float(np.sqrt(vals[-2])), float(np.sqrt(vals[-1]))
+                if nrm < 1e-3 * w0:
+                    hs = []
                     for i in range(j + 1):
-                        cc = self.dot(top, V[i], w)
-                        H[i, j] += cc
-                        w -= cc * V[i]
-                H[j + 1, j] = np.sqrt(self.dot(top, w, w))
+                        cc = self.dot_dev(top, V[i], w)
+                        w.sub_(cc * V[i])
+                        hs.append(cc)
+                    nrm = self.dot_dev(top, w, w)
+                    vals = host(torch.cat(hs + [nrm]))
+                    H[:j + 1, j] += vals[:j + 1]
+                    nrm = float(np.sqrt(vals[-1]))
+                H[j + 1, j] = nrm
                 brk = H[j + 1, j] == 0.0
                 if not brk:
                     w /= H[j + 1, j]
