@@ -157,19 +157,24 @@ class DistGMG:
             self.inv.append(torch.reciprocal(diag))
             lev.flags = FL[l]
             lev.diag = diag
-        self.spectra = [self._spectra(l) for l in range(len(self.L))]
+        recs = [self._cg_records(l) for l in range(len(self.L))]
+        host_recs = host(torch.stack([t for pair in recs for t in pair]))    # one host sync
+        self.spectra = [tuple(self._spectra_from(host_recs[2 * l + k]) for k in range(2))
+                        for l in range(len(self.L))]
         self._buffers()
         return self
 
-    def _spectra(self, l):
-        """Jacobi-PCG Lanczos per block with distributed dots (krylov.py:146-198)."""
+    def _cg_records(self, l):
+        """Jacobi-PCG of both blocks of level l (krylov.py:146-185) with distributed
+        dots kept on the device: returns per block the 1 + 2 n scalars
+        (rz_0, pAp_1, rz_1, pAp_2, ...) -- no host synchronisation here."""
         lev, op = self.L[l], self.ops[l]
-        out = []
+        recs = []
         for k in range(2):
             blk = slice(0, lev.dim * lev.V) if k == 0 else slice(lev.dim * lev.V, lev.n)
             nk = lev.dim if k == 0 else 1
             # the reference's PCG64 probe over the GLOBAL block, sliced to the slab
-            ng = (lev.dim if k == 0 else 1) * lev.info_g.n_vertices
+            ng = nk * lev.info_g.n_vertices
             full = probe_vector(self.seed + 31 * l + 7 * k, ng)
             b = to_local(full, nk, lev.info_g, lev.slab) if lev.sharded else full.clone()
             b = b.contiguous().clone()
@@ -182,32 +187,42 @@ class DistGMG:
             z = r / diag
             p = z.clone()
             Ap = torch.empty_like(p)
-            rz = bl.dot(self, r, z)
-            al, be = [], []
+            rz = bl.dot_dev(self, r, z)
+            rec = [rz]
             for _ in range(self.eig_iters):
-                if rz <= 0.0 or not np.isfinite(rz):
-                    break
                 lev.halo.exchange(p, nk)
                 op.apply_dev(k, p, Ap, pre=True)
-                pAp = bl.dot(self, p, Ap)
-                if pAp <= 0.0 or not np.isfinite(pAp):
-                    break
-                a = rz / pAp
-                al.append(a)
-                r = r - a * Ap
+                pAp = bl.dot_dev(self, p, Ap)
+                r = r - (rz / pAp) * Ap
                 z = r / diag
-                rz_new = bl.dot(self, r, z)
-                if rz_new <= 1e-28 * rz or not np.isfinite(rz_new):
-                    break
-                be.append(rz_new / rz)
-                p = z + be[-1] * p
+                rz_new = bl.dot_dev(self, r, z)
+                p = z + (rz_new / rz) * p
+                rec += [pAp, rz_new]
                 rz = rz_new
-            scal = np.zeros(8 + 128)
-            scal[4], scal[5] = len(al), len(be)
-            scal[8:8 + len(al)] = al
-            scal[8 + 64:8 + 64 + len(be)] = be
-            out.append(lanczos_extremes(scal, self.eig_iters))
-        return tuple(out)
+            recs.append(torch.cat(rec))
+        return recs
+
+    def _spectra_from(self, rec):
+        """The reference's breakdown rules replayed on the recorded scalars (krylov.py:168-198)."""
+        rz = rec[0]
+        al, be = [], []
+        for it in range(self.eig_iters):
+            if rz <= 0.0 or not np.isfinite(rz):
+                break
+            pAp = rec[1 + 2 * it]
+            if pAp <= 0.0 or not np.isfinite(pAp):
+                break
+            al.append(rz / pAp)
+            rz_new = rec[2 + 2 * it]
+            if rz_new <= 1e-28 * rz or not np.isfinite(rz_new):
+                break
+            be.append(rz_new / rz)
+            rz = rz_new
+        scal = np.zeros(8 + 128)
+        scal[4], scal[5] = len(al), len(be)
+        scal[8:8 + len(al)] = al
+        scal[8 + 64:8 + 64 + len(be)] = be
+        return lanczos_extremes(scal, self.eig_iters)
 
     def _buffers(self):
         from .mgsolve import LevelContext, _NativeCycle
@@ -361,10 +376,10 @@ class _BlockView:
         self.slices = [slice(c * lev.V + a, c * lev.V + b) for c in range(nk)]
         self.sharded = lev.sharded
 
-    def dot(self, solver, x, y):
+    def dot_dev(self, solver, x, y):
         t = torch.zeros(1, dtype=torch.float64, device=x.device)
         for s in self.slices:
             t += torch.dot(x[s], y[s])
         if self.sharded:
             allreduce_(t, solver.group)
-        return float(t.item())
+        return t
