@@ -12,24 +12,26 @@ namespace pffmg {
 // local plane p of a lattice is global plane p + plane0.  Kernels iterate over
 // the owned planes [own_lo, own_hi) of their output lattice only.
 
-// i-th point of the owned planes of L (x fastest) -> local lattice coordinates
-__device__ __forceinline__ void owned_coords(const Lat& L, int64_t i, int& x, int& y, int& z) {
-    const int64_t nxv = L.nx + 1;
-    x = (int)(i % nxv);
-    const int64_t t = i / nxv;
+// Launch geometry of the point kernels: x = block column, grid.y / grid.z = the
+// owned rows / planes (no 64-bit index divisions per point).
+__device__ __forceinline__ bool grid_point(const Lat& L, int& x, int& y, int& z) {
+    x = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+    if (x > L.nx) return false;
     if (L.dim == 3) {
-        const int64_t nyv = L.ny + 1;
-        y = (int)(t % nyv);
-        z = (int)(t / nyv) + L.own_lo;
+        y = (int)blockIdx.y;
+        z = (int)blockIdx.z + L.own_lo;
     } else {
-        y = (int)t + L.own_lo;
+        y = (int)blockIdx.y + L.own_lo;
         z = 0;
     }
+    return true;
 }
 
-__host__ __device__ __forceinline__ int64_t owned_points(const Lat& L) {
-    const int64_t plane = L.dim == 3 ? (int64_t)(L.nx + 1) * (L.ny + 1) : (int64_t)(L.nx + 1);
-    return plane * (L.own_hi - L.own_lo);
+static dim3 grid_points(const Lat& L, int threads) {
+    const unsigned gx = (unsigned)((L.nx + 1 + threads - 1) / threads);
+    const int own = L.own_hi - L.own_lo;
+    if (L.dim == 3) return dim3(gx, (unsigned)(L.ny + 1), (unsigned)own);
+    return dim3(gx, (unsigned)own, 1);
 }
 
 // fine local coordinates of the fine lattice point 2*(coarse point) + (a, b, c)
@@ -48,13 +50,11 @@ __device__ __forceinline__ void fine_of(const Lat& Lc, const Lat& Lf, int x, int
 // vc[k] = sum_{fine f} P[f, c] vf[k][f]  for owned coarse vertices c, then masking.
 __global__ void restrict_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vf,
                                 double* __restrict__ vc, const uint8_t* __restrict__ cflags) {
-    const int64_t npts = owned_points(Lc);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int x, y, z;
-        owned_coords(Lc, i, x, y, z);
+    int x, y, z;
+    if (!grid_point(Lc, x, y, z)) return;
+    {
         const int64_t cid = vertex_id(Lc, x, y, z);
-        if (cid < 0) continue;
+        if (cid < 0) return;
         const uint8_t fl = cflags ? cflags[cid] : 0;
         const int zlo = Lc.dim == 3 ? -1 : 0, zhi = Lc.dim == 3 ? 1 : 0;
         // fine neighbours in increasing id order (the CSR product order); each
@@ -87,14 +87,12 @@ __global__ void restrict_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const doub
 __global__ void prolongate_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vc,
                                   double* __restrict__ vf, const uint8_t* __restrict__ fflags,
                                   int accumulate) {
-    const int64_t npts = owned_points(Lf);
     const int D = Lf.dim;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int X, Y, Z;
-        owned_coords(Lf, i, X, Y, Z);
+    int X, Y, Z;
+    if (!grid_point(Lf, X, Y, Z)) return;
+    {
         const int64_t fid = vertex_id(Lf, X, Y, Z);
-        if (fid < 0) continue;
+        if (fid < 0) return;
         const uint8_t fl = fflags ? fflags[fid] : 0;
         // global coordinate along the cut axis decides the parity
         const int Yg = D == 3 ? Y : Y + Lf.plane0, Zg = D == 3 ? Z + Lf.plane0 : 0;
@@ -224,13 +222,11 @@ __global__ void prolongate_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const
 
 __global__ void inject_f64_kernel(Lat Lc, Lat Lf, int ncomp, const double* __restrict__ vf,
                                   double* __restrict__ vc) {
-    const int64_t npts = owned_points(Lc);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int x, y, z;
-        owned_coords(Lc, i, x, y, z);
+    int x, y, z;
+    if (!grid_point(Lc, x, y, z)) return;
+    {
         const int64_t cid = vertex_id(Lc, x, y, z);
-        if (cid < 0) continue;
+        if (cid < 0) return;
         int fx, fy, fz;
         fine_of(Lc, Lf, x, y, z, 0, 0, 0, fx, fy, fz);
         const int64_t fid = vertex_id(Lf, fx, fy, fz);
@@ -240,13 +236,11 @@ __global__ void inject_f64_kernel(Lat Lc, Lat Lf, int ncomp, const double* __res
 
 __global__ void inject_u8_kernel(Lat Lc, Lat Lf, const uint8_t* __restrict__ ff, uint8_t* __restrict__ fc,
                                  int64_t* __restrict__ map) {
-    const int64_t npts = owned_points(Lc);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int x, y, z;
-        owned_coords(Lc, i, x, y, z);
+    int x, y, z;
+    if (!grid_point(Lc, x, y, z)) return;
+    {
         const int64_t cid = vertex_id(Lc, x, y, z);
-        if (cid < 0) continue;
+        if (cid < 0) return;
         int fx, fy, fz;
         fine_of(Lc, Lf, x, y, z, 0, 0, 0, fx, fy, fz);
         const int64_t fid = vertex_id(Lf, fx, fy, fz);
@@ -282,8 +276,6 @@ static int check_pair(const pffmg_lattice* c, const pffmg_lattice* f, Lat* Lc, L
     return PFFMG_OK;
 }
 
-static int64_t box_points_host(const Lat& L) { return owned_points(L); }
-
 static dim3 grid_for(int64_t n) {
     int64_t b = (n + 255) / 256;
     const int64_t cap = (int64_t)sm_count() * 16;
@@ -310,7 +302,7 @@ extern "C" int pffmg_restrict(const pffmg_lattice* coarse, const pffmg_lattice* 
             Lc, Lf, n_comp, comp0, vf, vc, coarse_flags);
         return check_launch("pffmg_restrict");
     }
-    restrict_kernel<<<grid_for(box_points_host(Lc)), 256, 0, as_stream(stream)>>>(Lc, Lf, n_comp, comp0, vf,
+    restrict_kernel<<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, n_comp, comp0, vf,
                                                                                 vc, coarse_flags);
     return check_launch("pffmg_restrict");
 }
@@ -329,7 +321,7 @@ extern "C" int pffmg_prolongate(const pffmg_lattice* coarse, const pffmg_lattice
             Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
         return check_launch("pffmg_prolongate");
     }
-    prolongate_kernel<<<grid_for(box_points_host(Lf)), 256, 0, as_stream(stream)>>>(
+    prolongate_kernel<<<grid_points(Lf, 128), 128, 0, as_stream(stream)>>>(
         Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
     return check_launch("pffmg_prolongate");
 }
@@ -340,7 +332,7 @@ extern "C" int pffmg_inject_f64(const pffmg_lattice* coarse, const pffmg_lattice
     int rc = check_pair(coarse, fine, &Lc, &Lf);
     if (rc) return rc;
     PFFMG_REQUIRE(vf && vc && n_comp >= 1, "pffmg_inject_f64: bad arguments");
-    inject_f64_kernel<<<grid_for(box_points_host(Lc)), 256, 0, as_stream(stream)>>>(Lc, Lf, n_comp, vf, vc);
+    inject_f64_kernel<<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, n_comp, vf, vc);
     return check_launch("pffmg_inject_f64");
 }
 
@@ -350,7 +342,7 @@ extern "C" int pffmg_inject_flags(const pffmg_lattice* coarse, const pffmg_latti
     int rc = check_pair(coarse, fine, &Lc, &Lf);
     if (rc) return rc;
     PFFMG_REQUIRE(ff && fc, "pffmg_inject_flags: bad arguments");
-    inject_u8_kernel<<<grid_for(box_points_host(Lc)), 256, 0, as_stream(stream)>>>(Lc, Lf, ff, fc, nullptr);
+    inject_u8_kernel<<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, ff, fc, nullptr);
     return check_launch("pffmg_inject_flags");
 }
 
@@ -360,6 +352,6 @@ extern "C" int pffmg_injection_map(const pffmg_lattice* coarse, const pffmg_latt
     int rc = check_pair(coarse, fine, &Lc, &Lf);
     if (rc) return rc;
     PFFMG_REQUIRE(out, "pffmg_injection_map: null out");
-    inject_u8_kernel<<<grid_for(box_points_host(Lc)), 256, 0, as_stream(stream)>>>(Lc, Lf, nullptr, nullptr, out);
+    inject_u8_kernel<<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, nullptr, nullptr, out);
     return check_launch("pffmg_injection_map");
 }

@@ -650,8 +650,6 @@ class _NativeCycle:
         self.target, self.cap = target, cap
         self.use_graph = comm is None and os.environ.get("PFFMG_GRAPHS", "1") != "0"
         self.graphs = {}
-        self.r_in = None
-        self.x_out = None
         self.coef = None
         self.struct = None
         self.set_spectra(contexts)
@@ -835,22 +833,18 @@ class _NativeCycle:
         self._cheb(L, k, ("s", l, k), False)
 
     def _body(self, kind):
-        top = self.levels[-1]
-        _lib.call("pffmg_masked_copy", _lib.ptr(top.flags), top.V, 0, top.dim + 1,
-                  _lib.ptr(self.r_in), _lib.ptr(top.r), _lib.stream())    # r[constrained] = 0
         if kind == "full":
             self._cycle(len(self.levels) - 1)
         else:
             for k in range(2):
                 self._block_cycle(k, len(self.levels) - 1)
-        self.x_out.copy_(top.x)
 
     def run(self, kind, r, out):
         top = self.levels[-1]
-        if self.r_in is None:
-            self.r_in = zeros(top.n)
-            self.x_out = zeros(top.n)
-        self.r_in.copy_(r)
+        # r[constrained] = 0 straight from the caller's vector into the fine level's
+        # rhs (mgsolve.py:271-272); the recorded cycle then reads fixed buffers only
+        _lib.call("pffmg_masked_copy", _lib.ptr(top.flags), top.V, 0, top.dim + 1,
+                  _lib.ptr(r), _lib.ptr(top.r), _lib.stream())
         if self.use_graph:
             g = self.graphs.get(kind)
             if g is None:
@@ -862,7 +856,7 @@ class _NativeCycle:
             g.replay()
         else:
             self._body(kind)
-        out.copy_(self.x_out)
+        out.copy_(top.x)
 
     def coarse(self, r, out):
         """Public coarse_solve: r is arbitrary (not masked), so no pre-mask hint."""
