@@ -48,6 +48,7 @@ __device__ __forceinline__ void fine_of(const Lat& Lc, const Lat& Lf, int x, int
 }
 
 // vc[k] = sum_{fine f} P[f, c] vf[k][f]  for owned coarse vertices c, then masking.
+template <int D>
 __global__ void restrict_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vf,
                                 double* __restrict__ vc, const uint8_t* __restrict__ cflags) {
     int x, y, z;
@@ -56,10 +57,11 @@ __global__ void restrict_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const doub
         const int64_t cid = vertex_id(Lc, x, y, z);
         if (cid < 0) return;
         const uint8_t fl = cflags ? cflags[cid] : 0;
-        const int zlo = Lc.dim == 3 ? -1 : 0, zhi = Lc.dim == 3 ? 1 : 0;
+        constexpr int zlo = D == 3 ? -1 : 0, zhi = D == 3 ? 1 : 0;
         // fine neighbours in increasing id order (the CSR product order); each
         // neighbour's id is looked up once for all components
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
         for (int c = zlo; c <= zhi; ++c)
 #pragma unroll
             for (int b = -1; b <= 1; ++b)
@@ -83,47 +85,45 @@ __global__ void restrict_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const doub
 }
 
 // vf[k][f] (=|+=) sum_c P[f, c] vc[k][c] for owned fine vertices, zeroed where
-// the fine dof is constrained.
+// the fine dof is constrained.  Coarse corners in bit order (x fastest), as
+// the COO entries of fem.py:323-339; corners with a zero weight are skipped.
+template <int D>
 __global__ void prolongate_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vc,
                                   double* __restrict__ vf, const uint8_t* __restrict__ fflags,
                                   int accumulate) {
-    const int D = Lf.dim;
     int X, Y, Z;
     if (!grid_point(Lf, X, Y, Z)) return;
-    {
-        const int64_t fid = vertex_id(Lf, X, Y, Z);
-        if (fid < 0) return;
-        const uint8_t fl = fflags ? fflags[fid] : 0;
-        // global coordinate along the cut axis decides the parity
-        const int Yg = D == 3 ? Y : Y + Lf.plane0, Zg = D == 3 ? Z + Lf.plane0 : 0;
-        const int shY = D == 3 ? 0 : Lc.plane0, shZ = D == 3 ? Lc.plane0 : 0;
-        // corners in bit order (x fastest), as the COO entries of fem.py:323-339
-        int64_t cid[8];
-        double wt[8];
-        int nn = 0;
-        const int lox = X >> 1, hix = (X + 1) >> 1;
-        const int loy = (Yg >> 1) - shY, hiy = ((Yg + 1) >> 1) - shY;
-        const int loz = (Zg >> 1) - shZ, hiz = ((Zg + 1) >> 1) - shZ;
-        const bool ox = X & 1, oy = Yg & 1, oz = Zg & 1;
-        for (int bits = 0; bits < (1 << D); ++bits) {
-            const bool bx = bits & 1, by = (bits >> 1) & 1, bz = (bits >> 2) & 1;
-            if ((bx && !ox) || (by && !oy) || (bz && !oz)) continue;
-            const double w = (ox ? 0.5 : 1.0) * (oy ? 0.5 : 1.0) * (D == 3 && oz ? 0.5 : 1.0);
-            cid[nn] = vertex_id(Lc, bx ? hix : lox, by ? hiy : loy, D == 3 ? (bz ? hiz : loz) : 0);
-            wt[nn] = w;
-            ++nn;
-        }
-        for (int k = 0; k < ncomp; ++k) {
-            double acc = 0.0;
-            for (int t = 0; t < nn; ++t)
-                if (cid[t] >= 0) acc += wt[t] * vc[(int64_t)k * Lc.V + cid[t]];
-            const int64_t g = (int64_t)k * Lf.V + fid;
-            if ((fl >> (comp0 + k)) & 1) acc = 0.0;
-            if (accumulate)
-                vf[g] += acc;
-            else
-                vf[g] = acc;
-        }
+    const int64_t fid = vertex_id(Lf, X, Y, Z);
+    if (fid < 0) return;
+    const uint8_t fl = fflags ? fflags[fid] : 0;
+    // global coordinate along the cut axis decides the parity
+    const int Yg = D == 3 ? Y : Y + Lf.plane0, Zg = D == 3 ? Z + Lf.plane0 : 0;
+    const int shY = D == 3 ? 0 : Lc.plane0, shZ = D == 3 ? Lc.plane0 : 0;
+    const int lox = X >> 1, hix = (X + 1) >> 1;
+    const int loy = (Yg >> 1) - shY, hiy = ((Yg + 1) >> 1) - shY;
+    const int loz = (Zg >> 1) - shZ, hiz = ((Zg + 1) >> 1) - shZ;
+    const bool ox = X & 1, oy = Yg & 1, oz = Zg & 1;
+    const double w = (ox ? 0.5 : 1.0) * (oy ? 0.5 : 1.0) * (D == 3 && oz ? 0.5 : 1.0);
+    int64_t cid[1 << D];
+#pragma unroll
+    for (int bits = 0; bits < (1 << D); ++bits) {
+        const bool bx = bits & 1, by = (bits >> 1) & 1, bz = (bits >> 2) & 1;
+        const bool used = !((bx && !ox) || (by && !oy) || (bz && !oz));
+        cid[bits] = used ? vertex_id(Lc, bx ? hix : lox, by ? hiy : loy, D == 3 ? (bz ? hiz : loz) : 0) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (k >= ncomp) break;
+        double acc = 0.0;
+#pragma unroll
+        for (int bits = 0; bits < (1 << D); ++bits)
+            if (cid[bits] >= 0) acc += w * __ldg(vc + (int64_t)k * Lc.V + cid[bits]);
+        const int64_t g = (int64_t)k * Lf.V + fid;
+        if ((fl >> (comp0 + k)) & 1) acc = 0.0;
+        if (accumulate)
+            vf[g] += acc;
+        else
+            vf[g] = acc;
     }
 }
 
@@ -302,7 +302,11 @@ extern "C" int pffmg_restrict(const pffmg_lattice* coarse, const pffmg_lattice* 
             Lc, Lf, n_comp, comp0, vf, vc, coarse_flags);
         return check_launch("pffmg_restrict");
     }
-    restrict_kernel<<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, n_comp, comp0, vf,
+    if (Lc.dim == 3)
+        restrict_kernel<3><<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, n_comp, comp0, vf, vc,
+                                                                               coarse_flags);
+    else
+        restrict_kernel<2><<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, n_comp, comp0, vf,
                                                                                 vc, coarse_flags);
     return check_launch("pffmg_restrict");
 }
@@ -321,7 +325,11 @@ extern "C" int pffmg_prolongate(const pffmg_lattice* coarse, const pffmg_lattice
             Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
         return check_launch("pffmg_prolongate");
     }
-    prolongate_kernel<<<grid_points(Lf, 128), 128, 0, as_stream(stream)>>>(
+    if (Lf.dim == 3)
+        prolongate_kernel<3><<<grid_points(Lf, 128), 128, 0, as_stream(stream)>>>(
+            Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
+    else
+        prolongate_kernel<2><<<grid_points(Lf, 128), 128, 0, as_stream(stream)>>>(
         Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
     return check_launch("pffmg_prolongate");
 }
