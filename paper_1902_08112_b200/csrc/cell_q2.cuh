@@ -224,4 +224,186 @@ __device__ __forceinline__ void cell_q2(const double (&cv)[ModeInfo<2, MODE, MIE
     }
 }
 
+
+// Row-factorised NoSplit cell kernel for the hot modes (FULL / UBLK / PBLK):
+// the 9 QPs are processed one QP row (fixed qy) at a time; every nodal field
+// is first contracted along y for that row (6 values), then evaluated at the
+// row's 3 QPs, and the transposed pass accumulates x first, then y -- about
+// half the flops of the per-QP evaluation, and no 9 x NF corner array held in
+// registers (fields are re-read through `load(f, c)`, an L1 hit).
+// nocoup: FULL without the G_phiu coupling (block-diagonal operator).
+template <int MODE, class Load>
+__device__ __forceinline__ void cell_q2_rows(Load&& load, const double* __restrict__ rho_q, const Consts& K,
+                                             const Q2Tab& T, bool nocoup,
+                                             double (&o)[ModeInfo<2, MODE>::NCO][9]) {
+    using MI = ModeInfo<2, MODE>;
+    constexpr int NCO = MI::NCO;
+    constexpr bool HAS_U = MODE == M_FULL || MODE == M_UBLK;
+    constexpr bool HAS_P = MODE == M_FULL || MODE == M_PBLK;
+    constexpr bool NEED_STRAIN = MODE == M_FULL || MODE == M_PBLK;
+#pragma unroll
+    for (int k = 0; k < NCO; ++k)
+#pragma unroll
+        for (int n = 0; n < 9; ++n) o[k][n] = 0.0;
+    const bool cpl = MODE == M_FULL && !nocoup;
+#pragma unroll 1
+    for (int qy = 0; qy < 3; ++qy) {
+        double By[3], Dy[3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            By[b] = T.B[qy][b];
+            Dy[b] = T.D[qy][b] * K.ih[1];
+        }
+        // y-contraction of field f for this QP row: yv[a], yd[a] per node column a
+        auto ycon = [&](int f, double (&yv)[3], double (&yd)[3]) {
+            double c[9];
+            load(f, c);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                yv[a] = fma(By[0], c[a], fma(By[1], c[a + 3], By[2] * c[a + 6]));
+                yd[a] = fma(Dy[0], c[a], fma(Dy[1], c[a + 3], Dy[2] * c[a + 6]));
+            }
+        };
+        // ---- state coefficients at the row's 3 QPs (model.py:274-309)
+        double gr[3], aq[3], t00[3], t11[3], t01[3];
+#pragma unroll
+        for (int qx = 0; qx < 3; ++qx) {
+            gr[qx] = 1.0;
+            aq[qx] = t00[qx] = t11[qx] = t01[qx] = 0.0;
+        }
+        double ea[3] = {0, 0, 0}, eb[3] = {0, 0, 0}, ec[3] = {0, 0, 0};
+        if (NEED_STRAIN) {
+            double y0v[3], y0d[3], y1v[3], y1d[3];
+            ycon(MI::F_U + 0, y0v, y0d);
+            ycon(MI::F_U + 1, y1v, y1d);
+#pragma unroll
+            for (int qx = 0; qx < 3; ++qx) {
+                double u0x = 0, u0y = 0, u1x = 0, u1y = 0;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const double dx = T.D[qx][a] * K.ih[0], bx = T.B[qx][a];
+                    u0x = fma(dx, y0v[a], u0x);
+                    u0y = fma(bx, y0d[a], u0y);
+                    u1x = fma(dx, y1v[a], u1x);
+                    u1y = fma(bx, y1d[a], u1y);
+                }
+                ea[qx] = u0x;
+                ec[qx] = u1y;
+                eb[qx] = 0.5 * (u0y + u1x);
+            }
+        }
+        if (MI::PT) {
+            double yv[3], yd[3];
+            ycon(MI::F_PT, yv, yd);
+#pragma unroll
+            for (int qx = 0; qx < 3; ++qx) {
+                const double pt = fma(T.B[qx][0], yv[0], fma(T.B[qx][1], yv[1], T.B[qx][2] * yv[2]));
+                gr[qx] = fma(K.omk, pt * pt, K.kappa);                    // model.py:135-137
+            }
+        }
+        double phq[3] = {0, 0, 0};
+        if (MODE == M_FULL && cpl) {
+            double yv[3], yd[3];
+            ycon(MI::F_U + 2, yv, yd);
+#pragma unroll
+            for (int qx = 0; qx < 3; ++qx)
+                phq[qx] = fma(T.B[qx][0], yv[0], fma(T.B[qx][1], yv[1], T.B[qx][2] * yv[2]));
+        }
+#pragma unroll
+        for (int qx = 0; qx < 3; ++qx) {
+            const double rho = rho_q ? __ldg(rho_q + 3 * qy + qx) : 1.0;
+            gr[qx] *= rho;
+            if (NEED_STRAIN) {
+                const double div = ea[qx] + ec[qx];
+                const double Ep = 0.5 * K.lam * div * div +
+                                  K.mu * (ea[qx] * ea[qx] + 2.0 * eb[qx] * eb[qx] + ec[qx] * ec[qx]);
+                aq[qx] = K.omk * rho * Ep + K.two_p * div + K.gc_over_eps;    // model.py:304-308
+                if (MODE == M_FULL && cpl) {                                  // model.py:299-303
+                    const double c = rho * K.omk * phq[qx];
+                    const double ld = K.lam * div;
+                    t00[qx] = c * (2.0 * K.mu * ea[qx] + ld) + K.two_p * phq[qx];
+                    t11[qx] = c * (2.0 * K.mu * ec[qx] + ld) + K.two_p * phq[qx];
+                    t01[qx] = c * (2.0 * K.mu * eb[qx]);
+                }
+            }
+        }
+        // ---- increments and the transposed pass
+        const double wy = T.w[qy] * T.vol;
+        double tv[NCO][3], td[NCO][3];
+#pragma unroll
+        for (int k = 0; k < NCO; ++k)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) tv[k][a] = td[k][a] = 0.0;
+        double w00[3], w01[3], w10[3], w11[3];
+        if (HAS_U) {
+            double y0v[3], y0d[3], y1v[3], y1d[3];
+            ycon(MI::F_V + 0, y0v, y0d);
+            ycon(MI::F_V + 1, y1v, y1d);
+#pragma unroll
+            for (int qx = 0; qx < 3; ++qx) {
+                w00[qx] = w01[qx] = w10[qx] = w11[qx] = 0.0;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const double dx = T.D[qx][a] * K.ih[0], bx = T.B[qx][a];
+                    w00[qx] = fma(dx, y0v[a], w00[qx]);
+                    w01[qx] = fma(bx, y0d[a], w01[qx]);
+                    w10[qx] = fma(dx, y1v[a], w10[qx]);
+                    w11[qx] = fma(bx, y1d[a], w11[qx]);
+                }
+                const double jxw = wy * T.w[qx];
+                const double e01 = 0.5 * (w01[qx] + w10[qx]), tre = w00[qx] + w11[qx];
+                const double g = jxw * gr[qx];                               // model.py:316-319
+                const double s00 = g * (2.0 * K.mu * w00[qx] + K.lam * tre);
+                const double s11 = g * (2.0 * K.mu * w11[qx] + K.lam * tre);
+                const double s01 = g * (2.0 * K.mu * e01);
+                // u rows: sum_j s_ij dN/dx_j -> x pass (F = 0)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const double dx = T.D[qx][a] * K.ih[0], bx = T.B[qx][a];
+                    tv[0][a] = fma(dx, s00, tv[0][a]);
+                    td[0][a] = fma(bx, s01, td[0][a]);
+                    tv[1][a] = fma(dx, s01, tv[1][a]);
+                    td[1][a] = fma(bx, s11, td[1][a]);
+                }
+            }
+        }
+        if (HAS_P) {
+            double yv[3], yd[3];
+            ycon(MODE == M_FULL ? MI::F_V + 2 : MI::F_V, yv, yd);
+            constexpr int kp = MODE == M_FULL ? 2 : 0;
+#pragma unroll
+            for (int qx = 0; qx < 3; ++qx) {
+                double val = 0, gx = 0, gy = 0;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const double dx = T.D[qx][a] * K.ih[0], bx = T.B[qx][a];
+                    val = fma(bx, yv[a], val);
+                    gx = fma(dx, yv[a], gx);
+                    gy = fma(bx, yd[a], gy);
+                }
+                const double jxw = wy * T.w[qx];
+                double coup = 0.0;
+                if (MODE == M_FULL && cpl)
+                    coup = t00[qx] * w00[qx] + t01[qx] * (w01[qx] + w10[qx]) + t11[qx] * w11[qx];
+                const double F = jxw * (coup + aq[qx] * val);
+                const double Gx = jxw * K.k_phi * gx, Gy = jxw * K.k_phi * gy;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const double dx = T.D[qx][a] * K.ih[0], bx = T.B[qx][a];
+                    tv[kp][a] = fma(bx, F, fma(dx, Gx, tv[kp][a]));
+                    td[kp][a] = fma(bx, Gy, td[kp][a]);
+                }
+            }
+        }
+        // y pass of the transposed contraction
+#pragma unroll
+        for (int k = 0; k < NCO; ++k)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    o[k][3 * b + a] = fma(By[b], tv[k][a], fma(Dy[b], td[k][a], o[k][3 * b + a]));
+    }
+}
+
 }  // namespace pffmg

@@ -44,7 +44,25 @@ __global__ void __launch_bounds__(128) op2q_kernel(const OpArgs A, const Q2Tab T
     for (int cy = cy0 - 1; cy < cy1; ++cy) {
         double o[NCO][9];
         const bool cell = cx >= 0 && cx < L.nx && cy >= 0 && cy < L.ny;
-        if (cell) {
+        constexpr bool ROWS = !MIE && (MODE == M_FULL || MODE == M_UBLK || MODE == M_PBLK);
+        if (ROWS && cell) {
+            // row-factorised kernel: nodal fields re-read per QP row (L1 hits)
+            const int64_t id0 = (int64_t)(2 * cy) * nxn + 2 * cx;
+            unsigned fl[9];
+#pragma unroll
+            for (int n = 0; n < 9; ++n)
+                fl[n] = (NV > 0 && !A.premasked) ? __ldg(A.flags + id0 + (n / 3) * nxn + n % 3) : 0u;
+            auto load = [&](int f, double (&c)[9]) {
+#pragma unroll
+                for (int n = 0; n < 9; ++n) {
+                    double x = __ldg(fsrc[f] + id0 + (n / 3) * nxn + n % 3);
+                    if (f < NV && ((fl[n] >> (MI::COMP0 + f)) & 1)) x = 0.0;   // fem.py:205-206
+                    c[n] = x;
+                }
+            };
+            const double* rq = A.rho ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * 9 : nullptr;
+            if constexpr (ROWS) cell_q2_rows<MODE>(load, rq, A.K, T, A.nocoup != 0, o);
+        } else if (cell) {
             double cv[NF][9];
 #pragma unroll
             for (int b = 0; b < 3; ++b)
