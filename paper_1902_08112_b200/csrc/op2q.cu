@@ -15,8 +15,12 @@
 
 namespace pffmg {
 
+#ifndef PFFMG_Q2_MINB
+#define PFFMG_Q2_MINB 3
+#endif
+
 template <int MODE, int EPI, bool MIE>
-__global__ void __launch_bounds__(128) op2q_kernel(const OpArgs A, const Q2Tab T) {
+__global__ void __launch_bounds__(128, MODE == M_FULL ? 2 : PFFMG_Q2_MINB) op2q_kernel(const OpArgs A, const Q2Tab T) {
     using MI = ModeInfo<2, MODE, MIE>;
     constexpr int NF = MI::NF, NCO = MI::NCO, NV = MI::NV;
     const Lat& L = A.L;
