@@ -27,7 +27,7 @@ def run(strips):
     torch.cuda.current_stream().synchronize()
 
 
-for strips in (2, 3, 4, 5, 6, 8, 10, 12):
+for strips in (1, 2, 3, 4, 6, 8, 12, 16):
     run(strips)
     ts = []
     for _ in range(30):
