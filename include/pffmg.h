@@ -36,6 +36,8 @@ extern "C" {
                                phi row = apply_block(1)): the operator of the block smoother */
 
 #define PFFMG_HINT_PREMASKED 1
+#define PFFMG_HINT_ENDS 2       /* finalise only the first and the last owned plane (slab
+                                   boundary rows once the halo has landed) */
 
 /*
  * Level geometry: a (possibly non-box) lattice of congruent cells.  Vertex
@@ -84,7 +86,10 @@ typedef struct {
     int32_t hints;              /* bit 0 (PFFMG_HINT_PREMASKED): every input vector of the
                                    call is already zero at constrained dofs, so the masked
                                    gather (fem.py:205-206) can be skipped.  Results are
-                                   identical; a wrong hint gives wrong results. */
+                                   identical; a wrong hint gives wrong results.
+                                   bit 1 (PFFMG_HINT_ENDS): operator calls finalise only
+                                   planes own_lo and own_hi-1 (one launch for both slab
+                                   boundary rows of an overlapped halo exchange). */
     const double* U;            /* (dim+1)*V linearisation point (may be NULL for the u block) */
     const double* phi_tilde;    /* V extrapolated phase field (may be NULL for the phi block) */
     const double* rho;          /* NULL (rho == 1) or modulus field per lattice cell x QP */

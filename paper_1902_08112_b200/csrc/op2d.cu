@@ -38,7 +38,7 @@ int launch2d(const OpArgs& A0, bool iso, cudaStream_t s) {
     using MI = ModeInfo<2, MODE>;
     const int sms = sm_count();
     const int nseg = (L.nx + 1 + 29) / 30;
-    const int rows = L.own_hi - L.own_lo;
+    const int rows = A.ends ? 2 : L.own_hi - L.own_lo;
     // strips of H vertex rows: aim for ~24 resident warps per SM in one wave,
     // H in [4, 64] (the first cell row of a strip is recomputed: overhead 1/H)
     int64_t per = ((int64_t)rows * nseg + 24LL * sms - 1) / (24LL * sms);
@@ -53,6 +53,7 @@ int launch2d(const OpArgs& A0, bool iso, cudaStream_t s) {
         return e ? atoi(e) : 0;
     }();
     if (forced > 0) per = forced;
+    if (A.ends) per = 1;
     A.planes_per_cta = (int)per;
     A.nseg = nseg;
     const int64_t warps = (int64_t)nseg * ((rows + per - 1) / per);

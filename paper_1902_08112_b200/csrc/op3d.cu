@@ -40,7 +40,7 @@ static int launch_stream(const OpArgs& A0, cudaStream_t s) {
     const int sms = sm_count();
     const int gx = (L.nx + 1 + 29) / 30;
     const int gy = (L.ny + 1 + TY3T - 2) / (TY3T - 1);
-    const int planes = L.own_hi - L.own_lo;
+    const int planes = A.ends ? 2 : L.own_hi - L.own_lo;
     // ~2 CTAs of work per SM per wave, strips of 4..32 planes
     int64_t per = ((int64_t)planes * gx * gy + 2LL * sms - 1) / (2LL * sms);
     static const int minp = [] {
@@ -53,6 +53,7 @@ static int launch_stream(const OpArgs& A0, cudaStream_t s) {
         return e ? atoi(e) : 0;
     }();
     if (forced > 0) per = forced;
+    if (A.ends) per = 1;
     A.planes_per_cta = (int)per;
     dim3 grid(gx, gy, (unsigned)((planes + per - 1) / per));
     constexpr int ROWS = TY3T + 1;
@@ -83,9 +84,10 @@ int launch3d(const OpArgs& A0, bool iso, cudaStream_t s) {
     const size_t smem = sizeof(double) * (2 * nf * TV + TY3D * 2 * MI::NCO * 32) + 2 * TV;
     const int gx = (L.nx + 1 + 30) / 31;
     const int gy = (L.ny + 1 + TY3D - 2) / (TY3D - 1);
-    const int planes = L.own_hi - L.own_lo;
+    const int planes = A.ends ? 2 : L.own_hi - L.own_lo;
     int per = (int)(((int64_t)planes * gx * gy + 2LL * sms - 1) / (2LL * sms));
     per = per < 4 ? 4 : (per > 32 ? 32 : per);
+    if (A.ends) per = 1;
     A.planes_per_cta = per;
     dim3 grid(gx, gy, (planes + per - 1) / per);
     if (A.split) {   // Miehe spectral split: general cells, per-QP Jacobi eigen-solve

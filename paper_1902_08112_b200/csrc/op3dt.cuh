@@ -34,8 +34,9 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int x0 = 30 * (int)blockIdx.x - 1;
     const int y0 = (TY - 1) * (int)blockIdx.y - 1;
-    const int vz0 = L.own_lo + (int)blockIdx.z * A.planes_per_cta;
-    const int vz1 = min(vz0 + A.planes_per_cta, L.own_hi);
+    const int vz0 = A.ends ? ((int)blockIdx.z == 0 ? L.own_lo : L.own_hi - 1)
+                           : L.own_lo + (int)blockIdx.z * A.planes_per_cta;
+    const int vz1 = A.ends ? vz0 + 1 : min(vz0 + A.planes_per_cta, L.own_hi);
     const int cx = x0 + lane, cy = y0 + w;
     const int V = (int)L.V;
     const int nwords = (V + 3) / 4 + 8;

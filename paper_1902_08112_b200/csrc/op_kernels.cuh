@@ -43,6 +43,7 @@ struct OpArgs {
     int planes_per_cta;
     int nseg;                          // 2D warp kernel: 30-column segments per row
     int premasked;                     // PFFMG_HINT_PREMASKED
+    int ends;                          // PFFMG_HINT_ENDS: strips = {own_lo}, {own_hi - 1}
     int split;                         // 0 NoSplit, 1 Miehe spectral split (2D)
 };
 
@@ -194,9 +195,10 @@ op2dw_kernel(const OpArgs A) {
     const Lat& L = A.L;
     const int gw = (int)blockIdx.x * NW + w;
     const int seg = gw % A.nseg, strip = gw / A.nseg;
-    const int vy0 = L.own_lo + strip * A.planes_per_cta;
+    if (A.ends && strip > 1) return;
+    const int vy0 = A.ends ? (strip == 0 ? L.own_lo : L.own_hi - 1) : L.own_lo + strip * A.planes_per_cta;
     if (vy0 >= L.own_hi) return;
-    const int vy1 = min(vy0 + A.planes_per_cta, L.own_hi);
+    const int vy1 = A.ends ? vy0 + 1 : min(vy0 + A.planes_per_cta, L.own_hi);
     const int x0 = 30 * seg - 1;
     const int cx = x0 + lane;
     const int V = (int)L.V;
@@ -362,8 +364,9 @@ __global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int cx0 = -1 + (int)blockIdx.x * 31;
     const int cy0 = -1 + (int)blockIdx.y * (TY - 1);
-    const int vz0 = L.own_lo + (int)blockIdx.z * A.planes_per_cta;
-    const int vz1 = min(vz0 + A.planes_per_cta, L.own_hi);
+    const int vz0 = A.ends ? ((int)blockIdx.z == 0 ? L.own_lo : L.own_hi - 1)
+                           : L.own_lo + (int)blockIdx.z * A.planes_per_cta;
+    const int vz1 = A.ends ? vz0 + 1 : min(vz0 + A.planes_per_cta, L.own_hi);
     const int cx = cx0 + lane, cy = cy0 + w;
 
     auto SV = [&](int buf, int f, int j) -> double& { return sv[(buf * NF + f) * TV + j]; };

@@ -43,6 +43,11 @@ static int fill_args(const pffmg_lattice* lat, const pffmg_state* st, OpArgs* A)
     A->rho = st->rho;
     A->flags = st->flags;
     A->premasked = (st->hints & PFFMG_HINT_PREMASKED) ? 1 : 0;
+    A->ends = (st->hints & PFFMG_HINT_ENDS) ? 1 : 0;
+    if (A->ends) {
+        PFFMG_REQUIRE(A->L.own_hi - A->L.own_lo >= 2 && A->L.order == 1,
+                      "PFFMG_HINT_ENDS needs >= 2 owned planes of a Q1 lattice");
+    }
     return PFFMG_OK;
 }
 

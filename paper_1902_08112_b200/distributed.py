@@ -286,8 +286,7 @@ class DistributedOperator:
             h = self.halo.start(v_loc, self.n_comp)
             self.local.apply_rows_dev(_lib.FULL, v_loc, out_loc, lo + 1, hi - 1)
             self.halo.finish(h)
-            self.local.apply_rows_dev(_lib.FULL, v_loc, out_loc, lo, lo + 1)
-            self.local.apply_rows_dev(_lib.FULL, v_loc, out_loc, hi - 1, hi)
+            self.local.apply_ends_dev(_lib.FULL, v_loc, out_loc)      # rows lo and hi-1, one launch
             return out_loc
         self.halo.exchange(v_loc, self.n_comp)
         if hasattr(self.local, "apply_dev") and v_loc.is_cuda:

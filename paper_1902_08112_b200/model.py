@@ -182,12 +182,18 @@ class PhaseFieldOperator:
         st_pre.hints = 1
         self._st_pre = st_pre
         self._stp_pre = ctypes.byref(st_pre)
+        # ... and with PFFMG_HINT_ENDS: only the first and last owned plane (slab boundaries)
+        st_ends = _lib.State()
+        ctypes.pointer(st_ends)[0] = st
+        st_ends.hints = 2
+        self._st_ends = st_ends
+        self._stp_ends = ctypes.byref(st_ends)
 
     def _rebind(self, U, phi_tilde, flags):
         """Point the operator at other device buffers of the same sizes (used
         to detach an earlier generation of solver contexts, mgsolve._Session)."""
         self._U, self._pt, self._flags = U, phi_tilde, flags
-        for st in (self._st, self._st_pre):
+        for st in (self._st, self._st_pre, self._st_ends):
             st.U = U.data_ptr()
             st.phi_tilde = phi_tilde.data_ptr()
             st.flags = flags.data_ptr()
@@ -268,6 +274,11 @@ class PhaseFieldOperator:
     def apply_rows_dev(self, which, x, out, lo, hi, pre=False):
         """apply_dev finalising only vertex planes [lo, hi) of the last axis."""
         _lib.call("pffmg_apply", self.lat.rows(lo, hi), self._sp(pre), which, _lib.ptr(x), _lib.ptr(out),
+                  _lib.stream())
+
+    def apply_ends_dev(self, which, x, out):
+        """apply_dev finalising only the first and the last owned plane (one launch)."""
+        _lib.call("pffmg_apply", self.lat.ref, self._stp_ends, which, _lib.ptr(x), _lib.ptr(out),
                   _lib.stream())
 
     def residual_dev(self, which, x, b, out, pre=False):

@@ -58,6 +58,11 @@ def test_slab_operator_stitches(name, world):
             op.local.apply_rows_dev(_lib.FULL, v_loc, out2, hi - 1, hi)
             for sl in op.owned:
                 assert torch.equal(out[sl], out2[sl])
+            out3 = torch.zeros_like(out)
+            op.local.apply_rows_dev(_lib.FULL, v_loc, out3, lo + 1, hi - 1)
+            op.local.apply_ends_dev(_lib.FULL, v_loc, out3)                # PFFMG_HINT_ENDS
+            for sl in op.owned:
+                assert torch.equal(out[sl], out3[sl])
         s = part.slab(L)
         a, b = int(offs[s.own_lo]), int(offs[s.own_hi])
         per = b - a
