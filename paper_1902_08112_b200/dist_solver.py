@@ -238,7 +238,7 @@ class DistGMG:
         """Refresh the ghost planes of a level-l vector (no-op on replicated levels)."""
         lev = self.L[l]
         if lev.sharded:
-            lev.halo.exchange(vec, n_comp)
+            lev.halo.exchange(vec, n_comp, persistent=True)     # level buffers of the cycle
 
     def restrict(self, l, fine, coarse, n_comp, comp0):
         """coarse (level l) = masked P^T fine (level l+1); agglomerated into a replicated level."""

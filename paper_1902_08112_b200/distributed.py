@@ -150,28 +150,42 @@ class Halo:
         self.recv_down = (int(self.offs[0]), int(self.offs[1])) if slab.has_lower else None
         self.send_up = (int(self.offs[hi_own - 1]), int(self.offs[hi_own])) if slab.has_upper else None
         self.recv_up = (int(self.offs[hi_own]), int(self.offs[hi_own + 1])) if slab.has_upper else None
+        self._ops = {}
 
-    def exchange(self, vec, n_comp):
+    def exchange(self, vec, n_comp, persistent=False):
         """Refresh ghost planes of `vec` (a 1-D tensor of n_comp * V entries) in place.
 
         With NCCL the planes go device to device; with gloo (CPU tests, or
         ranks sharing one GPU in tests) CUDA planes are staged through host memory."""
-        self.finish(self.start(vec, n_comp))
+        self.finish(self.start(vec, n_comp, persistent))
         return vec
 
-    def start(self, vec, n_comp):
+    def start(self, vec, n_comp, persistent=False):
         """Post the exchange; returns a handle for finish().  Under NCCL the
         transfers run on NCCL's stream, concurrently with work enqueued on the
-        current stream afterwards (which must not touch the ghost planes)."""
+        current stream afterwards (which must not touch the ghost planes).
+        `persistent`: `vec` is a long-lived buffer, so its device-to-device op
+        list is built once and reused (the per-call host work is then one
+        batched NCCL group)."""
         if self.world == 1 or self.slab.replicated:
             return None
         stage = vec.is_cuda and _backend(self.group) != "nccl"
-        ops, back = [], []
+        if not stage:
+            key = (vec.data_ptr(), vec.numel(), n_comp)
+            ops = self._ops.get(key) if persistent else None
+            if ops is None:
+                ops = self._build_ops(vec, n_comp, lambda t: t, [])
+                if persistent:
+                    self._ops[key] = ops
+            return (dist.batch_isend_irecv(ops) if ops else []), []
+        back = []
+        ops = self._build_ops(vec, n_comp, lambda t: t.cpu(), back)
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        return reqs, back
+
+    def _build_ops(self, vec, n_comp, buf, back):
+        ops = []
         V = self.V
-
-        def buf(t):
-            return t.cpu() if stage else t
-
         for c in range(n_comp):
             base = c * V
             for send, recv, peer in ((self.send_down, self.recv_down, self.rank - 1),
@@ -183,10 +197,9 @@ class Halo:
                 a, b = recv
                 r = buf(vec[base + a:base + b])
                 ops.append(dist.P2POp(dist.irecv, r, peer, self.group))
-                if stage:
+                if r.data_ptr() != vec[base + a:base + b].data_ptr():
                     back.append((vec[base + a:base + b], r))
-        reqs = dist.batch_isend_irecv(ops) if ops else []
-        return reqs, back
+        return ops
 
     @staticmethod
     def finish(handle):
@@ -283,7 +296,7 @@ class DistributedOperator:
         if (hasattr(self.local, "apply_rows_dev") and v_loc.is_cuda and self.world > 1
                 and hi - lo >= 3 and not self.slab.replicated):
             from . import _lib
-            h = self.halo.start(v_loc, self.n_comp)
+            h = self.halo.start(v_loc, self.n_comp, persistent=True)
             self.local.apply_rows_dev(_lib.FULL, v_loc, out_loc, lo + 1, hi - 1)
             self.halo.finish(h)
             self.local.apply_ends_dev(_lib.FULL, v_loc, out_loc)      # rows lo and hi-1, one launch
