@@ -154,7 +154,10 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8d)",
-        "config": {"workload": f"{args.config} vmult", "n_dofs": prob.n_dofs},
+        "config": {"workload": (f"{args.config} vmult" if args.gpus <= 1 else
+                                f"{args.config} x{args.gpus} stacked vmult (CPU sample: one {args.config} "
+                                f"square; the CPU rate per DoF does not depend on the stacking)"),
+                   "n_dofs": prob.n_dofs},
         "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": threads, "kind": "port",
                          "sample": f"{args.config} full-size vmult x{args.steps} (oracle/ numpy "
                                    f"restatement of model.py:368-375, {threads} threads); "
