@@ -386,10 +386,13 @@ def run_gpu(args):
          "cfg3": "cfg3: 2D pressurised cracks 512^2 Q2 (3x3 Gauss) NoSplit vmult, p = 1e-3",
          "cfg4": "cfg4: 3D L-prism 786k Q1 hexes NoSplit vmult",
          "cfg5": "cfg5: 3D cube 384^3 Q1 hexes NoSplit vmult"}.get(args.config, args.config)
+    if ws > 1 and args.config != "cfg2":
+        workload += f", strong scaling: {ws} slabs of the last axis, {args.backend} halo exchange"
     line = {
         "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if (ws == 1 or args.config == "cfg2") else "strong", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic (seeded state/vector, SURVEY §8d; random-init, no dataset)",
         "config": {"workload": workload,
                    "n_dofs": n, "n_vertices": mesh.n_vertices, "n_cells": mesh.n_cells,
