@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -24,6 +25,14 @@ int check_launch(const char* what) {
         return PFFMG_ERR_CUDA;
     }
     return PFFMG_OK;
+}
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("PFFMG_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 int sm_count() {

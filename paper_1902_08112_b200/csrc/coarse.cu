@@ -77,6 +77,7 @@ struct CoarseCell {
 
 template <int D, int KIND>
 __global__ void __launch_bounds__(CT, 1) coarse_cheb_kernel(const CoarseArgs C) {
+    pdl_wait();
     using CC = CoarseCell<D, KIND>;
     constexpr int NCO = CC::NCO, NPC = CC::NPC;
     extern __shared__ double cellbuf[];                       // [cells][NCO][NPC]
@@ -182,7 +183,7 @@ static int launch_coarse(const CoarseArgs& C, size_t smem, cudaStream_t s) {
         cudaFuncSetAttribute(coarse_cheb_kernel<D, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         done = true;
     }
-    coarse_cheb_kernel<D, KIND><<<1, CT, smem, s>>>(C);
+    pdl_launch(coarse_cheb_kernel<D, KIND>, dim3(1), dim3(CT), smem, s, C);
     return check_launch("pffmg_coarse_cheb");
 }
 

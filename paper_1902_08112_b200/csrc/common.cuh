@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include "../../include/pffmg.h"
 
 namespace pffmg {
@@ -257,6 +259,32 @@ struct SFr {
         }
     }
 };
+
+// Programmatic dependent launch ---------------------------------------------
+// Every libpffmg kernel is launched with the programmatic-stream-serialization
+// attribute (pdl_launch) and begins with pdl_wait(): the next kernel of a
+// chain (a V-cycle, a CG run) is scheduled while the previous one drains, and
+// waits for its completion (and memory flush) before touching data.  The wait
+// returns at once when there is no prerequisite grid.  PFFMG_PDL=0 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Deterministic block reduction helpers --------------------------------------
 

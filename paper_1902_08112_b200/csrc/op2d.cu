@@ -15,7 +15,7 @@ static void launch_w(const OpArgs& A, dim3 grid, size_t smem, cudaStream_t s) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         done = smem;
     }
-    op2dw_kernel<MODE, EPI, NW2D, ISO, RHO, BOX, PRE, MIE><<<grid, 32 * NW2D, smem, s>>>(A);
+    pdl_launch(op2dw_kernel<MODE, EPI, NW2D, ISO, RHO, BOX, PRE, MIE>, dim3(grid), dim3(32 * NW2D), smem, s, A);
 }
 
 template <int MODE, int EPI, bool ISO, bool RHO, bool MIE = false>

@@ -21,6 +21,7 @@ namespace pffmg {
 
 template <int MODE, int EPI, bool MIE>
 __global__ void __launch_bounds__(128, MODE == M_FULL ? 2 : PFFMG_Q2_MINB) op2q_kernel(const OpArgs A, const Q2Tab T) {
+    pdl_wait();
     using MI = ModeInfo<2, MODE, MIE>;
     constexpr int NF = MI::NF, NCO = MI::NCO, NV = MI::NV;
     const Lat& L = A.L;
@@ -147,9 +148,9 @@ int launch2q(const OpArgs& A0, cudaStream_t s) {
     const dim3 grid((unsigned)((warps + 3) / 4));
     const Q2Tab T = make_q2_host(L.hx, L.hy);
     if (A.split)
-        op2q_kernel<MODE, EPI, true><<<grid, 128, 0, s>>>(A, T);
+        pdl_launch(op2q_kernel<MODE, EPI, true>, dim3(grid), dim3(128), 0, s, A, T);
     else
-        op2q_kernel<MODE, EPI, false><<<grid, 128, 0, s>>>(A, T);
+        pdl_launch(op2q_kernel<MODE, EPI, false>, dim3(grid), dim3(128), 0, s, A, T);
     return PFFMG_OK;
 }
 

@@ -29,7 +29,7 @@ static void launch_t(const OpArgs& A, dim3 grid, size_t smem, cudaStream_t s) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         done = smem;
     }
-    op3dt_kernel<MODE, EPI, TY3T, RHO, BOX, PRE><<<grid, 32 * TY3T, smem, s>>>(A);
+    pdl_launch(op3dt_kernel<MODE, EPI, TY3T, RHO, BOX, PRE>, dim3(grid), dim3(32 * TY3T), smem, s, A);
 }
 
 template <int MODE, int EPI>
@@ -92,13 +92,13 @@ int launch3d(const OpArgs& A0, bool iso, cudaStream_t s) {
     dim3 grid(gx, gy, (planes + per - 1) / per);
     if (A.split) {   // Miehe spectral split: general cells, per-QP Jacobi eigen-solve
         set_smem<MODE, EPI, false, true>(smem);
-        op3d_kernel<MODE, EPI, TY3D, false, true><<<grid, 32 * TY3D, smem, s>>>(A);
+        pdl_launch(op3d_kernel<MODE, EPI, TY3D, false, true>, dim3(grid), dim3(32 * TY3D), smem, s, A);
     } else if (iso) {
         set_smem<MODE, EPI, true>(smem);
-        op3d_kernel<MODE, EPI, TY3D, true><<<grid, 32 * TY3D, smem, s>>>(A);
+        pdl_launch(op3d_kernel<MODE, EPI, TY3D, true>, dim3(grid), dim3(32 * TY3D), smem, s, A);
     } else {
         set_smem<MODE, EPI, false>(smem);
-        op3d_kernel<MODE, EPI, TY3D, false><<<grid, 32 * TY3D, smem, s>>>(A);
+        pdl_launch(op3d_kernel<MODE, EPI, TY3D, false>, dim3(grid), dim3(32 * TY3D), smem, s, A);
     }
     return PFFMG_OK;
 }

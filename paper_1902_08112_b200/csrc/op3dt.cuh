@@ -18,6 +18,7 @@ template <int MODE, int EPI, int TY, bool RHO, bool BOX, bool PRE>
 #define PFFMG_3D_FULL_MINB 1
 #endif
 __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB : 2) op3dt_kernel(const OpArgs A) {
+    pdl_wait();
     using MI = ModeInfo<3, MODE>;
     constexpr int NF = MI::NF, NCO = MI::NCO, NV = MI::NV;
     constexpr int RING = 4, ROWS = TY + 1, W = 32;

@@ -179,6 +179,7 @@ template <int MODE, int EPI, int NW, bool ISO, bool RHO, bool BOX, bool PRE, boo
 #endif
 __global__ void __launch_bounds__(32 * NW, MIE ? 2 : (MODE == M_FULL ? PFFMG_MINB_FULL : PFFMG_MINB_BLK))
 op2dw_kernel(const OpArgs A) {
+    pdl_wait();
     constexpr int D = 2, NP = 4;
     using MI = ModeInfo<D, MODE, MIE>;
     constexpr int NF = MI::NF, NCO = MI::NCO, NV = MI::NV;
@@ -348,6 +349,7 @@ op2dw_kernel(const OpArgs A) {
 
 template <int MODE, int EPI, int TY, bool ISO, bool MIE = false>
 __global__ void __launch_bounds__(32 * TY) op3d_kernel(const OpArgs A) {
+    pdl_wait();
     constexpr int D = 3, NP = 8;
     using MI = ModeInfo<D, MODE, MIE>;
     constexpr int NF = MI::NF, NCO = MI::NCO;

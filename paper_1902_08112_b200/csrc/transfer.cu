@@ -51,6 +51,7 @@ __device__ __forceinline__ void fine_of(const Lat& Lc, const Lat& Lf, int x, int
 template <int D>
 __global__ void restrict_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vf,
                                 double* __restrict__ vc, const uint8_t* __restrict__ cflags) {
+    pdl_wait();
     int x, y, z;
     if (!grid_point(Lc, x, y, z)) return;
     {
@@ -91,6 +92,7 @@ template <int D>
 __global__ void prolongate_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vc,
                                   double* __restrict__ vf, const uint8_t* __restrict__ fflags,
                                   int accumulate) {
+    pdl_wait();
     int X, Y, Z;
     if (!grid_point(Lf, X, Y, Z)) return;
     const int64_t fid = vertex_id(Lf, X, Y, Z);
@@ -162,6 +164,7 @@ __device__ __forceinline__ int q2_prolong_taps(int j, int (&idx)[3], double (&w)
 // Lc / Lf are the NODE lattices (nx = 2 * cells): nxn = nx + 1 nodes per row
 __global__ void restrict_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vf,
                                    double* __restrict__ vc, const uint8_t* __restrict__ cflags) {
+    pdl_wait();
     const int nxc = Lc.nx + 1, nyc = Lc.ny + 1, nxf = Lf.nx + 1, nyf = Lf.ny + 1;
     const int64_t npts = (int64_t)nxc * nyc;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
@@ -196,6 +199,7 @@ __global__ void restrict_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const d
 __global__ void prolongate_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vc,
                                      double* __restrict__ vf, const uint8_t* __restrict__ fflags,
                                      int accumulate) {
+    pdl_wait();
     const int nxc = Lc.nx + 1, nxf = Lf.nx + 1, nyf = Lf.ny + 1;
     const int64_t npts = (int64_t)nxf * nyf;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
@@ -222,6 +226,7 @@ __global__ void prolongate_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const
 
 __global__ void inject_f64_kernel(Lat Lc, Lat Lf, int ncomp, const double* __restrict__ vf,
                                   double* __restrict__ vc) {
+    pdl_wait();
     int x, y, z;
     if (!grid_point(Lc, x, y, z)) return;
     {
@@ -236,6 +241,7 @@ __global__ void inject_f64_kernel(Lat Lc, Lat Lf, int ncomp, const double* __res
 
 __global__ void inject_u8_kernel(Lat Lc, Lat Lf, const uint8_t* __restrict__ ff, uint8_t* __restrict__ fc,
                                  int64_t* __restrict__ map) {
+    pdl_wait();
     int x, y, z;
     if (!grid_point(Lc, x, y, z)) return;
     {
@@ -298,15 +304,14 @@ extern "C" int pffmg_restrict(const pffmg_lattice* coarse, const pffmg_lattice* 
     PFFMG_REQUIRE(vf && vc && n_comp >= 1 && comp0 >= 0 && comp0 + n_comp <= Lc.dim + 1,
                   "pffmg_restrict: bad arguments");
     if (q2) {
-        restrict_q2_kernel<<<grid_for((int64_t)(Lc.nx + 1) * (Lc.ny + 1)), 256, 0, as_stream(stream)>>>(
-            Lc, Lf, n_comp, comp0, vf, vc, coarse_flags);
+        pdl_launch(restrict_q2_kernel, dim3(grid_for((int64_t)(Lc.nx + 1) * (Lc.ny + 1))), dim3(256), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vf, vc, coarse_flags);
         return check_launch("pffmg_restrict");
     }
     if (Lc.dim == 3)
-        restrict_kernel<3><<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, n_comp, comp0, vf, vc,
+        pdl_launch(restrict_kernel<3>, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vf, vc,
                                                                                coarse_flags);
     else
-        restrict_kernel<2><<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, n_comp, comp0, vf,
+        pdl_launch(restrict_kernel<2>, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vf,
                                                                                 vc, coarse_flags);
     return check_launch("pffmg_restrict");
 }
@@ -321,16 +326,13 @@ extern "C" int pffmg_prolongate(const pffmg_lattice* coarse, const pffmg_lattice
     PFFMG_REQUIRE(vf && vc && n_comp >= 1 && comp0 >= 0 && comp0 + n_comp <= Lc.dim + 1,
                   "pffmg_prolongate: bad arguments");
     if (q2) {
-        prolongate_q2_kernel<<<grid_for((int64_t)(Lf.nx + 1) * (Lf.ny + 1)), 256, 0, as_stream(stream)>>>(
-            Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
+        pdl_launch(prolongate_q2_kernel, dim3(grid_for((int64_t)(Lf.nx + 1) * (Lf.ny + 1))), dim3(256), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
         return check_launch("pffmg_prolongate");
     }
     if (Lf.dim == 3)
-        prolongate_kernel<3><<<grid_points(Lf, 128), 128, 0, as_stream(stream)>>>(
-            Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
+        pdl_launch(prolongate_kernel<3>, dim3(grid_points(Lf, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
     else
-        prolongate_kernel<2><<<grid_points(Lf, 128), 128, 0, as_stream(stream)>>>(
-        Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
+        pdl_launch(prolongate_kernel<2>, dim3(grid_points(Lf, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
     return check_launch("pffmg_prolongate");
 }
 
@@ -340,7 +342,7 @@ extern "C" int pffmg_inject_f64(const pffmg_lattice* coarse, const pffmg_lattice
     int rc = check_pair(coarse, fine, &Lc, &Lf);
     if (rc) return rc;
     PFFMG_REQUIRE(vf && vc && n_comp >= 1, "pffmg_inject_f64: bad arguments");
-    inject_f64_kernel<<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, n_comp, vf, vc);
+    pdl_launch(inject_f64_kernel, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, n_comp, vf, vc);
     return check_launch("pffmg_inject_f64");
 }
 
@@ -350,7 +352,7 @@ extern "C" int pffmg_inject_flags(const pffmg_lattice* coarse, const pffmg_latti
     int rc = check_pair(coarse, fine, &Lc, &Lf);
     if (rc) return rc;
     PFFMG_REQUIRE(ff && fc, "pffmg_inject_flags: bad arguments");
-    inject_u8_kernel<<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, ff, fc, nullptr);
+    pdl_launch(inject_u8_kernel, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, ff, fc, nullptr);
     return check_launch("pffmg_inject_flags");
 }
 
@@ -360,6 +362,6 @@ extern "C" int pffmg_injection_map(const pffmg_lattice* coarse, const pffmg_latt
     int rc = check_pair(coarse, fine, &Lc, &Lf);
     if (rc) return rc;
     PFFMG_REQUIRE(out, "pffmg_injection_map: null out");
-    inject_u8_kernel<<<grid_points(Lc, 128), 128, 0, as_stream(stream)>>>(Lc, Lf, nullptr, nullptr, out);
+    pdl_launch(inject_u8_kernel, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, nullptr, nullptr, out);
     return check_launch("pffmg_injection_map");
 }

@@ -74,6 +74,7 @@ __device__ __forceinline__ void block_sum2(double& a0, double& a1) {
 // Generic fused "elementwise update + up to two sums + scalar finisher".
 template <class Op>
 __global__ void __launch_bounds__(RT) fused_kernel(Op op, int64_t n, Scratch* S) {
+    pdl_wait();
     if (op.skip()) return;
     op.prepare();
     double a0 = 0.0, a1 = 0.0;
@@ -113,7 +114,7 @@ static int run_fused(const Op& op, int64_t n, cudaStream_t s, const char* what) 
     Scratch* S;
     int rc = scratch(s, &S);
     if (rc) return rc;
-    fused_kernel<Op><<<red_blocks(n), RT, 0, s>>>(op, n, S);
+    pdl_launch(fused_kernel<Op>, dim3(red_blocks(n)), dim3(RT), 0, s, op, n, S);
     return check_launch(what);
 }
 
@@ -291,6 +292,7 @@ static dim3 vgrid(int64_t n) {
 }
 
 __global__ void pack_flags_k(const uint8_t* m, int nc, int64_t V, uint8_t* f) {
+    pdl_wait();
     GRID_STRIDE(v, V) {
         uint8_t b = 0;
         for (int c = 0; c < nc; ++c) b |= (uint8_t)((m[(int64_t)c * V + v] != 0) << c);
@@ -298,12 +300,14 @@ __global__ void pack_flags_k(const uint8_t* m, int nc, int64_t V, uint8_t* f) {
     }
 }
 __global__ void unpack_flags_k(const uint8_t* f, int nc, int64_t V, uint8_t* m) {
+    pdl_wait();
     GRID_STRIDE(v, V) {
         const uint8_t b = f[v];
         for (int c = 0; c < nc; ++c) m[(int64_t)c * V + v] = (b >> c) & 1;
     }
 }
 __global__ void masked_copy_k(const uint8_t* f, int64_t V, int comp0, int nc, const double* in, double* out) {
+    pdl_wait();
     GRID_STRIDE(i, V * nc) {
         const int c = (int)(i / V);
         const int64_t v = i - (int64_t)c * V;
@@ -311,10 +315,12 @@ __global__ void masked_copy_k(const uint8_t* f, int64_t V, int comp0, int nc, co
     }
 }
 __global__ void reciprocal_k(const double* d, double* o, int64_t n) {
+    pdl_wait();
     GRID_STRIDE(i, n) o[i] = 1.0 / d[i];
 }
 __global__ void cheb_init_zero_k(const double* b, const double* inv, double theta_v, const double* theta_p,
                                  double* r, double* d, double* x, int64_t n) {
+    pdl_wait();
     const double theta = theta_p ? *theta_p : theta_v;
     GRID_STRIDE(i, n) {
         const double ri = b[i];
@@ -326,10 +332,12 @@ __global__ void cheb_init_zero_k(const double* b, const double* inv, double thet
 }
 __global__ void jacobi_update_k(const double* r, const double* inv, double theta_v, const double* theta_p,
                                 double* x, int64_t n) {
+    pdl_wait();
     const double theta = theta_p ? *theta_p : theta_v;
     GRID_STRIDE(i, n) x[i] += (inv[i] * r[i]) / theta;   // mgsolve.py:99
 }
 __global__ void axpby_k(double a, const double* x, double b, double* y, int64_t n, int mode) {
+    pdl_wait();
     GRID_STRIDE(i, n) {
         if (mode == 0) y[i] = fma(a, x[i], y[i]);
         else if (mode == 1) y[i] = a * x[i] + b * y[i];
@@ -338,6 +346,7 @@ __global__ void axpby_k(double a, const double* x, double b, double* y, int64_t 
     }
 }
 __global__ void sub_k(const double* x, const double* y, double* o, int64_t n) {
+    pdl_wait();
     GRID_STRIDE(i, n) o[i] = x[i] - y[i];
 }
 // Primal-dual active set of the phase field (nonlinear.py:75-89):
@@ -346,6 +355,7 @@ __global__ void sub_k(const double* x, const double* y, double* o, int64_t n) {
 // so the set is bit-exact for identical inputs.
 __global__ void active_set_k(const double* R, const double* U, const double* phi_old, const double* minv,
                              double c, const uint8_t* dflags, int comp, int64_t V, uint8_t* active) {
+    pdl_wait();
     GRID_STRIDE(v, V) {
         const double ind = __dadd_rn(__dmul_rn(minv[v], R[v]), __dmul_rn(c, __dsub_rn(U[v], phi_old[v])));
         bool a = ind > 0.0;
@@ -356,6 +366,7 @@ __global__ void active_set_k(const double* R, const double* U, const double* phi
 
 // x += sum_k y[k] * Z_k   (krylov.py:132: x + Z[:j].T @ y)
 __global__ void multi_axpy_k(const double* Z, int64_t ld, int k, const double* y, double* x, int64_t n) {
+    pdl_wait();
     __shared__ double ys[64];
     if (threadIdx.x < k) ys[threadIdx.x] = y[threadIdx.x];
     __syncthreads();
@@ -374,39 +385,40 @@ using namespace pffmg;
 
 extern "C" int pffmg_pack_flags(const uint8_t* mask, int n_comp, int64_t V, uint8_t* flags, void* stream) {
     PFFMG_REQUIRE(mask && flags && n_comp >= 1 && n_comp <= 8 && V >= 0, "pffmg_pack_flags: bad args");
-    pack_flags_k<<<vgrid(V), 256, 0, as_stream(stream)>>>(mask, n_comp, V, flags);
+    pdl_launch(pack_flags_k, dim3(vgrid(V)), dim3(256), 0, as_stream(stream), mask, n_comp, V, flags);
     VCHECK("pffmg_pack_flags");
 }
 extern "C" int pffmg_unpack_flags(const uint8_t* flags, int n_comp, int64_t V, uint8_t* mask, void* stream) {
     PFFMG_REQUIRE(mask && flags && n_comp >= 1 && n_comp <= 8 && V >= 0, "pffmg_unpack_flags: bad args");
-    unpack_flags_k<<<vgrid(V), 256, 0, as_stream(stream)>>>(flags, n_comp, V, mask);
+    pdl_launch(unpack_flags_k, dim3(vgrid(V)), dim3(256), 0, as_stream(stream), flags, n_comp, V, mask);
     VCHECK("pffmg_unpack_flags");
 }
 extern "C" int pffmg_masked_copy(const uint8_t* flags, int64_t V, int comp0, int n_comp, const double* in,
                                  double* out, void* stream) {
     PFFMG_REQUIRE(flags && in && out && n_comp >= 1 && comp0 >= 0, "pffmg_masked_copy: bad args");
-    masked_copy_k<<<vgrid(V * n_comp), 256, 0, as_stream(stream)>>>(flags, V, comp0, n_comp, in, out);
+    pdl_launch(masked_copy_k, dim3(vgrid(V * n_comp)), dim3(256), 0, as_stream(stream), flags, V, comp0, n_comp, in, out);
     VCHECK("pffmg_masked_copy");
 }
 extern "C" int pffmg_reciprocal(const double* diag, double* out, int64_t n, void* stream) {
     PFFMG_REQUIRE(diag && out, "pffmg_reciprocal: bad args");
-    reciprocal_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(diag, out, n);
+    pdl_launch(reciprocal_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), diag, out, n);
     VCHECK("pffmg_reciprocal");
 }
 extern "C" int pffmg_cheb_init_zero(const double* b, const double* invdiag, double theta, double* r,
                                     double* d, double* x, int64_t n, void* stream) {
     PFFMG_REQUIRE(b && invdiag && r && d && x, "pffmg_cheb_init_zero: bad args");
-    cheb_init_zero_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(b, invdiag, theta, nullptr, r, d, x, n);
+    pdl_launch(cheb_init_zero_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), b, invdiag, theta, nullptr, r, d, x, n);
     VCHECK("pffmg_cheb_init_zero");
 }
 extern "C" int pffmg_cheb_init_zero_dc(const double* b, const double* invdiag, const double* theta, double* r,
                                        double* d, double* x, int64_t n, void* stream) {
     PFFMG_REQUIRE(b && invdiag && theta && r && d && x, "pffmg_cheb_init_zero_dc: bad args");
-    cheb_init_zero_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(b, invdiag, 0.0, theta, r, d, x, n);
+    pdl_launch(cheb_init_zero_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), b, invdiag, 0.0, theta, r, d, x, n);
     VCHECK("pffmg_cheb_init_zero_dc");
 }
 __global__ void cheb_init_zero_bd_k(const double* b, const double* inv, const double* tu, const double* tp,
                                     int64_t n_u, double* r, double* d, double* x, int64_t n) {
+    pdl_wait();
     const double thu = *tu, thp = *tp;
     GRID_STRIDE(i, n) {
         const double ri = b[i];
@@ -421,44 +433,44 @@ extern "C" int pffmg_cheb_init_zero_bd(const double* b, const double* invdiag, c
                                        int64_t n, void* stream) {
     PFFMG_REQUIRE(b && invdiag && theta_u && theta_p && r && d && x && n_u >= 0 && n_u <= n,
                   "pffmg_cheb_init_zero_bd: bad args");
-    cheb_init_zero_bd_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(b, invdiag, theta_u, theta_p, n_u, r, d, x, n);
+    pdl_launch(cheb_init_zero_bd_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), b, invdiag, theta_u, theta_p, n_u, r, d, x, n);
     VCHECK("pffmg_cheb_init_zero_bd");
 }
 extern "C" int pffmg_jacobi_update(const double* r, const double* invdiag, double theta, double* x,
                                    int64_t n, void* stream) {
     PFFMG_REQUIRE(r && invdiag && x, "pffmg_jacobi_update: bad args");
-    jacobi_update_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(r, invdiag, theta, nullptr, x, n);
+    pdl_launch(jacobi_update_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), r, invdiag, theta, nullptr, x, n);
     VCHECK("pffmg_jacobi_update");
 }
 extern "C" int pffmg_jacobi_update_dc(const double* r, const double* invdiag, const double* theta, double* x,
                                       int64_t n, void* stream) {
     PFFMG_REQUIRE(r && invdiag && theta && x, "pffmg_jacobi_update_dc: bad args");
-    jacobi_update_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(r, invdiag, 0.0, theta, x, n);
+    pdl_launch(jacobi_update_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), r, invdiag, 0.0, theta, x, n);
     VCHECK("pffmg_jacobi_update_dc");
 }
 extern "C" int pffmg_axpy(double a, const double* x, double* y, int64_t n, void* stream) {
     PFFMG_REQUIRE(x && y, "pffmg_axpy: bad args");
-    axpby_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(a, x, 1.0, y, n, 0);
+    pdl_launch(axpby_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), a, x, 1.0, y, n, 0);
     VCHECK("pffmg_axpy");
 }
 extern "C" int pffmg_axpby(double a, const double* x, double b, double* y, int64_t n, void* stream) {
     PFFMG_REQUIRE(x && y, "pffmg_axpby: bad args");
-    axpby_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(a, x, b, y, n, 1);
+    pdl_launch(axpby_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), a, x, b, y, n, 1);
     VCHECK("pffmg_axpby");
 }
 extern "C" int pffmg_scale(double a, double* x, int64_t n, void* stream) {
     PFFMG_REQUIRE(x, "pffmg_scale: bad args");
-    axpby_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(a, x, 0.0, x, n, 2);
+    pdl_launch(axpby_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), a, x, 0.0, x, n, 2);
     VCHECK("pffmg_scale");
 }
 extern "C" int pffmg_copy(const double* x, double* y, int64_t n, void* stream) {
     PFFMG_REQUIRE(x && y, "pffmg_copy: bad args");
-    axpby_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(0.0, x, 0.0, y, n, 3);
+    pdl_launch(axpby_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), 0.0, x, 0.0, y, n, 3);
     VCHECK("pffmg_copy");
 }
 extern "C" int pffmg_sub(const double* x, const double* y, double* out, int64_t n, void* stream) {
     PFFMG_REQUIRE(x && y && out, "pffmg_sub: bad args");
-    sub_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(x, y, out, n);
+    pdl_launch(sub_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), x, y, out, n);
     VCHECK("pffmg_sub");
 }
 // ------------------------------------------------------------ QoIs
@@ -639,7 +651,7 @@ extern "C" int pffmg_multi_axpy(const double* Z, int64_t ld, int k, const double
                                 void* stream) {
     PFFMG_REQUIRE(Z && y && x && k >= 0 && k <= 64 && ld >= n, "pffmg_multi_axpy: bad args");
     if (k == 0) return PFFMG_OK;
-    multi_axpy_k<<<vgrid(n), 256, 0, as_stream(stream)>>>(Z, ld, k, y, x, n);
+    pdl_launch(multi_axpy_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), Z, ld, k, y, x, n);
     VCHECK("pffmg_multi_axpy");
 }
 
@@ -649,7 +661,7 @@ extern "C" int pffmg_active_set(const double* R_phi, const double* U_phi, const 
     PFFMG_REQUIRE(R_phi && U_phi && phi_old && mass_inv_phi && active_phi && V >= 0 && phi_comp >= 0 &&
                       phi_comp < 8,
                   "pffmg_active_set: bad args");
-    active_set_k<<<vgrid(V), 256, 0, as_stream(stream)>>>(R_phi, U_phi, phi_old, mass_inv_phi, c,
+    pdl_launch(active_set_k, dim3(vgrid(V)), dim3(256), 0, as_stream(stream), R_phi, U_phi, phi_old, mass_inv_phi, c,
                                                           dirichlet_flags, phi_comp, V, active_phi);
     VCHECK("pffmg_active_set");
 }
