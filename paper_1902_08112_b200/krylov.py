@@ -80,6 +80,8 @@ class _Workspace:
         self.ctl = torch.zeros(3 + 64, dtype=torch.float64, device="cuda")
         self.r = torch.empty(n, dtype=torch.float64, device="cuda")
         self.y = torch.zeros(m, dtype=torch.float64, device="cuda")
+        self.hpin = torch.zeros(m + 1, dtype=torch.float64).pin_memory()
+        self.event = torch.cuda.Event()
 
 
 _WS = {}
@@ -152,17 +154,30 @@ def gmres(op, precond, b, control=None, x0=None):
         torch.div(r, r_norm, out=V[0])                  # krylov.py:72
         g[0] = r_norm
         j_used = 0
+        # With a device-native preconditioner the next direction's preconditioning
+        # is enqueued before the host reads this column (V[j+1] is normalised on
+        # the device), so the GPU works through the host's Givens update; the
+        # one speculative application after convergence is discarded.
+        speculate = pcf is not None and hasattr(pcf, "_pffmg_into")
+        ready = False                                    # Z[j] already enqueued
         for j in range(m):
-            if pcf is None:
-                Z[j].copy_(V[j])
-            else:
-                _into(pcf, V[j], Z[j])
+            if not ready:
+                if pcf is None:
+                    Z[j].copy_(V[j])
+                else:
+                    _into(pcf, V[j], Z[j])
             _into(opf, Z[j], V[j + 1])                   # w lives in V[j+1]
             total += 1
             hcol = ws.H[j]
             _lib.call("pffmg_arnoldi_mgs", _lib.ptr(V), V.stride(0), j, _lib.ptr(V[j + 1]), n,
                       _lib.ptr(hcol), _lib.ptr(ws.ctl), _lib.stream())
-            H[:j + 2, j] = host(hcol[:j + 2])
+            ws.hpin[:j + 2].copy_(hcol[:j + 2], non_blocking=True)
+            ws.event.record()
+            ready = speculate and j + 1 < m
+            if ready:
+                _into(pcf, V[j + 1], Z[j + 1])
+            ws.event.synchronize()
+            H[:j + 2, j] = ws.hpin[:j + 2].numpy()
             breakdown = H[j + 1, j] == 0.0
             for i in range(j):                           # krylov.py:111-114
                 t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
