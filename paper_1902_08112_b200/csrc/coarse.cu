@@ -30,11 +30,21 @@ struct CoarseArgs {
     Q2Tab T;
 };
 
-// KIND: 0 Q1 NoSplit (generic cell kernel), 1 Q1 Miehe, 2 Q2 NoSplit, 3 Q2 Miehe
+// The level's vectors while the kernel runs: shared-memory copies.
+struct CoarseData {
+    const double* U;
+    const double* pt;
+    const uint8_t* fl;
+    const double* d;
+};
+
+// KIND: 0 Q1 NoSplit (generic cell kernel), 1 Q1 Miehe, 2 Q2 NoSplit, 3 Q2 Miehe,
+//       4 Q1 NoSplit on isotropic cells (folded-constant kernel)
 template <int D, int KIND>
 struct CoarseCell {
-    static constexpr bool Q2 = KIND >= 2;
+    static constexpr bool Q2 = KIND == 2 || KIND == 3;
     static constexpr bool MIE = KIND == 1 || KIND == 3;
+    static constexpr bool ISO = KIND == 4;
     static constexpr int NPC = Q2 ? 9 : (1 << D);
     using MI = ModeInfo<D, M_FULL, MIE>;
     static constexpr int NF = MI::NF, NCO = MI::NCO;
@@ -44,7 +54,8 @@ struct CoarseCell {
         return vertex_id(L, cx + (n & 1), cy + ((n >> 1) & 1), D == 3 ? cz + ((n >> 2) & 1) : 0);
     }
 
-    __device__ static void compute(const CoarseArgs& C, int cx, int cy, int cz, double (&o)[NCO][NPC]) {
+    __device__ static void compute(const CoarseArgs& C, const CoarseData& S, int cx, int cy, int cz,
+                                   double (&o)[NCO][NPC]) {
         const OpArgs& A = C.A;
         const Lat& L = A.L;
         const int64_t V = L.V;
@@ -52,17 +63,22 @@ struct CoarseCell {
 #pragma unroll
         for (int n = 0; n < NPC; ++n) {
             const int64_t id = node(L, cx, cy, cz, n);
-            const unsigned fl = A.flags[id];
+            const unsigned fl = S.fl[id];
 #pragma unroll
-            for (int i = 0; i < MI::NV; ++i) cv[MI::F_V + i][n] = ((fl >> i) & 1) ? 0.0 : C.d[(int64_t)i * V + id];
+            for (int i = 0; i < MI::NV; ++i) cv[MI::F_V + i][n] = ((fl >> i) & 1) ? 0.0 : S.d[(int64_t)i * V + id];
 #pragma unroll
-            for (int i = 0; i < MI::NU; ++i) cv[MI::F_U + i][n] = A.U[(int64_t)i * V + id];
-            cv[MI::F_PT][n] = A.pt[id];
+            for (int i = 0; i < MI::NU; ++i) cv[MI::F_U + i][n] = S.U[(int64_t)i * V + id];
+            cv[MI::F_PT][n] = S.pt[id];
             cv[MI::F_U + D][n] = 0.0;       // block-diagonal operator: no G_phiu coupling
         }
         const int64_t cell = (int64_t)cx + (int64_t)L.nx * (cy + (int64_t)L.ny * cz);
         const double* rq = A.rho ? A.rho + cell * NPC : nullptr;
-        if constexpr (Q2) {
+        if constexpr (ISO) {
+            if (rq)
+                cell_kernel_iso<D, M_FULL, true>(cv, rq, A.K, A.I, o);
+            else
+                cell_kernel_iso<D, M_FULL, false>(cv, rq, A.K, A.I, o);
+        } else if constexpr (Q2) {
             cell_q2<M_FULL, MIE>(cv, rq, A.K, C.T, o);
         } else if constexpr (MIE) {
             if constexpr (D == 2)
@@ -80,13 +96,32 @@ __global__ void __launch_bounds__(CT, 1) coarse_cheb_kernel(const CoarseArgs C) 
     pdl_wait();
     using CC = CoarseCell<D, KIND>;
     constexpr int NCO = CC::NCO, NPC = CC::NPC;
-    extern __shared__ double cellbuf[];                       // [cells][NCO][NPC]
+    extern __shared__ double smem[];
     const OpArgs& A = C.A;
     const Lat& L = A.L;
     const int64_t V = L.V;
     const int ncell = L.nx * L.ny * (D == 3 ? L.nz : 1);
     const int tid = threadIdx.x;
     const int nu = D;                                         // displacement components
+    constexpr int NC = D + 1;
+    // shared memory: cell outputs, then the level's vectors (the level is small)
+    double* cellbuf = smem;                                   // [cells][NCO][NPC]
+    double* sU = cellbuf + (int64_t)ncell * NCO * NPC;
+    double* spt = sU + NC * V;
+    double* sinv = spt + V;
+    double* sr = sinv + NC * V;
+    double* sd = sr + NC * V;
+    double* sx = sd + NC * V;
+    uint8_t* sfl = reinterpret_cast<uint8_t*>(sx + NC * V);
+    for (int i = tid; i < NC * (int)V; i += CT) {
+        sU[i] = A.U[i];
+        sinv[i] = C.inv[i];
+    }
+    for (int i = tid; i < (int)V; i += CT) {
+        spt[i] = A.pt[i];
+        sfl[i] = A.flags[i];
+    }
+    const CoarseData S{sU, spt, sfl, sd};
     // lattice points of the vertex pass
     const int px = CC::Q2 ? 2 * L.nx + 1 : L.nx + 1;
     const int py = CC::Q2 ? 2 * L.ny + 1 : L.ny + 1;
@@ -98,9 +133,9 @@ __global__ void __launch_bounds__(CT, 1) coarse_cheb_kernel(const CoarseArgs C) 
     for (int i = tid; i < (D + 1) * (int)V; i += CT) {
         const double ri = C.b[i];
         const double di = (C.inv[i] * ri) / (i < nu * V ? thu : thp);
-        C.r[i] = ri;
-        C.d[i] = di;
-        C.x[i] = 0.0 + di;
+        sr[i] = ri;
+        sd[i] = di;
+        sx[i] = 0.0 + di;
     }
     const int steps = max(C.deg_u, C.deg_p) - 1;
     for (int s = 0; s < steps; ++s) {
@@ -110,7 +145,7 @@ __global__ void __launch_bounds__(CT, 1) coarse_cheb_kernel(const CoarseArgs C) 
             const int cy = D == 3 ? t % L.ny : t, cz = D == 3 ? t / L.ny : 0;
             double o[NCO][NPC];
             if (CC::Q2 || cell_exists<D>(L, cx, cy, cz)) {
-                CC::compute(C, cx, cy, cz, o);
+                CC::compute(C, S, cx, cy, cz, o);
 #pragma unroll
                 for (int k = 0; k < NCO; ++k)
 #pragma unroll
@@ -157,31 +192,33 @@ __global__ void __launch_bounds__(CT, 1) coarse_cheb_kernel(const CoarseArgs C) 
                             for (int k = 0; k < NCO; ++k) acc[k] += cellbuf[((int64_t)c * NCO + k) * NPC + n];
                         }
             }
-            const unsigned fl = A.flags[vid];
+            const unsigned fl = sfl[vid];
 #pragma unroll
             for (int k = 0; k < NCO; ++k) {
                 const bool phi = k == D;
                 if (phi ? !up_p : !up_u) continue;
                 const int64_t g = (int64_t)k * V + vid;
-                const double dk = C.d[g];
+                const double dk = sd[g];
                 const double Av = ((fl >> k) & 1) ? dk : acc[k];          // identity rows
                 const double* cf = phi ? C.coef_p : C.coef_u;
-                const double rr = C.r[g] - Av;
-                const double dn = cf[1 + 2 * s] * dk + cf[2 + 2 * s] * (C.inv[g] * rr);
-                C.r[g] = rr;
-                C.d[g] = dn;
-                C.x[g] = C.x[g] + dn;
+                const double rr = sr[g] - Av;
+                const double dn = cf[1 + 2 * s] * dk + cf[2 + 2 * s] * (sinv[g] * rr);
+                sr[g] = rr;
+                sd[g] = dn;
+                sx[g] = sx[g] + dn;
             }
         }
     }
+    __syncthreads();
+    for (int i = tid; i < (D + 1) * (int)V; i += CT) C.x[i] = sx[i];    // the solve's result
 }
 
 template <int D, int KIND>
 static int launch_coarse(const CoarseArgs& C, size_t smem, cudaStream_t s) {
-    static bool done = false;
-    if (!done && smem > 48 * 1024) {
+    static size_t done = 0;
+    if (smem > 48 * 1024 && smem > done) {
         cudaFuncSetAttribute(coarse_cheb_kernel<D, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        done = true;
+        done = smem;
     }
     pdl_launch(coarse_cheb_kernel<D, KIND>, dim3(1), dim3(CT), smem, s, C);
     return check_launch("pffmg_coarse_cheb");
@@ -228,16 +265,23 @@ extern "C" int pffmg_coarse_cheb(const pffmg_lattice* lat, const pffmg_state* st
     C.T = make_q2_host(L.hx, L.hy);
     const int nco = L.dim + 1;
     const int npc = L.order == 2 ? 9 : (1 << L.dim);
-    const size_t smem = sizeof(double) * (size_t)ncell * nco * npc;
+    const size_t smem = sizeof(double) * ((size_t)ncell * nco * npc + (size_t)L.V * (5 * nco + 1)) +
+                        (size_t)L.V + 16;
+    PFFMG_REQUIRE(smem <= 200 * 1024, "pffmg_coarse_cheb: level too large for one CTA");
+    C.A.I = make_iso_host(C.A.K);
     const cudaStream_t s = as_stream(stream);
-    const int kind = (L.order == 2 ? 2 : 0) + (st->split == 1 ? 1 : 0);
+    const bool iso = L.order == 1 && L.hx == L.hy && (L.dim == 2 || L.hz == L.hx);
+    int kind = (L.order == 2 ? 2 : 0) + (st->split == 1 ? 1 : 0);
+    if (kind == 0 && iso) kind = 4;
     if (L.dim == 2) {
         switch (kind) {
             case 0: return launch_coarse<2, 0>(C, smem, s);
             case 1: return launch_coarse<2, 1>(C, smem, s);
             case 2: return launch_coarse<2, 2>(C, smem, s);
-            default: return launch_coarse<2, 3>(C, smem, s);
+            case 3: return launch_coarse<2, 3>(C, smem, s);
+            default: return launch_coarse<2, 4>(C, smem, s);
         }
     }
-    return kind == 0 ? launch_coarse<3, 0>(C, smem, s) : launch_coarse<3, 1>(C, smem, s);
+    return kind == 0 ? launch_coarse<3, 0>(C, smem, s)
+                     : (kind == 1 ? launch_coarse<3, 1>(C, smem, s) : launch_coarse<3, 4>(C, smem, s));
 }
