@@ -54,7 +54,7 @@ struct CoarseCell {
         return vertex_id(L, cx + (n & 1), cy + ((n >> 1) & 1), D == 3 ? cz + ((n >> 2) & 1) : 0);
     }
 
-    __device__ static void compute(const CoarseArgs& C, const CoarseData& S, int cx, int cy, int cz,
+    __device__ static void compute(const CoarseArgs& C, const CoarseData& S, const int* ids, int64_t cell,
                                    double (&o)[NCO][NPC]) {
         const OpArgs& A = C.A;
         const Lat& L = A.L;
@@ -62,7 +62,7 @@ struct CoarseCell {
         double cv[NF][NPC];
 #pragma unroll
         for (int n = 0; n < NPC; ++n) {
-            const int64_t id = node(L, cx, cy, cz, n);
+            const int64_t id = ids[n];
             const unsigned fl = S.fl[id];
 #pragma unroll
             for (int i = 0; i < MI::NV; ++i) cv[MI::F_V + i][n] = ((fl >> i) & 1) ? 0.0 : S.d[(int64_t)i * V + id];
@@ -71,7 +71,6 @@ struct CoarseCell {
             cv[MI::F_PT][n] = S.pt[id];
             cv[MI::F_U + D][n] = 0.0;       // block-diagonal operator: no G_phiu coupling
         }
-        const int64_t cell = (int64_t)cx + (int64_t)L.nx * (cy + (int64_t)L.ny * cz);
         const double* rq = A.rho ? A.rho + cell * NPC : nullptr;
         if constexpr (ISO) {
             if (rq)
@@ -112,7 +111,10 @@ __global__ void __launch_bounds__(CT, 1) coarse_cheb_kernel(const CoarseArgs C) 
     double* sr = sinv + NC * V;
     double* sd = sr + NC * V;
     double* sx = sd + NC * V;
-    uint8_t* sfl = reinterpret_cast<uint8_t*>(sx + NC * V);
+    constexpr int MAXA = CC::Q2 ? 4 : (1 << D);               // cells sharing a vertex / node
+    int* cnodes = reinterpret_cast<int*>(sx + NC * V);        // [cells][NPC] node ids, -1: no cell
+    int* vadj = cnodes + ncell * NPC;                         // [V][MAXA] cell * NPC + corner, -1 pad
+    uint8_t* sfl = reinterpret_cast<uint8_t*>(vadj + (int64_t)V * MAXA);
     for (int i = tid; i < NC * (int)V; i += CT) {
         sU[i] = A.U[i];
         sinv[i] = C.inv[i];
@@ -127,6 +129,42 @@ __global__ void __launch_bounds__(CT, 1) coarse_cheb_kernel(const CoarseArgs C) 
     const int py = CC::Q2 ? 2 * L.ny + 1 : L.ny + 1;
     const int pz = D == 3 ? L.nz + 1 : 1;
     const int npts = px * py * pz;
+    // index tables, once: the nodes of every cell, and for every vertex its
+    // (cell, corner) pairs in increasing cell order (the fixed summation order)
+    for (int c = tid; c < ncell; c += CT) {
+        const int cx = c % L.nx, t = c / L.nx;
+        const int cy = D == 3 ? t % L.ny : t, cz = D == 3 ? t / L.ny : 0;
+        const bool ex = CC::Q2 || cell_exists<D>(L, cx, cy, cz);
+#pragma unroll
+        for (int n = 0; n < NPC; ++n) cnodes[c * NPC + n] = ex ? (int)CC::node(L, cx, cy, cz, n) : -1;
+    }
+    for (int p = tid; p < npts; p += CT) {
+        const int X = p % px, t = p / px;
+        const int Y = D == 3 ? t % py : t, Z = D == 3 ? t / py : 0;
+        const int64_t vid = CC::Q2 ? (int64_t)Y * px + X : vertex_id(L, X, Y, Z);
+        if (vid < 0) continue;
+        int k = 0;
+        if (CC::Q2) {
+            const int cx0 = (X & 1) ? X >> 1 : (X >> 1) - 1, cx1 = X >> 1;
+            const int cy0 = (Y & 1) ? Y >> 1 : (Y >> 1) - 1, cy1 = Y >> 1;
+            for (int cy = cy0; cy <= min(cy1, L.ny - 1); ++cy) {
+                if (cy < 0) continue;
+                for (int cx = cx0; cx <= min(cx1, L.nx - 1); ++cx) {
+                    if (cx < 0) continue;
+                    vadj[vid * MAXA + k++] = (cx + L.nx * cy) * NPC + (X - 2 * cx) + 3 * (Y - 2 * cy);
+                }
+            }
+        } else {
+            for (int dz = (D == 3 ? 1 : 0); dz >= 0; --dz)
+                for (int dy = 1; dy >= 0; --dy)
+                    for (int dx = 1; dx >= 0; --dx) {
+                        const int cx = X - dx, cy = Y - dy, cz = D == 3 ? Z - dz : 0;
+                        if (!cell_exists<D>(L, cx, cy, cz)) continue;
+                        vadj[vid * MAXA + k++] = (cx + L.nx * (cy + L.ny * cz)) * NPC + (dx | (dy << 1) | (dz << 2));
+                    }
+        }
+        for (; k < MAXA; ++k) vadj[vid * MAXA + k] = -1;
+    }
 
     // x = d = inv b / theta, r = b            (mgsolve.py:95, 103-106 from x = 0)
     const double thu = C.coef_u[0], thp = C.coef_p[0];
@@ -140,12 +178,10 @@ __global__ void __launch_bounds__(CT, 1) coarse_cheb_kernel(const CoarseArgs C) 
     const int steps = max(C.deg_u, C.deg_p) - 1;
     for (int s = 0; s < steps; ++s) {
         __syncthreads();                                      // d of the previous step complete
-        if (tid < ncell) {
-            const int cx = tid % L.nx, t = tid / L.nx;
-            const int cy = D == 3 ? t % L.ny : t, cz = D == 3 ? t / L.ny : 0;
+        if (tid < ncell && cnodes[tid * NPC] >= 0) {
             double o[NCO][NPC];
-            if (CC::Q2 || cell_exists<D>(L, cx, cy, cz)) {
-                CC::compute(C, S, cx, cy, cz, o);
+            {
+                CC::compute(C, S, cnodes + tid * NPC, tid, o);
 #pragma unroll
                 for (int k = 0; k < NCO; ++k)
 #pragma unroll
@@ -154,43 +190,17 @@ __global__ void __launch_bounds__(CT, 1) coarse_cheb_kernel(const CoarseArgs C) 
         }
         __syncthreads();
         const bool up_u = s < C.deg_u - 1, up_p = s < C.deg_p - 1;
-        for (int p = tid; p < npts; p += CT) {
-            const int X = p % px, t = p / px;
-            const int Y = D == 3 ? t % py : t, Z = D == 3 ? t / py : 0;
-            int64_t vid;
-            if (CC::Q2)
-                vid = (int64_t)Y * px + X;
-            else
-                vid = vertex_id(L, X, Y, Z);
-            if (vid < 0) continue;
+        for (int vid = tid; vid < (int)V; vid += CT) {
             double acc[NCO];
 #pragma unroll
             for (int k = 0; k < NCO; ++k) acc[k] = 0.0;
-            // adjacent cells in increasing cell order; corner = position inside the cell
-            if (CC::Q2) {
-                const int cx0 = (X & 1) ? X >> 1 : (X >> 1) - 1, cx1 = X >> 1;
-                const int cy0 = (Y & 1) ? Y >> 1 : (Y >> 1) - 1, cy1 = Y >> 1;
-                for (int cy = cy0; cy <= min(cy1, L.ny - 1); ++cy) {
-                    if (cy < 0) continue;
-                    for (int cx = cx0; cx <= min(cx1, L.nx - 1); ++cx) {
-                        if (cx < 0) continue;
-                        const int n = (X - 2 * cx) + 3 * (Y - 2 * cy);
-                        const int c = cx + L.nx * cy;
 #pragma unroll
-                        for (int k = 0; k < NCO; ++k) acc[k] += cellbuf[((int64_t)c * NCO + k) * NPC + n];
-                    }
-                }
-            } else {
-                for (int dz = (D == 3 ? 1 : 0); dz >= 0; --dz)
-                    for (int dy = 1; dy >= 0; --dy)
-                        for (int dx = 1; dx >= 0; --dx) {
-                            const int cx = X - dx, cy = Y - dy, cz = D == 3 ? Z - dz : 0;
-                            if (!cell_exists<D>(L, cx, cy, cz)) continue;
-                            const int n = dx | (dy << 1) | (dz << 2);
-                            const int c = cx + L.nx * (cy + L.ny * cz);
+            for (int a = 0; a < MAXA; ++a) {
+                const int e = vadj[vid * MAXA + a];
+                if (e < 0) break;
+                const int c = e / NPC, n = e - c * NPC;
 #pragma unroll
-                            for (int k = 0; k < NCO; ++k) acc[k] += cellbuf[((int64_t)c * NCO + k) * NPC + n];
-                        }
+                for (int k = 0; k < NCO; ++k) acc[k] += cellbuf[((int64_t)c * NCO + k) * NPC + n];
             }
             const unsigned fl = sfl[vid];
 #pragma unroll
@@ -265,8 +275,9 @@ extern "C" int pffmg_coarse_cheb(const pffmg_lattice* lat, const pffmg_state* st
     C.T = make_q2_host(L.hx, L.hy);
     const int nco = L.dim + 1;
     const int npc = L.order == 2 ? 9 : (1 << L.dim);
+    const int maxa = L.order == 2 ? 4 : (1 << L.dim);
     const size_t smem = sizeof(double) * ((size_t)ncell * nco * npc + (size_t)L.V * (5 * nco + 1)) +
-                        (size_t)L.V + 16;
+                        sizeof(int) * ((size_t)ncell * npc + (size_t)L.V * maxa) + (size_t)L.V + 16;
     PFFMG_REQUIRE(smem <= 200 * 1024, "pffmg_coarse_cheb: level too large for one CTA");
     C.A.I = make_iso_host(C.A.K);
     const cudaStream_t s = as_stream(stream);
