@@ -77,6 +77,12 @@ struct CoarseCell {
                 cell_kernel_iso<D, M_FULL, true>(cv, rq, A.K, A.I, o);
             else
                 cell_kernel_iso<D, M_FULL, false>(cv, rq, A.K, A.I, o);
+        } else if constexpr (Q2 && !MIE) {
+            auto load = [&](int f, double (&c)[9]) {
+#pragma unroll
+                for (int n = 0; n < 9; ++n) c[n] = cv[f][n];
+            };
+            cell_q2_rows<M_FULL>(load, rq, A.K, C.T, true, o);   // block-diagonal: no coupling
         } else if constexpr (Q2) {
             cell_q2<M_FULL, MIE>(cv, rq, A.K, C.T, o);
         } else if constexpr (MIE) {
