@@ -158,7 +158,9 @@ def gmres(op, precond, b, control=None, x0=None):
         # is enqueued before the host reads this column (V[j+1] is normalised on
         # the device), so the GPU works through the host's Givens update; the
         # one speculative application after convergence is discarded.
-        speculate = pcf is not None and hasattr(pcf, "_pffmg_into")
+        # (only for problems whose V-cycle is short next to the host round trip:
+        # on very large levels the discarded application would cost more)
+        speculate = pcf is not None and hasattr(pcf, "_pffmg_into") and n <= (1 << 24)
         ready = False                                    # Z[j] already enqueued
         for j in range(m):
             if not ready:
