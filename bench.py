@@ -368,7 +368,7 @@ def run_gpu(args):
     b_c, b_f = algorithmic_bytes(prob.dim, mesh.n_vertices, mesh.n_cells,
                                  9 if getattr(mesh, "order", 1) == 2 else None)
     traffic = flops = None
-    prof = os.path.join(ROOT, "profiles", "ncu_vmult_cfg2.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_vmult_cfg2_r1.json")   # this round's capture
     if os.path.exists(prof) and args.config == "cfg2":
         try:
             with open(prof) as f:

@@ -1,7 +1,9 @@
 """Summarise ncu captures into profiles/ (run here, on the CPU box).
 
     python tools/ncu_summary.py --rep gpurun_out/prof_bench.ncu-rep \
-        --launches gpurun_out/launches.csv --name vmult_cfg2 --bench gpurun_out/bench.json
+        --launches gpurun_out/launches.csv --name vmult_cfg2_r1 --bench gpurun_out/bench.json
+
+(name the summaries per round: bench.py reads profiles/ncu_vmult_cfg2_r<N>.json)
 
 Writes profiles/ncu_<name>.json (the numbers bench.py reads: DRAM bytes per
 launch, duration, pipe utilisation) and profiles/ncu_<name>.md.
