@@ -195,7 +195,8 @@ def run_gpu(args):
         from paper_1902_08112_b200 import distributed as D
         from paper_1902_08112_b200.lattice import info_from_mesh
         levels = prob.disc.hierarchy.levels
-        part = D.SlabPartition([int(info_from_mesh(m).ncell[-1]) for m in levels], ws, rank)
+        part = D.SlabPartition([int(info_from_mesh(m).ncell[-1]) for m in levels], ws, rank,
+                               order=getattr(info_from_mesh(mesh), "order", 1))
         dop = D.DistributedOperator(mesh, len(levels) - 1, part, prob.state, cmask, prob.params,
                                     SplitKind.NOSPLIT)
         op = dop.local

@@ -67,9 +67,12 @@ typedef struct {
      * slab of a larger level); transfers use it to pair coarse and fine slabs. */
     int32_t plane0;
     /* Element order: 0 or 1 = trilinear/bilinear Q1 (the reference's element,
-     * fem.py:1-8); 2 = biquadratic Q2 (2D box lattices, whole lattice only):
-     * dofs live on the nodes of the half-spacing lattice, (2nx+1)(2ny+1) of
-     * them, x fastest; 3x3 Gauss points (BASELINE configs[2]). */
+     * fem.py:1-8); 2 = biquadratic Q2 (2D box lattices): dofs live on the
+     * nodes of the half-spacing lattice, (2nx+1)(2ny+1) of them, x fastest;
+     * 3x3 Gauss points (BASELINE configs[2]).  For Q2 the "planes" of
+     * own_lo/own_hi/plane0 are NODE rows (2ny+1 of them); a slab starts on a
+     * cell boundary (plane0 even) and a sharded operator needs two ghost node
+     * rows below own_lo (four for restriction) and one above. */
     int32_t order;
 } pffmg_lattice;
 

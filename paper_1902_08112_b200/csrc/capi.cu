@@ -60,8 +60,8 @@ int make_lat(const pffmg_lattice* in, Lat* out) {
         PFFMG_REQUIRE((int64_t)(2 * in->nx + 1) * (2 * in->ny + 1) == in->n_vertices,
                       "Q2 box has %lld nodes, n_vertices=%lld",
                       (long long)(2 * in->nx + 1) * (2 * in->ny + 1), (long long)in->n_vertices);
-        PFFMG_REQUIRE(in->own_lo == 0 && (in->own_hi == 0 || in->own_hi == 2 * in->ny + 1) && in->plane0 == 0,
-                      "Q2 lattices are whole (no slabs)");
+        // slabs of a Q2 level start on a cell boundary: plane0 (a node row) is even
+        PFFMG_REQUIRE(in->plane0 % 2 == 0, "Q2 slab must start on an even node row (plane0=%d)", in->plane0);
     }
     const bool has_rows = in->vrow_off != nullptr;
     PFFMG_REQUIRE(has_rows == (in->vrow_lo != nullptr) && has_rows == (in->vrow_hi != nullptr) &&

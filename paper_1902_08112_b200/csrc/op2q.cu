@@ -28,9 +28,12 @@ __global__ void __launch_bounds__(128, MODE == M_FULL ? 2 : PFFMG_Q2_MINB) op2q_
     const int lane = threadIdx.x & 31;
     const int gw = (int)blockIdx.x * 4 + (threadIdx.x >> 5);
     const int seg = gw % A.nseg, strip = gw / A.nseg;
-    const int cy0 = strip * A.planes_per_cta;
-    if (cy0 > L.ny) return;
-    const int cy1 = min(cy0 + A.planes_per_cta, L.ny + 1);   // cell rows whose node rows are finalised
+    // cell row cy finalises node rows 2cy and 2cy+1 (those inside the owned
+    // node rows [own_lo, own_hi) of a slab); cy = ny only its bottom row
+    const int cyA = L.own_lo >> 1, cyB = (L.own_hi + 1) >> 1;
+    const int cy0 = cyA + strip * A.planes_per_cta;
+    if (cy0 >= cyB) return;
+    const int cy1 = min(cy0 + A.planes_per_cta, cyB);
     const int cx = 31 * seg - 1 + lane;
     const int nxn = 2 * L.nx + 1;
     const int64_t V = L.V;
@@ -112,6 +115,7 @@ __global__ void __launch_bounds__(128, MODE == M_FULL ? 2 : PFFMG_Q2_MINB) op2q_
                 const int dx = t & 1, dy = t >> 1;
                 if (dx == 1 && cx >= L.nx) continue;
                 if (dy == 1 && cy >= L.ny) continue;
+                if (2 * cy + dy < L.own_lo || 2 * cy + dy >= L.own_hi) continue;
                 const int64_t id = (int64_t)(2 * cy + dy) * nxn + 2 * cx + dx;
                 double acc[NCO], vin[NCO];
 #pragma unroll
@@ -139,7 +143,7 @@ int launch2q(const OpArgs& A0, cudaStream_t s) {
     const Lat& L = A.L;
     const int sms = sm_count();
     const int nseg = (L.nx + 1 + 30) / 31;
-    const int rows = L.ny + 1;
+    const int rows = ((L.own_hi + 1) >> 1) - (L.own_lo >> 1);
     int64_t per = ((int64_t)rows * nseg + 16LL * sms - 1) / (16LL * sms);
     per = per < 1 ? 1 : (per > 32 ? 32 : per);
     A.planes_per_cta = (int)per;

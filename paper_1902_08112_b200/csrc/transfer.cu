@@ -161,21 +161,24 @@ __device__ __forceinline__ int q2_prolong_taps(int j, int (&idx)[3], double (&w)
     return 3;
 }
 
-// Lc / Lf are the NODE lattices (nx = 2 * cells): nxn = nx + 1 nodes per row
+// Lc / Lf are the NODE lattices (nx = 2 * cells): nxn = nx + 1 nodes per row.
+// Slabs: the output lattice's owned node rows only; tap parities and the
+// coarse/fine row pairing use global rows (local row + plane0).
 __global__ void restrict_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vf,
                                    double* __restrict__ vc, const uint8_t* __restrict__ cflags) {
     pdl_wait();
-    const int nxc = Lc.nx + 1, nyc = Lc.ny + 1, nxf = Lf.nx + 1, nyf = Lf.ny + 1;
-    const int64_t npts = (int64_t)nxc * nyc;
+    const int nxc = Lc.nx + 1, nxf = Lf.nx + 1, nyf = Lf.ny + 1;
+    const int64_t npts = (int64_t)nxc * (Lc.own_hi - Lc.own_lo);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(i % nxc), y = (int)(i / nxc);
+        const int x = (int)(i % nxc), y = Lc.own_lo + (int)(i / nxc);
+        const int yg = y + Lc.plane0;
         int ox[5], oy[5];
         double wx[5], wy[5];
-        const int nx5 = q2_restrict_taps(x, ox, wx), ny5 = q2_restrict_taps(y, oy, wy);
+        const int nx5 = q2_restrict_taps(x, ox, wx), ny5 = q2_restrict_taps(yg, oy, wy);
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         for (int b = 0; b < ny5; ++b) {                    // increasing fine id (CSR order)
-            const int fy = 2 * y + oy[b];
+            const int fy = 2 * yg + oy[b] - Lf.plane0;
             if (fy < 0 || fy >= nyf) continue;
             for (int a = 0; a < nx5; ++a) {
                 const int fx = 2 * x + ox[a];
@@ -187,11 +190,12 @@ __global__ void restrict_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const d
                     if (k < ncomp) acc[k] += w * __ldg(vf + (int64_t)k * Lf.V + fid);
             }
         }
-        const uint8_t fl = cflags ? cflags[i] : 0;
+        const int64_t cid = (int64_t)y * nxc + x;
+        const uint8_t fl = cflags ? cflags[cid] : 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (k >= ncomp) break;
-            vc[(int64_t)k * Lc.V + i] = ((fl >> (comp0 + k)) & 1) ? 0.0 : acc[k];
+            vc[(int64_t)k * Lc.V + cid] = ((fl >> (comp0 + k)) & 1) ? 0.0 : acc[k];
         }
     }
 }
@@ -200,21 +204,22 @@ __global__ void prolongate_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const
                                      double* __restrict__ vf, const uint8_t* __restrict__ fflags,
                                      int accumulate) {
     pdl_wait();
-    const int nxc = Lc.nx + 1, nxf = Lf.nx + 1, nyf = Lf.ny + 1;
-    const int64_t npts = (int64_t)nxf * nyf;
+    const int nxc = Lc.nx + 1, nxf = Lf.nx + 1;
+    const int64_t npts = (int64_t)nxf * (Lf.own_hi - Lf.own_lo);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int X = (int)(i % nxf), Y = (int)(i / nxf);
+        const int X = (int)(i % nxf), Y = Lf.own_lo + (int)(i / nxf);
         int ix[3], iy[3];
         double wx[3], wy[3];
-        const int nx3 = q2_prolong_taps(X, ix, wx), ny3 = q2_prolong_taps(Y, iy, wy);
-        const uint8_t fl = fflags ? fflags[i] : 0;
+        const int nx3 = q2_prolong_taps(X, ix, wx), ny3 = q2_prolong_taps(Y + Lf.plane0, iy, wy);
+        const int64_t fid = (int64_t)Y * nxf + X;
+        const uint8_t fl = fflags ? fflags[fid] : 0;
         for (int k = 0; k < ncomp; ++k) {
             double acc = 0.0;
             for (int b = 0; b < ny3; ++b)
                 for (int a = 0; a < nx3; ++a)
-                    acc += (wx[a] * wy[b]) * vc[(int64_t)k * Lc.V + (int64_t)iy[b] * nxc + ix[a]];
-            const int64_t g = (int64_t)k * Lf.V + i;
+                    acc += (wx[a] * wy[b]) * vc[(int64_t)k * Lc.V + (int64_t)(iy[b] - Lc.plane0) * nxc + ix[a]];
+            const int64_t g = (int64_t)k * Lf.V + fid;
             if ((fl >> (comp0 + k)) & 1) acc = 0.0;
             if (accumulate)
                 vf[g] += acc;
@@ -304,7 +309,7 @@ extern "C" int pffmg_restrict(const pffmg_lattice* coarse, const pffmg_lattice* 
     PFFMG_REQUIRE(vf && vc && n_comp >= 1 && comp0 >= 0 && comp0 + n_comp <= Lc.dim + 1,
                   "pffmg_restrict: bad arguments");
     if (q2) {
-        pdl_launch(restrict_q2_kernel, dim3(grid_for((int64_t)(Lc.nx + 1) * (Lc.ny + 1))), dim3(256), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vf, vc, coarse_flags);
+        pdl_launch(restrict_q2_kernel, dim3(grid_for((int64_t)(Lc.nx + 1) * (Lc.own_hi - Lc.own_lo))), dim3(256), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vf, vc, coarse_flags);
         return check_launch("pffmg_restrict");
     }
     if (Lc.dim == 3)
@@ -326,7 +331,7 @@ extern "C" int pffmg_prolongate(const pffmg_lattice* coarse, const pffmg_lattice
     PFFMG_REQUIRE(vf && vc && n_comp >= 1 && comp0 >= 0 && comp0 + n_comp <= Lc.dim + 1,
                   "pffmg_prolongate: bad arguments");
     if (q2) {
-        pdl_launch(prolongate_q2_kernel, dim3(grid_for((int64_t)(Lf.nx + 1) * (Lf.ny + 1))), dim3(256), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
+        pdl_launch(prolongate_q2_kernel, dim3(grid_for((int64_t)(Lf.nx + 1) * (Lf.own_hi - Lf.own_lo))), dim3(256), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
         return check_launch("pffmg_prolongate");
     }
     if (Lf.dim == 3)

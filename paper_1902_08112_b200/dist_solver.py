@@ -63,7 +63,8 @@ class DistGMG:
         self.world, self.rank, self.group = world, rank, group
         infos = [info_from_mesh(m) for m in levels]
         self.dim = infos[0].dim
-        self.part = SlabPartition([int(i.ncell[-1]) for i in infos], world, rank, min_layers)
+        self.part = SlabPartition([int(i.ncell[-1]) for i in infos], world, rank, min_layers,
+                                  order=getattr(infos[0], "order", 1))
         self.L = [_Level(l, infos[l], self.part.slab(l), rank, world, group) for l in range(len(levels))]
         self.degree, self.target, self.cap = degree, coarse_target, coarse_cap
         self.eig_iters, self.seed = eig_iters, seed

@@ -17,6 +17,12 @@ injection is rank-local and restriction/prolongation only need the ghost
 planes that the halo exchange already provides.  Levels too thin to give
 every rank `min_layers` cell layers are replicated on every rank.
 
+Q2 levels (order 2, BASELINE configs[2]) are cut the same way in cell
+layers, but their planes are NODE rows (two per cell layer): rank r owns
+node rows [2a, 2b) and stores four ghost rows below (the 3x3-node cells of
+the layer below need two, the Q2 restriction stencil reaches three) and one
+above.
+
 Communication goes through torch.distributed (NCCL over NVLink on GPUs,
 gloo on CPUs for the tests); the per-rank compute is a pluggable "local
 operator" (the CUDA PhaseFieldOperator on the slab by default).
@@ -41,6 +47,7 @@ class Slab:
     lo: int               # stored planes [lo, hi] (owned + ghosts)
     hi: int
     replicated: bool = False
+    ghost_lo: int = 1     # ghost planes stored below own_lo (when there is a lower neighbour)
 
     @property
     def has_lower(self):
@@ -59,8 +66,9 @@ def split_layers(n, world):
 class SlabPartition:
     """Nested slab partition of a hierarchy with `n_cells[l]` cell layers on level l."""
 
-    def __init__(self, n_cells, world, rank, min_layers=2):
+    def __init__(self, n_cells, world, rank, min_layers=2, order=1):
         self.world, self.rank = world, rank
+        self.order = order
         self.n_cells = list(n_cells)
         L = len(self.n_cells)
         # coarsest level that gives every rank at least min_layers layers
@@ -72,15 +80,18 @@ class SlabPartition:
         ls = self.first_sharded
         cuts = split_layers(self.n_cells[ls], world)
         self.slabs = []
+        q = 2 if order == 2 else 1                  # planes per cell layer
+        gl = 4 if order == 2 else 1
         for l in range(L):
             n = self.n_cells[l]
+            N = q * n                                # index of the last plane
             if l < ls or world == 1:
-                self.slabs.append(Slab(n, 0, n + 1, 0, n, replicated=world > 1))
+                self.slabs.append(Slab(n, 0, N + 1, 0, N, replicated=world > 1, ghost_lo=gl))
                 continue
             k = 2 ** (l - ls)
-            a, b = cuts[rank] * k, cuts[rank + 1] * k
-            own_hi = b if rank < world - 1 else n + 1
-            self.slabs.append(Slab(n, a, own_hi, max(a - 1, 0), min(own_hi, n)))
+            a, b = q * cuts[rank] * k, q * cuts[rank + 1] * k
+            own_hi = b if rank < world - 1 else N + 1
+            self.slabs.append(Slab(n, a, own_hi, max(a - gl, 0), min(own_hi, N), ghost_lo=gl))
 
     def slab(self, l):
         return self.slabs[l]
@@ -146,10 +157,12 @@ class Halo:
         self.rank, self.world, self.group = rank, world, group
         lo_own = slab.own_lo - slab.lo          # local index of the first owned plane
         hi_own = slab.own_hi - slab.lo          # one past the last owned plane
-        self.send_down = (int(self.offs[lo_own]), int(self.offs[lo_own + 1])) if slab.has_lower else None
-        self.recv_down = (int(self.offs[0]), int(self.offs[1])) if slab.has_lower else None
-        self.send_up = (int(self.offs[hi_own - 1]), int(self.offs[hi_own])) if slab.has_upper else None
-        self.recv_up = (int(self.offs[hi_own]), int(self.offs[hi_own + 1])) if slab.has_upper else None
+        g = slab.ghost_lo                       # the upper neighbour stores g planes of ours
+        o = self.offs
+        self.send_down = (int(o[lo_own]), int(o[lo_own + 1])) if slab.has_lower else None
+        self.recv_down = (int(o[0]), int(o[lo_own])) if slab.has_lower else None
+        self.send_up = (int(o[hi_own - g]), int(o[hi_own])) if slab.has_upper else None
+        self.recv_up = (int(o[hi_own]), int(o[hi_own + 1])) if slab.has_upper else None
         self._ops = {}
 
     def exchange(self, vec, n_comp, persistent=False):
@@ -294,9 +307,17 @@ class DistributedOperator:
         the two boundary rows run after it lands."""
         lo, hi = self.info.own if self.info.own != (0, 0) else (0, self.info.n_planes)
         if (hasattr(self.local, "apply_rows_dev") and v_loc.is_cuda and self.world > 1
-                and hi - lo >= 3 and not self.slab.replicated):
+                and hi - lo >= 4 and not self.slab.replicated):
             from . import _lib
             h = self.halo.start(v_loc, self.n_comp, persistent=True)
+            if self.info.order == 2:
+                # Q2: node row lo+1 is interior to the first owned cell layer; rows
+                # hi-2 and hi-1 belong to the top layer, whose cells read ghost row hi
+                self.local.apply_rows_dev(_lib.FULL, v_loc, out_loc, lo + 1, hi - 2)
+                self.halo.finish(h)
+                self.local.apply_rows_dev(_lib.FULL, v_loc, out_loc, lo, lo + 1)
+                self.local.apply_rows_dev(_lib.FULL, v_loc, out_loc, hi - 2, hi)
+                return out_loc
             self.local.apply_rows_dev(_lib.FULL, v_loc, out_loc, lo + 1, hi - 1)
             self.halo.finish(h)
             self.local.apply_ends_dev(_lib.FULL, v_loc, out_loc)      # rows lo and hi-1, one launch

@@ -232,7 +232,8 @@ class LatticeInfo:
 
     @property
     def n_planes(self):
-        return int(self.ncell[-1]) + 1
+        """Planes of the last axis: vertex planes (Q1) or node rows (Q2)."""
+        return (2 if getattr(self, "order", 1) == 2 else 1) * int(self.ncell[-1]) + 1
 
     def plane_offsets(self):
         """Vertex id of the first vertex of every plane of the last axis (+ V)."""
@@ -252,7 +253,10 @@ class LatticeInfo:
         planes `own` = (own_lo, own_hi) given in global plane numbers."""
         offs = self.plane_offsets()
         ncell = self.ncell.copy()
-        ncell[-1] = hi - lo
+        q2 = getattr(self, "order", 1) == 2
+        if q2:                             # planes are node rows; a slab is whole cell layers
+            assert lo % 2 == 0 and hi % 2 == 0, (lo, hi)
+        ncell[-1] = (hi - lo) // 2 if q2 else hi - lo
         rows = None
         if self.rows is not None:
             voff, vlo, vhi, clo, chi = self.rows
@@ -263,6 +267,7 @@ class LatticeInfo:
             rows = (np.asarray(voff[vs], np.int64) - offs[lo], vlo[vs], vhi[vs], clo[cs], chi[cs])
         out = LatticeInfo(self.dim, ncell, self.h, int(offs[hi + 1] - offs[lo]), self.is_box, rows)
         out.own = (own[0] - lo, own[1] - lo)
+        out.order = 2 if q2 else 1
         out.global_offset = int(offs[lo])
         out.plane_lo = int(lo)
         return out

@@ -55,7 +55,9 @@ def _worker(rank, world, port, name, levels, min_layers, q):
 
 
 @pytest.mark.parametrize("name,levels,world,min_layers", [("cfg1", None, 2, 2), ("cfg1", None, 2, 8),
-                                                          ("cfg1", None, 3, 4), ("cfg4", 3, 2, 2)])
+                                                          ("cfg1", None, 3, 4), ("cfg4", 3, 2, 2),
+                                                          ("cfg3", 3, 2, 2), ("cfg3", 4, 2, 4),
+                                                          ("cfg3", 4, 3, 2)])
 def test_distributed_newton_solve_matches_single_gpu(name, levels, world, min_layers):
     from paper_1902_08112_b200 import krylov, mgsolve
     from paper_1902_08112_b200.lattice import info_from_mesh
