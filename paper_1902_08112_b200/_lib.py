@@ -37,7 +37,7 @@ class State(C.Structure):
                 ("kappa", C.c_double), ("eps", C.c_double), ("pressure", C.c_double),
                 ("split", C.c_int32), ("hints", C.c_int32),
                 ("U", vp), ("phi_tilde", vp), ("rho", vp), ("flags", vp),
-                ("split_band", C.c_double)]
+                ("split_band", C.c_double), ("phi_coef", vp)]
 
 
 # name -> argtypes (restype is always c_int status unless noted)
@@ -47,6 +47,7 @@ _SIGS = {
     "pffmg_apply": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp],
     "pffmg_residual": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp],
     "pffmg_diagonal": [C.POINTER(Lattice), C.POINTER(State), vp, vp],
+    "pffmg_phi_coef": [C.POINTER(Lattice), C.POINTER(State), vp, vp],
     "pffmg_semilinear_residual": [C.POINTER(Lattice), C.POINTER(State), vp, vp],
     "pffmg_cheb_step": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp,
                         C.c_double, C.c_double, C.c_int, vp],

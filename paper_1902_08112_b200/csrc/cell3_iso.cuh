@@ -15,12 +15,84 @@
 
 namespace pffmg {
 
-template <int MODE, bool RHO, class Corners, class Emit>
+// JxW-scaled a_phiphi of the 8 QPs of one cell from the corners of U
+// (fields 0..2 of `C`): the phi-block coefficient of _build_caches
+// (model.py:304-308), the same expression cell3_iso evaluates in the PBLK /
+// FULL modes.  Used to build the per-QP table of pffmg_phi_coef.
+template <bool RHO, class Corners>
+__device__ __forceinline__ void phi_coef3(const Corners& C, const double* __restrict__ rho_q, const Consts& K,
+                                          const IsoK& I, double (&aj)[8]) {
+    using S = SFr<3>;
+    constexpr int NP = 8;
+    auto expand = [](const double (&r)[4], int j, int q) { return r[drop_bit(q, j)]; };
+    auto deriv = [&](int field, int j, double (&g)[4]) {
+        double c[NP];
+        C.load(field, c);
+        S::deriv(c, j, g, K);
+    };
+    double rd[3][4], trr[NP], e2[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) trr[q] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        deriv(i, i, rd[i]);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) trr[q] += expand(rd[i], i, q);
+    }
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        const double ld = I.lam * trr[q];
+        e2[q] = ld * trr[q];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            const double r2 = I.two_mu * expand(rd[i], i, q);
+            e2[q] = fma(r2, expand(rd[i], i, q), e2[q]);
+        }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = i + 1; j < 3; ++j) {
+            double a[4], b[4];
+            deriv(i, j, a);
+            deriv(j, i, b);
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                const double s = expand(a, j, q) + expand(b, i, q);
+                const double ms = I.mu * s;
+                e2[q] = fma(ms, s, e2[q]);
+            }
+        }
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        const double ce = RHO ? I.cS * __ldg(rho_q + q) : I.cS;
+        aj[q] = fma(ce, e2[q], fma(I.cdiv, trr[q], I.c0));
+    }
+}
+
+// TAB (PBLK only): a_phiphi read from the per-QP table (`tq[q * tstride]`)
+// instead of being recomputed from U -- the phi block then stages v only.
+template <int MODE, bool RHO, class Corners, class Emit, bool TAB = false>
 __device__ __forceinline__ void cell3_iso(const Corners& C, const double* __restrict__ rho_q,
-                                          const Consts& K, const IsoK& I, Emit&& emit) {
+                                          const Consts& K, const IsoK& I, Emit&& emit,
+                                          const double* __restrict__ tq = nullptr, int64_t tstride = 0) {
     using MI = ModeInfo<3, MODE>;
     using S = SFr<3>;
     constexpr int NP = 8;
+    if constexpr (TAB) {
+        static_assert(MODE == M_PBLK, "the a_phiphi table serves the phi block");
+        double cp[NP], f[NP];
+        C.load(MI::F_V, cp);
+        S::value(cp, f, K);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) f[q] = __ldg(tq + q * tstride) * f[q];
+        mass_transpose<3>(f, K);
+        corner_laplacian<3>(cp, I, f);
+        emit(0, f);
+        return;
+    }
     constexpr bool RES = MODE == M_RES;
     constexpr bool HAS_W = MODE == M_FULL || MODE == M_UBLK;     // v displacement gradient
     constexpr bool HAS_R = MODE == M_FULL || MODE == M_PBLK || RES;   // U displacement gradient

@@ -13,14 +13,16 @@
 
 namespace pffmg {
 
-template <int MODE, int EPI, int TY, bool RHO, bool BOX, bool PRE>
+// TAB (phi block only): a_phiphi comes from the per-QP table A.ptab, so only
+// v is staged (no U planes) -- the phi block becomes an HBM-bound stencil.
+template <int MODE, int EPI, int TY, bool RHO, bool BOX, bool PRE, bool TAB = false>
 #ifndef PFFMG_3D_FULL_MINB
 #define PFFMG_3D_FULL_MINB 1
 #endif
-__global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB : 2) op3dt_kernel(const OpArgs A) {
+__global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB : (TAB ? 4 : 2)) op3dt_kernel(const OpArgs A) {
     pdl_wait();
     using MI = ModeInfo<3, MODE>;
-    constexpr int NF = MI::NF, NCO = MI::NCO, NV = MI::NV;
+    constexpr int NF = TAB ? MI::NV : MI::NF, NCO = MI::NCO, NV = MI::NV;
     constexpr int RING = 4, ROWS = TY + 1, W = 32;
     constexpr int SLOT = NF * ROWS * W;          // doubles per staged plane
     constexpr int FB = 48;                       // flag bytes per staged row
@@ -61,9 +63,11 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
     const double* fsrc[NF];
 #pragma unroll
     for (int i = 0; i < NV; ++i) fsrc[MI::F_V + i] = A.v + (int64_t)i * V;
+    if constexpr (!TAB) {
 #pragma unroll
-    for (int i = 0; i < MI::NU; ++i) fsrc[MI::F_U + i] = A.U + (int64_t)i * V;
-    if (MI::PT) fsrc[MI::F_PT] = A.pt;
+        for (int i = 0; i < MI::NU; ++i) fsrc[MI::F_U + i] = A.U + (int64_t)i * V;
+        if (MI::PT) fsrc[MI::F_PT] = A.pt;
+    }
     const uint32_t* fw = reinterpret_cast<const uint32_t*>(A.flags);
 
     auto vid_of = [&](int x, int y, int z) -> int {
@@ -164,8 +168,9 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
         const bool cell = lane_cell && (BOX ? ((unsigned)cx < (unsigned)L.nx && (unsigned)cy < (unsigned)L.ny &&
                                                (unsigned)cz < (unsigned)L.nz)
                                             : cell_exists<3>(L, cx, cy, cz));
-        const double* rq = (RHO && cell) ? A.rho + ((int64_t)cx + (int64_t)L.nx * (cy + (int64_t)L.ny * cz)) * 8
-                                         : A.rho;
+        const int64_t lcell = (int64_t)cx + (int64_t)L.nx * (cy + (int64_t)L.ny * cz);
+        const double* rq = (RHO && cell) ? A.rho + lcell * 8 : A.rho;
+        const double* tq = (TAB && cell) ? A.ptab + lcell : A.ptab;
         double vp[NCO][2];                       // this vertex column's (y=0) partials, per z corner
         auto emit = [&](int k, double (&o)[8]) {
 #pragma unroll
@@ -182,7 +187,8 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
                         vp[k][zb] = part;
                 }
         };
-        cell3_iso<MODE, RHO>(C, rq, A.K, A.I, emit);
+        cell3_iso<MODE, RHO, Corners, decltype(emit)&, TAB>(C, rq, A.K, A.I, emit, tq,
+                                                            (int64_t)L.nx * L.ny * L.nz);
         __syncthreads();                         // y partials visible; planes fully read
 
         if (w >= 1) {

@@ -28,6 +28,7 @@ struct OpArgs {
     const double* __restrict__ U;
     const double* __restrict__ pt;
     const double* __restrict__ rho;
+    const double* __restrict__ ptab;   // per-QP a_phiphi table (pffmg_phi_coef) or NULL
     const uint8_t* __restrict__ flags;
     // epilogue operands (block base pointers, component stride V)
     const double* __restrict__ b;

@@ -42,6 +42,9 @@ static int fill_args(const pffmg_lattice* lat, const pffmg_state* st, OpArgs* A)
     A->pt = st->phi_tilde;
     A->rho = st->rho;
     A->flags = st->flags;
+    // the a_phiphi table serves the phi block of 3D isotropic NoSplit Q1 lattices only
+    const bool iso3 = A->L.dim == 3 && A->L.order == 1 && A->L.hx == A->L.hy && A->L.hz == A->L.hx;
+    A->ptab = (st->phi_coef && iso3 && st->split == 0) ? st->phi_coef : nullptr;
     A->premasked = (st->hints & PFFMG_HINT_PREMASKED) ? 1 : 0;
     A->ends = (st->hints & PFFMG_HINT_ENDS) ? 1 : 0;
     if (A->ends) {
@@ -78,6 +81,18 @@ static int dispatch_which(const OpArgs& A, int which, cudaStream_t s, const char
 }  // namespace pffmg
 
 using namespace pffmg;
+
+extern "C" int pffmg_phi_coef(const pffmg_lattice* lat, const pffmg_state* st, double* out, void* stream) {
+    OpArgs A;
+    int rc = fill_args(lat, st, &A);
+    if (rc) return rc;
+    PFFMG_REQUIRE(out && A.U, "pffmg_phi_coef: needs U and out");
+    PFFMG_REQUIRE(A.L.dim == 3 && A.L.order == 1 && A.L.hx == A.L.hy && A.L.hz == A.L.hx && A.split == 0,
+                  "pffmg_phi_coef: 3D isotropic Q1 NoSplit lattices only");
+    PFFMG_REQUIRE(out != st->phi_coef, "pffmg_phi_coef: out aliases state.phi_coef");
+    launch_phi_coef3(A, out, as_stream(stream));
+    return check_launch("pffmg_phi_coef");
+}
 
 extern "C" int pffmg_apply(const pffmg_lattice* lat, const pffmg_state* st, int which,
                            const double* v, double* out, void* stream) {

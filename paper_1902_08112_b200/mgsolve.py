@@ -376,6 +376,7 @@ class _Session:
             D.inject_dev(self.P2[l + 1], self.P2[l], l, self.nc)
             D.inject_dev(self.PT[l + 1], self.PT[l], l, 1)
         for l in range(self.L):
+            self.ops[l].build_phi_coef()                   # _build_caches (model.py:260)
             self.ops[l].diagonal_dev(self.diag[l])
             _lib.call("pffmg_reciprocal", _lib.ptr(self.diag[l]), _lib.ptr(self.inv[l]),
                       self.diag[l].numel(), s)
@@ -453,7 +454,7 @@ class _Session:
             if l == L - 1:
                 mask._host_fn = fine_host
             op = PhaseFieldOperator(self.D.spaces[l], st, mask, self.params, self.split, self.threads,
-                                    _flags=self.flags[l], _rho=self.ops[l]._rho)
+                                    _flags=self.flags[l], _rho=self.ops[l]._rho, _ptab=self.ops[l]._ptab)
             ctx = LevelContext(l, op, self.diag[l], self.spectra[l], None, disc, self.flags[l],
                                inv=self.inv[l])
             ctx._session, ctx._gen = self, self.gen

@@ -20,6 +20,8 @@ from dataclasses import dataclass, replace
 from enum import Enum
 from typing import Callable, Optional
 
+import os
+
 import numpy as np
 import torch
 
@@ -138,7 +140,7 @@ def _split_code(split):
 class PhaseFieldOperator:
     """Matrix-free constrained Jacobian of one level (reference model.py:242-413)."""
 
-    def __init__(self, space, state, mask, params, split, threads=1, *, _flags=None, _rho=None):
+    def __init__(self, space, state, mask, params, split, threads=1, *, _flags=None, _rho=None, _ptab=None):
         _lib.require_cuda()
         self.space = space
         self.state = state
@@ -188,15 +190,44 @@ class PhaseFieldOperator:
         st_ends.hints = 2
         self._st_ends = st_ends
         self._stp_ends = ctypes.byref(st_ends)
+        # per-QP a_phiphi of the phi block, cached like _build_caches does
+        # (model.py:260, 304-308): 3D isotropic NoSplit levels only
+        self._ptab = None
+        info = self.lat.info
+        h = np.asarray(info.h, float)
+        if (self.dim == 3 and getattr(info, "order", 1) == 1 and code == 0 and np.all(h == h[0])
+                and os.environ.get("PFFMG_PHI_TABLE", "1") != "0"):
+            if _ptab is not None:            # a table already built from this state (mgsolve._Session)
+                self._ptab = _ptab
+                for st in (self._st, self._st_pre, self._st_ends):
+                    st.phi_coef = _ptab.data_ptr()
+            else:
+                self._ptab = empty(8 * self.lat.n_lattice_cells)
+                self.build_phi_coef()
+
+    def build_phi_coef(self):
+        """(Re)build the phi-block coefficient table from the current U (device
+        work on the current stream; graph-capturable) and point the states at it."""
+        if self._ptab is None:
+            return
+        for st in (self._st, self._st_pre, self._st_ends):
+            st.phi_coef = None
+        _lib.call("pffmg_phi_coef", self.lat.ref, self._stp, _lib.ptr(self._ptab), _lib.stream())
+        for st in (self._st, self._st_pre, self._st_ends):
+            st.phi_coef = self._ptab.data_ptr()
 
     def _rebind(self, U, phi_tilde, flags):
         """Point the operator at other device buffers of the same sizes (used
         to detach an earlier generation of solver contexts, mgsolve._Session)."""
         self._U, self._pt, self._flags = U, phi_tilde, flags
+        if self._ptab is not None:
+            self._ptab = self._ptab.clone()
         for st in (self._st, self._st_pre, self._st_ends):
             st.U = U.data_ptr()
             st.phi_tilde = phi_tilde.data_ptr()
             st.flags = flags.data_ptr()
+            if self._ptab is not None:
+                st.phi_coef = self._ptab.data_ptr()
         if isinstance(self.mask, DeviceMask):
             self.mask.flags = flags
 

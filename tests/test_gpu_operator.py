@@ -227,3 +227,37 @@ def test_blockdiag_operator_equals_blocks(golden, name, split):
     assert rel_err(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-14
     assert rel_err(out[:d].cpu().numpy(), ref[:d].cpu().numpy()) <= 1e-14
     assert rel_err(out[d:].cpu().numpy(), ref[d:].cpu().numpy()) <= 1e-14
+
+
+@pytest.mark.parametrize("name,variant", [t for t in OP_TAGS if MESHES[t[0]][2] == 3])
+def test_phi_block_table_matches_recomputed(golden, name, variant, monkeypatch):
+    """3D isotropic levels cache a_phiphi per QP (pffmg_phi_coef, the reference's
+    _build_caches entry model.py:304-308): the phi block, its Chebyshev step
+    and residual read the table; they must agree with the path that re-derives
+    a_phiphi from U (PFFMG_PHI_TABLE=0) and with the reference golden."""
+    from paper_1902_08112_b200 import _lib
+    g = golden["operator"]
+    op, tag = _op(g, name, variant)
+    if not np.all(np.asarray(op.lat.info.h) == op.lat.info.h[0]):
+        pytest.skip("anisotropic cells: generic kernel, no table")
+    assert op._ptab is not None and op._st.phi_coef == op._ptab.data_ptr()
+    monkeypatch.setenv("PFFMG_PHI_TABLE", "0")
+    op0, _ = _op(g, name, variant)
+    assert op0._ptab is None
+    d = op.dim * op.V
+    v = torch.as_tensor(g[f"{tag}/v"][d:], device="cuda")
+    a, b = torch.empty_like(v), torch.empty_like(v)
+    op.apply_dev(1, v, a)
+    op0.apply_dev(1, v, b)
+    assert rel_err(a.cpu().numpy(), b.cpu().numpy()) <= 1e-13
+    assert rel_err(a.cpu().numpy(), g[f"{tag}/apply_phi"]) <= TOL
+    r0 = torch.randn_like(v)
+    x0 = torch.randn_like(v)
+    inv = torch.rand_like(v) + 1.0
+    outs = []
+    for o in (op, op0):
+        r, x, dd = r0.clone(), x0.clone(), torch.empty_like(v)
+        o.cheb_step_dev(1, v, dd, r, x, inv, 0.3, 0.2)
+        outs.append((r, x, dd))
+    for p, q in zip(*outs):
+        assert (p - q).norm() <= 1e-13 * q.norm()
