@@ -70,19 +70,52 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
     }
     const uint32_t* fw = reinterpret_cast<const uint32_t*>(A.flags);
 
-    auto vid_of = [&](int x, int y, int z) -> int {
+    // Non-box lattices: the row tables of the tile's vertex rows (off, lo, hi)
+    // and cell rows (lo, hi) are staged per plane into a ring of RR slots, four
+    // planes ahead of the cell work, so vertex ids come from shared memory
+    // (the dependent global row-table loads were the kernel's top stall).
+    constexpr int RR = 8;
+    struct RowI {
+        long long off;
+        int lo, hi;
+    };
+    __shared__ RowI srow[BOX ? 1 : RR][ROWS];
+    __shared__ int2 scell[BOX ? 1 : RR][TY];
+    const int zbase = vz0 - 1;
+    auto rslot = [&](int z) { return (z - zbase) & (RR - 1); };
+    auto fetch_rows = [&](int z) {
+        if (BOX) return;
+        const int sl = rslot(z);
+        if (tid < ROWS) {
+            const int y = y0 + tid;
+            const bool ok = (unsigned)y <= (unsigned)L.ny && (unsigned)z <= (unsigned)L.nz;
+            const int r = ok ? y + (L.ny + 1) * z : 0;
+            cp_async8(&srow[sl][tid].off, L.vrow_off + r, ok);
+            cp_async4(&srow[sl][tid].lo, L.vrow_lo + r, ok);
+            cp_async4(&srow[sl][tid].hi, L.vrow_hi + r, ok);
+        } else if (tid < ROWS + TY) {
+            const int k = tid - ROWS, y = y0 + k;
+            const bool ok = (unsigned)y < (unsigned)L.ny && (unsigned)z < (unsigned)L.nz;
+            const int c = ok ? y + L.ny * z : 0;
+            cp_async4(&scell[sl][k].x, L.crow_lo + c, ok);
+            cp_async4(&scell[sl][k].y, L.crow_hi + c, ok);
+        }
+    };
+    // vertex (x, y0 + rr, z) of the tile
+    auto vid_of = [&](int x, int rr, int z) -> int {
         if (BOX) {
+            const int y = y0 + rr;
             if ((unsigned)x > (unsigned)L.nx || (unsigned)y > (unsigned)L.ny || (unsigned)z > (unsigned)L.nz)
                 return -1;
             return (z * (L.ny + 1) + y) * (L.nx + 1) + x;
         }
-        return (int)vertex_id(L, x, y, z);
+        const RowI& R = srow[rslot(z)][rr];
+        return (x >= R.lo && x < R.hi) ? (int)(R.off + (x - R.lo)) : -1;
     };
-    auto vid_virtual = [&](int x, int y, int z) -> int {
-        if (BOX) return (z * (L.ny + 1) + y) * (L.nx + 1) + x;
-        if ((unsigned)y > (unsigned)L.ny || (unsigned)z > (unsigned)L.nz) return 0;
-        const int r = y + (L.ny + 1) * z;
-        return (int)__ldg(L.vrow_off + r) + (x - __ldg(L.vrow_lo + r));
+    auto vid_virtual = [&](int x, int rr, int z) -> int {
+        if (BOX) return (z * (L.ny + 1) + y0 + rr) * (L.nx + 1) + x;
+        const RowI& R = srow[rslot(z)][rr];
+        return (int)(R.off + (x - R.lo));
     };
 
     // stage plane z into slot: row rr of the tile (rr = 0..TY), column = lane
@@ -90,7 +123,7 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
         double* dst = sv + slot * SLOT;
         for (int e = tid; e < ROWS * W; e += 32 * TY) {
             const int rr = e / W, col = e % W;
-            const int vid = vid_of(x0 + col, y0 + rr, z);
+            const int vid = vid_of(x0 + col, rr, z);
             const bool ok = vid >= 0;
             const int off = ok ? vid : 0;
 #pragma unroll
@@ -98,7 +131,7 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
         }
         for (int e = tid; e < ROWS * 9; e += 32 * TY) {
             const int rr = e / 9, k = e % 9;
-            const int v0 = vid_virtual(x0, y0 + rr, z);
+            const int v0 = vid_virtual(x0, rr, z);
             const int w0 = v0 >> 2;
             const int wi = w0 + k;
             const bool okw = wi >= 0 && wi < nwords && (unsigned)(y0 + rr) <= (unsigned)L.ny &&
@@ -123,6 +156,12 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
         }
     };
 
+    if (!BOX) {
+        for (int z = vz0 - 1; z <= vz0 + 2; ++z) fetch_rows(z);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+    }
     issue(vz0 - 1, 0);
     issue(vz0, 1);
     double carry[NCO];
@@ -133,9 +172,10 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
     for (int cz = vz0 - 1; cz < vz1; ++cz, ++it) {
         const int s0 = it & 3, s1 = (it + 1) & 3;
         // vertex finalised this iteration and its epilogue operands (loaded early)
-        const int vid_f = (w >= 1 && cz >= vz0 && lane >= 1 && lane <= 30) ? vid_of(cx, cy, cz) : -1;
+        const int vid_f = (w >= 1 && cz >= vz0 && lane >= 1 && lane <= 30) ? vid_of(cx, w, cz) : -1;
         EpiIn<NCO, EPI> ein;
         if (vid_f >= 0) epi_load<NCO, EPI>(A, vid_f, ein);
+        if (cz + 4 <= vz1 + 1) fetch_rows(cz + 4);     // committed with the plane below
         if (cz + 2 <= vz1)
             issue(cz + 2, (it + 2) & 3);
         else
@@ -167,7 +207,7 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
 
         const bool cell = lane_cell && (BOX ? ((unsigned)cx < (unsigned)L.nx && (unsigned)cy < (unsigned)L.ny &&
                                                (unsigned)cz < (unsigned)L.nz)
-                                            : cell_exists<3>(L, cx, cy, cz));
+                                            : (cx >= scell[rslot(cz)][w].x && cx < scell[rslot(cz)][w].y));
         const int64_t lcell = (int64_t)cx + (int64_t)L.nx * (cy + (int64_t)L.ny * cz);
         const double* rq = (RHO && cell) ? A.rho + lcell * 8 : A.rho;
         const double* tq = (TAB && cell) ? A.ptab + lcell : A.ptab;
