@@ -7,42 +7,25 @@ namespace pffmg {
 
 constexpr int NW2D = 4;   // warps per CTA of the warp-independent 2D kernel
 
+// Strips of `per` vertex rows per warp (the first cell row of a strip is
+// recomputed for the y carry: overhead 1/per).  The warps are independent, so
+// the strip height is chosen to give ONE wave of resident warps (occupancy of
+// the instantiation x SMs): a partial second wave left ~30% of the SMs idle
+// for a whole strip (cfg2 vmult 41 -> 39 us).
 template <int MODE, int EPI, bool ISO, bool RHO, bool BOX, bool PRE, bool MIE>
-static void launch_w(const OpArgs& A, dim3 grid, size_t smem, cudaStream_t s) {
+static void launch_w(const OpArgs& A0, int nseg, int rows, size_t smem, cudaStream_t s) {
+    auto kern = op2dw_kernel<MODE, EPI, NW2D, ISO, RHO, BOX, PRE, MIE>;
     static size_t done = 0;
-    if (smem > 48 * 1024 && done < smem) {
-        cudaFuncSetAttribute(op2dw_kernel<MODE, EPI, NW2D, ISO, RHO, BOX, PRE, MIE>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static int occ = 0;
+    if (done < smem || occ == 0) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         done = smem;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * NW2D, smem) != cudaSuccess || occ < 1)
+            occ = 1;
     }
-    pdl_launch(op2dw_kernel<MODE, EPI, NW2D, ISO, RHO, BOX, PRE, MIE>, dim3(grid), dim3(32 * NW2D), smem, s, A);
-}
-
-template <int MODE, int EPI, bool ISO, bool RHO, bool MIE = false>
-static void launch_box(const OpArgs& A, bool pre, dim3 grid, size_t smem, cudaStream_t s) {
-    const bool box = A.L.vrow_off == nullptr;
-    if (box && pre)
-        launch_w<MODE, EPI, ISO, RHO, true, true, MIE>(A, grid, smem, s);
-    else if (box)
-        launch_w<MODE, EPI, ISO, RHO, true, false, MIE>(A, grid, smem, s);
-    else if (pre)
-        launch_w<MODE, EPI, ISO, RHO, false, true, MIE>(A, grid, smem, s);
-    else
-        launch_w<MODE, EPI, ISO, RHO, false, false, MIE>(A, grid, smem, s);
-}
-
-template <int MODE, int EPI>
-int launch2d(const OpArgs& A0, bool iso, cudaStream_t s) {
     OpArgs A = A0;
-    const Lat& L = A.L;
-    using MI = ModeInfo<2, MODE>;
-    const int sms = sm_count();
-    const int nseg = (L.nx + 1 + 29) / 30;
-    const int rows = A.ends ? 2 : L.own_hi - L.own_lo;
-    // strips of H vertex rows: aim for ~24 resident warps per SM in one wave,
-    // H in [4, 64] (the first cell row of a strip is recomputed: overhead 1/H)
-    int64_t per = ((int64_t)rows * nseg + 24LL * sms - 1) / (24LL * sms);
-    // (small levels: short strips -- their kernels are latency-, not work-bound)
+    const int64_t slots = (int64_t)sm_count() * occ * NW2D;
+    int64_t per = ((int64_t)rows * nseg + slots - 1) / slots;
     static const int minrows = [] {
         const char* e = getenv("PFFMG_2D_MINROWS");
         return e ? atoi(e) : 1;
@@ -57,21 +40,43 @@ int launch2d(const OpArgs& A0, bool iso, cudaStream_t s) {
     A.planes_per_cta = (int)per;
     A.nseg = nseg;
     const int64_t warps = (int64_t)nseg * ((rows + per - 1) / per);
-    dim3 grid((unsigned)((warps + NW2D - 1) / NW2D));
+    const dim3 grid((unsigned)((warps + NW2D - 1) / NW2D));
+    pdl_launch(kern, grid, dim3(32 * NW2D), smem, s, A);
+}
+
+template <int MODE, int EPI, bool ISO, bool RHO, bool MIE = false>
+static void launch_box(const OpArgs& A, bool pre, int nseg, int rows, size_t smem, cudaStream_t s) {
+    const bool box = A.L.vrow_off == nullptr;
+    if (box && pre)
+        launch_w<MODE, EPI, ISO, RHO, true, true, MIE>(A, nseg, rows, smem, s);
+    else if (box)
+        launch_w<MODE, EPI, ISO, RHO, true, false, MIE>(A, nseg, rows, smem, s);
+    else if (pre)
+        launch_w<MODE, EPI, ISO, RHO, false, true, MIE>(A, nseg, rows, smem, s);
+    else
+        launch_w<MODE, EPI, ISO, RHO, false, false, MIE>(A, nseg, rows, smem, s);
+}
+
+template <int MODE, int EPI>
+int launch2d(const OpArgs& A, bool iso, cudaStream_t s) {
+    const Lat& L = A.L;
+    using MI = ModeInfo<2, MODE>;
+    const int nseg = (L.nx + 1 + 29) / 30;
+    const int rows = A.ends ? 2 : L.own_hi - L.own_lo;
     const int nf = A.split ? ModeInfo<2, MODE, true>::NF : MI::NF;
     const size_t smem = NW2D * (sizeof(double) * 4 * nf * 32 + 4 * 48 + 4 * sizeof(int));
     const bool rho = A.rho != nullptr;
     const bool pre = A.premasked != 0;
     if (A.split)   // Miehe split: general-cell kernel, modulus field resolved in-kernel
-        launch_box<MODE, EPI, false, false, true>(A, pre, grid, smem, s);
+        launch_box<MODE, EPI, false, false, true>(A, pre, nseg, rows, smem, s);
     else if (iso && rho)
-        launch_box<MODE, EPI, true, true>(A, pre, grid, smem, s);
+        launch_box<MODE, EPI, true, true>(A, pre, nseg, rows, smem, s);
     else if (iso)
-        launch_box<MODE, EPI, true, false>(A, pre, grid, smem, s);
+        launch_box<MODE, EPI, true, false>(A, pre, nseg, rows, smem, s);
     else if (rho)
-        launch_box<MODE, EPI, false, true>(A, pre, grid, smem, s);
+        launch_box<MODE, EPI, false, true>(A, pre, nseg, rows, smem, s);
     else
-        launch_box<MODE, EPI, false, false>(A, pre, grid, smem, s);
+        launch_box<MODE, EPI, false, false>(A, pre, nseg, rows, smem, s);
     return PFFMG_OK;
 }
 

@@ -137,24 +137,38 @@ __global__ void __launch_bounds__(128, MODE == M_FULL ? 2 : PFFMG_Q2_MINB) op2q_
     }
 }
 
-template <int MODE, int EPI>
-int launch2q(const OpArgs& A0, cudaStream_t s) {
+// One wave of resident warps (see op2d.cu): strips of `per` cell rows.
+template <int MODE, int EPI, bool MIE>
+static void launch_q(const OpArgs& A0, int nseg, int rows, const Q2Tab& T, cudaStream_t s) {
+    auto kern = op2q_kernel<MODE, EPI, MIE>;
+    static int occ = 0;
+    if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0) != cudaSuccess || occ < 1))
+        occ = 1;
     OpArgs A = A0;
-    const Lat& L = A.L;
-    const int sms = sm_count();
-    const int nseg = (L.nx + 1 + 30) / 31;
-    const int rows = ((L.own_hi + 1) >> 1) - (L.own_lo >> 1);
-    int64_t per = ((int64_t)rows * nseg + 16LL * sms - 1) / (16LL * sms);
+    const int64_t slots = (int64_t)sm_count() * occ * 4;
+    int64_t per = ((int64_t)rows * nseg + slots - 1) / slots;
     per = per < 1 ? 1 : (per > 32 ? 32 : per);
+    static const int forced = [] {
+        const char* e = getenv("PFFMG_Q2_ROWS");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced > 0) per = forced;
     A.planes_per_cta = (int)per;
     A.nseg = nseg;
     const int64_t warps = (int64_t)nseg * ((rows + per - 1) / per);
-    const dim3 grid((unsigned)((warps + 3) / 4));
+    pdl_launch(kern, dim3((unsigned)((warps + 3) / 4)), dim3(128), 0, s, A, T);
+}
+
+template <int MODE, int EPI>
+int launch2q(const OpArgs& A, cudaStream_t s) {
+    const Lat& L = A.L;
+    const int nseg = (L.nx + 1 + 30) / 31;
+    const int rows = ((L.own_hi + 1) >> 1) - (L.own_lo >> 1);
     const Q2Tab T = make_q2_host(L.hx, L.hy);
     if (A.split)
-        pdl_launch(op2q_kernel<MODE, EPI, true>, dim3(grid), dim3(128), 0, s, A, T);
+        launch_q<MODE, EPI, true>(A, nseg, rows, T, s);
     else
-        pdl_launch(op2q_kernel<MODE, EPI, false>, dim3(grid), dim3(128), 0, s, A, T);
+        launch_q<MODE, EPI, false>(A, nseg, rows, T, s);
     return PFFMG_OK;
 }
 
