@@ -179,6 +179,9 @@ def run_gpu(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
+        # one collective over every rank before the first point-to-point halo
+        # batch (batch_isend_irecv must not be a communicator's first operation)
+        dist.all_reduce(torch.zeros(1, device="cuda") if args.backend == "nccl" else torch.zeros(1))
     from paper_1902_08112_b200 import _lib, configs, krylov, mgsolve
     from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, SplitKind
 
