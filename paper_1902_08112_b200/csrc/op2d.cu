@@ -64,7 +64,7 @@ int launch2d(const OpArgs& A, bool iso, cudaStream_t s) {
     const int nseg = (L.nx + 1 + 29) / 30;
     const int rows = A.ends ? 2 : L.own_hi - L.own_lo;
     const int nf = A.split ? ModeInfo<2, MODE, true>::NF : MI::NF;
-    const size_t smem = NW2D * (sizeof(double) * 4 * nf * 32 + 4 * 48 + 4 * sizeof(int));
+    const size_t smem = NW2D * sizeof(double) * 4 * nf * 32;
     const bool rho = A.rho != nullptr;
     const bool pre = A.premasked != 0;
     if (A.split)   // Miehe split: general-cell kernel, modulus field resolved in-kernel

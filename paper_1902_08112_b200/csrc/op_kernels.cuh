@@ -185,14 +185,10 @@ op2dw_kernel(const OpArgs A) {
     using MI = ModeInfo<D, MODE, MIE>;
     constexpr int NF = MI::NF, NCO = MI::NCO, NV = MI::NV;
     constexpr int RING = 4, W = 32, SLOT = NF * W;
-    constexpr int FB = 48;                      // flag bytes per slot (9 words + pad)
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double* sv = reinterpret_cast<double*>(smem_raw) + w * (RING * SLOT);
-    unsigned char* sfl = smem_raw + sizeof(double) * NW * RING * SLOT + w * (RING * FB);
-    int* sfo = reinterpret_cast<int*>(smem_raw + sizeof(double) * NW * RING * SLOT + NW * RING * FB) +
-               w * RING;
 
     const Lat& L = A.L;
     const int gw = (int)blockIdx.x * NW + w;
@@ -203,59 +199,52 @@ op2dw_kernel(const OpArgs A) {
     const int vy1 = A.ends ? vy0 + 1 : min(vy0 + A.planes_per_cta, L.own_hi);
     const int x0 = 30 * seg - 1;
     const int cx = x0 + lane;
-    const int V = (int)L.V;
-    const int nwords = (V + 3) / 4 + 8;          // readable flag words (padded buffer)
     const bool col_cell = lane <= 30 && cx >= 0 && cx < L.nx;
     const bool col_fin = lane >= 1 && lane <= 30;
 
     const double* fsrc[NF];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) fsrc[MI::F_V + i] = A.v + (int64_t)i * V;
+    for (int i = 0; i < NV; ++i) fsrc[MI::F_V + i] = A.v + (int64_t)i * L.V;
 #pragma unroll
-    for (int i = 0; i < MI::NU; ++i) fsrc[MI::F_U + i] = A.U + (int64_t)i * V;
+    for (int i = 0; i < MI::NU; ++i) fsrc[MI::F_U + i] = A.U + (int64_t)i * L.V;
     if (MI::PT) fsrc[MI::F_PT] = A.pt;
-    const uint32_t* fw = reinterpret_cast<const uint32_t*>(A.flags);
 
-    auto issue = [&](int y, int slot) {
+    // Stage row y into the ring slot (one column per lane); the lane's own
+    // constraint byte of that row comes back in a register (a plain load: it
+    // is first read one to three iterations later, so its latency is hidden
+    // and no shared-memory flag words / offsets are needed).
+    auto issue = [&](int y, int slot) -> unsigned {
         double* dst = sv + slot * SLOT + lane;
         const int vid = RowAddr<BOX>::id(L, cx, y);
         const bool ok = vid >= 0;
         const int off = ok ? vid : 0;
 #pragma unroll
         for (int f = 0; f < NF; ++f) cp_async8(dst + f * W, fsrc[f] + off, ok);
-        const int v0 = RowAddr<BOX>::vid_virtual(L, x0, y);
-        const int w0 = v0 >> 2;                  // floor division (v0 may be -1)
-        if (lane < 9) {
-            const int wi = w0 + lane;
-            const bool okw = wi >= 0 && wi < nwords && (unsigned)y <= (unsigned)L.ny;
-            cp_async4(sfl + slot * FB + 4 * lane, fw + (okw ? wi : 0), okw);
-        }
-        if (lane == 0) sfo[slot] = v0 - 4 * w0;  // byte of column x0 inside the staged words
         cp_async_commit();
+        return ok ? (unsigned)__ldg(A.flags + off) : 0u;
     };
-    auto flag = [&](int slot) -> unsigned { return sfl[slot * FB + sfo[slot] + lane]; };
-    auto mask_row = [&](int slot) {              // fem.py:205-206, once per vertex
+    auto mask_row = [&](int slot, unsigned fl) {   // fem.py:205-206, once per vertex
         if (PRE || NV == 0) return;
-        const unsigned fl = flag(slot);
         double* row = sv + slot * SLOT;
 #pragma unroll
         for (int i = 0; i < NV; ++i)
             if ((fl >> (MI::COMP0 + i)) & 1) row[i * W + lane] = 0.0;
     };
 
-    issue(vy0 - 1, 0);
-    issue(vy0, 1);
-    issue(vy0 + 1, 2);
+    // flags of rows cy (bottom), cy+1 (top), cy+2 (in flight)
+    unsigned fl_bot = issue(vy0 - 1, 0);
+    unsigned fl_top = issue(vy0, 1);
+    unsigned fl_nxt = issue(vy0 + 1, 2);
     cp_async_wait<1>();                          // rows vy0-1, vy0 landed
     __syncwarp();
     double raw_bot[NV > 0 ? NV : 1];             // raw own-column v of the bottom row
 #pragma unroll
     for (int i = 0; i < NV; ++i) raw_bot[i] = sv[0 * SLOT + i * W + lane];
-    mask_row(0);
+    mask_row(0, fl_bot);
     double raw_top[NV > 0 ? NV : 1];
 #pragma unroll
     for (int i = 0; i < NV; ++i) raw_top[i] = sv[1 * SLOT + i * W + lane];
-    mask_row(1);
+    mask_row(1, fl_top);
 
     double carry[NCO];
 #pragma unroll
@@ -276,10 +265,11 @@ op2dw_kernel(const OpArgs A) {
                 raw_bot[i] = raw_top[i];
                 raw_top[i] = sv[s1 * SLOT + i * W + lane];
             }
-            mask_row(s1);
+            mask_row(s1, fl_top);
         }
+        unsigned fl_new = 0;
         if (cy + 3 <= vy1)
-            issue(cy + 3, (it + 3) & 3);
+            fl_new = issue(cy + 3, (it + 3) & 3);
         else
             cp_async_commit();
         if (!PRE) __syncwarp();                  // neighbour lanes' masking visible
@@ -287,15 +277,22 @@ op2dw_kernel(const OpArgs A) {
         const double* r0 = sv + s0 * SLOT;
         const double* r1 = sv + s1 * SLOT;
         double o[NCO][NP];
+        // FULL (operator / residual / block-diagonal smoother): every lane runs
+        // the cell kernel (lane 31 and absent cells on a copy of a valid
+        // column, outputs zeroed by a select) -- no divergent branch around
+        // the cell work (cfg2 vmult 36.1 -> 34.5 us, ncu).  The register-capped
+        // block modes keep the branch (the select costs them spills).
+        constexpr bool BRANCHLESS = MODE == M_FULL;
         const bool cell = col_cell && (BOX ? (cy >= 0 && cy < L.ny) : cell_exists<D>(L, cx, cy, 0));
-        if (cell) {
+        if (BRANCHLESS || cell) {
+            const int ll = lane < 31 ? lane : 30;
             double cv[NF][NP];
 #pragma unroll
             for (int i = 0; i < NF; ++i) {
-                cv[i][0] = r0[i * W + lane];
-                cv[i][1] = r0[i * W + lane + 1];
-                cv[i][2] = r1[i * W + lane];
-                cv[i][3] = r1[i * W + lane + 1];
+                cv[i][0] = r0[i * W + ll];
+                cv[i][1] = r0[i * W + ll + 1];
+                cv[i][2] = r1[i * W + ll];
+                cv[i][3] = r1[i * W + ll + 1];
             }
             if constexpr (MODE == M_FULL) {      // block-diagonal operator: no G_phiu coupling
                 if (A.nocoup) {                  // (T_phiu = 0 when phi(U) reads 0, model.py:299-303)
@@ -303,15 +300,21 @@ op2dw_kernel(const OpArgs A) {
                     for (int n = 0; n < NP; ++n) cv[MI::F_U + D][n] = 0.0;
                 }
             }
-            const double* rq = RHO ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * NP : nullptr;
+            const int64_t lc = cell ? ((int64_t)cx + (int64_t)L.nx * cy) : 0;   // rho row of a real cell
+            const double* rq = RHO ? A.rho + lc * NP : nullptr;
             if constexpr (MIE) {   // spectral split: modulus field resolved at run time
-                cell_kernel_miehe2<MODE>(cv, A.rho ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * NP : nullptr,
-                                         A.K, o);
+                cell_kernel_miehe2<MODE>(cv, A.rho ? A.rho + lc * NP : nullptr, A.K, o);
             } else {
                 if (ISO)
                     cell_kernel_iso<D, MODE, RHO>(cv, rq, A.K, A.I, o);
                 else
                     cell_kernel<D, MODE>(cv, rq, A.K, o);
+            }
+            if (BRANCHLESS) {
+#pragma unroll
+                for (int k = 0; k < NCO; ++k)
+#pragma unroll
+                    for (int n = 0; n < NP; ++n) o[k][n] = cell ? o[k][n] : 0.0;
             }
         } else {
 #pragma unroll
@@ -335,10 +338,13 @@ op2dw_kernel(const OpArgs A) {
                 acc[k] = carry[k] + bot[k];
                 vin[k] = (MODE == M_DIAG) ? 0.0 : raw_bot[k < NV ? k : 0];
             }
-            epilogue<NCO, MI::COMP0, EPI>(A, vid_f, (uint8_t)flag(s0), acc, vin, ein);
+            epilogue<NCO, MI::COMP0, EPI>(A, vid_f, (uint8_t)fl_bot, acc, vin, ein);
         }
 #pragma unroll
         for (int k = 0; k < NCO; ++k) carry[k] = top[k];
+        fl_bot = fl_top;
+        fl_top = fl_nxt;
+        fl_nxt = fl_new;
         __syncwarp();                            // slot s0 free for the next issue
     }
     cp_async_wait<0>();
