@@ -160,8 +160,12 @@ def gmres(op, precond, b, control=None, x0=None):
         # one speculative application after convergence is discarded.
         # (only for problems whose V-cycle is short next to the host round trip:
         # on very large levels the discarded application would cost more)
+        # The speculation is also skipped when this iteration is predicted to
+        # converge (residual estimate extrapolated from the last two, with a
+        # 4x margin): the discarded application would be a whole V-cycle.
         speculate = pcf is not None and hasattr(pcf, "_pffmg_into") and n <= (1 << 24)
         ready = False                                    # Z[j] already enqueued
+        res_prev, res_cur = None, r_norm                 # |g| before / after the last column
         for j in range(m):
             if not ready:
                 if pcf is None:
@@ -175,7 +179,9 @@ def gmres(op, precond, b, control=None, x0=None):
                       _lib.ptr(hcol), _lib.ptr(ws.ctl), _lib.stream())
             ws.hpin[:j + 2].copy_(hcol[:j + 2], non_blocking=True)
             ws.event.record()
-            ready = speculate and j + 1 < m
+            likely_done = res_prev is not None and res_prev > 0.0 and \
+                res_cur * (res_cur / res_prev) <= 4.0 * tol
+            ready = speculate and j + 1 < m and not likely_done
             if ready:
                 _into(pcf, V[j + 1], Z[j + 1])
             ws.event.synchronize()
@@ -192,6 +198,7 @@ def gmres(op, precond, b, control=None, x0=None):
             H[j + 1, j] = 0.0
             g[j + 1] = -sn[j] * g[j]
             g[j] = cs[j] * g[j]
+            res_prev, res_cur = res_cur, abs(g[j + 1])
             j_used = j + 1
             if abs(g[j + 1]) <= tol or breakdown:
                 break

@@ -163,12 +163,13 @@ def _is_native(op):
     return isinstance(op, PhaseFieldOperator)
 
 
-def _cg_native(op, diag_dev, eig_iters, seed):
-    """Enqueue the device CG-Lanczos of both blocks (no host sync); returns the
+def _cg_native(op, diag_dev, eig_iters, seed, blocks=(0, 1)):
+    """Enqueue the device CG-Lanczos of the given blocks (no host sync); returns the
     device scalar arrays.  Seed rule seed + 31*level + 7*k (mgsolve.py:135-136)."""
     level = getattr(getattr(op, "space", None), "level", None)
     out = []
-    for k, blk in enumerate(op.blocks):
+    for k in blocks:
+        blk = op.blocks[k]
         sd = seed + 31 * level + 7 * k if level is not None else seed + 7 * k
         n = blk.stop - blk.start
         b = probe_vector(sd, n).clone()
@@ -383,15 +384,18 @@ class _Session:
         # the 2L block CG-Lanczos runs are independent: one stream per level, so the
         # latency-bound coarse-level ones overlap the fine level's (each stream has
         # its own reduction scratch in libpffmg)
+        # (one stream per level AND block: the u and phi chains of a level are
+        # independent too)
         main = torch.cuda.current_stream()
         if self._streams is None:
-            self._streams = [torch.cuda.Stream() for _ in range(self.L)]
-        scals = [None] * self.L
+            self._streams = [torch.cuda.Stream() for _ in range(2 * self.L)]
+        scals = [[None, None] for _ in range(self.L)]
         for l in range(self.L - 1, -1, -1):
-            st = self._streams[l]
-            st.wait_stream(main)
-            with torch.cuda.stream(st):
-                scals[l] = _cg_native(self.ops[l], self.diag[l], self.eig_iters, self.seed)
+            for k in range(2):
+                st = self._streams[2 * l + k]
+                st.wait_stream(main)
+                with torch.cuda.stream(st):
+                    scals[l][k] = _cg_native(self.ops[l], self.diag[l], self.eig_iters, self.seed, (k,))[0]
         for st in self._streams:
             main.wait_stream(st)
         return torch.stack([t for pair in scals for t in pair])

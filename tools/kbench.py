@@ -14,7 +14,7 @@ from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, Spli
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg2")
 ap.add_argument("--levels", type=int, default=None)
-ap.add_argument("--mode", default="full", choices=["full", "u", "phi", "diag", "chebu", "chebp", "resid"])
+ap.add_argument("--mode", default="full", choices=["full", "u", "phi", "diag", "chebu", "chebp", "resid", "chebbd", "initbd"])
 ap.add_argument("--reps", type=int, default=200)
 ap.add_argument("--pre", action="store_true", help="use the pre-masked hint (inputs zeroed at constraints)")
 args = ap.parse_args()
@@ -33,6 +33,7 @@ r = torch.randn(n, dtype=torch.float64, device="cuda")
 x = torch.randn(n, dtype=torch.float64, device="cuda")
 inv = torch.rand(n, dtype=torch.float64, device="cuda") + 1.0
 d2 = torch.empty_like(v)
+cf = torch.tensor([0.3, 0.2], dtype=torch.float64, device="cuda")
 flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
 
 
@@ -49,6 +50,10 @@ def run():
         op.residual_dev(_lib.FULL, v, r, out, pre=P)
     elif args.mode == "chebu":
         op.cheb_step_dev(0, v[:d], d2[:d], r[:d], x[:d], inv[:d], 0.3, 0.2, pre=P)
+    elif args.mode == "chebbd":      # the block-diagonal smoother step of the V-cycle
+        op.cheb_step_bd(v, d2, r, x, inv, cf, cf, pre=P)
+    elif args.mode == "initbd":      # its first step from a non-zero x (r = b - A x)
+        op.cheb_init_bd(x, v, r, d2, inv, cf[:1], cf[:1], pre=P)
     elif args.mode == "chebp":
         op.cheb_step_dev(1, v[d:], d2[d:], r[d:], x[d:], inv[d:], 0.3, 0.2, pre=P)
 
@@ -66,7 +71,7 @@ for _ in range(args.reps):
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
-ndof = {"full": n, "resid": n, "diag": n, "u": d, "chebu": d, "phi": V, "chebp": V}[args.mode]
+ndof = {"full": n, "resid": n, "diag": n, "chebbd": n, "initbd": n, "u": d, "chebu": d, "phi": V, "chebp": V}[args.mode]
 # the event timer ticks in ~2 us steps on these boxes: the mean over many reps
 # resolves below a tick, the median does not
 print(f"{args.config} {args.mode}{' pre' if P else ''}: mean {np.mean(ts)*1e3:.2f} us  median {np.median(ts)*1e3:.1f} us  "

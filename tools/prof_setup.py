@@ -15,8 +15,18 @@ prob = configs.make(sys.argv[1] if len(sys.argv) > 1 else "cfg2")
 rhs = torch.as_tensor(configs.fallback_rhs(prob), device="cuda")
 
 
+from paper_1902_08112_b200 import model as M  # noqa: E402
+
+# the state as a Newton loop holds it: on the device (bench.py newton_step)
+state_dev = M.LinearizationState(
+    U=torch.as_tensor(prob.state.U, device="cuda"), U_prev1=torch.as_tensor(prob.state.U_prev1, device="cuda"),
+    U_prev2=torch.as_tensor(prob.state.U_prev2, device="cuda"), t=prob.state.t,
+    t_prev1=prob.state.t_prev1, t_prev2=prob.state.t_prev2,
+    phi_tilde=torch.as_tensor(prob.state.phi_tilde, device="cuda"))
+
+
 def setup():
-    return mgsolve.build_level_contexts(prob.disc, prob.state, prob.active, prob.dirichlet,
+    return mgsolve.build_level_contexts(prob.disc, state_dev, prob.active, prob.dirichlet,
                                         prob.params, SplitKind.NOSPLIT)
 
 
@@ -32,7 +42,8 @@ pr.enable()
 ctxs = setup()
 torch.cuda.synchronize()
 pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(30)
+pstats.Stats(pr).sort_stats("tottime").print_stats(15)
 pc = mgsolve.VCyclePreconditioner(ctxs, degree=prob.degree)
 ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8)
 x, its = krylov.gmres(ctxs[-1].op.apply, pc, rhs, ctl)
