@@ -9,6 +9,9 @@
 // Scalars that steer later kernels (GMRES H entries, CG alpha/beta, stop
 // flags) stay in device memory so no host round trip is needed between steps.
 #include <cmath>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 #include <mutex>
 #include <unordered_map>
 
@@ -619,10 +622,178 @@ extern "C" int pffmg_dot_scaled(const double* x, const double* y, const double* 
     return run_fused(DotOp{x, y, s, result}, n, as_stream(stream), "pffmg_dot_scaled");
 }
 
+// ------------------------------------------------- one-launch Arnoldi step
+// The whole MGS step of krylov.py:97-110 (sweep, norm, conditional second
+// sweep, V_{j+1} = w / h) as ONE cooperative launch: CTA b keeps its slice of
+// w in shared memory for the whole step, so w crosses HBM twice (load, final
+// store) instead of four vector passes per basis vector; every inner product
+// is a deterministic two-level sum (fixed per-CTA tree, then every CTA adds the
+// CTA partials in index order after one grid barrier).  Same arithmetic order
+// per element as the multi-launch path: w -= h_{i-1} V_{i-1} fused with the
+// dot against V_i.
+constexpr int MGS_T = 1024;
+
+__device__ __forceinline__ double mgs_block_sum(double a, double* red) {
+    a = warp_sum(a);
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    if (lane == 0) red[wi] = a;
+    __syncthreads();
+    if (wi == 0) {
+        a = lane < MGS_T / 32 ? red[lane] : 0.0;
+        a = warp_sum(a);
+    }
+    return a;   // valid in warp 0
+}
+
+struct MgsSums {   // grid-wide fixed-order sums of up to two per-CTA partials
+    double* part;  // [2 buffers][2 sums][gridDim.x]
+    int phase;
+    __device__ void post(double a0, double a1, double* red) {
+        const double s0 = mgs_block_sum(a0, red);
+        __syncthreads();
+        const double s1 = mgs_block_sum(a1, red);
+        double* p = part + (phase & 1) * 2 * gridDim.x;
+        if (threadIdx.x == 0) {
+            p[blockIdx.x] = s0;
+            p[gridDim.x + blockIdx.x] = s1;
+        }
+    }
+    // after the grid barrier: the same totals in every CTA
+    __device__ void fetch(double& t0, double& t1, double* red) {
+        const double* p = part + (phase & 1) * 2 * gridDim.x;
+        if (threadIdx.x < 32) {
+            double a = 0.0, b = 0.0;
+            for (unsigned k = threadIdx.x; k < gridDim.x; k += 32) {
+                a += __ldcg(p + k);
+                b += __ldcg(p + gridDim.x + k);
+            }
+            a = warp_sum(a);
+            b = warp_sum(b);
+            if (threadIdx.x == 0) {
+                red[32] = a;
+                red[33] = b;
+            }
+        }
+        __syncthreads();
+        t0 = red[32];
+        t1 = red[33];
+        __syncthreads();
+        ++phase;
+    }
+};
+
+__global__ void __launch_bounds__(MGS_T, 1) mgs_coop_kernel(const double* __restrict__ Vb, int64_t ld, int j,
+                                                            double* w, int64_t n, int64_t chunk, double* h,
+                                                            double* ctl, double* part) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double sw[];
+    __shared__ double red[40];
+    const int64_t c0 = (int64_t)blockIdx.x * chunk;
+    const int64_t c1 = c0 + chunk < n ? c0 + chunk : n;
+    const int m = c1 > c0 ? (int)(c1 - c0) : 0;
+    for (int k = threadIdx.x; k < m; k += MGS_T) sw[k] = w[c0 + k];
+    __syncthreads();
+    MgsSums S{part, 0};
+    auto V = [&](int i) { return Vb + (int64_t)i * ld + c0; };
+    double hv[66];   // H[0..j+1, j] (local memory; indexed by the uniform pass counter)
+    double w0n2 = 0.0;
+    bool reorth = false;
+    for (int sweep = 0; sweep < 2; ++sweep) {
+        if (sweep == 1 && !reorth) break;
+        double hprev = 0.0;
+        for (int i = 0; i <= j + 1; ++i) {
+            const double* vp = i ? V(i - 1) : nullptr;
+            const double* vc = i <= j ? V(i) : nullptr;
+            const bool nrm = (sweep == 0 && i == 0) || i == j + 1;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+            for (int k = threadIdx.x; k < m; k += MGS_T) {
+                double wk = sw[k];
+                if (vp) {
+                    wk = fma(-hprev, __ldcg(vp + k), wk);
+                    sw[k] = wk;
+                }
+                if (vc) a0 = fma(__ldcg(vc + k), wk, a0);
+                if (nrm) a1 = fma(wk, wk, a1);
+            }
+            S.post(a0, a1, red);
+            grid.sync();
+            double t0, t1;
+            S.fetch(t0, t1, red);
+            if (i <= j) {
+                if (sweep == 0) {
+                    hv[i] = t0;                       // H[i, j]
+                    if (i == 0) w0n2 = t1;            // ||w0||^2
+                    hprev = t0;
+                } else {
+                    hv[i] += t0;                      // H[i, j] += correction (krylov.py:103-105)
+                    hprev = t0;
+                    if (blockIdx.x == 0 && threadIdx.x == 0) ctl[3 + i] = t0;
+                }
+            } else {
+                const double wn = sqrt(t1);
+                hv[j + 1] = wn;                       // H[j+1, j]
+                if (sweep == 0) reorth = wn < 1e-3 * sqrt(w0n2);   // krylov.py:101
+                if (blockIdx.x == 0 && threadIdx.x == 0) ctl[1] = t1;
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl[0] = w0n2;
+        ctl[2] = reorth ? 1.0 : 0.0;
+        for (int i = 0; i <= j + 1; ++i) h[i] = hv[i];
+    }
+    const double hn = hv[j + 1];
+    for (int k = threadIdx.x; k < m; k += MGS_T) w[c0 + k] = hn != 0.0 ? sw[k] / hn : sw[k];   // krylov.py:108-110
+}
+
+static int mgs_coop(const double* Vb, int64_t ld, int j, double* w, int64_t n, double* h, double* ctl,
+                    cudaStream_t s) {
+    static int grid = -1;
+    static int64_t cap = 0;
+    static double* part = nullptr;
+    if (grid < 0) {
+        grid = 0;
+        int dev = 0, sms = 0, coop = 0, maxsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const int smem = maxsm - 2048;
+        if (coop && smem > 0 &&
+            cudaFuncSetAttribute(mgs_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess &&
+            cudaMalloc(&part, sizeof(double) * 4 * sms) == cudaSuccess) {
+            int occ = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mgs_coop_kernel, MGS_T, smem) == cudaSuccess &&
+                occ >= 1) {
+                grid = sms;
+                cap = (int64_t)sms * (smem / (int64_t)sizeof(double));
+            }
+        }
+        cudaGetLastError();
+    }
+    if (grid <= 0 || n > cap || n < (int64_t)grid * MGS_T) return 1;   // not applicable: multi-launch path
+    int64_t chunk = (n + grid - 1) / grid;
+    const size_t smem = (size_t)chunk * sizeof(double);
+    void* args[] = {(void*)&Vb, (void*)&ld, (void*)&j, (void*)&w, (void*)&n, (void*)&chunk, (void*)&h,
+                    (void*)&ctl, (void*)&part};
+    if (cudaLaunchCooperativeKernel((void*)mgs_coop_kernel, dim3(grid), dim3(MGS_T), args, smem, s) != cudaSuccess) {
+        cudaGetLastError();
+        return 1;
+    }
+    return 0;
+}
+
 extern "C" int pffmg_arnoldi_mgs(double* Vb, int64_t ld, int j, double* w, int64_t n, double* h,
                                  double* ctl, void* stream) {
     PFFMG_REQUIRE(Vb && w && h && ctl && j >= 0 && j < 64 && ld >= n, "pffmg_arnoldi_mgs: bad args");
     cudaStream_t s = as_stream(stream);
+    static const bool coop_off = [] {
+        const char* e = getenv("PFFMG_MGS_COOP");
+        return e && e[0] == '0';
+    }();
+    if (!coop_off && mgs_coop(Vb, ld, j, w, n, h, ctl, s) == 0) return check_launch("arnoldi_mgs");
     auto V = [&](int i) { return (const double*)(Vb + (int64_t)i * ld); };
     int rc;
     // modified Gram-Schmidt sweep
