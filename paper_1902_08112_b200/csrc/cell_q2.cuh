@@ -17,6 +17,10 @@ struct Q2Tab {
     double D[3][3];   // reference derivatives
     double w[3];      // Gauss weights (5, 8, 5) / 18
     double vol;       // cell volume
+    // folded on the host (the kernels use them as constant-bank operands
+    // instead of re-multiplying in registers): physical derivatives and JxW
+    double Dx[3][3], Dy[3][3];   // D / hx, D / hy
+    double W[3][3];              // W[qy][qx] = (w[qy] vol) w[qx]
 };
 
 inline Q2Tab make_q2_host(double hx, double hy) {
@@ -35,6 +39,12 @@ inline Q2Tab make_q2_host(double hx, double hy) {
     T.w[1] = 8.0 / 18.0;
     T.w[2] = 5.0 / 18.0;
     T.vol = hx * hy;
+    for (int q = 0; q < 3; ++q)
+        for (int a = 0; a < 3; ++a) {
+            T.Dx[q][a] = T.D[q][a] * (1.0 / hx);
+            T.Dy[q][a] = T.D[q][a] * (1.0 / hy);
+            T.W[q][a] = (T.w[q] * T.vol) * T.w[a];   // the row kernel's order: (w_qy vol) w_qx
+        }
     return T;
 }
 
@@ -252,7 +262,7 @@ __device__ __forceinline__ void cell_q2_rows(Load&& load, const double* __restri
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
             By[b] = T.B[qy][b];
-            Dy[b] = T.D[qy][b] * K.ih[1];
+            Dy[b] = T.Dy[qy][b];
         }
         // y-contraction of field f for this QP row: yv[a], yd[a] per node column a
         auto ycon = [&](int f, double (&yv)[3], double (&yd)[3]) {
@@ -281,7 +291,7 @@ __device__ __forceinline__ void cell_q2_rows(Load&& load, const double* __restri
                 double u0x = 0, u0y = 0, u1x = 0, u1y = 0;
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    const double dx = T.D[qx][a] * K.ih[0], bx = T.B[qx][a];
+                    const double dx = T.Dx[qx][a], bx = T.B[qx][a];
                     u0x = fma(dx, y0v[a], u0x);
                     u0y = fma(bx, y0d[a], u0y);
                     u1x = fma(dx, y1v[a], u1x);
@@ -328,7 +338,6 @@ __device__ __forceinline__ void cell_q2_rows(Load&& load, const double* __restri
             }
         }
         // ---- increments and the transposed pass
-        const double wy = T.w[qy] * T.vol;
         double tv[NCO][3], td[NCO][3];
 #pragma unroll
         for (int k = 0; k < NCO; ++k)
@@ -344,13 +353,13 @@ __device__ __forceinline__ void cell_q2_rows(Load&& load, const double* __restri
                 w00[qx] = w01[qx] = w10[qx] = w11[qx] = 0.0;
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    const double dx = T.D[qx][a] * K.ih[0], bx = T.B[qx][a];
+                    const double dx = T.Dx[qx][a], bx = T.B[qx][a];
                     w00[qx] = fma(dx, y0v[a], w00[qx]);
                     w01[qx] = fma(bx, y0d[a], w01[qx]);
                     w10[qx] = fma(dx, y1v[a], w10[qx]);
                     w11[qx] = fma(bx, y1d[a], w11[qx]);
                 }
-                const double jxw = wy * T.w[qx];
+                const double jxw = T.W[qy][qx];
                 const double e01 = 0.5 * (w01[qx] + w10[qx]), tre = w00[qx] + w11[qx];
                 const double g = jxw * gr[qx];                               // model.py:316-319
                 const double s00 = g * (2.0 * K.mu * w00[qx] + K.lam * tre);
@@ -359,7 +368,7 @@ __device__ __forceinline__ void cell_q2_rows(Load&& load, const double* __restri
                 // u rows: sum_j s_ij dN/dx_j -> x pass (F = 0)
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    const double dx = T.D[qx][a] * K.ih[0], bx = T.B[qx][a];
+                    const double dx = T.Dx[qx][a], bx = T.B[qx][a];
                     tv[0][a] = fma(dx, s00, tv[0][a]);
                     td[0][a] = fma(bx, s01, td[0][a]);
                     tv[1][a] = fma(dx, s01, tv[1][a]);
@@ -376,12 +385,12 @@ __device__ __forceinline__ void cell_q2_rows(Load&& load, const double* __restri
                 double val = 0, gx = 0, gy = 0;
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    const double dx = T.D[qx][a] * K.ih[0], bx = T.B[qx][a];
+                    const double dx = T.Dx[qx][a], bx = T.B[qx][a];
                     val = fma(bx, yv[a], val);
                     gx = fma(dx, yv[a], gx);
                     gy = fma(bx, yd[a], gy);
                 }
-                const double jxw = wy * T.w[qx];
+                const double jxw = T.W[qy][qx];
                 double coup = 0.0;
                 if (MODE == M_FULL && cpl)
                     coup = t00[qx] * w00[qx] + t01[qx] * (w01[qx] + w10[qx]) + t11[qx] * w11[qx];
@@ -389,7 +398,7 @@ __device__ __forceinline__ void cell_q2_rows(Load&& load, const double* __restri
                 const double Gx = jxw * K.k_phi * gx, Gy = jxw * K.k_phi * gy;
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    const double dx = T.D[qx][a] * K.ih[0], bx = T.B[qx][a];
+                    const double dx = T.Dx[qx][a], bx = T.B[qx][a];
                     tv[kp][a] = fma(bx, F, fma(dx, Gx, tv[kp][a]));
                     td[kp][a] = fma(bx, Gy, td[kp][a]);
                 }
