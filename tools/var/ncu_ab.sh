@@ -6,7 +6,7 @@ K=$1; shift
 for v in tools/var/lib_*.so; do
   cp $v $LIB
   for args in "$@"; do
-    ncu --metrics gpu__time_duration.sum --clock-control none -k regex:$K --csv python tools/kbench.py $args --reps 12 2>/dev/null \
+    ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"$K" --csv python tools/kbench.py $args --reps 12 2>/dev/null \
       | python -c "
 import sys,csv
 r=[x for x in csv.reader(sys.stdin) if len(x)>10 and x[-3]=='gpu__time_duration.sum']
