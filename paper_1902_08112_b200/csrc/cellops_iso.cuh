@@ -347,4 +347,94 @@ __device__ __forceinline__ void cell_kernel_iso(const double (&cv)[ModeInfo<D, M
     }
 }
 
+// JxW-scaled a_phiphi of the 4 QPs of a 2D isotropic cell from the corners of
+// U's displacement (cu0, cu1): the phi-block coefficient of _build_caches
+// (model.py:304-308), with the exact arithmetic of cell_kernel_iso's state
+// part (so a table of it reproduces the on-the-fly operator bit for bit).
+template <bool RHO>
+__device__ __forceinline__ void phi_coef2(const double (&cu0)[4], const double (&cu1)[4],
+                                          const double* __restrict__ rho_q, const Consts& K, const IsoK& I,
+                                          double (&aj)[4]) {
+    constexpr int D = 2, NP = 4, NR = 2;
+    using S = SFr<D>;
+    double rr[D][D][NR];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        S::deriv(cu0, j, rr[0][j], K);
+        S::deriv(cu1, j, rr[1][j], K);
+    }
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        double r[D][D];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) r[i][j] = rr[i][j][drop_bit(q, j)];
+        double dv = r[0][0];
+#pragma unroll
+        for (int i = 1; i < D; ++i) dv += r[i][i];
+        const double ld = I.lam * dv;
+        double e2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const double sd = fma(I.two_mu, r[i][i], ld);
+            e2 = fma(sd, r[i][i], e2);
+        }
+        {
+            const double sv = r[0][1] + r[1][0];
+            const double so = I.mu * sv;
+            e2 = fma(so, sv, e2);
+        }
+        const double ce = RHO ? I.cS * __ldg(rho_q + q) : I.cS;
+        aj[q] = fma(ce, e2, fma(I.cdiv, dv, I.c0));
+    }
+}
+
+// Block-diagonal operator (FULL without G_phiu) of a 2D isotropic cell with
+// the phi-block coefficient read from the per-QP table (tq[q * tstride]):
+// cv = {v_0, v_1, v_phi, phi_tilde} -- U is not needed at all.  Same
+// arithmetic as cell_kernel_iso<2, M_FULL> with nocoup.
+template <bool RHO>
+__device__ __forceinline__ void cell_bd_tab2(const double (&cv)[4][4], const double* __restrict__ rho_q,
+                                             const double* __restrict__ tq, int64_t tstride, const Consts& K,
+                                             const IsoK& I, double (&o)[3][4]) {
+    using S = SFr<2>;
+    {
+        const double cu[3][4] = {{cv[0][0], cv[0][1], cv[0][2], cv[0][3]},
+                                 {cv[1][0], cv[1][1], cv[1][2], cv[1][3]},
+                                 {cv[3][0], cv[3][1], cv[3][2], cv[3][3]}};
+        double ou[2][4];
+        cell_kernel_iso<2, M_UBLK, RHO>(cu, rho_q, K, I, ou);
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int n = 0; n < 4; ++n) o[k][n] = ou[k][n];
+    }
+    double f[4];
+    S::value(cv[2], f, K);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f[q] = fma(__ldg(tq + q * tstride), f[q], 0.0);
+    mass_transpose<2>(f, K);
+    corner_laplacian<2>(cv[2], I, f);
+#pragma unroll
+    for (int n = 0; n < 4; ++n) o[2][n] = f[n];
+}
+
+// Phi block of a 2D isotropic cell with a_phiphi from the per-QP table
+// (same arithmetic as cell_kernel_iso<2, M_PBLK>): only v is staged.
+__device__ __forceinline__ void cell_pblk_tab2(const double (&cv)[1][4], const double* __restrict__ tq,
+                                               int64_t tstride, const Consts& K, const IsoK& I,
+                                               double (&o)[1][4]) {
+    using S = SFr<2>;
+    double f[4];
+    S::value(cv[0], f, K);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f[q] = __ldg(tq + q * tstride) * f[q];
+    mass_transpose<2>(f, K);
+    corner_laplacian<2>(cv[0], I, f);
+#pragma unroll
+    for (int n = 0; n < 4; ++n) o[0][n] = f[n];
+}
+
 }  // namespace pffmg
+

@@ -171,7 +171,10 @@ struct RowAddr {
     }
 };
 
-template <int MODE, int EPI, int NW, bool ISO, bool RHO, bool BOX, bool PRE, bool MIE = false>
+// TAB (isotropic NoSplit; FULL mode only with nocoup): the block-diagonal
+// operator / the phi block with a_phiphi read from the per-QP table A.ptab --
+// U is not staged.
+template <int MODE, int EPI, int NW, bool ISO, bool RHO, bool BOX, bool PRE, bool MIE = false, bool TAB = false>
 #ifndef PFFMG_MINB_FULL
 #define PFFMG_MINB_FULL 4
 #endif
@@ -183,7 +186,9 @@ op2dw_kernel(const OpArgs A) {
     pdl_wait();
     constexpr int D = 2, NP = 4;
     using MI = ModeInfo<D, MODE, MIE>;
-    constexpr int NF = MI::NF, NCO = MI::NCO, NV = MI::NV;
+    static_assert(!TAB || ((MODE == M_FULL || MODE == M_PBLK) && ISO && !MIE),
+                  "the table path is the isotropic block-diagonal operator or phi block");
+    constexpr int NF = TAB ? (MODE == M_FULL ? MI::NV + 1 : MI::NV) : MI::NF, NCO = MI::NCO, NV = MI::NV;
     constexpr int RING = 4, W = 32, SLOT = NF * W;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -205,9 +210,13 @@ op2dw_kernel(const OpArgs A) {
     const double* fsrc[NF];
 #pragma unroll
     for (int i = 0; i < NV; ++i) fsrc[MI::F_V + i] = A.v + (int64_t)i * L.V;
+    if constexpr (TAB) {
+        if constexpr (MODE == M_FULL) fsrc[NV] = A.pt;
+    } else {
 #pragma unroll
-    for (int i = 0; i < MI::NU; ++i) fsrc[MI::F_U + i] = A.U + (int64_t)i * L.V;
-    if (MI::PT) fsrc[MI::F_PT] = A.pt;
+        for (int i = 0; i < MI::NU; ++i) fsrc[MI::F_U + i] = A.U + (int64_t)i * L.V;
+        if (MI::PT) fsrc[MI::F_PT] = A.pt;
+    }
 
     // Stage row y into the ring slot (one column per lane); the lane's own
     // constraint byte of that row comes back in a register (a plain load: it
@@ -294,7 +303,7 @@ op2dw_kernel(const OpArgs A) {
                 cv[i][2] = r1[i * W + ll];
                 cv[i][3] = r1[i * W + ll + 1];
             }
-            if constexpr (MODE == M_FULL) {      // block-diagonal operator: no G_phiu coupling
+            if constexpr (MODE == M_FULL && !TAB) {   // block-diagonal operator: no G_phiu coupling
                 if (A.nocoup) {                  // (T_phiu = 0 when phi(U) reads 0, model.py:299-303)
 #pragma unroll
                     for (int n = 0; n < NP; ++n) cv[MI::F_U + D][n] = 0.0;
@@ -302,7 +311,11 @@ op2dw_kernel(const OpArgs A) {
             }
             const int64_t lc = cell ? ((int64_t)cx + (int64_t)L.nx * cy) : 0;   // rho row of a real cell
             const double* rq = RHO ? A.rho + lc * NP : nullptr;
-            if constexpr (MIE) {   // spectral split: modulus field resolved at run time
+            if constexpr (TAB && MODE == M_FULL) {
+                cell_bd_tab2<RHO>(cv, rq, A.ptab + lc, (int64_t)L.nx * L.ny, A.K, A.I, o);
+            } else if constexpr (TAB) {
+                cell_pblk_tab2(cv, A.ptab + lc, (int64_t)L.nx * L.ny, A.K, A.I, o);
+            } else if constexpr (MIE) {   // spectral split: modulus field resolved at run time
                 cell_kernel_miehe2<MODE>(cv, A.rho ? A.rho + lc * NP : nullptr, A.K, o);
             } else {
                 if (ISO)

@@ -42,9 +42,10 @@ static int fill_args(const pffmg_lattice* lat, const pffmg_state* st, OpArgs* A)
     A->pt = st->phi_tilde;
     A->rho = st->rho;
     A->flags = st->flags;
-    // the a_phiphi table serves the phi block of 3D isotropic NoSplit Q1 lattices only
-    const bool iso3 = A->L.dim == 3 && A->L.order == 1 && A->L.hx == A->L.hy && A->L.hz == A->L.hx;
-    A->ptab = (st->phi_coef && iso3 && st->split == 0) ? st->phi_coef : nullptr;
+    // the a_phiphi table serves the phi block of isotropic NoSplit Q1 lattices
+    // (3D phi block; 2D block-diagonal smoother)
+    const bool iso = A->L.order == 1 && A->L.hx == A->L.hy && (A->L.dim == 2 || A->L.hz == A->L.hx);
+    A->ptab = (st->phi_coef && iso && st->split == 0) ? st->phi_coef : nullptr;
     A->premasked = (st->hints & PFFMG_HINT_PREMASKED) ? 1 : 0;
     A->ends = (st->hints & PFFMG_HINT_ENDS) ? 1 : 0;
     if (A->ends) {
@@ -87,10 +88,13 @@ extern "C" int pffmg_phi_coef(const pffmg_lattice* lat, const pffmg_state* st, d
     int rc = fill_args(lat, st, &A);
     if (rc) return rc;
     PFFMG_REQUIRE(out && A.U, "pffmg_phi_coef: needs U and out");
-    PFFMG_REQUIRE(A.L.dim == 3 && A.L.order == 1 && A.L.hx == A.L.hy && A.L.hz == A.L.hx && A.split == 0,
-                  "pffmg_phi_coef: 3D isotropic Q1 NoSplit lattices only");
+    PFFMG_REQUIRE(A.L.order == 1 && A.L.hx == A.L.hy && (A.L.dim == 2 || A.L.hz == A.L.hx) && A.split == 0,
+                  "pffmg_phi_coef: isotropic Q1 NoSplit lattices only");
     PFFMG_REQUIRE(out != st->phi_coef, "pffmg_phi_coef: out aliases state.phi_coef");
-    launch_phi_coef3(A, out, as_stream(stream));
+    if (A.L.dim == 3)
+        launch_phi_coef3(A, out, as_stream(stream));
+    else
+        launch_phi_coef2(A, out, as_stream(stream));
     return check_launch("pffmg_phi_coef");
 }
 
