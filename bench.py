@@ -427,7 +427,7 @@ def run_gpu(args):
                          else "per rank: pinned H2D of the slab, halo exchange + vmult, D2H; bytes per rank")},
         # our kernels per step: the fused vmult; on a slab (N > 1) the interior rows
         # and, after the halo lands, the two boundary rows
-        "gpu_launches": args.steps * (2 if ws > 1 else 1),
+        "gpu_launches": args.steps * (1 if ws == 1 else (3 if getattr(mesh, "order", 1) == 2 else 2)),
         "solve": solve,
         "wall_s_timed_region": wall,
         "step_ms_min_max": [float(np.min(step_ms)), float(np.max(step_ms))],
