@@ -253,6 +253,35 @@ def lanczos_extremes(scal_host, n_iters):
     return SpectrumEstimate(float(ev[0]), float(ev[-1]), fallback=False)
 
 
+def lanczos_extremes_batch(scal_rows, n_iters):
+    """lanczos_extremes of many CG runs at once: the tridiagonals of equal size
+    go through one batched eigvalsh (numpy loops LAPACK over the stack, so every
+    result equals the one-by-one call); the T entries use the same formulas."""
+    rows = np.asarray(scal_rows, dtype=np.float64)
+    out = [None] * len(rows)
+    groups = {}
+    for i, r in enumerate(rows):
+        k = int(r[4])
+        if k < 2:
+            out[i] = SpectrumEstimate(1.0, 1.0, fallback=True)
+        else:
+            groups.setdefault(k, []).append(i)
+    for k, idx in groups.items():
+        a = rows[idx][:, 8:8 + k]
+        b = rows[idx][:, 8 + CG_MAXIT:8 + CG_MAXIT + k - 1]
+        T = np.zeros((len(idx), k, k))
+        T[:, 0, 0] = 1.0 / a[:, 0]
+        for i in range(1, k):
+            T[:, i, i] = 1.0 / a[:, i] + b[:, i - 1] / a[:, i - 1]
+            off = np.sqrt(b[:, i - 1]) / a[:, i - 1]
+            T[:, i, i - 1] = off
+            T[:, i - 1, i] = off
+        ev = np.linalg.eigvalsh(T)
+        for j, i in enumerate(idx):
+            out[i] = SpectrumEstimate(float(ev[j, 0]), float(ev[j, -1]), fallback=False)
+    return out
+
+
 def cg_lanczos_dev(apply_into, diag, b, n_iters, keep_host=True):
     """Device Jacobi-PCG; apply_into(src, dst) computes dst = A src."""
     if n_iters > CG_MAXIT:

@@ -30,7 +30,7 @@ import torch
 from . import _lib
 from .arrays import DeviceCallable, dev, empty, flags_buffer, host, is_tensor, like, pack_flags, zeros
 from .fem import Discretization
-from .krylov import cg_lanczos_dev, estimate_spectrum, lanczos_extremes, probe_vector
+from .krylov import cg_lanczos_dev, estimate_spectrum, lanczos_extremes, lanczos_extremes_batch, probe_vector
 from .model import DeviceMask, LinearizationState, PhaseFieldOperator
 
 __all__ = ["ChebyshevMode", "ChebyshevParams", "PreconditionerKind", "LevelContext",
@@ -447,8 +447,8 @@ class _Session:
             scal = self.scal
         scal_host = host(scal)                             # one sync for all levels
         ei = self.eig_iters
-        self.spectra = [tuple(lanczos_extremes(scal_host[2 * l + k], ei) for k in range(2))
-                        for l in range(L)]
+        sp = lanczos_extremes_batch(scal_host, ei)
+        self.spectra = [(sp[2 * l], sp[2 * l + 1]) for l in range(L)]
         self.gen += 1
         contexts = []
         for l in range(L):

@@ -34,3 +34,21 @@ def test_active_set_bit_exact(name):
                                  dirichlet_flags=g[f"{name}/{k}/dflags"] if k == 2 else None)
         assert got.dtype == bool
         assert np.array_equal(got, g[f"{name}/{k}/active"])
+
+
+def test_lanczos_batch_equals_one_by_one():
+    """Batched spectrum extraction (the setup's one host step) is bit-identical
+    to the per-run lanczos_extremes (krylov.py:187-198), fallbacks included."""
+    from paper_1902_08112_b200.krylov import CG_MAXIT, lanczos_extremes, lanczos_extremes_batch
+    rng = np.random.default_rng(7)
+    rows = []
+    for k in (10, 10, 7, 1, 10, 3, 0, 2, 10):
+        r = np.zeros(8 + 2 * CG_MAXIT)
+        r[4], r[5] = k, max(k - 1, 0)
+        r[8:8 + k] = rng.uniform(0.1, 2.0, k)
+        r[8 + CG_MAXIT:8 + CG_MAXIT + max(k - 1, 0)] = rng.uniform(0.01, 1.0, max(k - 1, 0))
+        rows.append(r)
+    one = [lanczos_extremes(r, 10) for r in rows]
+    batch = lanczos_extremes_batch(np.array(rows), 10)
+    for a, b in zip(one, batch):
+        assert (a.lambda_min_hat, a.lambda_max_hat, a.fallback) == (b.lambda_min_hat, b.lambda_max_hat, b.fallback)
