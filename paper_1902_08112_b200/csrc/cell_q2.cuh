@@ -235,6 +235,48 @@ __device__ __forceinline__ void cell_q2(const double (&cv)[ModeInfo<2, MODE, MIE
 }
 
 
+// a_phiphi (model.py:304-308) of the 9 QPs of a Q2 cell from the nine-node
+// U displacement (u0, u1): the arithmetic of cell_q2_rows' state part, so a
+// table of it reproduces the on-the-fly phi block bit for bit.
+__device__ __forceinline__ void phi_coef_q2(const double (&u0)[9], const double (&u1)[9],
+                                            const double* __restrict__ rho_q, const Consts& K, const Q2Tab& T,
+                                            double (&aq)[9]) {
+#pragma unroll 1
+    for (int qy = 0; qy < 3; ++qy) {
+        double By[3], Dy[3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            By[b] = T.B[qy][b];
+            Dy[b] = T.Dy[qy][b];
+        }
+        double y0v[3], y0d[3], y1v[3], y1d[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            y0v[a] = fma(By[0], u0[a], fma(By[1], u0[a + 3], By[2] * u0[a + 6]));
+            y0d[a] = fma(Dy[0], u0[a], fma(Dy[1], u0[a + 3], Dy[2] * u0[a + 6]));
+            y1v[a] = fma(By[0], u1[a], fma(By[1], u1[a + 3], By[2] * u1[a + 6]));
+            y1d[a] = fma(Dy[0], u1[a], fma(Dy[1], u1[a + 3], Dy[2] * u1[a + 6]));
+        }
+#pragma unroll
+        for (int qx = 0; qx < 3; ++qx) {
+            double u0x = 0, u0y = 0, u1x = 0, u1y = 0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double dx = T.Dx[qx][a], bx = T.B[qx][a];
+                u0x = fma(dx, y0v[a], u0x);
+                u0y = fma(bx, y0d[a], u0y);
+                u1x = fma(dx, y1v[a], u1x);
+                u1y = fma(bx, y1d[a], u1y);
+            }
+            const double ea = u0x, ec = u1y, eb = 0.5 * (u0y + u1x);
+            const double rho = rho_q ? __ldg(rho_q + 3 * qy + qx) : 1.0;
+            const double div = ea + ec;
+            const double Ep = 0.5 * K.lam * div * div + K.mu * (ea * ea + 2.0 * eb * eb + ec * ec);
+            aq[3 * qy + qx] = K.omk * rho * Ep + K.two_p * div + K.gc_over_eps;
+        }
+    }
+}
+
 // Row-factorised NoSplit cell kernel for the hot modes (FULL / UBLK / PBLK):
 // the 9 QPs are processed one QP row (fixed qy) at a time; every nodal field
 // is first contracted along y for that row (6 values), then evaluated at the
@@ -242,15 +284,19 @@ __device__ __forceinline__ void cell_q2(const double (&cv)[ModeInfo<2, MODE, MIE
 // half the flops of the per-QP evaluation, and no 9 x NF corner array held in
 // registers (fields are re-read through `load(f, c)`, an L1 hit).
 // nocoup: FULL without the G_phiu coupling (block-diagonal operator).
-template <int MODE, class Load>
+// TAB: a_phiphi of the 9 QPs from the per-QP table (tq[q * tstride], q = 3 qy + qx,
+// pffmg_phi_coef) -- the phi block and the block-diagonal operator (nocoup)
+// then need no state strain.
+template <int MODE, bool TAB = false, class Load>
 __device__ __forceinline__ void cell_q2_rows(Load&& load, const double* __restrict__ rho_q, const Consts& K,
                                              const Q2Tab& T, bool nocoup,
-                                             double (&o)[ModeInfo<2, MODE>::NCO][9]) {
+                                             double (&o)[ModeInfo<2, MODE>::NCO][9],
+                                             const double* __restrict__ tq = nullptr, int64_t tstride = 0) {
     using MI = ModeInfo<2, MODE>;
     constexpr int NCO = MI::NCO;
     constexpr bool HAS_U = MODE == M_FULL || MODE == M_UBLK;
     constexpr bool HAS_P = MODE == M_FULL || MODE == M_PBLK;
-    constexpr bool NEED_STRAIN = MODE == M_FULL || MODE == M_PBLK;
+    constexpr bool NEED_STRAIN = (MODE == M_FULL || MODE == M_PBLK) && !TAB;
 #pragma unroll
     for (int k = 0; k < NCO; ++k)
 #pragma unroll
@@ -323,6 +369,7 @@ __device__ __forceinline__ void cell_q2_rows(Load&& load, const double* __restri
         for (int qx = 0; qx < 3; ++qx) {
             const double rho = rho_q ? __ldg(rho_q + 3 * qy + qx) : 1.0;
             gr[qx] *= rho;
+            if (TAB) aq[qx] = __ldg(tq + (3 * qy + qx) * tstride);
             if (NEED_STRAIN) {
                 const double div = ea[qx] + ec[qx];
                 const double Ep = 0.5 * K.lam * div * div +

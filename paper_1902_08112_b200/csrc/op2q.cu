@@ -19,7 +19,8 @@ namespace pffmg {
 #define PFFMG_Q2_MINB 3
 #endif
 
-template <int MODE, int EPI, bool MIE>
+// TAB: the phi block / block-diagonal operator with a_phiphi from the per-QP table.
+template <int MODE, int EPI, bool MIE, bool TAB = false>
 __global__ void __launch_bounds__(128, MODE == M_FULL ? 2 : PFFMG_Q2_MINB) op2q_kernel(const OpArgs A, const Q2Tab T) {
     pdl_wait();
     using MI = ModeInfo<2, MODE, MIE>;
@@ -69,7 +70,10 @@ __global__ void __launch_bounds__(128, MODE == M_FULL ? 2 : PFFMG_Q2_MINB) op2q_
                 }
             };
             const double* rq = A.rho ? A.rho + ((int64_t)cx + (int64_t)L.nx * cy) * 9 : nullptr;
-            if constexpr (ROWS) cell_q2_rows<MODE>(load, rq, A.K, T, A.nocoup != 0, o);
+            if constexpr (ROWS)
+                cell_q2_rows<MODE, TAB>(load, rq, A.K, T, A.nocoup != 0, o,
+                                        TAB ? A.ptab + ((int64_t)cx + (int64_t)L.nx * cy) : nullptr,
+                                        (int64_t)L.nx * L.ny);
         } else if (cell) {
             double cv[NF][9];
 #pragma unroll
@@ -138,9 +142,9 @@ __global__ void __launch_bounds__(128, MODE == M_FULL ? 2 : PFFMG_Q2_MINB) op2q_
 }
 
 // One wave of resident warps (see op2d.cu): strips of `per` cell rows.
-template <int MODE, int EPI, bool MIE>
+template <int MODE, int EPI, bool MIE, bool TAB = false>
 static void launch_q(const OpArgs& A0, int nseg, int rows, const Q2Tab& T, cudaStream_t s) {
-    auto kern = op2q_kernel<MODE, EPI, MIE>;
+    auto kern = op2q_kernel<MODE, EPI, MIE, TAB>;
     static int occ = 0;
     if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0) != cudaSuccess || occ < 1))
         occ = 1;
@@ -165,10 +169,52 @@ int launch2q(const OpArgs& A, cudaStream_t s) {
     const int nseg = (L.nx + 1 + 30) / 31;
     const int rows = ((L.own_hi + 1) >> 1) - (L.own_lo >> 1);
     const Q2Tab T = make_q2_host(L.hx, L.hy);
+    if constexpr (MODE == M_PBLK || MODE == M_FULL) {
+        // phi block / block-diagonal operator: a_phiphi from the table (no state strain)
+        if (!A.split && A.ptab && (MODE == M_PBLK || A.nocoup)) {
+            launch_q<MODE, EPI, false, true>(A, nseg, rows, T, s);
+            return PFFMG_OK;
+        }
+    }
     if (A.split)
         launch_q<MODE, EPI, true>(A, nseg, rows, T, s);
     else
         launch_q<MODE, EPI, false>(A, nseg, rows, T, s);
+    return PFFMG_OK;
+}
+
+// Per-QP a_phiphi table of a Q2 level (model.py:304-308), QP-major:
+// tab[q * C + c], q = 3 qy + qx, c = cx + nx cy, C = nx ny.
+__global__ void __launch_bounds__(256) phi_coefq_kernel(const OpArgs A, const Q2Tab T, double* __restrict__ tab) {
+    pdl_wait();
+    const Lat& L = A.L;
+    const int64_t C = (int64_t)L.nx * L.ny;
+    const int nxn = 2 * L.nx + 1;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int cx = (int)(c % L.nx), cy = (int)(c / L.nx);
+        const int64_t id0 = (int64_t)(2 * cy) * nxn + 2 * cx;
+        double u0[9], u1[9], aq[9];
+#pragma unroll
+        for (int n = 0; n < 9; ++n) {
+            const int64_t id = id0 + (n / 3) * nxn + n % 3;
+            u0[n] = __ldg(A.U + id);
+            u1[n] = __ldg(A.U + L.V + id);
+        }
+        phi_coef_q2(u0, u1, A.rho ? A.rho + c * 9 : nullptr, A.K, T, aq);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) tab[q * C + c] = aq[q];
+    }
+}
+
+int launch_phi_coefq(const OpArgs& A, double* tab, cudaStream_t s) {
+    const int64_t C = (int64_t)A.L.nx * A.L.ny;
+    int64_t blocks = (C + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    const Q2Tab T = make_q2_host(A.L.hx, A.L.hy);
+    pdl_launch(phi_coefq_kernel, dim3((unsigned)blocks), dim3(256), 0, s, A, T, tab);
     return PFFMG_OK;
 }
 

@@ -25,6 +25,7 @@ int launch2q(const OpArgs& A, cudaStream_t s);    // Q2 lattices (op2q.cu)
 
 int launch_phi_coef3(const OpArgs& A, double* tab, cudaStream_t s);   // op3d.cu
 int launch_phi_coef2(const OpArgs& A, double* tab, cudaStream_t s);   // op2d.cu
+int launch_phi_coefq(const OpArgs& A, double* tab, cudaStream_t s);   // op2q.cu
 
 #define PFFMG_INST2(F, M, E) template int F<M, E>(const OpArgs&, cudaStream_t);
 #define PFFMG_INSTANTIATE_LAUNCH2(F)                                                         \

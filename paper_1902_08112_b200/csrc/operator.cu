@@ -45,7 +45,7 @@ static int fill_args(const pffmg_lattice* lat, const pffmg_state* st, OpArgs* A)
     // the a_phiphi table serves the phi block of isotropic NoSplit Q1 lattices
     // (3D phi block; 2D block-diagonal smoother)
     const bool iso = A->L.order == 1 && A->L.hx == A->L.hy && (A->L.dim == 2 || A->L.hz == A->L.hx);
-    A->ptab = (st->phi_coef && iso && st->split == 0) ? st->phi_coef : nullptr;
+    A->ptab = (st->phi_coef && (iso || A->L.order == 2) && st->split == 0) ? st->phi_coef : nullptr;
     A->premasked = (st->hints & PFFMG_HINT_PREMASKED) ? 1 : 0;
     A->ends = (st->hints & PFFMG_HINT_ENDS) ? 1 : 0;
     if (A->ends) {
@@ -88,10 +88,12 @@ extern "C" int pffmg_phi_coef(const pffmg_lattice* lat, const pffmg_state* st, d
     int rc = fill_args(lat, st, &A);
     if (rc) return rc;
     PFFMG_REQUIRE(out && A.U, "pffmg_phi_coef: needs U and out");
-    PFFMG_REQUIRE(A.L.order == 1 && A.L.hx == A.L.hy && (A.L.dim == 2 || A.L.hz == A.L.hx) && A.split == 0,
-                  "pffmg_phi_coef: isotropic Q1 NoSplit lattices only");
+    PFFMG_REQUIRE(A.split == 0 && (A.L.order == 2 || (A.L.hx == A.L.hy && (A.L.dim == 2 || A.L.hz == A.L.hx))),
+                  "pffmg_phi_coef: NoSplit Q2 or isotropic Q1 lattices only");
     PFFMG_REQUIRE(out != st->phi_coef, "pffmg_phi_coef: out aliases state.phi_coef");
-    if (A.L.dim == 3)
+    if (A.L.order == 2)
+        launch_phi_coefq(A, out, as_stream(stream));
+    else if (A.L.dim == 3)
         launch_phi_coef3(A, out, as_stream(stream));
     else
         launch_phi_coef2(A, out, as_stream(stream));

@@ -191,19 +191,20 @@ class PhaseFieldOperator:
         self._st_ends = st_ends
         self._stp_ends = ctypes.byref(st_ends)
         # per-QP a_phiphi of the phi block, cached like _build_caches does
-        # (model.py:260, 304-308): isotropic NoSplit Q1 levels (3D phi block,
-        # 2D block-diagonal smoother)
+        # (model.py:260, 304-308): NoSplit Q2 and isotropic Q1 levels (phi
+        # block, block-diagonal smoother)
         self._ptab = None
         info = self.lat.info
         h = np.asarray(info.h, float)
-        if (getattr(info, "order", 1) == 1 and code == 0 and np.all(h == h[0])
+        order = getattr(info, "order", 1)
+        if (code == 0 and (order == 2 or np.all(h == h[0]))
                 and os.environ.get("PFFMG_PHI_TABLE", "1") != "0"):
             if _ptab is not None:            # a table already built from this state (mgsolve._Session)
                 self._ptab = _ptab
                 for st in (self._st, self._st_pre, self._st_ends):
                     st.phi_coef = _ptab.data_ptr()
             else:
-                self._ptab = empty((1 << self.dim) * self.lat.n_lattice_cells)
+                self._ptab = empty((9 if order == 2 else 1 << self.dim) * self.lat.n_lattice_cells)
                 self.build_phi_coef()
 
     def build_phi_coef(self):
