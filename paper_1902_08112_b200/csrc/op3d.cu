@@ -96,7 +96,9 @@ static int launch_stream(const OpArgs& A, cudaStream_t s) {
     const double frac = std::min(1.0, (double)L.V / ((double)(L.nx + 1) * (L.ny + 1) * (L.nz + 1)));
     constexpr int ROWS = TY3T + 1;
     const bool tab = MODE == M_PBLK && A.ptab != nullptr;
-    const size_t smem = sizeof(double) * (4 * (tab ? MI::NV : MI::NF) * ROWS * 32 + TY3T * MI::NCO * 2 * 32) +
+    const size_t smem = sizeof(double) * (4 * (tab ? MI::NV : MI::NF) * ROWS * 32 + TY3T * MI::NCO * 2 * 32 +
+                                          ((MODE == M_UBLK || (MODE == M_FULL && (EPI == E_CHEB || EPI == E_CHEB0)))
+                                               ? 32 * TY3T * EpiIn<MI::NCO, EPI>::NL * MI::NCO : 0)) +
                         4 * ROWS * 48 + 4 * ROWS * sizeof(int);
     const bool rho = A.rho != nullptr, box = L.vrow_off == nullptr, pre = A.premasked != 0;
 #define PFFMG_T(R, B, P, T) launch_t<MODE, EPI, R, B, P, T>(A, gx, gy, planes, frac, smem, s)

@@ -30,7 +30,13 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* sv = reinterpret_cast<double*>(smem_raw);                          // [RING][NF][ROWS][W]
     double* sy = sv + RING * SLOT;                                              // [TY][NCO][2][W]
-    unsigned char* sfl = reinterpret_cast<unsigned char*>(sy + TY * NCO * 2 * W);  // [RING][ROWS][FB]
+    // epilogue operands staged in shared memory where a register prefetch
+    // spills (u block, and the Chebyshev variants of FULL); elsewhere they
+    // stay in registers (ncu: staging costs the table phi block and RESID ~4%)
+    constexpr bool STAGE = MODE == M_UBLK || (MODE == M_FULL && (EPI == E_CHEB || EPI == E_CHEB0));
+    constexpr int NLE = STAGE ? EpiIn<NCO, EPI>::NL : 0;                        // staged epilogue operands
+    double* sepi = sy + TY * NCO * 2 * W;                                       // [32 TY][NLE][NCO]
+    unsigned char* sfl = reinterpret_cast<unsigned char*>(sepi + 32 * TY * NLE * NCO);  // [RING][ROWS][FB]
     int* sfo = reinterpret_cast<int*>(sfl + RING * ROWS * FB);                 // [RING][ROWS]
 
     const Lat& L = A.L;
@@ -173,8 +179,10 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
         const int s0 = it & 3, s1 = (it + 1) & 3;
         // vertex finalised this iteration and its epilogue operands (loaded early)
         const int vid_f = (w >= 1 && cz >= vz0 && lane >= 1 && lane <= 30) ? vid_of(cx, w, cz) : -1;
+        double* eslot = sepi + tid * (NLE * NCO);
         EpiIn<NCO, EPI> ein;
-        if (vid_f >= 0) epi_load<NCO, EPI>(A, vid_f, ein);
+        if (STAGE && vid_f >= 0) epi_stage<NCO, EPI>(A, vid_f, eslot);   // committed with the plane below
+        if (!STAGE && vid_f >= 0) epi_load<NCO, EPI>(A, vid_f, ein);
         if (cz + 4 <= vz1 + 1) fetch_rows(cz + 4);     // committed with the plane below
         if (cz + 2 <= vz1)
             issue(cz + 2, (it + 2) & 3);
@@ -241,6 +249,10 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
             if (vid_f >= 0) {
                 const int vid = vid_f;
                 const unsigned fl = flag(s0, w, lane);
+                if (STAGE && NLE > 0) {
+                    cp_async_wait<0>();          // this thread's staged operands (issued at the step's start)
+                    epi_unstage<NCO, EPI>(eslot, ein);
+                }
                 double vin[NCO];
 #pragma unroll
                 for (int k = 0; k < NCO; ++k) {

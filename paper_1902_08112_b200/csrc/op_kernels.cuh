@@ -77,6 +77,38 @@ __device__ __forceinline__ void epi_load(const OpArgs& A, int64_t vid, EpiIn<NCO
     }
 }
 
+// The same operands staged into shared memory with cp.async (slot = NL x NCO
+// doubles of the calling thread): the prefetch then holds no registers across
+// the cell work (in the register-capped 3D kernels a register prefetch was
+// spilled, and the spill store waited for the load).
+template <int NCO, int EPI>
+__device__ __forceinline__ void epi_stage(const OpArgs& A, int64_t vid, double* slot) {
+    const int64_t V = A.L.V;
+#pragma unroll
+    for (int k = 0; k < NCO; ++k) {
+        const int64_t g = (int64_t)k * V + vid;
+        if (EPI == E_CHEB) {
+            cp_async8(slot + 0 * NCO + k, A.r + g, true);
+            cp_async8(slot + 1 * NCO + k, A.inv + g, true);
+            cp_async8(slot + 2 * NCO + k, A.x + g, true);
+        } else if (EPI == E_CHEB0) {
+            cp_async8(slot + 0 * NCO + k, A.b + g, true);
+            cp_async8(slot + 1 * NCO + k, A.inv + g, true);
+        } else if (EPI == E_RESID) {
+            cp_async8(slot + 0 * NCO + k, A.b + g, true);
+        }
+    }
+}
+
+template <int NCO, int EPI>
+__device__ __forceinline__ void epi_unstage(const double* slot, EpiIn<NCO, EPI>& e) {
+    constexpr int NL = EpiIn<NCO, EPI>::NL;
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+#pragma unroll
+        for (int k = 0; k < NCO; ++k) e.a[l][k] = slot[l * NCO + k];
+}
+
 // Vertex epilogue (model.py:373-374, 390-391, 412, 459; mgsolve.py:95-111, 227)
 // with the operands from epi_load.
 template <int NCO, int COMP0, int EPI>
