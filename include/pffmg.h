@@ -100,10 +100,11 @@ typedef struct {
     double split_band;          /* MaterialParams.split_band: C^1 blend half-width of the
                                    spectral split (model.py:56-86); 0 = hard split */
     const double* phi_coef;     /* NULL, or the per-QP a_phiphi table of pffmg_phi_coef built
-                                   from this state's U (3D isotropic NoSplit lattices): the
-                                   phi block (which = 1) then reads it instead of
-                                   re-deriving a_phiphi from U (model.py:304-308 cached, as
-                                   _build_caches does).  Ignored on other lattices. */
+                                   from this state's U (NoSplit: isotropic Q1 or Q2
+                                   lattices): the phi block (which = 1) and, in 2D, the
+                                   block-diagonal operator (which = 2) then read it instead
+                                   of re-deriving a_phiphi from U (model.py:304-308 cached,
+                                   as _build_caches does).  Ignored elsewhere. */
     /* flags: V packed constraint bits: bit c <=> dof c*V+v constrained; the
      * buffer must stay readable (any content) up to 4*ceil(V/4) + 40 bytes:
      * kernels read aligned 32-bit words.
@@ -132,11 +133,12 @@ int pffmg_residual(const pffmg_lattice* lat, const pffmg_state* st, int which,
 int pffmg_semilinear_residual(const pffmg_lattice* lat, const pffmg_state* st, double* out,
                               void* stream);
 
-/* Per-QP phi-block coefficient table of a 3D isotropic Q1 NoSplit lattice:
- * out[q * C + c] = JxW * a_phiphi at QP q of lattice cell c (c = cx + nx (cy +
- * ny cz), C = nx ny nz; rho included), the a_phiphi entry of the reference's
- * _build_caches (model.py:270-309, 304-308).  8*C doubles; cells absent from a
- * non-box lattice get 0.  Point state.phi_coef at it afterwards. */
+/* Per-QP phi-block coefficient table of a NoSplit lattice (isotropic Q1 in 2D
+ * or 3D, or Q2): out[q * C + c] = a_phiphi at QP q of lattice cell c (c = cx +
+ * nx (cy + ny cz), C = lattice cells; Q1: JxW and rho included, Q2: rho
+ * included), the a_phiphi entry of the reference's _build_caches
+ * (model.py:270-309, 304-308).  2^dim * C (Q1) or 9 * C (Q2) doubles; cells
+ * absent from a non-box lattice get 0.  Point state.phi_coef at it afterwards. */
 int pffmg_phi_coef(const pffmg_lattice* lat, const pffmg_state* st, double* out, void* stream);
 
 /* Exact operator diagonal, constrained entries = 1.0 (model.py:394-413). */
