@@ -125,15 +125,26 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
     };
 
     // stage plane z into slot: row rr of the tile (rr = 0..TY), column = lane
+    // Without PRE the staged v entries of constrained dofs read 0 (fem.py:205-206).
+    // Each thread masks exactly the entries it copied itself, with their flag
+    // bytes loaded into registers at issue time: the masking then needs only the
+    // thread's own cp.async wait, and the next plane barrier publishes it.
+    constexpr bool OWNMASK = !PRE && NV > 0;
+    constexpr int EPT = (ROWS * W + 32 * TY - 1) / (32 * TY);   // staged entries per thread
+    unsigned ifl[EPT];                                          // flags of the last issued plane
     auto issue = [&](int z, int slot) {
         double* dst = sv + slot * SLOT;
-        for (int e = tid; e < ROWS * W; e += 32 * TY) {
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+            const int e = tid + j * 32 * TY;
+            if (e >= ROWS * W) break;
             const int rr = e / W, col = e % W;
             const int vid = vid_of(x0 + col, rr, z);
             const bool ok = vid >= 0;
             const int off = ok ? vid : 0;
 #pragma unroll
             for (int f = 0; f < NF; ++f) cp_async8(dst + (f * ROWS + rr) * W + col, fsrc[f] + off, ok);
+            if (OWNMASK) ifl[j] = ok ? (unsigned)__ldg(A.flags + off) : 0u;
         }
         for (int e = tid; e < ROWS * 9; e += 32 * TY) {
             const int rr = e / 9, k = e % 9;
@@ -150,15 +161,17 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
     auto flag = [&](int slot, int rr, int col) -> unsigned {
         return sfl[(slot * ROWS + rr) * FB + sfo[slot * ROWS + rr] + col];
     };
-    auto mask_plane = [&](int slot) {            // fem.py:205-206, once per staged vertex
-        if (PRE || NV == 0) return;
+    auto mask_own = [&](int slot, const unsigned (&fl)[EPT]) {   // after this thread's cp.async wait
+        if (!OWNMASK) return;
         double* p = sv + slot * SLOT;
-        for (int e = tid; e < ROWS * W; e += 32 * TY) {
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+            const int e = tid + j * 32 * TY;
+            if (e >= ROWS * W) break;
             const int rr = e / W, col = e % W;
-            const unsigned fl = flag(slot, rr, col);
 #pragma unroll
             for (int i = 0; i < NV; ++i)
-                if ((fl >> (MI::COMP0 + i)) & 1) p[(i * ROWS + rr) * W + col] = 0.0;
+                if ((fl[j] >> (MI::COMP0 + i)) & 1) p[(i * ROWS + rr) * W + col] = 0.0;
         }
     };
 
@@ -169,7 +182,17 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
         __syncthreads();
     }
     issue(vz0 - 1, 0);
-    issue(vz0, 1);
+    if (OWNMASK) {
+        unsigned fl0[EPT];
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) fl0[j] = ifl[j];
+        issue(vz0, 1);
+        cp_async_wait<0>();
+        mask_own(0, fl0);
+        mask_own(1, ifl);
+    } else {
+        issue(vz0, 1);
+    }
     double carry[NCO];
 #pragma unroll
     for (int k = 0; k < NCO; ++k) carry[k] = 0.0;
@@ -184,17 +207,13 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
         if (STAGE && vid_f >= 0) epi_stage<NCO, EPI>(A, vid_f, eslot);   // committed with the plane below
         if (!STAGE && vid_f >= 0) epi_load<NCO, EPI>(A, vid_f, ein);
         if (cz + 4 <= vz1 + 1) fetch_rows(cz + 4);     // committed with the plane below
-        if (cz + 2 <= vz1)
+        const bool issued = cz + 2 <= vz1;
+        if (issued)
             issue(cz + 2, (it + 2) & 3);
         else
             cp_async_commit();
         cp_async_wait<1>();                      // planes cz, cz+1 landed (this thread's copies)
-        __syncthreads();                         // ... and everyone else's
-        if (!PRE) {
-            if (it == 0) mask_plane(s0);
-            mask_plane(s1);
-            __syncthreads();
-        }
+        __syncthreads();                         // ... and everyone else's (masked: see the loop end)
 
         const double* p0 = sv + s0 * SLOT;
         const double* p1 = sv + s1 * SLOT;
@@ -265,6 +284,10 @@ __global__ void __launch_bounds__(32 * TY, MODE == M_FULL ? PFFMG_3D_FULL_MINB :
             }
 #pragma unroll
             for (int k = 0; k < NCO; ++k) carry[k] = top[k];
+        }
+        if (OWNMASK && issued) {                 // plane cz+2: masked before the next step's barrier
+            cp_async_wait<0>();
+            mask_own((it + 2) & 3, ifl);
         }
     }
     cp_async_wait<0>();
