@@ -369,28 +369,28 @@ class _Session:
 
     # -- device work of one setup (recorded once, replayed per Newton step)
     def _device_setup(self):
+        """Fine level first: each level's state injection (mgsolve.py:173-186),
+        phi table (_build_caches, model.py:260), diagonal and inverse diagonal go
+        on the main stream, and its two block CG-Lanczos runs start on their own
+        streams right after -- the fine level's chains (the critical path) no
+        longer wait for the coarse levels' setup kernels.  The 2L chains are
+        independent (each stream has its own reduction scratch in libpffmg)."""
         D, s = self.D, _lib.stream()
-        for l in range(self.L - 2, -1, -1):                # mgsolve.py:173-186
-            D.inject_flags_dev(self.flags[l + 1], self.flags[l], l)
-            D.inject_dev(self.U[l + 1], self.U[l], l, self.nc)
-            D.inject_dev(self.P1[l + 1], self.P1[l], l, self.nc)
-            D.inject_dev(self.P2[l + 1], self.P2[l], l, self.nc)
-            D.inject_dev(self.PT[l + 1], self.PT[l], l, 1)
-        for l in range(self.L):
-            self.ops[l].build_phi_coef()                   # _build_caches (model.py:260)
-            self.ops[l].diagonal_dev(self.diag[l])
-            _lib.call("pffmg_reciprocal", _lib.ptr(self.diag[l]), _lib.ptr(self.inv[l]),
-                      self.diag[l].numel(), s)
-        # the 2L block CG-Lanczos runs are independent: one stream per level, so the
-        # latency-bound coarse-level ones overlap the fine level's (each stream has
-        # its own reduction scratch in libpffmg)
-        # (one stream per level AND block: the u and phi chains of a level are
-        # independent too)
         main = torch.cuda.current_stream()
         if self._streams is None:
             self._streams = [torch.cuda.Stream() for _ in range(2 * self.L)]
         scals = [[None, None] for _ in range(self.L)]
         for l in range(self.L - 1, -1, -1):
+            if l < self.L - 1:
+                D.inject_flags_dev(self.flags[l + 1], self.flags[l], l)
+                D.inject_dev(self.U[l + 1], self.U[l], l, self.nc)
+                D.inject_dev(self.P1[l + 1], self.P1[l], l, self.nc)
+                D.inject_dev(self.P2[l + 1], self.P2[l], l, self.nc)
+                D.inject_dev(self.PT[l + 1], self.PT[l], l, 1)
+            self.ops[l].build_phi_coef()
+            self.ops[l].diagonal_dev(self.diag[l])
+            _lib.call("pffmg_reciprocal", _lib.ptr(self.diag[l]), _lib.ptr(self.inv[l]),
+                      self.diag[l].numel(), s)
             for k in range(2):
                 st = self._streams[2 * l + k]
                 st.wait_stream(main)
