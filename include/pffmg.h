@@ -228,6 +228,16 @@ int pffmg_restrict(const pffmg_lattice* coarse, const pffmg_lattice* fine, int n
                    int comp0, const double* vf, double* vc, const uint8_t* coarse_flags,
                    void* stream);
 
+/* V-cycle descent (mgsolve.py:228-229 then 95, 103-106): vc = P^T vf over all
+ * dim+1 components with constrained coarse entries 0, fused with the coarse
+ * level's block-diagonal Chebyshev start from x = 0: r = vc, d = invdiag vc /
+ * theta (theta_u for the displacement block, theta_p for phi; device scalars),
+ * x = d.  Q1 lattices. */
+int pffmg_restrict_init_bd(const pffmg_lattice* coarse, const pffmg_lattice* fine, const double* vf,
+                           double* vc, const uint8_t* coarse_flags, const double* invdiag,
+                           const double* theta_u, const double* theta_p, double* r, double* d,
+                           double* x, void* stream);
+
 /* vf = P vc per component (fine_flags == NULL, accumulate == 0) or
  * vf += (fine constrained ? 0 : P vc) (mgsolve.py:232-234, accumulate = 1). */
 int pffmg_prolongate(const pffmg_lattice* coarse, const pffmg_lattice* fine, int n_comp,

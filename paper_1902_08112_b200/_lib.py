@@ -65,6 +65,7 @@ _SIGS = {
     "pffmg_cheb_init_zero_dc": [vp, vp, vp, vp, vp, vp, C.c_int64, vp],
     "pffmg_jacobi_update_dc": [vp, vp, vp, vp, C.c_int64, vp],
     "pffmg_restrict": [C.POINTER(Lattice), C.POINTER(Lattice), C.c_int, C.c_int, vp, vp, vp, vp],
+    "pffmg_restrict_init_bd": [C.POINTER(Lattice), C.POINTER(Lattice), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
     "pffmg_prolongate": [C.POINTER(Lattice), C.POINTER(Lattice), C.c_int, C.c_int, vp, vp, vp,
                          C.c_int, vp],
     "pffmg_inject_f64": [C.POINTER(Lattice), C.POINTER(Lattice), C.c_int, vp, vp, vp],

@@ -85,6 +85,53 @@ __global__ void restrict_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const doub
     }
 }
 
+// Restriction of all components into the coarse level's right-hand side fused
+// with the start of its block-diagonal Chebyshev smoother from x = 0
+// (mgsolve.py:95, 103-106; the arithmetic of cheb_init_zero_bd_k): per coarse
+// dof rc = (P^T vf)[masked]; vc = r = rc; d = inv rc / theta_block; x = d.
+template <int D>
+__global__ void restrict_init_bd_kernel(Lat Lc, Lat Lf, const double* __restrict__ vf, double* __restrict__ vc,
+                                        const uint8_t* __restrict__ cflags, const double* __restrict__ inv,
+                                        const double* __restrict__ tu, const double* __restrict__ tp,
+                                        double* __restrict__ r, double* __restrict__ d, double* __restrict__ x) {
+    pdl_wait();
+    int X, Y, Z;
+    if (!grid_point(Lc, X, Y, Z)) return;
+    const int64_t cid = vertex_id(Lc, X, Y, Z);
+    if (cid < 0) return;
+    constexpr int NC = D + 1;
+    const uint8_t fl = cflags[cid];
+    constexpr int zlo = D == 3 ? -1 : 0, zhi = D == 3 ? 1 : 0;
+    double acc[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) acc[k] = 0.0;
+#pragma unroll
+    for (int c = zlo; c <= zhi; ++c)
+#pragma unroll
+        for (int b = -1; b <= 1; ++b)
+#pragma unroll
+            for (int a = -1; a <= 1; ++a) {
+                int fx, fy, fz;
+                fine_of(Lc, Lf, X, Y, Z, a, b, c, fx, fy, fz);
+                const int64_t fid = vertex_id(Lf, fx, fy, fz);
+                if (fid < 0) continue;
+                const double w = (a ? 0.5 : 1.0) * (b ? 0.5 : 1.0) * (c ? 0.5 : 1.0);
+#pragma unroll
+                for (int k = 0; k < NC; ++k) acc[k] += w * __ldg(vf + (int64_t)k * Lf.V + fid);
+            }
+    const double thu = *tu, thp = *tp;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        const int64_t g = (int64_t)k * Lc.V + cid;
+        const double ri = ((fl >> k) & 1) ? 0.0 : acc[k];
+        const double di = (__ldg(inv + g) * ri) / (k < D ? thu : thp);
+        vc[g] = ri;
+        r[g] = ri;
+        d[g] = di;
+        x[g] = 0.0 + di;
+    }
+}
+
 // vf[k][f] (=|+=) sum_c P[f, c] vc[k][c] for owned fine vertices, zeroed where
 // the fine dof is constrained.  Coarse corners in bit order (x fastest), as
 // the COO entries of fem.py:323-339; corners with a zero weight are skipped.
@@ -369,4 +416,24 @@ extern "C" int pffmg_injection_map(const pffmg_lattice* coarse, const pffmg_latt
     PFFMG_REQUIRE(out, "pffmg_injection_map: null out");
     pdl_launch(inject_u8_kernel, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, nullptr, nullptr, out);
     return check_launch("pffmg_injection_map");
+}
+
+extern "C" int pffmg_restrict_init_bd(const pffmg_lattice* coarse, const pffmg_lattice* fine, const double* vf,
+                                      double* vc, const uint8_t* coarse_flags, const double* invdiag,
+                                      const double* theta_u, const double* theta_p, double* r, double* d,
+                                      double* x, void* stream) {
+    Lat Lc, Lf;
+    bool q2 = false;
+    int rc = check_pair(coarse, fine, &Lc, &Lf, &q2);
+    if (rc) return rc;
+    PFFMG_REQUIRE(!q2, "pffmg_restrict_init_bd: Q1 lattices only");
+    PFFMG_REQUIRE(vf && vc && coarse_flags && invdiag && theta_u && theta_p && r && d && x,
+                  "pffmg_restrict_init_bd: bad arguments");
+    if (Lc.dim == 3)
+        pdl_launch(restrict_init_bd_kernel<3>, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf,
+                   vf, vc, coarse_flags, invdiag, theta_u, theta_p, r, d, x);
+    else
+        pdl_launch(restrict_init_bd_kernel<2>, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf,
+                   vf, vc, coarse_flags, invdiag, theta_u, theta_p, r, d, x);
+    return check_launch("pffmg_restrict_init_bd");
 }

@@ -133,6 +133,14 @@ class Discretization:
         _lib.call("pffmg_restrict", c.ref, f.ref, n_comp, comp0, _lib.ptr(vf), _lib.ptr(vc),
                   _lib.ptr(coarse_flags), _lib.stream())
 
+    def restrict_init_bd_dev(self, vf, vc, l, coarse_flags, inv, theta_u, theta_p, r, d, x):
+        """restrict_dev of all components fused with the coarse level's
+        block-diagonal Chebyshev start from x = 0 (pffmg_restrict_init_bd)."""
+        c, f = self._pair(l)
+        _lib.call("pffmg_restrict_init_bd", c.ref, f.ref, _lib.ptr(vf), _lib.ptr(vc), _lib.ptr(coarse_flags),
+                  _lib.ptr(inv), _lib.ptr(theta_u), _lib.ptr(theta_p), _lib.ptr(r), _lib.ptr(d), _lib.ptr(x),
+                  _lib.stream())
+
     def prolongate_dev(self, vc, vf, l, n_comp, comp0=0, fine_flags=None, accumulate=False):
         c, f = self._pair(l)
         _lib.call("pffmg_prolongate", c.ref, f.ref, n_comp, comp0, _lib.ptr(vc), _lib.ptr(vf),

@@ -240,6 +240,9 @@ BLOCKDIAG_SMOOTH = os.environ.get("PFFMG_BLOCKDIAG_SMOOTH", "1") != "0"
 # Coarsest-level solve in one kernel (pffmg_coarse_cheb) when the level is small;
 # PFFMG_COARSE_KERNEL=0: one kernel per Chebyshev step.
 COARSE_KERNEL = os.environ.get("PFFMG_COARSE_KERNEL", "1") != "0"
+# Restriction into a level fused with that level's smoother start from x = 0
+# (pffmg_restrict_init_bd); PFFMG_FUSED_DESCENT=0: separate kernels.
+FUSED_DESCENT = os.environ.get("PFFMG_FUSED_DESCENT", "1") != "0"
 
 
 def build_level_contexts(disc, state, active_mask, dirichlet_mask, params, split,
@@ -752,20 +755,29 @@ class _NativeCycle:
         if pending:                                        # degree 1 from a non-zero x
             _lib.call("pffmg_axpy", 1.0, _lib.ptr(d_in), _lib.ptr(x), nb, s)
 
-    def _cheb_pair(self, L, su, sp, x_is_zero, pre=True):
+    def _bd_pair_ok(self, L, su, sp, x_is_zero):
+        _, pu, degu = self.slot[su]
+        _, pp, degp = self.slot[sp]
+        return not (not BLOCKDIAG_SMOOTH or not L.bd_ok or degu or degp or
+                    (pu.degree != pp.degree and not x_is_zero))
+
+    def _cheb_pair(self, L, su, sp, x_is_zero, pre=True, init_done=False):
         """Chebyshev on both diagonal blocks (independent, mgsolve.py:200-206) with
-        one block-diagonal kernel per step while both recurrences run."""
+        one block-diagonal kernel per step while both recurrences run.
+        init_done: the x = 0 start (r, d, x) was already written by the fused
+        restriction (pffmg_restrict_init_bd)."""
         ou, pu, degu = self.slot[su]
         op_, pp, degp = self.slot[sp]
-        if (not BLOCKDIAG_SMOOTH or not L.bd_ok or degu or degp or
-                (pu.degree != pp.degree and not x_is_zero)):
+        if not self._bd_pair_ok(L, su, sp, x_is_zero):
             self._cheb(L, 0, su, x_is_zero, pre)
             self._cheb(L, 1, sp, x_is_zero, pre)
             return
         op, coef, s = L.op, self.coef, _lib.stream()
         x, r, rhs, inv, d_in, d_out = L.x, L.cr, L.r, L.inv, L.d0, L.d1
         tu, tp = coef[ou:ou + 1], coef[op_:op_ + 1]
-        if x_is_zero:
+        if x_is_zero and init_done:
+            pending = False
+        elif x_is_zero:
             _lib.call("pffmg_cheb_init_zero_bd", _lib.ptr(rhs), _lib.ptr(inv), _lib.ptr(tu), _lib.ptr(tp),
                       L.dim * L.V, _lib.ptr(r), _lib.ptr(d_in), _lib.ptr(x), L.n, s)
             pending = False
@@ -791,8 +803,15 @@ class _NativeCycle:
                                 False, pre=pre)
                 di, do = do, di
 
-    def _smooth(self, l, x_is_zero):
-        self._cheb_pair(self.levels[l], ("s", l, 0), ("s", l, 1), x_is_zero)
+    def _smooth(self, l, x_is_zero, init_done=False):
+        self._cheb_pair(self.levels[l], ("s", l, 0), ("s", l, 1), x_is_zero, init_done=init_done)
+
+    def _fused_descent_ok(self, l):
+        """Restriction into level l can carry level l's smoother start (x = 0)."""
+        Lc = self.levels[l]
+        return (FUSED_DESCENT and self.comm is None and l >= 1 and
+                getattr(Lc.op.lat.info, "order", 1) == 1 and
+                self._bd_pair_ok(Lc, ("s", l, 0), ("s", l, 1), True))
 
     def _coarse_into_x(self, pre=True):
         L = self.levels[0]
@@ -807,16 +826,23 @@ class _NativeCycle:
             return
         self._cheb_pair(L, ("c", 0, 0), ("c", 0, 1), True, pre)
 
-    def _cycle(self, l):                                   # mgsolve.py:221-235
+    def _cycle(self, l, init_done=False):                  # mgsolve.py:221-235
         if l == 0:
             self._coarse_into_x()
             return
         L, Lc = self.levels[l], self.levels[l - 1]
-        self._smooth(l, True)
+        self._smooth(l, True, init_done)
         self._halo(L, L.x, L.dim + 1)
         L.op.residual_dev(_lib.FULL, L.x, L.r, L.res, pre=True)
-        self._restrict(l - 1, L.res, Lc.r, L.dim + 1, 0, Lc.flags)
-        self._cycle(l - 1)
+        if self._fused_descent_ok(l - 1):
+            ou, _, _ = self.slot[("s", l - 1, 0)]
+            op_, _, _ = self.slot[("s", l - 1, 1)]
+            self.disc.restrict_init_bd_dev(L.res, Lc.r, l - 1, Lc.flags, Lc.inv, self.coef[ou:ou + 1],
+                                           self.coef[op_:op_ + 1], Lc.cr, Lc.d0, Lc.x)
+            self._cycle(l - 1, init_done=True)
+        else:
+            self._restrict(l - 1, L.res, Lc.r, L.dim + 1, 0, Lc.flags)
+            self._cycle(l - 1)
         self._prolongate(l - 1, Lc.x, L.x, L.dim + 1, 0, L.flags)
         self._smooth(l, False)
 
