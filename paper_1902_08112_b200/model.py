@@ -140,7 +140,8 @@ def _split_code(split):
 class PhaseFieldOperator:
     """Matrix-free constrained Jacobian of one level (reference model.py:242-413)."""
 
-    def __init__(self, space, state, mask, params, split, threads=1, *, _flags=None, _rho=None, _ptab=None):
+    def __init__(self, space, state, mask, params, split, threads=1, *, _flags=None, _rho=None, _ptab=None,
+                 _no_table=False):
         _lib.require_cuda()
         self.space = space
         self.state = state
@@ -197,7 +198,7 @@ class PhaseFieldOperator:
         info = self.lat.info
         h = np.asarray(info.h, float)
         order = getattr(info, "order", 1)
-        if (code == 0 and (order == 2 or np.all(h == h[0]))
+        if (code == 0 and (order == 2 or np.all(h == h[0])) and not _no_table
                 and os.environ.get("PFFMG_PHI_TABLE", "1") != "0"):
             if _ptab is not None:            # a table already built from this state (mgsolve._Session)
                 self._ptab = _ptab
@@ -407,18 +408,20 @@ def _lattice_qp_coords(mesh):
 def residual(space, state, mask, params, split, threads=1):
     """Discrete semilinear form A_h(U) with constrained rows zeroed (reference
     model.py:420-460), on the GPU.  Returns the kind of `state.U`."""
-    op = PhaseFieldOperator(space, state, mask, params, split, threads)
+    # one-shot operators: the full operator / residual / diagonal never read
+    # the phi-block table, so none is built
+    op = PhaseFieldOperator(space, state, mask, params, split, threads, _no_table=True)
     out = empty(op.n_dofs)
     op.semilinear_dev(out)
     return like(out, state.U)
 
 
 def jacobian_vmult(space, state, mask, params, split, v, threads=1):
-    return PhaseFieldOperator(space, state, mask, params, split, threads).apply(v)
+    return PhaseFieldOperator(space, state, mask, params, split, threads, _no_table=True).apply(v)
 
 
 def diagonal(space, state, mask, params, split, threads=1):
-    return PhaseFieldOperator(space, state, mask, params, split, threads).diagonal()
+    return PhaseFieldOperator(space, state, mask, params, split, threads, _no_table=True).diagonal()
 
 
 # ------------------------------------------------------------------ QoIs
