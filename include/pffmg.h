@@ -262,6 +262,15 @@ int pffmg_unpack_flags(const uint8_t* flags, int n_comp, int64_t V, uint8_t* mas
 /* out = constrained ? 0 : in over components [comp0, comp0+n_comp). */
 int pffmg_masked_copy(const uint8_t* flags, int64_t V, int comp0, int n_comp,
                       const double* in, double* out, void* stream);
+
+/* V-cycle entry (mgsolve.py:271-272 then 95, 103-106): rhs = in with the dofs
+ * constrained in flags set to 0 (n_comp = dim+1 components), fused with the
+ * block-diagonal Chebyshev start from x = 0: r = rhs, d = invdiag rhs / theta
+ * (theta_u for the displacement components, theta_p for phi; device scalars),
+ * x = d. */
+int pffmg_masked_copy_init_bd(const uint8_t* flags, int64_t V, int n_comp, const double* in,
+                              double* rhs, const double* invdiag, const double* theta_u,
+                              const double* theta_p, double* r, double* d, double* x, void* stream);
 /* invdiag = 1 / diag. */
 int pffmg_reciprocal(const double* diag, double* out, int64_t n, void* stream);
 /* Chebyshev start from x = 0 (mgsolve.py:95, 103-106): r = b; d = (inv*r)/theta; x = d. */

@@ -74,6 +74,7 @@ _SIGS = {
     "pffmg_pack_flags": [vp, C.c_int, C.c_int64, vp, vp],
     "pffmg_unpack_flags": [vp, C.c_int, C.c_int64, vp, vp],
     "pffmg_masked_copy": [vp, C.c_int64, C.c_int, C.c_int, vp, vp, vp],
+    "pffmg_masked_copy_init_bd": [vp, C.c_int64, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp],
     "pffmg_reciprocal": [vp, vp, C.c_int64, vp],
     "pffmg_cheb_init_zero": [vp, vp, C.c_double, vp, vp, vp, C.c_int64, vp],
     "pffmg_jacobi_update": [vp, vp, C.c_double, vp, C.c_int64, vp],

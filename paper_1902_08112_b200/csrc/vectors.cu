@@ -317,6 +317,25 @@ __global__ void masked_copy_k(const uint8_t* f, int64_t V, int comp0, int nc, co
         out[i] = ((f[v] >> (comp0 + c)) & 1) ? 0.0 : in[i];
     }
 }
+// V-cycle entry (mgsolve.py:271-272 then 95, 103-106): the masked right-hand
+// side and the fine level's block-diagonal Chebyshev start from x = 0 in one
+// pass (the arithmetic of masked_copy_k then cheb_init_zero_bd_k).
+__global__ void masked_copy_init_bd_k(const uint8_t* f, int64_t V, int nc, const double* in, double* rhs,
+                                      const double* inv, const double* tu, const double* tp, double* r,
+                                      double* d, double* x) {
+    pdl_wait();
+    const double thu = *tu, thp = *tp;
+    GRID_STRIDE(i, V * nc) {
+        const int c = (int)(i / V);
+        const int64_t v = i - (int64_t)c * V;
+        const double ri = ((f[v] >> c) & 1) ? 0.0 : in[i];
+        const double di = (inv[i] * ri) / (c < nc - 1 ? thu : thp);
+        rhs[i] = ri;
+        r[i] = ri;
+        d[i] = di;
+        x[i] = 0.0 + di;
+    }
+}
 __global__ void reciprocal_k(const double* d, double* o, int64_t n) {
     pdl_wait();
     GRID_STRIDE(i, n) o[i] = 1.0 / d[i];
@@ -401,6 +420,16 @@ extern "C" int pffmg_masked_copy(const uint8_t* flags, int64_t V, int comp0, int
     PFFMG_REQUIRE(flags && in && out && n_comp >= 1 && comp0 >= 0, "pffmg_masked_copy: bad args");
     pdl_launch(masked_copy_k, dim3(vgrid(V * n_comp)), dim3(256), 0, as_stream(stream), flags, V, comp0, n_comp, in, out);
     VCHECK("pffmg_masked_copy");
+}
+extern "C" int pffmg_masked_copy_init_bd(const uint8_t* flags, int64_t V, int n_comp, const double* in,
+                                         double* rhs, const double* invdiag, const double* theta_u,
+                                         const double* theta_p, double* r, double* d, double* x, void* stream) {
+    PFFMG_REQUIRE(flags && in && rhs && invdiag && theta_u && theta_p && r && d && x && V >= 0 && n_comp >= 2 &&
+                      n_comp <= 4,
+                  "pffmg_masked_copy_init_bd: bad args");
+    pdl_launch(masked_copy_init_bd_k, dim3(vgrid(V * n_comp)), dim3(256), 0, as_stream(stream), flags, V, n_comp, in,
+               rhs, invdiag, theta_u, theta_p, r, d, x);
+    VCHECK("pffmg_masked_copy_init_bd");
 }
 extern "C" int pffmg_reciprocal(const double* diag, double* out, int64_t n, void* stream) {
     PFFMG_REQUIRE(diag && out, "pffmg_reciprocal: bad args");

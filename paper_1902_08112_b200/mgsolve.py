@@ -863,29 +863,51 @@ class _NativeCycle:
         self._prolongate(l - 1, Lc.x[Lc.blk(k)], L.x[b], ncomp, comp0, L.flags)
         self._cheb(L, k, ("s", l, k), False)
 
+    def _entry_fused(self, kind):
+        """The V-cycle input's masking carries the fine level's smoother start."""
+        top = len(self.levels) - 1
+        return (kind == "full" and FUSED_DESCENT and self.comm is None and top >= 1 and
+                self._bd_pair_ok(self.levels[top], ("s", top, 0), ("s", top, 1), True))
+
     def _body(self, kind):
         if kind == "full":
-            self._cycle(len(self.levels) - 1)
+            self._cycle(len(self.levels) - 1, init_done=self._entry_fused(kind))
         else:
             for k in range(2):
                 self._block_cycle(k, len(self.levels) - 1)
 
     def run(self, kind, r, out):
         top = self.levels[-1]
-        # r[constrained] = 0 straight from the caller's vector into the fine level's
-        # rhs (mgsolve.py:271-272); the recorded cycle then reads fixed buffers only
-        _lib.call("pffmg_masked_copy", _lib.ptr(top.flags), top.V, 0, top.dim + 1,
-                  _lib.ptr(r), _lib.ptr(top.r), _lib.stream())
+        fused = self._entry_fused(kind)
+
+        def entry():
+            # r[constrained] = 0 straight from the caller's vector into the fine level's
+            # rhs (mgsolve.py:271-272); the recorded cycle then reads fixed buffers only
+            if fused:                        # ... together with the smoother's x = 0 start
+                t = len(self.levels) - 1
+                ou, _, _ = self.slot[("s", t, 0)]
+                op_, _, _ = self.slot[("s", t, 1)]
+                _lib.call("pffmg_masked_copy_init_bd", _lib.ptr(top.flags), top.V, top.dim + 1, _lib.ptr(r),
+                          _lib.ptr(top.r), _lib.ptr(top.inv), _lib.ptr(self.coef[ou:ou + 1]),
+                          _lib.ptr(self.coef[op_:op_ + 1]), _lib.ptr(top.cr), _lib.ptr(top.d0),
+                          _lib.ptr(top.x), _lib.stream())
+            else:
+                _lib.call("pffmg_masked_copy", _lib.ptr(top.flags), top.V, 0, top.dim + 1,
+                          _lib.ptr(r), _lib.ptr(top.r), _lib.stream())
+
         if self.use_graph:
             g = self.graphs.get(kind)
             if g is None:
+                entry()
                 self._body(kind)                       # warm-up (allocator, lazy attributes)
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
                     self._body(kind)
                 self.graphs[kind] = g
+            entry()                                    # (the fused entry state is consumed by a cycle)
             g.replay()
         else:
+            entry()
             self._body(kind)
         out.copy_(top.x)
 
