@@ -49,6 +49,7 @@ extern "C" {
  * x in [crow_lo[s], crow_hi[s]) exist.  All table pointers are DEVICE pointers.
  */
 typedef struct {
+    int32_t struct_size;    /* = sizeof(pffmg_lattice); checked by every entry point (ABI guard) */
     int32_t dim;            /* 2 or 3 */
     int32_t nx, ny, nz;     /* cells per axis of the bounding lattice (nz = 0 in 2D) */
     double hx, hy, hz;      /* cell edge lengths (LevelMesh.cell_size) */
@@ -83,6 +84,7 @@ typedef struct {
  * phi_tilde (SURVEY §8d "model F").
  */
 typedef struct {
+    int32_t struct_size;        /* = sizeof(pffmg_state); checked by every entry point (ABI guard) */
     double mu, lam, g_c, kappa, eps;
     double pressure;            /* MaterialParams.pressure(state.t) */
     int32_t split;              /* 0 = NOSPLIT; 1 = MIEHE spectral split */
@@ -113,6 +115,8 @@ typedef struct {
 } pffmg_state;
 
 const char* pffmg_last_error(void);
+/* ABI version: 2 (struct_size guards; pffmg_state.phi_coef). */
+#define PFFMG_ABI_VERSION 2
 int pffmg_version(void);
 int pffmg_device_sm_count(int* out);
 
@@ -304,11 +308,12 @@ int pffmg_dot_scaled(const double* x, const double* y, const double* s, int64_t 
  *   for i in 0..j: h[i] = V_i . w ; w -= h[i] V_i      (modified Gram-Schmidt)
  * with the conditional second pass when ||w|| < 1e-3 ||w0||, then
  * h[j+1] = ||w||, V_{j+1} = w / h[j+1] (if nonzero).  Vb is the (m+1) x ld
- * row-major basis, h is a device array of length >= j+2.  Returns nothing on
- * the host; the caller reads h. */
+ * row-major basis, h is a device array of length >= j+2, scratch a device
+ * array of length >= j+4 (any j >= 0: restart lengths are not limited).
+ * Returns nothing on the host; the caller reads h. */
 int pffmg_arnoldi_mgs(double* Vb, int64_t ld, int j, double* w, int64_t n, double* h,
                       double* scratch, void* stream);
-/* x += sum_i y[i] * Z_i, i < k (krylov.py:132); y is a DEVICE array. */
+/* x += sum_i y[i] * Z_i, i < k (krylov.py:132); y is a DEVICE array; any k >= 0. */
 int pffmg_multi_axpy(const double* Z, int64_t ld, int k, const double* y, double* x,
                      int64_t n, void* stream);
 

@@ -20,9 +20,21 @@ c_double_p = C.POINTER(C.c_double)
 vp = C.c_void_p
 
 
-class Lattice(C.Structure):
+ABI_VERSION = 2
+
+
+class _Sized(C.Structure):
+    """Structs of the ABI carry their own size as the first member (the
+    library rejects a caller whose layout differs from its own)."""
+
+    def __init__(self, *args, **kw):
+        super().__init__(*args, **kw)
+        self.struct_size = C.sizeof(self)
+
+
+class Lattice(_Sized):
     """pffmg_lattice (include/pffmg.h)."""
-    _fields_ = [("dim", C.c_int32), ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
+    _fields_ = [("struct_size", C.c_int32), ("dim", C.c_int32), ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
                 ("hx", C.c_double), ("hy", C.c_double), ("hz", C.c_double),
                 ("n_vertices", C.c_int64),
                 ("vrow_off", vp), ("vrow_lo", vp), ("vrow_hi", vp),
@@ -31,9 +43,9 @@ class Lattice(C.Structure):
                 ("plane0", C.c_int32), ("order", C.c_int32)]
 
 
-class State(C.Structure):
+class State(_Sized):
     """pffmg_state (include/pffmg.h)."""
-    _fields_ = [("mu", C.c_double), ("lam", C.c_double), ("g_c", C.c_double),
+    _fields_ = [("struct_size", C.c_int32), ("mu", C.c_double), ("lam", C.c_double), ("g_c", C.c_double),
                 ("kappa", C.c_double), ("eps", C.c_double), ("pressure", C.c_double),
                 ("split", C.c_int32), ("hints", C.c_int32),
                 ("U", vp), ("phi_tilde", vp), ("rho", vp), ("flags", vp),
@@ -135,7 +147,20 @@ def require_cuda():
     load()
 
 
+_DEVICE = None
+
+
 def stream():
+    """Current torch stream as a cudaStream_t.  libpffmg keeps per-process
+    launch caches (occupancy, cooperative-grid scratch) for the device it was
+    first used on, so one process drives one device (one rank per GPU)."""
+    global _DEVICE
+    d = torch.cuda.current_device()
+    if _DEVICE is None:
+        _DEVICE = d
+    elif d != _DEVICE:
+        raise PffmgError(f"libpffmg was first used on cuda:{_DEVICE} in this process; "
+                         f"cuda:{d} needs its own process (one rank per GPU)")
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 

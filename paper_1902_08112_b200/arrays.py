@@ -79,14 +79,29 @@ class DeviceCallable:
         if not self.numpy_mode:
             try:
                 out = self.fn(v)
-            except _lib.PffmgError:
+            except (_lib.PffmgError, torch.cuda.OutOfMemoryError):
                 raise
-            except (TypeError, RuntimeError):
-                # numpy-only callable (e.g. `lambda v: A @ v` with a numpy A)
+            except (TypeError, RuntimeError) as e:
+                # only a numpy-only callable (e.g. `lambda v: A @ v` with a numpy A)
+                # switches to host round trips; CUDA failures propagate
+                if not _is_numpy_conversion_error(e):
+                    raise
                 self.numpy_mode = True
             else:
                 return dev(out)
         return dev(self.fn(host(v)))
+
+
+_CONVERSION_HINTS = ("numpy", "ndarray", "can't convert", "cannot convert", "__array__")
+
+
+def _is_numpy_conversion_error(e):
+    """True for the errors a numpy-only callable raises when handed a CUDA
+    tensor (TypeError from numpy's conversion, or torch refusing an ndarray)."""
+    msg = str(e)
+    if "CUDA" in msg and "error" in msg.lower():
+        return False
+    return isinstance(e, TypeError) or any(h in msg for h in _CONVERSION_HINTS)
 
 
 def pack_flags(mask_bool, n_comp, V):

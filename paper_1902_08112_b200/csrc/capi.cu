@@ -49,6 +49,9 @@ int sm_count() {
 
 int make_lat(const pffmg_lattice* in, Lat* out) {
     PFFMG_REQUIRE(in, "null lattice");
+    PFFMG_REQUIRE(in->struct_size == (int32_t)sizeof(pffmg_lattice),
+                  "pffmg_lattice.struct_size = %d, this library expects %d (ABI version %d)",
+                  in->struct_size, (int)sizeof(pffmg_lattice), PFFMG_ABI_VERSION);
     PFFMG_REQUIRE(in->dim == 2 || in->dim == 3, "lattice dim must be 2 or 3 (got %d)", in->dim);
     PFFMG_REQUIRE(in->nx >= 1 && in->ny >= 1 && (in->dim == 2 ? in->nz == 0 : in->nz >= 1),
                   "bad lattice extents %d x %d x %d", in->nx, in->ny, in->nz);
@@ -101,6 +104,10 @@ int make_lat(const pffmg_lattice* in, Lat* out) {
 }
 
 int make_consts(const pffmg_lattice* lat, const pffmg_state* st, Consts* K) {
+    PFFMG_REQUIRE(st, "null state");
+    PFFMG_REQUIRE(st->struct_size == (int32_t)sizeof(pffmg_state),
+                  "pffmg_state.struct_size = %d, this library expects %d (ABI version %d)",
+                  st->struct_size, (int)sizeof(pffmg_state), PFFMG_ABI_VERSION);
     PFFMG_REQUIRE(lat->hx > 0 && lat->hy > 0 && (lat->dim == 2 || lat->hz > 0), "cell sizes must be > 0");
     PFFMG_REQUIRE(st->eps > 0, "eps must be > 0");
     // fem.py:33-34
@@ -132,7 +139,7 @@ using namespace pffmg;
 
 extern "C" const char* pffmg_last_error(void) { return g_err; }
 
-extern "C" int pffmg_version(void) { return 1; }
+extern "C" int pffmg_version(void) { return PFFMG_ABI_VERSION; }
 
 extern "C" int pffmg_device_sm_count(int* out) {
     PFFMG_REQUIRE(out, "null out");

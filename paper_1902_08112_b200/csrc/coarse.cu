@@ -284,7 +284,10 @@ extern "C" int pffmg_coarse_cheb(const pffmg_lattice* lat, const pffmg_state* st
     const int maxa = L.order == 2 ? 4 : (1 << L.dim);
     const size_t smem = sizeof(double) * ((size_t)ncell * nco * npc + (size_t)L.V * (5 * nco + 1)) +
                         sizeof(int) * ((size_t)ncell * npc + (size_t)L.V * maxa) + (size_t)L.V + 16;
-    PFFMG_REQUIRE(smem <= 200 * 1024, "pffmg_coarse_cheb: level too large for one CTA");
+    if (smem > 200 * 1024) {
+        set_error("pffmg_coarse_cheb: level needs %zu B of shared memory > 200 KiB (use the per-step kernels)", smem);
+        return PFFMG_ERR_UNSUPPORTED;
+    }
     C.A.I = make_iso_host(C.A.K);
     const cudaStream_t s = as_stream(stream);
     const bool iso = L.order == 1 && L.hx == L.hy && (L.dim == 2 || L.hz == L.hx);

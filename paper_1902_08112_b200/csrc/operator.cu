@@ -30,7 +30,6 @@ static int fill_args(const pffmg_lattice* lat, const pffmg_state* st, OpArgs* A)
     rc = make_consts(lat, st, &A->K);
     if (rc) return rc;
     A->I = make_iso_host(A->K);
-    if (rc) return rc;
     if (st->split != 0 && st->split != 1) {
         set_error("unknown split kind %d (0 NoSplit, 1 Miehe)", st->split);
         return PFFMG_ERR_ARG;

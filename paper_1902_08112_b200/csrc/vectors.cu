@@ -661,6 +661,7 @@ extern "C" int pffmg_dot_scaled(const double* x, const double* y, const double* 
 // per element as the multi-launch path: w -= h_{i-1} V_{i-1} fused with the
 // dot against V_i.
 constexpr int MGS_T = 1024;
+constexpr int MGS_MAXJ = 64;   // largest Arnoldi index of the one-launch form (larger j: multi-launch path)
 
 __device__ __forceinline__ double mgs_block_sum(double a, double* red) {
     a = warp_sum(a);
@@ -725,7 +726,7 @@ __global__ void __launch_bounds__(MGS_T, 1) mgs_coop_kernel(const double* __rest
     __syncthreads();
     MgsSums S{part, 0};
     auto V = [&](int i) { return Vb + (int64_t)i * ld + c0; };
-    double hv[66];   // H[0..j+1, j] (local memory; indexed by the uniform pass counter)
+    double hv[MGS_MAXJ + 2];   // H[0..j+1, j] (local memory; indexed by the uniform pass counter)
     double w0n2 = 0.0;
     bool reorth = false;
     for (int sweep = 0; sweep < 2; ++sweep) {
@@ -816,13 +817,14 @@ static int mgs_coop(const double* Vb, int64_t ld, int j, double* w, int64_t n, d
 
 extern "C" int pffmg_arnoldi_mgs(double* Vb, int64_t ld, int j, double* w, int64_t n, double* h,
                                  double* ctl, void* stream) {
-    PFFMG_REQUIRE(Vb && w && h && ctl && j >= 0 && j < 64 && ld >= n, "pffmg_arnoldi_mgs: bad args");
+    PFFMG_REQUIRE(Vb && w && h && ctl && j >= 0 && ld >= n, "pffmg_arnoldi_mgs: bad args");
     cudaStream_t s = as_stream(stream);
     static const bool coop_off = [] {
         const char* e = getenv("PFFMG_MGS_COOP");
         return e && e[0] == '0';
     }();
-    if (!coop_off && mgs_coop(Vb, ld, j, w, n, h, ctl, s) == 0) return check_launch("arnoldi_mgs");
+    // the one-launch form keeps H[0..j+1, j] in registers/local memory: j < MGS_MAXJ
+    if (!coop_off && j < MGS_MAXJ && mgs_coop(Vb, ld, j, w, n, h, ctl, s) == 0) return check_launch("arnoldi_mgs");
     auto V = [&](int i) { return (const double*)(Vb + (int64_t)i * ld); };
     int rc;
     // modified Gram-Schmidt sweep
@@ -849,10 +851,16 @@ extern "C" int pffmg_arnoldi_mgs(double* Vb, int64_t ld, int j, double* w, int64
 
 extern "C" int pffmg_multi_axpy(const double* Z, int64_t ld, int k, const double* y, double* x, int64_t n,
                                 void* stream) {
-    PFFMG_REQUIRE(Z && y && x && k >= 0 && k <= 64 && ld >= n, "pffmg_multi_axpy: bad args");
-    if (k == 0) return PFFMG_OK;
-    pdl_launch(multi_axpy_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), Z, ld, k, y, x, n);
-    VCHECK("pffmg_multi_axpy");
+    PFFMG_REQUIRE(Z && y && x && k >= 0 && ld >= n, "pffmg_multi_axpy: bad args");
+    // groups of up to 64 basis vectors per launch (restart lengths above 64 take several)
+    for (int k0 = 0; k0 < k; k0 += 64) {
+        const int kk = k - k0 < 64 ? k - k0 : 64;
+        pdl_launch(multi_axpy_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), Z + (int64_t)k0 * ld, ld, kk,
+                   y + k0, x, n);
+        const int rc = check_launch("pffmg_multi_axpy");
+        if (rc) return rc;
+    }
+    return PFFMG_OK;
 }
 
 extern "C" int pffmg_active_set(const double* R_phi, const double* U_phi, const double* phi_old,

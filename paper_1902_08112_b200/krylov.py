@@ -77,7 +77,7 @@ class _Workspace:
         self.V = torch.zeros((m + 1, n), dtype=torch.float64, device="cuda")
         self.Z = torch.zeros((m, n), dtype=torch.float64, device="cuda")
         self.H = torch.zeros((m, m + 1), dtype=torch.float64, device="cuda")   # column j = H[:, j]
-        self.ctl = torch.zeros(3 + 64, dtype=torch.float64, device="cuda")
+        self.ctl = torch.zeros(3 + m + 1, dtype=torch.float64, device="cuda")   # pffmg_arnoldi_mgs scratch
         self.r = torch.empty(n, dtype=torch.float64, device="cuda")
         self.y = torch.zeros(m, dtype=torch.float64, device="cuda")
         self.hpin = torch.zeros(m + 1, dtype=torch.float64).pin_memory()

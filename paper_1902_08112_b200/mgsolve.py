@@ -191,12 +191,9 @@ def _estimate_blocks(op, diag_dev, eig_iters, seed):
         return tuple(lanczos_extremes(s, eig_iters) for s in scals)
     for k, blk in enumerate(op.blocks):
         sd = seed + 31 * level + 7 * k if level is not None else seed + 7 * k
-        if False:
-            pass
-        else:
-            spectra.append(estimate_spectrum(lambda vb, k=k: op.apply_block(k, vb),
-                                             diag_dev[blk], n_iters=eig_iters, seed=sd,
-                                             constrained=np.asarray(op.mask.is_constrained)[blk]))
+        spectra.append(estimate_spectrum(lambda vb, k=k: op.apply_block(k, vb),
+                                         diag_dev[blk], n_iters=eig_iters, seed=sd,
+                                         constrained=np.asarray(op.mask.is_constrained)[blk]))
     return tuple(spectra)
 
 
@@ -592,6 +589,18 @@ def _gen_block(ctxs, cons, D, k, rb, l, degree, target, cap, n_comp):
 
 # ---------------------------------------------------------- native V-cycle
 
+COARSE_SMEM_MAX = 200 * 1024
+
+
+def coarse_smem_bytes(dim, ncell, V, order=1):
+    """Shared-memory footprint of pffmg_coarse_cheb on a level (the formula of
+    csrc/coarse.cu); levels above COARSE_SMEM_MAX run the per-step kernels."""
+    nco = dim + 1
+    npc = 9 if order == 2 else (1 << dim)
+    maxa = 4 if order == 2 else (1 << dim)
+    return 8 * (ncell * nco * npc + V * (5 * nco + 1)) + 4 * (ncell * npc + V * maxa) + V + 16
+
+
 class _Level:
     """Device buffers of one level for the native cycle."""
 
@@ -617,7 +626,9 @@ class _Level:
         self.index = ctx.level
         self.bd_ok = self.dim == 2 or self.V < (1 << 17)
         info = op.lat.info
-        self.coarse_ok = int(np.prod(info.ncell)) <= 256 and tuple(info.own) == (0, 0)
+        self.coarse_ok = (int(np.prod(info.ncell)) <= 256 and tuple(info.own) == (0, 0)
+                          and coarse_smem_bytes(self.dim, int(np.prod(info.ncell)), self.V,
+                                                getattr(info, "order", 1)) <= COARSE_SMEM_MAX)
 
     def blk(self, k):
         return slice(0, self.dim * self.V) if k == 0 else slice(self.dim * self.V, self.n)

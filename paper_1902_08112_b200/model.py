@@ -157,6 +157,16 @@ class PhaseFieldOperator:
         code = _split_code(split)
         self._U = dev(state.U)
         self._pt = dev(state.phi_tilde)
+        if _flags is None and not _no_table:
+            # the reference caches every coefficient at construction
+            # (model.py:260, 270-309): a caller's CUDA state is snapshotted so a
+            # later in-place update of state.U cannot mix old and new
+            # coefficients (internal callers own their buffers and pass _flags;
+            # the one-shot helpers below use the operator immediately)
+            if is_tensor(state.U) and self._U.data_ptr() == state.U.data_ptr():
+                self._U = self._U.clone()
+            if is_tensor(state.phi_tilde) and self._pt.data_ptr() == state.phi_tilde.data_ptr():
+                self._pt = self._pt.clone()
         if self._U.numel() != self.nc * V or self._pt.numel() != V:
             raise ValueError(f"state sizes {self._U.numel()}/{self._pt.numel()} do not match "
                              f"the level ({self.nc}x{V} dofs)")

@@ -350,6 +350,73 @@ def gen_configs():
     save("configs", **out)
 
 
+FULL_CASES = (("cfg2", None), ("cfg4", None), ("cfg5", 6))
+FULL_SAMPLES = 4096
+
+
+def sample_index(n, seed=11):
+    """Fixed sample of entries stored for full-size vectors (the whole vector
+    would be tens of MB): 4096 sorted indices from default_rng(seed)."""
+    return np.sort(np.random.default_rng(seed).choice(n, size=min(n, FULL_SAMPLES), replace=False))
+
+
+def vec_summary(x):
+    """Size-independent fingerprint of a full-size vector: 2-norm, sum, sum of
+    |x|, and the entries at sample_index(n)."""
+    return np.array([np.linalg.norm(x), x.sum(), np.abs(x).sum()]), x[sample_index(x.size)]
+
+
+def gen_configs_full(threads=8):
+    """Reference outputs at the BENCHMARKED sizes (cfg2 1024^2, cfg4 full,
+    cfg5 at 96^3 = 6 levels): vmult, diagonal and Newton-residual
+    fingerprints, per-level spectra, and the Newton-step GMRES iteration count
+    and solution fingerprint (GMRES(30), rel 1e-8, FULL V(1,1))."""
+    from paper_1902_08112_b200 import configs
+    path = os.path.join(HERE, "configs_full.npz")
+    out = dict(np.load(path)) if os.path.exists(path) else {}
+    only = os.environ.get("FULL_ONLY")
+    for name, levels in FULL_CASES:
+        tag = name if levels is None else f"{name}_l{levels}"
+        if only and tag not in only.split(","):
+            continue
+        t0 = time.time()
+        prob = configs.make(name, levels)
+        disc, state, params, dirichlet = _ref_problem(prob)
+        space = disc.finest
+        mask = dirichlet.combined_with(prob.active, np.zeros(prob.n_dofs))
+        op = model.PhaseFieldOperator(space, state, ConstraintMask(mask.is_constrained,
+                                                                   mask.inhomogeneity),
+                                      params, SplitKind.NOSPLIT, threads=threads)
+        out[f"{tag}/checksum"] = np.array([state.U.sum(), prob.v.sum(),
+                                           float(mask.is_constrained.sum())])
+        for key, vec in (("apply", op.apply(prob.v)), ("diagonal", op.diagonal()),
+                         ("residual", model.residual(space, state, dirichlet, params,
+                                                     SplitKind.NOSPLIT, threads=threads))):
+            out[f"{tag}/{key}_stats"], out[f"{tag}/{key}_sample"] = vec_summary(vec)
+        t1 = time.time()
+        ctxs = mgsolve.build_level_contexts(disc, state, prob.active, dirichlet, params,
+                                            SplitKind.NOSPLIT, threads=threads)
+        t_setup = time.time() - t1
+        for l, c in enumerate(ctxs):
+            out[f"{tag}/{l}/spectra"] = np.array([[s.lambda_min_hat, s.lambda_max_hat, s.fallback]
+                                                  for s in c.spectra], dtype=float)
+        R = -model.residual(space, state, dirichlet, params, SplitKind.NOSPLIT, threads=threads)
+        R[mask.is_constrained] = 0.0
+        ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+        t1 = time.time()
+        x, its = krylov.gmres(ctxs[-1].op.apply,
+                              lambda v: mgsolve.vcycle(ctxs, mgsolve.PreconditionerKind.FULL, v,
+                                                       degree=prob.degree), R, ctl)
+        t_gmres = time.time() - t1
+        out[f"{tag}/gmres_x_stats"], out[f"{tag}/gmres_x_sample"] = vec_summary(x)
+        out[f"{tag}/gmres_iters"] = np.array(its)
+        out[f"{tag}/ref_seconds"] = np.array([t_setup, t_gmres, float(threads)])
+        print(f"  {tag}: n={prob.n_dofs} gmres {its} its, |x|={np.linalg.norm(x):.6e} "
+              f"setup {t_setup:.1f}s gmres {t_gmres:.1f}s total {time.time() - t0:.1f}s", flush=True)
+        np.savez_compressed(path, **out)
+    print(f"  wrote configs_full.npz ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
 def gen_krylov():
     out = {}
     K = np.zeros((9, 9))

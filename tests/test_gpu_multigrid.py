@@ -275,3 +275,39 @@ def test_coarse_kernel_matches_per_step(golden, name, monkeypatch):
     assert rel_err(out[0][0], out[1][0]) <= 1e-12
     assert rel_err(out[0][1], out[1][1]) <= 1e-12
     assert rel_err(out[0][1], g[f"{name}/coarse"]) <= 1e-10
+
+
+@pytest.mark.parametrize("name", MG)
+def test_fused_descent_and_entry_match_separate_kernels(golden, name, monkeypatch):
+    """pffmg_restrict_init_bd (fused descent) and pffmg_masked_copy_init_bd (fused
+    V-cycle entry) are bitwise the separate kernels they replace."""
+    from paper_1902_08112_b200 import mgsolve
+    g = golden["multigrid"]
+    r = torch.as_tensor(g[f"{name}/r"], device="cuda")
+    out = []
+    for flag in (True, False):
+        monkeypatch.setattr(mgsolve, "FUSED_DESCENT", flag)
+        mgsolve._Session._cache.clear()
+        mgsolve._NativeCycle._cache.clear()
+        disc, ctxs = _contexts(g, name)
+        out.append(mgsolve.vcycle(ctxs, mgsolve.PreconditionerKind.FULL, r))
+    assert torch.equal(out[0], out[1])
+
+
+def test_gmres_restart_above_64():
+    """Restart lengths above the one-launch MGS bound (64) take the multi-launch
+    Arnoldi path and still match the oracle (reference krylov.py:50-136 accepts any m)."""
+    from oracle import solvers
+    from paper_1902_08112_b200 import krylov
+    rng = np.random.default_rng(5)
+    n = 300
+    A = np.diag(np.linspace(1.0, 400.0, n)) + 1e-3 * rng.standard_normal((n, n))
+    b = rng.standard_normal(n)
+    At = torch.as_tensor(A, device="cuda")
+    ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-10, restart=100, max_iters=1000)
+    x, its = krylov.gmres(lambda v: At @ v, None, b, ctl)
+    xo, its_o = solvers.gmres(lambda v: A @ v, None, b,
+                              solvers.Control(abs_tol=0.0, rel_tol=1e-10, restart=100, max_iters=1000))
+    assert its > 64
+    assert abs(its - its_o) <= 1
+    assert rel_err(x, xo) <= 1e-8

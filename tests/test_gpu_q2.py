@@ -134,3 +134,29 @@ def test_q2_vcycle_and_gmres_match_oracle():
                               solvers.Control(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000))
     assert abs(its - its_o) <= 1
     assert rel_err(x, xo) <= 1e-6
+
+
+def test_q2_fused_descent_and_entry_match_separate_kernels(monkeypatch):
+    """The fused descent / V-cycle entry on Q2 levels are bitwise the separate kernels."""
+    from paper_1902_08112_b200 import mgsolve
+    from paper_1902_08112_b200 import model as M
+    levels, tables, tr = _oracle()
+    T = tables[-1]
+    U, pt, rng = _state(T, 9)
+    n = T.n_dofs
+    active = np.zeros(n, bool)
+    active[2 * T.n_vertices + np.flatnonzero(rng.random(T.n_vertices) < 0.1)] = True
+    dirichlet = np.zeros(n, bool)
+    r = torch.as_tensor(rng.standard_normal(n), device="cuda")
+    out = []
+    for flag in (True, False):
+        monkeypatch.setattr(mgsolve, "FUSED_DESCENT", flag)
+        mgsolve._Session._cache.clear()
+        mgsolve._NativeCycle._cache.clear()
+        disc = _product()
+        params = params_for(disc.finest, None, cls=M.MaterialParams)
+        st = M.LinearizationState(U=U, U_prev1=U, U_prev2=U, t=0.1, t_prev1=0.0, t_prev2=0.0, phi_tilde=pt)
+        ctxs = mgsolve.build_level_contexts(disc, st, active, M.ConstraintMask(dirichlet, np.zeros(n)),
+                                            params, M.SplitKind.NOSPLIT)
+        out.append(mgsolve.vcycle(ctxs, mgsolve.PreconditionerKind.FULL, r))
+    assert torch.equal(out[0], out[1])

@@ -3,6 +3,7 @@ tables against the reference's meshes, and the C ABI library surface."""
 import ctypes
 import os
 import re
+import subprocess
 
 import numpy as np
 import pytest
@@ -68,7 +69,7 @@ def test_library_exports_every_header_symbol():
 
 def test_library_reports_argument_errors_without_a_gpu():
     lib = _lib.load()
-    assert lib.pffmg_version() == 1
+    assert lib.pffmg_version() == 2
     rc = lib.pffmg_apply(None, None, -1, None, None, None)
     assert rc == 1
     assert b"null" in lib.pffmg_last_error()
@@ -86,3 +87,66 @@ def test_product_has_no_oracle_imports():
             if f.endswith(".py"):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
+
+
+def _integration_structs():
+    """Execute the ctypes struct definitions of INTEGRATION.md's binding snippet."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = re.findall(r"```python\n(import ctypes as C.*?)```", doc, flags=re.S)
+    assert block, "INTEGRATION.md has no ctypes binding snippet"
+    src = block[0]
+    defs = src[src.index("class Lattice"):src.index("lib.pffmg_apply.argtypes")]
+    ns = {"C": ctypes}
+    exec(defs, ns)
+    return ns["Lattice"], ns["State"]
+
+
+def _c_layout(tmp_path):
+    """sizeof/offsetof of pffmg_lattice and pffmg_state as the C compiler lays them out."""
+    fields = {"pffmg_lattice": [f for f, _ in _lib.Lattice._fields_],
+              "pffmg_state": [f for f, _ in _lib.State._fields_]}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "pffmg.h"', "int main(void){"]
+    for s, fs in fields.items():
+        lines.append(f'printf("{s} size %zu\\n", sizeof({s}));')
+        for f in fs:
+            lines.append(f'printf("{s} {f} %zu\\n", offsetof({s}, {f}));')
+    lines.append("return 0;}")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+    lay = {}
+    for line in out.splitlines():
+        s, f, v = line.split()
+        lay[(s, f)] = int(v)
+    return lay
+
+
+def test_integration_snippet_structs_match_header(tmp_path):
+    """The binding INTEGRATION.md tells a maintainer to write has the header's
+    layout (size and every offset), as does _lib's binding."""
+    lay = _c_layout(tmp_path)
+    doc_lat, doc_st = _integration_structs()
+    for cname, doc_cls, lib_cls in (("pffmg_lattice", doc_lat, _lib.Lattice),
+                                    ("pffmg_state", doc_st, _lib.State)):
+        assert ctypes.sizeof(doc_cls) == lay[(cname, "size")] == ctypes.sizeof(lib_cls), cname
+        assert [f for f, _ in doc_cls._fields_] == [f for f, _ in lib_cls._fields_], cname
+        for f, _ in lib_cls._fields_:
+            assert getattr(doc_cls, f).offset == lay[(cname, f)] == getattr(lib_cls, f).offset, (cname, f)
+
+
+def test_struct_size_guard_rejects_foreign_layouts():
+    lib = _lib.load()
+    L = _lib.Lattice()
+    L.dim, L.nx, L.ny, L.n_vertices = 2, 4, 4, 25
+    L.struct_size = ctypes.sizeof(L) - 8          # a binding that lacks the trailing fields
+    st = _lib.State()
+    rc = lib.pffmg_apply(ctypes.byref(L), ctypes.byref(st), -1, None, None, None)
+    assert rc == 1 and b"struct_size" in lib.pffmg_last_error()
+    L.struct_size = ctypes.sizeof(L)
+    st.struct_size = ctypes.sizeof(st) - 8        # the round-1 pffmg_state without phi_coef
+    st.eps = 1.0
+    L.hx = L.hy = 0.25
+    rc = lib.pffmg_apply(ctypes.byref(L), ctypes.byref(st), -1, None, None, None)
+    assert rc == 1 and b"pffmg_state.struct_size" in lib.pffmg_last_error()
