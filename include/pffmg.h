@@ -190,6 +190,16 @@ int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st, int which,
                      const double* h_v, double* h_out, double* d_v, double* d_out,
                      const int64_t* h_plane_off, int n_strips, void* stream);
 
+/* Boundary load (model.py:511-547): sum over the n_faces boundary faces
+ * (face_cell[i] = lattice cell index cx + nx (cy + ny cz), face_id[i] =
+ * 2 axis + side, LevelMesh.bf_face) of the face-Gauss integral of
+ * sign(side) * (g(phi) rho sigma+ + rho sigma-)[direction, axis]; rho_face is
+ * NULL (rho = 1) or the modulus field at the 2^(dim-1) face points of each
+ * face (fem.py:265-292 order).  Q1 lattices; deterministic reduction into
+ * the DEVICE double *result. */
+int pffmg_boundary_load(const pffmg_lattice* lat, const pffmg_state* st, const int64_t* face_cell,
+                        const int32_t* face_id, int64_t n_faces, int direction,
+                        const double* rho_face, double* result, void* stream);
 /* Quantities of interest (model.py:472-506) as one deterministic cell-integral
  * reduction into the device scalar *result: kind 0 = crack_energy (uses eps,
  * g_c), 1 = bulk_energy (split, band, modulus field, pressure; U's own phi

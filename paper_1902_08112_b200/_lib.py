@@ -67,6 +67,7 @@ _SIGS = {
                         C.c_double, vp],
     "pffmg_apply_host": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, C.c_int, vp],
     "pffmg_qoi": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp],
+    "pffmg_boundary_load": [C.POINTER(Lattice), C.POINTER(State), vp, vp, C.c_int64, C.c_int, vp, vp, vp],
     "pffmg_coarse_cheb": [C.POINTER(Lattice), C.POINTER(State), vp, vp, vp, vp, vp, vp, C.c_int, vp, C.c_int, vp],
     "pffmg_cheb_step_bd": [C.POINTER(Lattice), C.POINTER(State), vp, vp, vp, vp, vp, vp, vp, C.c_int, vp],
     "pffmg_cheb_init_bd": [C.POINTER(Lattice), C.POINTER(State), vp, vp, vp, vp, vp, vp, vp, vp],

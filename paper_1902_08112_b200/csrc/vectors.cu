@@ -623,6 +623,138 @@ struct QoiOp {
     __device__ void finish(double s0, double) const { *result = scale * s0; }
 };
 
+// Boundary load (reference model.py:511-547): traction component `dir` of the
+// transmitted stress g(phi) rho sigma+ + rho sigma- integrated over a list of
+// boundary faces (lattice cell, face f = 2 axis + side) with the 2^(D-1)-point
+// Gauss rule on each face (fem.py:265-292); one thread per face, the dots'
+// deterministic reduction.
+template <int D>
+struct BoundaryLoadOp {
+    static constexpr bool REDUCES = true;
+    Lat L;
+    Consts K;
+    const double* U;
+    const double* rho;      // NULL or (n_faces, 2^(D-1)) modulus at the face points
+    const int64_t* fcell;   // lattice cell index cx + nx (cy + ny cz)
+    const int32_t* fface;   // 2 axis + side
+    int dir;
+    int split;
+    double vol;             // cell volume (LevelMesh.cell_volume)
+    double* result;
+    __device__ bool skip() const { return false; }
+    __device__ void prepare() {}
+    __device__ void elem(int64_t i, double& a0, double&) const {
+        constexpr int NP = 1 << D, NQ = 1 << (D - 1);
+        const int64_t c = fcell[i];
+        const int f = fface[i];
+        const int axis = f >> 1, side = f & 1;
+        const int cx = (int)(c % L.nx);
+        const int64_t t = c / L.nx;
+        const int cy = D == 3 ? (int)(t % L.ny) : (int)t;
+        const int cz = D == 3 ? (int)(t / L.ny) : 0;
+        double cv[D + 1][NP];
+#pragma unroll
+        for (int n = 0; n < NP; ++n) {
+            const int64_t vid = vertex_id(L, cx + (n & 1), cy + ((n >> 1) & 1), D == 3 ? cz + ((n >> 2) & 1) : 0);
+#pragma unroll
+            for (int k = 0; k <= D; ++k) cv[k][n] = U[(int64_t)k * L.V + vid];
+        }
+        const double h[3] = {L.hx, L.hy, L.hz};
+        const double wq = (D == 2 ? 0.5 : 0.25) * (vol / h[axis]);     // w * area (fem.py:286-290)
+        const double sign = side == 1 ? 1.0 : -1.0;
+        int other[2] = {0, 0};
+        for (int a = 0, o = 0; a < D; ++a)
+            if (a != axis) other[o++] = a;
+        double sum = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            double x[3] = {0.0, 0.0, 0.0};
+            x[axis] = (double)side;
+            x[other[0]] = (D == 3 ? (q >> 1) : q) ? K.g1 : K.g0;       // meshgrid(pts, pts, "ij").ravel()
+            if (D == 3) x[other[1]] = (q & 1) ? K.g1 : K.g0;
+            double gu[D][D], phi = 0.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = 0; b < D; ++b) gu[a][b] = 0.0;
+#pragma unroll
+            for (int n = 0; n < NP; ++n) {
+                double B[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a) B[a] = ((n >> a) & 1) ? x[a] : 1.0 - x[a];
+                double N = 1.0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) N *= B[a];
+                phi = fma(N, cv[D][n], phi);
+#pragma unroll
+                for (int b = 0; b < D; ++b) {
+                    double g = ((n >> b) & 1) ? 1.0 : -1.0;
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+                        if (a != b) g *= B[a];
+                    g /= h[b];
+#pragma unroll
+                    for (int k = 0; k < D; ++k) gu[k][b] = fma(cv[k][n], g, gu[k][b]);
+                }
+            }
+            double sp, sm;   // sigma+[dir][axis], sigma-[dir][axis]
+            if (split == 0) {
+                double tr = 0.0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) tr += gu[a][a];
+                const double e = 0.5 * (gu[dir][axis] + gu[axis][dir]);
+                sp = 2.0 * K.mu * e + (dir == axis ? K.lam * tr : 0.0);
+                sm = 0.0;
+            } else if (D == 2) {
+                Spec2 S;
+                spectral2(gu[0][0], 0.5 * (gu[0][1] + gu[1][0]), gu[D - 1][D - 1], K, S);
+                sp = S.sp[dir][axis];
+                sm = S.sm[dir][axis];
+            } else {
+                const double e6[6] = {gu[0][0], gu[1 % D][1 % D], gu[D - 1][D - 1],
+                                      0.5 * (gu[0][1 % D] + gu[1 % D][0]),
+                                      0.5 * (gu[0][D - 1] + gu[D - 1][0]),
+                                      0.5 * (gu[1 % D][D - 1] + gu[D - 1][1 % D])};
+                Spec3 S;
+                spectral3(e6, K, S);
+                const int lo = dir < axis ? dir : axis, hi = dir < axis ? axis : dir;
+                const int m = lo == hi ? lo : (lo == 0 ? (hi == 1 ? 3 : 4) : 5);   // (00,11,22,01,02,12)
+                sp = S.sp[m];
+                sm = S.sm[m];
+            }
+            const double r = rho ? rho[i * NQ + q] : 1.0;
+            const double g = K.omk * (phi * phi) + K.kappa;
+            sum = fma(wq, sign * (g * r * sp + r * sm), sum);
+        }
+        a0 += sum;
+    }
+    __device__ void finish(double s0, double) const { *result = s0; }
+};
+
+extern "C" int pffmg_boundary_load(const pffmg_lattice* lat, const pffmg_state* st, const int64_t* face_cell,
+                                   const int32_t* face_id, int64_t n_faces, int direction, const double* rho_face,
+                                   double* result, void* stream) {
+    PFFMG_REQUIRE(lat && st && st->U && result && n_faces >= 0 && (n_faces == 0 || (face_cell && face_id)),
+                  "pffmg_boundary_load: bad args");
+    PFFMG_REQUIRE(st->split == 0 || st->split == 1, "pffmg_boundary_load: unknown split %d", st->split);
+    Lat L;
+    Consts K;
+    int rc = make_lat(lat, &L);
+    if (rc) return rc;
+    rc = make_consts(lat, st, &K);
+    if (rc) return rc;
+    PFFMG_REQUIRE(L.order == 1, "pffmg_boundary_load: Q1 lattices only (reference model.py:511-547)");
+    PFFMG_REQUIRE(direction >= 0 && direction < L.dim, "pffmg_boundary_load: direction %d", direction);
+    const double vol = L.dim == 3 ? L.hx * L.hy * L.hz : L.hx * L.hy;
+    const cudaStream_t s = as_stream(stream);
+    if (L.dim == 2)
+        return run_fused(BoundaryLoadOp<2>{L, K, st->U, rho_face, face_cell, face_id, direction, st->split, vol,
+                                           result},
+                         n_faces, s, "pffmg_boundary_load");
+    return run_fused(BoundaryLoadOp<3>{L, K, st->U, rho_face, face_cell, face_id, direction, st->split, vol, result},
+                     n_faces, s, "pffmg_boundary_load");
+}
+
 extern "C" int pffmg_qoi(const pffmg_lattice* lat, const pffmg_state* st, int kind, double* result,
                          void* stream) {
     PFFMG_REQUIRE(lat && st && st->U && result && kind >= 0 && kind <= 2, "pffmg_qoi: bad args");

@@ -87,8 +87,9 @@ class Hierarchy:
         return self.levels[-1]
 
 
-def build_hierarchy(blocks, n_levels, dim):
-    return Hierarchy(dim, _build_levels(blocks, n_levels, dim))
+def build_hierarchy(blocks, n_levels, dim, tagger=None):
+    """Lattice-native twin of mesh._build_hierarchy (mesh.py:219-222)."""
+    return Hierarchy(dim, _build_levels(blocks, n_levels, dim, tagger))
 
 
 def build_q2_hierarchy(lo, hi, n_coarse, n_levels):

@@ -36,7 +36,8 @@ class LatticeMesh:
     key_mod, vertices, cells) -- the array ones lazily.
     """
 
-    def __init__(self, blocks, level, dim):
+    def __init__(self, blocks, level, dim, tagger=None):
+        self.tagger = tagger                                     # mesh.py:196-206 (None: all OUTER)
         blocks = np.asarray(blocks, dtype=float).reshape(-1, 2, dim)
         n = 2 ** level
         spacing = (blocks[0, 1] - blocks[0, 0]) / n
@@ -120,15 +121,75 @@ class LatticeMesh:
         return np.where((x >= lo) & (x < hi), ids, -1)
 
     @cached_property
-    def cells(self):
-        """Cells block by block, x fastest inside a block, corners x fastest
-        (mesh.py:180-194)."""
+    def cell_coords(self):
+        """Lattice coordinates (relative to kmin) of every cell, in mesh cell
+        order: block by block, x fastest inside a block (mesh.py:180-194)."""
         n = self.level_refinement
         grids = np.meshgrid(*([np.arange(n)] * self.dim), indexing="ij")
         local = np.stack([g.ravel() for g in grids[::-1]], axis=1)
-        base = (self.block_lows[:, None, :] + local[None, :, :]).reshape(-1, self.dim)
-        corners = base[:, None, :] + corner_bits(self.dim)[None, :, :]
+        return (self.block_lows[:, None, :] + local[None, :, :]).reshape(-1, self.dim)
+
+    @cached_property
+    def cells(self):
+        """Cells block by block, x fastest inside a block, corners x fastest
+        (mesh.py:180-194)."""
+        corners = self.cell_coords[:, None, :] + corner_bits(self.dim)[None, :, :]
         return self.vertex_ids(corners)
+
+    def lattice_cell_index(self, cell_ids):
+        """Lattice cell index cx + nx (cy + ny cz) of mesh cells."""
+        c = self.cell_coords[np.asarray(cell_ids, dtype=np.int64)]
+        idx = c[:, -1]
+        for a in range(self.dim - 2, -1, -1):
+            idx = idx * self.ncell[a] + c[:, a]
+        return idx.astype(np.int64)
+
+    # -- boundary faces (mesh.py:149-161, 196-206) -----------------------------
+    @cached_property
+    def _boundary(self):
+        occ = self._occupancy(False)                     # (z, y, x) / (y, x) cell occupancy
+        c = self.cell_coords
+        nf = 2 * self.dim
+        bnd = np.zeros((c.shape[0], nf), dtype=bool)
+        for f in range(nf):
+            a, side = f // 2, f % 2
+            nb = c.copy()
+            nb[:, a] += 1 if side else -1
+            inside = (nb[:, a] >= 0) & (nb[:, a] < self.ncell[a])
+            nbc = np.clip(nb, 0, self.ncell - 1)
+            exists = occ[tuple(nbc[:, ::-1].T)] & inside
+            bnd[:, f] = ~exists
+        rows = np.nonzero(bnd.ravel())[0]                # cell-major, face-minor: the reference order
+        bf_cell, bf_face = rows // nf, rows % nf
+        lo = (c[bf_cell] + self.kmin).astype(float) * self.cell_size
+        hi = (c[bf_cell] + self.kmin + 1).astype(float) * self.cell_size
+        axis, side = bf_face // 2, bf_face % 2
+        k = np.arange(len(bf_face))
+        plane = (c[bf_cell, axis] + self.kmin[axis] + side).astype(float) * self.cell_size[axis]
+        lo[k, axis] = plane
+        hi[k, axis] = plane
+        if self.tagger is None:
+            tag = np.zeros(len(bf_cell), dtype=np.int64)
+        else:
+            tag = np.asarray(self.tagger(lo, hi, axis, side), dtype=np.int64)
+        return bf_cell.astype(np.int64), bf_face.astype(np.int64), tag
+
+    @property
+    def bf_cell(self):
+        return self._boundary[0]
+
+    @property
+    def bf_face(self):
+        return self._boundary[1]
+
+    @property
+    def bf_tag(self):
+        return self._boundary[2]
+
+    def cell_lower_corners(self, cell_ids):
+        """Coordinates of the low corner of mesh cells (LevelMesh.cell_bounds()[0])."""
+        c = self.cell_coords[np.asarray(cell_ids, dtype=np.int64)]
+        return (c + self.kmin).astype(float) * self.cell_size
 
 
 def _row_runs(occ):
@@ -144,9 +205,10 @@ def _row_runs(occ):
     return lo.astype(np.int32), hi.astype(np.int32), cnt.astype(np.int64)
 
 
-def build_hierarchy(blocks, n_levels, dim):
-    """Levels 0 (coarsest) .. n_levels-1 of a block union (mesh.py:219-222)."""
-    return [LatticeMesh(blocks, l, dim) for l in range(n_levels)]
+def build_hierarchy(blocks, n_levels, dim, tagger=None):
+    """Levels 0 (coarsest) .. n_levels-1 of a block union (mesh.py:219-222);
+    `tagger(fv_lo, fv_hi, axis, side)` tags the boundary faces as there."""
+    return [LatticeMesh(blocks, l, dim, tagger) for l in range(n_levels)]
 
 
 class Q2LatticeMesh:

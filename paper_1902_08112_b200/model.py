@@ -31,7 +31,7 @@ from .lattice import LatticeMesh, device_lattice
 
 __all__ = ["SplitKind", "MaterialParams", "LinearizationState", "ConstraintMask", "residual",
            "PhaseFieldOperator", "extrapolate", "degradation", "jacobian_vmult", "diagonal",
-           "crack_energy", "bulk_energy", "fracture_volume"]
+           "crack_energy", "bulk_energy", "fracture_volume", "boundary_load"]
 
 
 class SplitKind(Enum):
@@ -474,3 +474,74 @@ def fracture_volume(space, U):
     """Integral of (1 - phi) (model.py:500-504)."""
     p = MaterialParams(mu=0.0, lam=0.0, g_c=0.0, eps=1.0)
     return _qoi(space, U, p, SplitKind.NOSPLIT, None, 2)
+
+
+BOUNDARY_IDS = (0, 1, 2, 3)     # mesh.BoundaryId: OUTER, FIXED, LOADED, TRACTION_FREE (mesh.py:24-28)
+
+
+def _face_points(dim, axis, side):
+    """Reference-cell face quadrature points (fem.py:265-281 order)."""
+    g = np.array([0.5 - 0.5 / np.sqrt(3.0), 0.5 + 0.5 / np.sqrt(3.0)])
+    other = [a for a in range(dim) if a != axis]
+    if dim == 2:
+        ref = np.zeros((2, dim))
+        ref[:, other[0]] = g
+    else:
+        g0, g1 = np.meshgrid(g, g, indexing="ij")
+        ref = np.zeros((4, dim))
+        ref[:, other[0]] = g0.ravel()
+        ref[:, other[1]] = g1.ravel()
+    ref[:, axis] = float(side)
+    return ref
+
+
+def boundary_load(space, state, params, split, boundary, direction):
+    """Traction component `direction` integrated over the faces tagged
+    `boundary` (reference model.py:511-547): g(phi) rho sigma+ + rho sigma-
+    at the face Gauss points, one deterministic device reduction
+    (libpffmg pffmg_boundary_load)."""
+    import ctypes
+    if int(boundary) not in BOUNDARY_IDS:
+        raise ValueError(f"unknown boundary tag {boundary!r}")
+    _lib.require_cuda()
+    mesh = space.mesh
+    lat = device_lattice(mesh)
+    if getattr(lat.info, "order", 1) != 1:
+        raise ValueError("boundary_load is defined for the reference's Q1 elements only")
+    dim = lat.dim
+    if not 0 <= int(direction) < dim:
+        raise ValueError(f"direction {direction!r} out of range for dim {dim}")
+    rows = np.nonzero(np.asarray(mesh.bf_tag) == int(boundary))[0]
+    cells = np.asarray(mesh.bf_cell)[rows]
+    faces = np.asarray(mesh.bf_face)[rows]
+    if isinstance(mesh, LatticeMesh):
+        lcell = mesh.lattice_cell_index(cells)
+    else:
+        lcell = np.asarray(lat.info.cell_perm, dtype=np.int64)[cells]
+    Ud = dev(state.U)
+    if Ud.numel() != (dim + 1) * lat.n_vertices:
+        raise ValueError(f"U has {Ud.numel()} entries, expected {(dim + 1) * lat.n_vertices}")
+    rho = None
+    if getattr(params, "modulus_field", None) is not None and len(rows):
+        if isinstance(mesh, LatticeMesh):
+            lo = mesh.cell_lower_corners(cells)
+        else:
+            lo = np.asarray(mesh.vertices)[np.asarray(mesh.cells)[cells, 0]]
+        h = np.asarray(mesh.cell_size, dtype=float)
+        coords = np.empty((len(rows), 2 ** (dim - 1), dim))
+        for f in np.unique(faces):
+            sel = faces == f
+            coords[sel] = lo[sel][:, None, :] + _face_points(dim, int(f) // 2, int(f) % 2)[None, :, :] * h
+        rho = dev(np.asarray(params.modulus_field(coords), dtype=float).ravel())
+    st = _lib.State()
+    st.mu, st.lam, st.g_c = float(params.mu), float(params.lam), float(params.g_c)
+    st.kappa, st.eps = float(params.kappa), float(params.eps)
+    st.split = _split_code(split)
+    st.split_band = float(getattr(params, "split_band", 0.0) or 0.0)
+    st.U = Ud.data_ptr()
+    fc = dev(lcell.astype(np.int64), torch.int64)
+    ff = dev(faces.astype(np.int32), torch.int32)
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    _lib.call("pffmg_boundary_load", lat.ref, ctypes.byref(st), _lib.ptr(fc), _lib.ptr(ff), len(rows),
+              int(direction), _lib.ptr(rho), _lib.ptr(out), _lib.stream())
+    return float(out.item())

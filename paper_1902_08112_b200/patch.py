@@ -21,7 +21,7 @@ MGSOLVE = ["build_level_contexts", "contexts_from_operators", "vcycle", "coarse_
 KRYLOV = ["gmres", "estimate_spectrum"]
 
 
-MODEL_PHYSICS = ["residual", "crack_energy", "bulk_energy", "fracture_volume"]
+MODEL_PHYSICS = ["residual", "crack_energy", "bulk_energy", "fracture_volume", "boundary_load"]
 NONLINEAR = ["compute_active_set"]
 
 
@@ -31,7 +31,7 @@ def install(fracmg=None, operator=False, physics=False):
     operator=True also replaces `fracmg.model.PhaseFieldOperator` (NoSplit
     and the Miehe split, 2D and 3D).  physics=True also replaces the Newton
     right-hand side `model.residual`, the QoIs `model.crack_energy /
-    bulk_energy / fracture_volume` and `nonlinear.compute_active_set`, which
+    bulk_energy / fracture_volume / boundary_load` and `nonlinear.compute_active_set`, which
     the reference's ActiveSetSolver and scenarios.run look up at call time
     (nonlinear.py:146-150, 195; scenarios.py:411-415)."""
     if fracmg is None:

@@ -28,7 +28,7 @@ from fracmg import fem, krylov, mesh, mgsolve, model, selfcheck  # noqa: E402
 from fracmg.fem import ConstraintMask, Discretization  # noqa: E402
 from fracmg.model import LinearizationState, MaterialParams, SplitKind  # noqa: E402
 
-from tests.golden.specs import MESHES, modulus, params_for  # noqa: E402
+from tests.golden.specs import MESHES, face_tagger, modulus, params_for  # noqa: E402
 
 
 def ref_hierarchy(spec):
@@ -153,6 +153,33 @@ def gen_qoi():
             out[f"{name}/{variant}/miehe_band/bulk_energy"] = np.array(
                 model.bulk_energy(space, state, params, SplitKind.MIEHE))
     save("qoi", **out)
+
+
+def gen_boundary():
+    """boundary_load (model.py:511-547) on every mesh with the face_tagger tags:
+    every tag x direction, NoSplit / Miehe / blended Miehe, with and without a
+    modulus field; plus the reference's boundary-face arrays."""
+    out = {}
+    rng = np.random.default_rng(20261022)
+    for name, (blocks, n_levels, dim) in MESHES.items():
+        hier = mesh._build_hierarchy(blocks, n_levels, dim, face_tagger)
+        disc = Discretization(hier)
+        space = disc.finest
+        m = space.mesh
+        out[f"{name}/bf_cell"] = m.bf_cell
+        out[f"{name}/bf_face"] = m.bf_face
+        out[f"{name}/bf_tag"] = m.bf_tag
+        state = selfcheck.random_state(space, rng, t=0.1)
+        out[f"{name}/U"] = state.U
+        for variant in ("plain", "modulus"):
+            params = params_for(space, modulus if variant == "modulus" else None)
+            for split, band in ((SplitKind.NOSPLIT, 0.0), (SplitKind.MIEHE, 0.0), (SplitKind.MIEHE, 0.05)):
+                params.split_band = band
+                key = split.value + ("_band" if band else "")
+                vals = np.array([[model.boundary_load(space, state, params, split, tag, d)
+                                  for d in range(dim)] for tag in range(4)])
+                out[f"{name}/{variant}/{key}/load"] = vals
+    save("boundary", **out)
 
 
 def gen_transfers():
@@ -350,7 +377,7 @@ def gen_configs():
     save("configs", **out)
 
 
-FULL_CASES = (("cfg2", None), ("cfg4", None), ("cfg5", 6))
+FULL_CASES = (("cfg2", None), ("cfg4", None), ("cfg5", 6), ("cfg5", 7))
 FULL_SAMPLES = 4096
 
 
@@ -442,7 +469,7 @@ def gen_krylov():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["meshes", "operator", "operator_band", "transfers", "multigrid", "multigrid_miehe", "qoi", "configs", "krylov"]
+    which = sys.argv[1:] or ["meshes", "operator", "operator_band", "transfers", "multigrid", "multigrid_miehe", "qoi", "boundary", "configs", "krylov"]
     for w in which:
         print(w)
         globals()[f"gen_{w}"]()

@@ -52,3 +52,16 @@ def params_for(space, modulus_field=None, cls=None):
     scale = 1.0 if space.mesh.cell_size[0] < 10 else 250.0
     return cls(mu=1.3, lam=0.9, g_c=0.7, kappa=1e-10, eps=2.0 * scale,
                pressure_fn=lambda t: 10.0 * t, modulus_field=modulus_field)
+
+
+def face_tagger(fv_lo, fv_hi, axis, side):
+    """Boundary tags of the boundary-load goldens (mesh.py:196-206 tagger
+    signature): y-low faces FIXED (1), y-high LOADED (2), x faces
+    TRACTION_FREE (3), the rest OUTER (0)."""
+    axis = np.asarray(axis)
+    side = np.asarray(side)
+    tag = np.zeros(len(axis), dtype=np.int64)
+    tag[axis == 0] = 3
+    tag[(axis == 1) & (side == 0)] = 1
+    tag[(axis == 1) & (side == 1)] = 2
+    return tag

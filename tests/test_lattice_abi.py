@@ -150,3 +150,16 @@ def test_struct_size_guard_rejects_foreign_layouts():
     L.hx = L.hy = 0.25
     rc = lib.pffmg_apply(ctypes.byref(L), ctypes.byref(st), -1, None, None, None)
     assert rc == 1 and b"pffmg_state.struct_size" in lib.pffmg_last_error()
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+def test_lattice_boundary_faces_match_reference(golden, name):
+    """LatticeMesh's boundary faces and tags (lattice-native) equal the
+    reference's _extract_boundary + tagger arrays (mesh.py:149-161, 196-206)."""
+    from tests.golden.specs import face_tagger
+    g = golden["boundary"]
+    blocks, n_levels, dim = MESHES[name]
+    m = lattice.build_hierarchy(blocks, n_levels, dim, face_tagger)[-1]
+    assert np.array_equal(m.bf_cell, g[f"{name}/bf_cell"])
+    assert np.array_equal(m.bf_face, g[f"{name}/bf_face"])
+    assert np.array_equal(m.bf_tag, g[f"{name}/bf_tag"])
