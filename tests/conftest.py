@@ -41,7 +41,7 @@ class Golden:
 
 @pytest.fixture(scope="session")
 def golden():
-    return {n: Golden(n) for n in ("meshes", "operator", "operator_band", "transfers", "multigrid", "multigrid_miehe", "qoi", "boundary", "configs", "configs_full", "krylov")}
+    return {n: Golden(n) for n in ("meshes", "operator", "operator_band", "transfers", "multigrid", "multigrid_miehe", "qoi", "boundary", "configs", "configs_full", "newton", "scenarios", "krylov")}
 
 
 def rel_err(a, b):

@@ -444,6 +444,56 @@ def gen_configs_full(threads=8):
     print(f"  wrote configs_full.npz ({os.path.getsize(path) / 1024:.0f} KiB)")
 
 
+def gen_newton(threads=8):
+    """One incremental step of the reference's own Newton driver
+    (nonlinear.ActiveSetSolver.solve_step, nonlinear.py:117-215), unpatched,
+    on cfg1 and cfg2 at 256^2: the converged U and active set and the
+    per-iteration history (set size, changed, filtered residual norm, GMRES
+    iterations).  tests/test_gpu_patch.py runs the same driver with the GPU
+    twins installed (patch.install) and compares."""
+    from fracmg import nonlinear
+    from paper_1902_08112_b200 import configs
+    out = {}
+    for name, levels in (("cfg1", None), ("cfg2", 6)):
+        tag = name if levels is None else f"{name}_l{levels}"
+        t0 = time.time()
+        prob = configs.make(name, levels)
+        disc, state, params, dirichlet = _ref_problem(prob)
+        V = disc.finest.dofmap.n_vertices
+        cfg = nonlinear.SolverConfig(cheb_degree=prob.degree, threads=threads)
+        solver = nonlinear.ActiveSetSolver(disc, params, SplitKind.NOSPLIT, cfg)
+        dim = disc.finest.dim
+        U, rep, active = solver.solve_step(state, dirichlet, state.U[dim * V:])
+        out[f"{tag}/U"] = U
+        out[f"{tag}/active"] = active
+        out[f"{tag}/history"] = np.array([[h.set_size, float(h.set_changed), h.residual_norm, h.gmres_iters]
+                                          for h in rep.history])
+        out[f"{tag}/converged"] = np.array(rep.converged)
+        print(f"  {tag}: {rep.iterations} active-set iterations, gmres {rep.gmres_iters} "
+              f"({time.time() - t0:.1f}s)")
+    save("newton", **out)
+
+
+from tests.golden.make_golden_specs import SCENARIOS, scenario  # noqa: E402
+
+
+def gen_scenarios():
+    """The reference's time loop scenarios.run (scenarios.py:345-426), unpatched:
+    per step the active-set iterations, GMRES iterations, boundary load,
+    crack and bulk energy and active-set size.  Pressurised fractures with the
+    noise modulus field (NoSplit), 2D / 3D L-shapes (Miehe split with the
+    run's C^1 band, LOADED boundary load)."""
+    from fracmg import scenarios
+    out = {}
+    for tag, _, _ in SCENARIOS:
+        t0 = time.time()
+        recs = scenarios.run(scenario(scenarios, tag))
+        out[f"{tag}/records"] = np.array([[r.step, r.time, r.active_set_iters, sum(r.gmres_iters_per_as_step),
+                                           r.load, r.crack_energy, r.bulk_energy, r.n_active] for r in recs])
+        print(f"  {tag}: {len(recs)} steps ({time.time() - t0:.1f}s)")
+    save("scenarios", **out)
+
+
 def gen_krylov():
     out = {}
     K = np.zeros((9, 9))
@@ -469,7 +519,7 @@ def gen_krylov():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["meshes", "operator", "operator_band", "transfers", "multigrid", "multigrid_miehe", "qoi", "boundary", "configs", "krylov"]
+    which = sys.argv[1:] or ["meshes", "operator", "operator_band", "transfers", "multigrid", "multigrid_miehe", "qoi", "boundary", "configs", "newton", "scenarios", "krylov"]
     for w in which:
         print(w)
         globals()[f"gen_{w}"]()
