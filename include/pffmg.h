@@ -343,6 +343,47 @@ int pffmg_cg_start(const double* b, const double* diag, double* r, double* z, do
 int pffmg_cg_step(const double* Ap, const double* diag, double* r, double* z, double* p,
                   int64_t n, double* scal, int phase, void* stream);
 
+/* ------------------------------------------ slab-sharded (multi-GPU) Krylov
+ * Reductions over a rank's OWNED rows only: element i of a block vector
+ * (component stride V) counts iff own_a <= i mod V < own_b (own_a = 0,
+ * own_b = V: every element).  Each returns the rank-local partial sum; the
+ * caller all-reduces it (one scalar / short vector per pass) before the next
+ * step consumes it.  Deterministic like pffmg_dot. */
+
+/* result = sum over owned rows of x*y. */
+int pffmg_dot_owned(const double* x, const double* y, int64_t n, int64_t V, int64_t own_a,
+                    int64_t own_b, double* result, void* stream);
+
+/* Jacobi-PCG Lanczos of estimate_spectrum (krylov.py:146-185) with owned-row
+ * partial reductions.  phase 0: r = b, z = D^-1 r, p = z, partial r.z ->
+ * scal[0]; 1: partial p.Ap -> scal[6]; 2: r -= alpha Ap, z = D^-1 r, partial
+ * r.z -> scal[7]; 3: p = z + beta p.  After all-reducing the partial,
+ * pffmg_cg_dist_finish(scal, phase) (phases 0..2) applies the reference's
+ * breakdown rules and records alpha / beta (scal layout of pffmg_cg_step). */
+int pffmg_cg_dist(int phase, const double* b_or_Ap, const double* diag, double* r, double* z, double* p,
+                  int64_t n, int64_t V, int64_t own_a, int64_t own_b, double* scal, void* stream);
+int pffmg_cg_dist_finish(double* scal, int phase, void* stream);
+
+/* Classical Gram-Schmidt passes of the distributed Arnoldi step (CGS2; the
+ * single-GPU path keeps the reference's MGS, pffmg_arnoldi_mgs).
+ * multi_dot: out[t] = owned V_{i0+t} . w for t < cnt, and (with_norm)
+ * out[cnt] = owned w . w;  gs_subtract: w -= sum_{t<k} c[t] V_t, hacc[t] +=
+ * c[t] (hacc may be NULL), and (norm2 != NULL) the owned partial of the new
+ * w . w into *norm2;  normalize: h = sqrt(*s2), *hout = h, dst = src / h
+ * (dst = src when h == 0, krylov.py:108-110). */
+int pffmg_multi_dot_owned(const double* Vb, int64_t ld, int i0, int cnt, const double* w, int with_norm,
+                          int64_t n, int64_t V, int64_t own_a, int64_t own_b, double* out, void* stream);
+int pffmg_gs_subtract(const double* Vb, int64_t ld, int k, const double* c, double* w, int64_t n,
+                      double* hacc, int64_t V, int64_t own_a, int64_t own_b, double* norm2, void* stream);
+int pffmg_normalize(const double* src, double* dst, int64_t n, const double* s2, double* hout,
+                    void* stream);
+
+/* Halo packing: pack (unpack = 0) buf[c len + t] = vec[c V + a + t] for
+ * c < n_comp, t < len, or unpack (unpack = 1) the reverse -- one contiguous
+ * message per neighbour instead of one per component. */
+int pffmg_pack_rows(double* vec, int64_t V, int n_comp, int64_t a, int64_t len, double* buf, int unpack,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

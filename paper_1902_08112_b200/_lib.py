@@ -103,6 +103,14 @@ _SIGS = {
     "pffmg_active_set": [vp, vp, vp, vp, C.c_double, vp, C.c_int, C.c_int64, vp, vp],
     "pffmg_cg_start": [vp, vp, vp, vp, vp, C.c_int64, vp, vp],
     "pffmg_cg_step": [vp, vp, vp, vp, vp, C.c_int64, vp, C.c_int, vp],
+    "pffmg_dot_owned": [vp, vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, vp, vp],
+    "pffmg_cg_dist": [C.c_int, vp, vp, vp, vp, vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, vp, vp],
+    "pffmg_cg_dist_finish": [vp, C.c_int, vp],
+    "pffmg_multi_dot_owned": [vp, C.c_int64, C.c_int, C.c_int, vp, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                              C.c_int64, vp, vp],
+    "pffmg_gs_subtract": [vp, C.c_int64, C.c_int, vp, vp, C.c_int64, vp, C.c_int64, C.c_int64, C.c_int64, vp, vp],
+    "pffmg_normalize": [vp, vp, C.c_int64, vp, vp, vp],
+    "pffmg_pack_rows": [vp, C.c_int64, C.c_int, C.c_int64, C.c_int64, vp, C.c_int, vp],
 }
 
 _lib = None

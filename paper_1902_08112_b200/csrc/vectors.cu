@@ -195,7 +195,7 @@ struct ScaleByInvOp {      // V_{j+1} = w / h  when h != 0 (krylov.py:108-110)
 
 // ------------------------------------------------ CG-Lanczos (krylov.py:146-185)
 // scal layout
-enum { C_RZ = 0, C_STOP = 1, C_ALPHA = 2, C_BETA = 3, C_K = 4, C_NB = 5, C_PAP = 6, C_HIST = 8 };
+enum { C_RZ = 0, C_STOP = 1, C_ALPHA = 2, C_BETA = 3, C_K = 4, C_NB = 5, C_PAP = 6, C_RZN = 7, C_HIST = 8 };
 constexpr int CG_MAXIT = 64;
 
 struct CgStartOp {
@@ -1020,4 +1020,253 @@ extern "C" int pffmg_cg_step(const double* Ap, const double* diag, double* r, do
     if (phase == 0) return run_fused(CgPApOp{p, Ap, scal}, n, s, "pffmg_cg_step");
     if (phase == 1) return run_fused(CgUpdateOp{Ap, diag, r, z, scal, 0.0}, n, s, "pffmg_cg_step");
     return run_fused(CgPOp{z, p, scal, 0.0}, n, s, "pffmg_cg_step");
+}
+
+// ================================================== slab-sharded Krylov (§8e)
+namespace pffmg {
+
+// owned-row predicate of a block vector with component stride V
+struct Own {
+    int64_t V, a, b;
+    __device__ __forceinline__ bool in(int64_t i) const {
+        if (a <= 0 && b >= V) return true;
+        const int64_t v = i % V;
+        return v >= a && v < b;
+    }
+};
+
+struct DotOwnOp {
+    static constexpr bool REDUCES = true;
+    const double *x, *y;
+    Own own;
+    double* result;
+    __device__ bool skip() const { return false; }
+    __device__ void prepare() {}
+    __device__ void elem(int64_t i, double& a0, double&) const {
+        if (own.in(i)) a0 = fma(x[i], y[i], a0);
+    }
+    __device__ void finish(double s0, double) const { *result = s0; }
+};
+
+// CG-Lanczos phases with owned partials (finish deferred to cg_dist_finish_k)
+struct CgDistOp {
+    static constexpr bool REDUCES = true;
+    int phase;
+    const double *in, *diag;
+    double *r, *z, *p, *scal;
+    Own own;
+    double alpha, beta;
+    __device__ bool skip() const { return phase != 0 && scal[C_STOP] != 0.0; }
+    __device__ void prepare() {
+        if (phase == 2) alpha = scal[C_ALPHA];
+        if (phase == 3) beta = scal[C_BETA];
+    }
+    __device__ void elem(int64_t i, double& a0, double&) const {
+        if (phase == 0) {                                   // krylov.py:163-166
+            const double ri = in[i];
+            const double zi = ri / diag[i];
+            r[i] = ri;
+            z[i] = zi;
+            p[i] = zi;
+            if (own.in(i)) a0 = fma(ri, zi, a0);
+        } else if (phase == 1) {
+            if (own.in(i)) a0 = fma(p[i], in[i], a0);
+        } else if (phase == 2) {
+            const double ri = r[i] - alpha * in[i];
+            const double zi = ri / diag[i];
+            r[i] = ri;
+            z[i] = zi;
+            if (own.in(i)) a0 = fma(ri, zi, a0);
+        } else {
+            p[i] = z[i] + beta * p[i];
+        }
+    }
+    __device__ void finish(double s0, double) const {
+        if (phase == 0) scal[C_RZ] = s0;
+        else if (phase == 1) scal[C_PAP] = s0;
+        else if (phase == 2) scal[C_RZN] = s0;
+    }
+};
+
+// the finish logic of CgStartOp / CgPApOp / CgUpdateOp on all-reduced sums
+__global__ void cg_dist_finish_k(double* scal, int phase) {
+    pdl_wait();
+    if (phase == 0) {
+        const double s0 = scal[C_RZ];
+        scal[C_STOP] = (s0 > 0.0 && isfinite(s0)) ? 0.0 : 1.0;
+        scal[C_K] = 0.0;
+        scal[C_NB] = 0.0;
+        return;
+    }
+    if (scal[C_STOP] != 0.0) return;
+    if (phase == 1) {
+        const double s0 = scal[C_PAP];
+        if (!(s0 > 0.0 && isfinite(s0))) {
+            scal[C_STOP] = 1.0;
+            return;
+        }
+        const double alpha = scal[C_RZ] / s0;
+        const int k = (int)scal[C_K];
+        scal[C_ALPHA] = alpha;
+        if (k < CG_MAXIT) scal[C_HIST + k] = alpha;
+        scal[C_K] = k + 1;
+    } else {
+        const double s0 = scal[C_RZN], rz = scal[C_RZ];
+        if (s0 <= 1e-28 * rz || !isfinite(s0)) {
+            scal[C_STOP] = 1.0;
+            return;
+        }
+        const double beta = s0 / rz;
+        const int nb = (int)scal[C_NB];
+        scal[C_BETA] = beta;
+        if (nb < CG_MAXIT) scal[C_HIST + CG_MAXIT + nb] = beta;
+        scal[C_NB] = nb + 1;
+        scal[C_RZ] = s0;
+    }
+}
+
+// up to two dots of V_i . w (and w . w) per launch: the fused two-sum kernel
+struct Dot2Op {
+    static constexpr bool REDUCES = true;
+    const double *v0, *v1, *w;   // v1 == nullptr -> the second sum is w . w (when norm) or unused
+    int norm;
+    Own own;
+    double *o0, *o1;
+    __device__ bool skip() const { return false; }
+    __device__ void prepare() {}
+    __device__ void elem(int64_t i, double& a0, double& a1) const {
+        if (!own.in(i)) return;
+        const double wi = w[i];
+        if (v0) a0 = fma(v0[i], wi, a0);
+        if (v1) a1 = fma(v1[i], wi, a1);
+        else if (norm) a1 = fma(wi, wi, a1);
+    }
+    __device__ void finish(double s0, double s1) const {
+        if (o0) *o0 = s0;
+        if (o1) *o1 = s1;
+    }
+};
+
+struct GsSubOp {
+    static constexpr bool REDUCES = true;
+    const double* Vb;
+    int64_t ld;
+    int k;
+    const double* c;
+    double* w;
+    double* hacc;
+    Own own;
+    double* norm2;
+    __device__ bool skip() const { return false; }
+    __device__ void prepare() {}
+    __device__ void elem(int64_t i, double& a0, double&) const {
+        double s = 0.0;
+        for (int t = 0; t < k; ++t) s = fma(__ldg(c + t), Vb[(int64_t)t * ld + i], s);
+        const double wi = w[i] - s;
+        w[i] = wi;
+        if (norm2 && own.in(i)) a0 = fma(wi, wi, a0);
+    }
+    __device__ void finish(double s0, double) const {
+        if (norm2) *norm2 = s0;
+        if (hacc)
+            for (int t = 0; t < k; ++t) hacc[t] += c[t];
+    }
+};
+
+struct NormalizeOp {
+    static constexpr bool REDUCES = true;    // (for the finisher: *hout)
+    const double* src;
+    double* dst;
+    const double* s2;
+    double* hout;
+    double hv;
+    __device__ bool skip() const { return false; }
+    __device__ void prepare() { hv = sqrt(*s2); }
+    __device__ void elem(int64_t i, double&, double&) const { dst[i] = hv != 0.0 ? src[i] / hv : src[i]; }
+    __device__ void finish(double, double) const {
+        if (hout) *hout = hv;
+    }
+};
+
+__global__ void pack_rows_k(double* vec, int64_t V, int nc, int64_t a, int64_t len, double* buf, int unpack) {
+    pdl_wait();
+    const int64_t n = len * nc;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / len, t = i - c * len;
+        double* g = vec + c * V + a + t;
+        if (unpack)
+            *g = buf[i];
+        else
+            buf[i] = *g;
+    }
+}
+
+}  // namespace pffmg
+
+extern "C" int pffmg_dot_owned(const double* x, const double* y, int64_t n, int64_t V, int64_t own_a,
+                               int64_t own_b, double* result, void* stream) {
+    PFFMG_REQUIRE(x && y && result && n >= 0 && V > 0, "pffmg_dot_owned: bad args");
+    return run_fused(DotOwnOp{x, y, Own{V, own_a, own_b}, result}, n, as_stream(stream), "pffmg_dot_owned");
+}
+
+extern "C" int pffmg_cg_dist(int phase, const double* b_or_Ap, const double* diag, double* r, double* z, double* p,
+                             int64_t n, int64_t V, int64_t own_a, int64_t own_b, double* scal, void* stream) {
+    PFFMG_REQUIRE(phase >= 0 && phase <= 3 && r && z && p && scal && V > 0 &&
+                      (phase == 3 || b_or_Ap) && (phase == 1 || phase == 3 || diag),
+                  "pffmg_cg_dist: bad args");
+    CgDistOp op{phase, b_or_Ap, diag, r, z, p, scal, Own{V, own_a, own_b}, 0.0, 0.0};
+    return run_fused(op, n, as_stream(stream), "pffmg_cg_dist");
+}
+
+extern "C" int pffmg_cg_dist_finish(double* scal, int phase, void* stream) {
+    PFFMG_REQUIRE(scal && phase >= 0 && phase <= 2, "pffmg_cg_dist_finish: bad args");
+    pdl_launch(cg_dist_finish_k, dim3(1), dim3(1), 0, as_stream(stream), scal, phase);
+    return check_launch("pffmg_cg_dist_finish");
+}
+
+extern "C" int pffmg_multi_dot_owned(const double* Vb, int64_t ld, int i0, int cnt, const double* w, int with_norm,
+                                     int64_t n, int64_t V, int64_t own_a, int64_t own_b, double* out,
+                                     void* stream) {
+    PFFMG_REQUIRE(Vb && w && out && i0 >= 0 && cnt >= 0 && ld >= n && V > 0, "pffmg_multi_dot_owned: bad args");
+    const Own own{V, own_a, own_b};
+    const cudaStream_t s = as_stream(stream);
+    // pairs of dots per launch; the norm rides in the free second slot of the last one
+    bool norm_done = !with_norm;
+    for (int t = 0; t < cnt; t += 2) {
+        const double* v0 = Vb + (int64_t)(i0 + t) * ld;
+        const double* v1 = t + 1 < cnt ? Vb + (int64_t)(i0 + t + 1) * ld : nullptr;
+        const bool nrm = !v1 && !norm_done;
+        Dot2Op op{v0, v1, w, nrm ? 1 : 0, own, out + t, v1 ? out + t + 1 : (nrm ? out + cnt : nullptr)};
+        if (nrm) norm_done = true;
+        const int rc = run_fused(op, n, s, "pffmg_multi_dot_owned");
+        if (rc) return rc;
+    }
+    if (!norm_done) {
+        Dot2Op op{nullptr, nullptr, w, 1, own, nullptr, out + cnt};
+        return run_fused(op, n, s, "pffmg_multi_dot_owned");
+    }
+    return PFFMG_OK;
+}
+
+extern "C" int pffmg_gs_subtract(const double* Vb, int64_t ld, int k, const double* c, double* w, int64_t n,
+                                 double* hacc, int64_t V, int64_t own_a, int64_t own_b, double* norm2,
+                                 void* stream) {
+    PFFMG_REQUIRE(Vb && c && w && k >= 0 && ld >= n && V > 0, "pffmg_gs_subtract: bad args");
+    return run_fused(GsSubOp{Vb, ld, k, c, w, hacc, Own{V, own_a, own_b}, norm2}, n, as_stream(stream),
+                     "pffmg_gs_subtract");
+}
+
+extern "C" int pffmg_normalize(const double* src, double* dst, int64_t n, const double* s2, double* hout,
+                               void* stream) {
+    PFFMG_REQUIRE(src && dst && s2 && n >= 0, "pffmg_normalize: bad args");
+    return run_fused(NormalizeOp{src, dst, s2, hout, 0.0}, n, as_stream(stream), "pffmg_normalize");
+}
+
+extern "C" int pffmg_pack_rows(double* vec, int64_t V, int n_comp, int64_t a, int64_t len, double* buf, int unpack,
+                               void* stream) {
+    PFFMG_REQUIRE(vec && buf && n_comp >= 1 && a >= 0 && len >= 0 && a + len <= V, "pffmg_pack_rows: bad args");
+    if (len == 0) return PFFMG_OK;
+    pdl_launch(pack_rows_k, dim3(vgrid(len * n_comp)), dim3(256), 0, as_stream(stream), vec, V, n_comp, a, len, buf,
+               unpack);
+    return check_launch("pffmg_pack_rows");
 }

@@ -10,9 +10,16 @@ run on the rank's slab lattice (`own_lo/own_hi/plane0` of pffmg_lattice):
 * every stencil kernel (block vmults / Chebyshev steps, V-cycle residual,
   restriction, prolongation) is preceded by a ghost-plane halo exchange of
   its input (NCCL send/recv of one plane per neighbour and component);
-* inner products sum the owned planes and all-reduce one scalar (GMRES
-  MGS, CG-Lanczos), so every rank sees identical Krylov scalars and the
-  same iteration count as a single GPU up to rounding;
+* inner products are libpffmg reductions over the rank's OWNED rows
+  (pffmg_dot_owned / pffmg_cg_dist / pffmg_multi_dot_owned) followed by one
+  all-reduce of the partials: CG-Lanczos takes 2 all-reduces per iteration
+  with alpha / beta and the breakdown rules applied on the device
+  (pffmg_cg_dist_finish), the Arnoldi step is CGS2 -- two classical
+  Gram-Schmidt passes, each one fused multi-dot and one all-reduce of the
+  whole column, then the norm -- 3 all-reduces per step instead of the j+2
+  sequential ones of distributed MGS (the single-GPU path keeps the
+  reference's MGS); every rank sees identical Krylov scalars, and the
+  iteration counts equal the single-GPU ones up to rounding;
 * the control flow is the reference's (krylov.py:50-136, mgsolve.py:82-283).
 """
 from __future__ import annotations
@@ -26,7 +33,7 @@ from . import _lib
 from .arrays import empty, flags_buffer, host, pack_flags, zeros
 from .distributed import (Halo, SlabMesh, SlabPartition, SlabSpace, allreduce_, local_info, owned_slices,
                           to_local)
-from .krylov import NoConvergence, SolverControl, lanczos_extremes, probe_vector
+from .krylov import CG_MAXIT, NoConvergence, SolverControl, lanczos_extremes, probe_vector
 from .lattice import device_lattice, info_from_mesh
 
 from .model import DeviceMask, LinearizationState, PhaseFieldOperator
@@ -53,6 +60,10 @@ class _Level:
         self.halo = Halo(self.info, slab, rank, world, group)
         self.owned = owned_slices(self.nc, self.info)
         self.sharded = not (slab.replicated or world == 1)
+        # owned vertex range [own_a, own_b) of the rank-local numbering (owned-row reductions)
+        offs = self.info.plane_offsets()
+        lo, hi = self.info.own if tuple(self.info.own) != (0, 0) else (0, self.info.n_planes)
+        self.own_ab = (int(offs[lo]), int(offs[hi]))
 
 
 class DistGMG:
@@ -82,22 +93,19 @@ class DistGMG:
                 self.virt[l - 1] = device_lattice(SlabMesh(vi))
 
     # --------------------------------------------------------------- helpers
-    def dot_dev(self, lev, x, y):
-        """Owned-dof inner product as a 1-element CUDA tensor, all-reduced (no host sync)."""
-        t = torch.zeros(1, dtype=torch.float64, device=x.device)
-        for s in lev.owned:
-            t += torch.dot(x[s], y[s])
+    def dot_dev(self, lev, x, y, out=None):
+        """Owned-row inner product (pffmg_dot_owned), all-reduced; a 1-element
+        device tensor (no host sync)."""
+        t = out if out is not None else torch.zeros(1, dtype=torch.float64, device=x.device)
+        a, b = lev.own_ab
+        _lib.call("pffmg_dot_owned", _lib.ptr(x), _lib.ptr(y), x.numel(), lev.V, a, b, _lib.ptr(t),
+                  _lib.stream())
         if lev.sharded:
             allreduce_(t, self.group)
         return t
 
     def dot(self, lev, x, y):
-        t = torch.zeros(1, dtype=torch.float64, device=x.device)
-        for s in lev.owned:
-            t += torch.dot(x[s], y[s])
-        if lev.sharded:
-            allreduce_(t, self.group)
-        return float(t.item())
+        return float(self.dot_dev(lev, x, y).item())
 
     def _inject(self, l, fine_vec, coarse_vec, ncomp, flags=False):
         """Coarse := fine at coincident vertices (owned coarse planes), then ghosts."""
@@ -160,17 +168,21 @@ class DistGMG:
             lev.diag = diag
         recs = [self._cg_records(l) for l in range(len(self.L))]
         host_recs = host(torch.stack([t for pair in recs for t in pair]))    # one host sync
-        self.spectra = [tuple(self._spectra_from(host_recs[2 * l + k]) for k in range(2))
+        self.spectra = [tuple(lanczos_extremes(host_recs[2 * l + k], self.eig_iters) for k in range(2))
                         for l in range(len(self.L))]
         self._buffers()
         return self
 
     def _cg_records(self, l):
-        """Jacobi-PCG of both blocks of level l (krylov.py:146-185) with distributed
-        dots kept on the device: returns per block the 1 + 2 n scalars
-        (rz_0, pAp_1, rz_1, pAp_2, ...) -- no host synchronisation here."""
+        """Jacobi-PCG of both blocks of level l (krylov.py:146-185) on the device:
+        owned-row partial sums (pffmg_cg_dist), one all-reduce per reduction
+        (2 per iteration), alpha / beta and the breakdown rules applied on the
+        device (pffmg_cg_dist_finish).  Returns the two scalar records (the
+        layout of pffmg_cg_step) -- no host synchronisation here."""
         lev, op = self.L[l], self.ops[l]
         recs = []
+        a, b_ = lev.own_ab
+        st = _lib.stream()
         for k in range(2):
             blk = slice(0, lev.dim * lev.V) if k == 0 else slice(lev.dim * lev.V, lev.n)
             nk = lev.dim if k == 0 else 1
@@ -181,49 +193,30 @@ class DistGMG:
             b = b.contiguous().clone()
             comp0 = 0 if k == 0 else lev.dim
             _lib.call("pffmg_masked_copy", _lib.ptr(lev.flags), lev.V, comp0, nk, _lib.ptr(b), _lib.ptr(b),
-                      _lib.stream())
+                      st)
             diag = lev.diag[blk]
-            bl = _BlockView(lev, k)
-            r = b.clone()
-            z = r / diag
-            p = z.clone()
-            Ap = torch.empty_like(p)
-            rz = bl.dot_dev(self, r, z)
-            rec = [rz]
+            n = b.numel()
+            r, z, p, Ap = empty(n), empty(n), empty(n), empty(n)
+            scal = torch.zeros(8 + 2 * CG_MAXIT, dtype=torch.float64, device="cuda")
+
+            def phase(ph, src):
+                _lib.call("pffmg_cg_dist", ph, _lib.ptr(src), _lib.ptr(diag), _lib.ptr(r), _lib.ptr(z),
+                          _lib.ptr(p), n, lev.V, a, b_, _lib.ptr(scal), st)
+                if ph < 3:
+                    if lev.sharded:
+                        slot = (0, 6, 7)[ph]
+                        allreduce_(scal[slot:slot + 1], self.group)
+                    _lib.call("pffmg_cg_dist_finish", _lib.ptr(scal), ph, st)
+
+            phase(0, b)
             for _ in range(self.eig_iters):
                 lev.halo.exchange(p, nk)
                 op.apply_dev(k, p, Ap, pre=True)
-                pAp = bl.dot_dev(self, p, Ap)
-                r = r - (rz / pAp) * Ap
-                z = r / diag
-                rz_new = bl.dot_dev(self, r, z)
-                p = z + (rz_new / rz) * p
-                rec += [pAp, rz_new]
-                rz = rz_new
-            recs.append(torch.cat(rec))
+                phase(1, Ap)
+                phase(2, Ap)
+                phase(3, Ap)
+            recs.append(scal)
         return recs
-
-    def _spectra_from(self, rec):
-        """The reference's breakdown rules replayed on the recorded scalars (krylov.py:168-198)."""
-        rz = rec[0]
-        al, be = [], []
-        for it in range(self.eig_iters):
-            if rz <= 0.0 or not np.isfinite(rz):
-                break
-            pAp = rec[1 + 2 * it]
-            if pAp <= 0.0 or not np.isfinite(pAp):
-                break
-            al.append(rz / pAp)
-            rz_new = rec[2 + 2 * it]
-            if rz_new <= 1e-28 * rz or not np.isfinite(rz_new):
-                break
-            be.append(rz_new / rz)
-            rz = rz_new
-        scal = np.zeros(8 + 128)
-        scal[4], scal[5] = len(al), len(be)
-        scal[8:8 + len(al)] = al
-        scal[8 + 64:8 + 64 + len(be)] = be
-        return lanczos_extremes(scal, self.eig_iters)
 
     def _buffers(self):
         from .mgsolve import LevelContext, _NativeCycle
@@ -248,7 +241,7 @@ class DistGMG:
         clat = c.lat if (c.sharded or not f.sharded) else self.virt[l]
         agglomerate = f.sharded and not c.sharded
         if agglomerate:
-            coarse.zero_()
+            _lib.call("pffmg_scale", 0.0, _lib.ptr(coarse), coarse.numel(), _lib.stream())
         _lib.call("pffmg_restrict", clat.ref, f.lat.ref, n_comp, comp0, _lib.ptr(fine), _lib.ptr(coarse),
                   _lib.ptr(c.flags), _lib.stream())
         if agglomerate:
@@ -274,14 +267,38 @@ class DistGMG:
         return out
 
     # ----------------------------------------------------------------- GMRES
+    def _arnoldi(self, top, V, j, hcol, scr):
+        """CGS2 Arnoldi step on w = V[j+1] (krylov.py:93-110 with classical
+        Gram-Schmidt twice): pass p: c = V_{0..j} . w over owned rows (fused
+        multi-dot), all-reduce the column, w -= V c, H[:, j] += c; then
+        ||w|| (fused into the second subtraction), all-reduce, V[j+1] = w / ||w||."""
+        a, b = top.own_ab
+        n = V.shape[1]
+        w = V[j + 1]
+        st = _lib.stream()
+        for ps in range(2):
+            _lib.call("pffmg_multi_dot_owned", _lib.ptr(V), V.stride(0), 0, j + 1, _lib.ptr(w), 0, n, top.V,
+                      a, b, _lib.ptr(scr), st)
+            if top.sharded:
+                allreduce_(scr[:j + 1], self.group)
+            _lib.call("pffmg_gs_subtract", _lib.ptr(V), V.stride(0), j + 1, _lib.ptr(scr), _lib.ptr(w), n,
+                      _lib.ptr(hcol), top.V, a, b, _lib.ptr(scr[j + 1:]) if ps == 1 else None, st)
+        if top.sharded:
+            allreduce_(scr[j + 1:j + 2], self.group)
+        _lib.call("pffmg_normalize", _lib.ptr(w), _lib.ptr(w), n, _lib.ptr(scr[j + 1:]), _lib.ptr(hcol[j + 1:]), st)
+
     def gmres(self, b, control=None):
-        """krylov.py:50-136 with distributed inner products; b, x are local slabs."""
+        """krylov.py:50-136 with distributed inner products; b, x are local slabs.
+        All vector work is libpffmg kernels (owned-row reductions, CGS2 Arnoldi,
+        multi-axpy); the host reads one Hessenberg column per step."""
         ctl = control or SolverControl()
         top = self.L[-1]
         n = b.numel()
         x = zeros(n)
         r = b.clone()
-        rn = float(np.sqrt(self.dot(top, r, r)))
+        st = _lib.stream()
+        s2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        rn = float(np.sqrt(self.dot_dev(top, r, r, s2).item()))
         tol = max(ctl.abs_tol, ctl.rel_tol * rn)
         if rn <= tol:
             return x, 0
@@ -289,47 +306,26 @@ class DistGMG:
         m = int(ctl.restart)
         V = torch.zeros((m + 1, n), dtype=torch.float64, device="cuda")
         Z = torch.zeros((m, n), dtype=torch.float64, device="cuda")
+        Hd = torch.zeros((m, m + 1), dtype=torch.float64, device="cuda")
+        scr = torch.zeros(m + 2, dtype=torch.float64, device="cuda")
+        yd = torch.zeros(m, dtype=torch.float64, device="cuda")
         while True:
             m = min(int(ctl.restart), int(ctl.max_iters) - total)
             if m <= 0:
                 raise NoConvergence(x, rn, total)
             H = np.zeros((m + 1, m))
             cs, sn, gg = np.zeros(m), np.zeros(m), np.zeros(m + 1)
-            V[0] = r / rn
+            _lib.call("pffmg_normalize", _lib.ptr(r), _lib.ptr(V[0]), n, _lib.ptr(s2), None, st)   # krylov.py:72
             gg[0] = rn
+            _lib.call("pffmg_scale", 0.0, _lib.ptr(Hd), Hd.numel(), st)
             used = 0
             for j in range(m):
                 self.vcycle(V[j], Z[j])
-                w = V[j + 1]
-                self.apply(Z[j], w)
+                self.apply(Z[j], V[j + 1])
                 total += 1
-                # MGS (krylov.py:93-107) with the dots kept on the device: each
-                # pass all-reduces one scalar and subtracts without a host round
-                # trip; the host reads the Hessenberg column once per pass set
-                w0 = self.dot_dev(top, w, w)
-                hs = []
-                for i in range(j + 1):
-                    h = self.dot_dev(top, V[i], w)
-                    w.sub_(h * V[i])
-                    hs.append(h)
-                nrm = self.dot_dev(top, w, w)
-                vals = host(torch.cat(hs + [w0, nrm]))
-                H[:j + 1, j] = vals[:j + 1]
-                w0, nrm = float(np.sqrt(vals[-2])), float(np.sqrt(vals[-1]))
-                if nrm < 1e-3 * w0:
-                    hs = []
-                    for i in range(j + 1):
-                        cc = self.dot_dev(top, V[i], w)
-                        w.sub_(cc * V[i])
-                        hs.append(cc)
-                    nrm = self.dot_dev(top, w, w)
-                    vals = host(torch.cat(hs + [nrm]))
-                    H[:j + 1, j] += vals[:j + 1]
-                    nrm = float(np.sqrt(vals[-1]))
-                H[j + 1, j] = nrm
+                self._arnoldi(top, V, j, Hd[j], scr)
+                H[:j + 2, j] = host(Hd[j, :j + 2])
                 brk = H[j + 1, j] == 0.0
-                if not brk:
-                    w /= H[j + 1, j]
                 for i in range(j):
                     t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
                     H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
@@ -345,10 +341,11 @@ class DistGMG:
             y = np.zeros(used)
             for i in range(used - 1, -1, -1):
                 y[i] = (gg[i] - H[i, i + 1:used] @ y[i + 1:]) / H[i, i]
-            x += torch.as_tensor(y, device="cuda") @ Z[:used]
+            yd[:used].copy_(torch.from_numpy(y))
+            _lib.call("pffmg_multi_axpy", _lib.ptr(Z), Z.stride(0), used, _lib.ptr(yd), _lib.ptr(x), n, st)
             self.apply(x, r)
-            r = b - r
-            rn = float(np.sqrt(self.dot(top, r, r)))
+            _lib.call("pffmg_sub", _lib.ptr(b), _lib.ptr(r), _lib.ptr(r), n, st)          # r = b - A x
+            rn = float(np.sqrt(self.dot_dev(top, r, r, s2).item()))
             if rn <= tol * (1.0 + 1e-8):
                 return x, total
             if total >= ctl.max_iters:
@@ -364,23 +361,3 @@ class DistGMG:
         """(global offset, owned values per component) of a local vector."""
         lev = self.L[l]
         return [host(x_local[s]) for s in lev.owned]
-
-
-class _BlockView:
-    """Owned slices of one block (k = 0 displacement, 1 phase field) of a level."""
-
-    def __init__(self, lev, k):
-        nk = lev.dim if k == 0 else 1
-        offs = lev.info.plane_offsets()
-        lo, hi = lev.info.own if lev.info.own != (0, 0) else (0, lev.info.n_planes)
-        a, b = int(offs[lo]), int(offs[hi])
-        self.slices = [slice(c * lev.V + a, c * lev.V + b) for c in range(nk)]
-        self.sharded = lev.sharded
-
-    def dot_dev(self, solver, x, y):
-        t = torch.zeros(1, dtype=torch.float64, device=x.device)
-        for s in self.slices:
-            t += torch.dot(x[s], y[s])
-        if self.sharded:
-            allreduce_(t, solver.group)
-        return t

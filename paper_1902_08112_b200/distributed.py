@@ -177,24 +177,19 @@ class Halo:
         """Post the exchange; returns a handle for finish().  Under NCCL the
         transfers run on NCCL's stream, concurrently with work enqueued on the
         current stream afterwards (which must not touch the ghost planes).
-        `persistent`: `vec` is a long-lived buffer, so its device-to-device op
-        list is built once and reused (the per-call host work is then one
-        batched NCCL group)."""
+
+        CUDA vectors go as ONE contiguous message per neighbour: the sent
+        planes of every component are packed by a libpffmg kernel
+        (pffmg_pack_rows) into a persistent buffer, received into another and
+        unpacked after the wait (`persistent` is accepted for the callers'
+        convenience; the packed path is always persistent).  CPU vectors (the
+        oracle-backed CPU tests) go per component."""
         if self.world == 1 or self.slab.replicated:
             return None
-        stage = vec.is_cuda and _backend(self.group) != "nccl"
-        if not stage:
-            key = (vec.data_ptr(), vec.numel(), n_comp)
-            ops = self._ops.get(key) if persistent else None
-            if ops is None:
-                ops = self._build_ops(vec, n_comp, lambda t: t, [])
-                if persistent:
-                    self._ops[key] = ops
-            return (dist.batch_isend_irecv(ops) if ops else []), []
-        back = []
-        ops = self._build_ops(vec, n_comp, lambda t: t.cpu(), back)
-        reqs = dist.batch_isend_irecv(ops) if ops else []
-        return reqs, back
+        if vec.is_cuda:
+            return self._start_packed(vec, n_comp)
+        ops = self._build_ops(vec, n_comp, lambda t: t, [])
+        return (dist.batch_isend_irecv(ops) if ops else []), []
 
     def _build_ops(self, vec, n_comp, buf, back):
         ops = []
@@ -214,15 +209,56 @@ class Halo:
                     back.append((vec[base + a:base + b], r))
         return ops
 
-    @staticmethod
-    def finish(handle):
+    def _bufs(self, n_comp, device):
+        key = (n_comp, str(device))
+        b = self._ops.get(key)
+        if b is None:
+            b = {}
+            for name, rng in (("sd", self.send_down), ("rd", self.recv_down), ("su", self.send_up),
+                              ("ru", self.recv_up)):
+                if rng is not None:
+                    b[name] = torch.empty(n_comp * (rng[1] - rng[0]), dtype=torch.float64, device=device)
+            self._ops[key] = b
+        return b
+
+    def _start_packed(self, vec, n_comp):
+        from . import _lib
+        stage = _backend(self.group) != "nccl"
+        b = self._bufs(n_comp, vec.device)
+        s = _lib.stream()
+        ops, back = [], []
+        for snd, rcv, sk, rk, peer in ((self.send_down, self.recv_down, "sd", "rd", self.rank - 1),
+                                       (self.send_up, self.recv_up, "su", "ru", self.rank + 1)):
+            if snd is None:
+                continue
+            _lib.call("pffmg_pack_rows", _lib.ptr(vec), self.V, n_comp, snd[0], snd[1] - snd[0], _lib.ptr(b[sk]),
+                      0, s)
+            sbuf = b[sk].cpu() if stage else b[sk]
+            rbuf = torch.empty(b[rk].numel(), dtype=torch.float64) if stage else b[rk]
+            ops.append(dist.P2POp(dist.isend, sbuf, peer, self.group))
+            ops.append(dist.P2POp(dist.irecv, rbuf, peer, self.group))
+            back.append((rcv, b[rk], rbuf if stage else None))
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        return reqs, [("unpack", vec, n_comp, back)]
+
+    def finish(self, handle):
         if handle is None:
             return
         reqs, back = handle
         for req in reqs:
             req.wait()
-        for dst, src in back:
-            dst.copy_(src)
+        for item in back:
+            if item[0] == "unpack":
+                from . import _lib
+                _, vec, n_comp, recvs = item
+                for rng, dbuf, hbuf in recvs:
+                    if hbuf is not None:                  # gloo: staged through the host
+                        dbuf.copy_(hbuf)
+                    _lib.call("pffmg_pack_rows", _lib.ptr(vec), self.V, n_comp, rng[0], rng[1] - rng[0],
+                              _lib.ptr(dbuf), 1, _lib.stream())
+            else:
+                dst, src = item
+                dst.copy_(src)
 
 
 def _backend(group=None):

@@ -112,8 +112,19 @@ def test_dist_gmg_single_rank_matches_native():
     gmg.vcycle(r, out)
     ref = mgsolve.vcycle(ctxs, mgsolve.PreconditionerKind.FULL, r, degree=prob.degree)
     assert (out - ref).norm() <= 1e-12 * ref.norm()
-    x, its = gmg.gmres(r, krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8))
+    gmg.gmres(r, krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8))          # warm
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        x, its = gmg.gmres(r, krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8))
+        torch.cuda.synchronize()
+    names = {e.name for e in prof.events() if e.device_type.name == "CUDA"}
+    kernels = {n for n in names if not n.startswith("Memcpy") and not n.startswith("Memset")}
+    # the distributed GMRES loop runs on libpffmg kernels only: no cuBLAS / ATen BLAS-1
+    # (the one ATen fill is the zero initial guess allocated before the loop)
+    foreign = {n for n in kernels if ("at::" in n and "FillFunctor" not in n) or "cublas" in n.lower()
+               or "gemv" in n.lower() or "gemm" in n.lower() or "dot_kernel" in n}
+    assert not foreign, sorted(foreign)
     x_ref, its_ref = krylov.gmres(ctxs[-1].op.apply, mgsolve.VCyclePreconditioner(ctxs, degree=prob.degree),
                                   r, krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8))
-    assert its == its_ref
-    assert (x - x_ref).norm() <= 1e-10 * x_ref.norm()
+    assert abs(its - its_ref) <= 1                   # CGS2 Arnoldi vs the reference's MGS: +-1
+    assert (x - x_ref).norm() <= 1e-8 * x_ref.norm()
