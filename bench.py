@@ -19,7 +19,13 @@ quads, 3,151,875 fp64 DoFs, NoSplit, 8-level GMG, Chebyshev degree 3.
   kernel implements) and ncu DRAM bytes reported beside it.
 * solve.hbm: sum of the algorithmic bytes of every kernel of one Newton step
   (tools/bytemodel.py over the eager launch list) / T_solve / P.
-* configs: the same vmult + Newton step on cfg3 (Q2) and cfg4 (3D L-prism).
+* configs: the same vmult + Newton step on cfg3 (Q2), cfg4 (3D L-prism) and
+  cfg5 (3D cube 384^3, 228M DoFs, on one GPU).
+* N > 1: `value` weak-scales the headline (one 1024^2 cfg2 slab per GPU, so
+  the driver's per-N ratios are a like-for-like efficiency); the north
+  star's strong scaling of the largest config is the `strong_scaling`
+  sub-result -- cfg5 cut into N z-slabs (sharded vmult and a DistGMG
+  Newton step), to be divided by configs.cfg5 of the N = 1 line.
 * parity: the GPU vmult against the CPU arm's output of the same vector, and
   the Newton step's GMRES iterations / solution fingerprint against the
   reference's (tests/golden/configs_full.npz).
@@ -521,7 +527,7 @@ def measure_solve(prob, mask, hbm, with_bytes=True):
     return out, x
 
 
-def measure_config(name, hbm, steps=20):
+def measure_config(name, hbm, steps=20, solve=True):
     """vmult + Newton step of another BASELINE config (sub-result of the bench line)."""
     import torch
     from paper_1902_08112_b200 import _lib, configs
@@ -538,18 +544,91 @@ def measure_config(name, hbm, steps=20):
     per = float(np.mean(ms)) * 1e-3
     b_c, b_f = algorithmic_bytes(prob.dim, mesh.n_vertices, mesh.n_cells,
                                  9 if getattr(mesh, "order", 1) == 2 else None)
-    solve, x = measure_solve(prob, mask, hbm, with_bytes=False)
+    del v, out
+    solve, x = measure_solve(prob, mask, hbm, with_bytes=False) if solve else (None, None)
     g = golden_full(name)
     res = {"vmult_ms": per * 1e3, "value": prob.n_dofs / per * 1e-9, "unit": "GDoF/s",
-           "frac_BC": b_c / per * 1e-9 / hbm, "frac_BF": b_f / per * 1e-9 / hbm,
-           "n_dofs": prob.n_dofs, "newton_step_ms": solve["ms_per_newton_step"],
-           "setup_ms": solve["setup_ms"], "gmres_ms": solve["gmres_ms"], "gmres_iters": solve["gmres_iters"],
-           "gmres_iters_ref": int(g["gmres_iters"]) if g is not None else None,
-           "gmres_x_fingerprint_err": fingerprint_err(x.cpu().numpy(), g, "gmres_x")}
+           "frac_BC": b_c / per * 1e-9 / hbm, "frac_BF": b_f / per * 1e-9 / hbm, "n_dofs": prob.n_dofs}
+    if solve is not None:
+        res.update({"newton_step_ms": solve["ms_per_newton_step"], "setup_ms": solve["setup_ms"],
+                    "gmres_ms": solve["gmres_ms"], "gmres_iters": solve["gmres_iters"],
+                    "gmres_iters_ref": int(g["gmres_iters"]) if g is not None else None,
+                    "gmres_x_fingerprint_err": fingerprint_err(x.cpu().numpy(), g, "gmres_x")})
     if name == "cfg3":
         res["parity_note"] = "Q2: no reference implementation (parity unpinned; oracle/q2.py known-answer pins)"
-    del op, v, out, flush
+    if name == "cfg5":
+        res["note"] = ("384^3: the reference fingerprint exists at 96^3 and 192^3 (tests/test_gpu_fullsize.py); "
+                       "the single-GPU figure the strong-scaling runs divide by")
+    del op, flush, x
+    from paper_1902_08112_b200 import mgsolve
+    mgsolve._Session._cache.clear()
+    mgsolve._NativeCycle._cache.clear()
     torch.cuda.empty_cache()
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_strong(name, ws, rank, args):
+    """Strong scaling of the north-star's largest configuration:
+    cfg5 (384^3, 228M DoFs) cut into ws z-slabs, one per GPU -- the sharded
+    fused vmult (halo exchange overlapped with the interior planes) and one
+    slab-distributed Newton-step solve (DistGMG).  Times are max over ranks;
+    the single-GPU reference is configs.cfg5 of the N = 1 line."""
+    import torch
+    from paper_1902_08112_b200 import configs, krylov
+    from paper_1902_08112_b200 import distributed as D
+    from paper_1902_08112_b200.lattice import info_from_mesh
+    from paper_1902_08112_b200.model import ConstraintMask, SplitKind
+    prob = configs.make(name)
+    mesh = prob.disc.hierarchy.finest
+    levels = prob.disc.hierarchy.levels
+    mask = prob.dirichlet.combined_with(prob.active, np.zeros(prob.n_dofs))
+    part = D.SlabPartition([int(info_from_mesh(m).ncell[-1]) for m in levels], ws, rank)
+    dop = D.DistributedOperator(mesh, len(levels) - 1, part, prob.state,
+                                ConstraintMask(mask.is_constrained, mask.inhomogeneity), prob.params,
+                                SplitKind.NOSPLIT)
+    v = torch.as_tensor(dop.to_local(prob.v), device="cuda")
+    out = torch.empty_like(v)
+    flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+    ms, _ = time_steps(lambda: dop.apply_local(v, out), args.steps, args.warmup, flush,
+                       torch.cuda.current_stream(), lambda: torch.distributed.barrier())
+    tt = torch.tensor([float(np.mean(ms))], device="cuda", dtype=torch.float64)
+    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    per = float(tt.item()) * 1e-3
+    res = {"config": name, "n_dofs": prob.n_dofs, "n_gpus": ws, "vmult_ms": per * 1e3,
+           "value": prob.n_dofs / per * 1e-9, "unit": "GDoF/s",
+           "what": "z-slab sharded fused vmult, halo exchange overlapped with the interior planes, "
+                   "time = max over ranks (the single-GPU figure: configs.cfg5 of the N = 1 line)"}
+    del v, out, dop, flush
+    torch.cuda.empty_cache()
+    if not args.no_solve:
+        from paper_1902_08112_b200.dist_solver import DistGMG
+        ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+
+        def newton_step():
+            torch.distributed.barrier()
+            t0 = time.perf_counter()
+            gmg = DistGMG(levels, ws, rank, degree=prob.degree)
+            gmg.setup(prob.state, prob.active, prob.dirichlet, prob.params, SplitKind.NOSPLIT)
+            b = torch.zeros(gmg.L[-1].n, dtype=torch.float64, device="cuda")
+            gmg.ops[-1].semilinear_dev(b)
+            b.neg_()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            x, its = gmg.gmres(b, ctl)
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            t = torch.tensor([t1 - t0, t2 - t1], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            del gmg, x, b
+            return float(t[0]), float(t[1]), its
+
+        newton_step()
+        setup_s, gmres_s, its = newton_step()
+        res["newton_step"] = {"setup_ms": setup_s * 1e3, "gmres_ms": gmres_s * 1e3, "gmres_iters": its,
+                              "ms": (setup_s + gmres_s) * 1e3,
+                              "control": "slab-distributed GMRES(30) rel 1e-8, V(1,1) FULL, CGS2 Arnoldi, "
+                                         "wall clock max over ranks"}
     return res
 
 
@@ -704,6 +783,13 @@ def run_gpu(args):
                             "%s halos + all-reduced dots" % (prob.degree, args.backend),
                  "timing": "wall clock, max over ranks"}
 
+    strong = None
+    if ws > 1 and args.strong:
+        try:
+            strong = measure_strong(args.strong, ws, rank, args)
+        except Exception as e:          # never lose the headline line to the sub-result
+            strong = {"config": args.strong, "error": f"{type(e).__name__}: {e}"[:300]}
+
     extra = {}
     if ws == 1 and args.extra:
         for name in [c for c in args.extra.split(",") if c and c != args.config]:
@@ -757,6 +843,7 @@ def run_gpu(args):
         "gpu_launches": args.steps * (1 if ws == 1 else (3 if getattr(mesh, "order", 1) == 2 else 2)),
         "solve": solve,
         "configs": extra or None,
+        "strong_scaling": strong,
         "wall_s_timed_region": wall,
         "step_ms_min_max": [float(np.min(step_ms)), float(np.max(step_ms))],
     }
@@ -797,8 +884,10 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--extra", default="cfg3,cfg4",
+    ap.add_argument("--extra", default="cfg3,cfg4,cfg5",
                     help="other configs measured as sub-results at N=1 (vmult + Newton step)")
+    ap.add_argument("--strong", default="cfg5",
+                    help="N > 1: the config of the strong-scaling sub-result ('' to skip)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: host-staged communication, for functional runs of N>1 on one GPU")
     args = ap.parse_args()
