@@ -75,7 +75,19 @@ typedef struct {
      * cell boundary (plane0 even) and a sharded operator needs two ghost node
      * rows below own_lo (four for restriction) and one above. */
     int32_t order;
+    /* Optional work list of the 3D streaming kernels (NULL: every tile of the
+     * bounding lattice).  The x-y plane of vertex columns is cut into tiles of
+     * PFFMG_TILE3 x PFFMG_TILE3 columns, (nx+1+T-1)/T x (ny+1+T-1)/T of them
+     * (x fastest); tiles3d lists, ascending, the n_tiles3d tile indices
+     * bx + ntx*by that hold at least one vertex of the lattice.  A DEVICE
+     * pointer.  Non-box lattices (the L-shapes) pass it so that the kernels
+     * distribute only occupied tiles over the SMs; listing an empty tile or
+     * every tile is always correct, omitting an occupied one is not. */
+    const int32_t* tiles3d;
+    int32_t n_tiles3d;
 } pffmg_lattice;
+
+#define PFFMG_TILE3 15
 
 /*
  * Linearisation state + material of one level (model.py:89-119, 270-309).
@@ -115,8 +127,8 @@ typedef struct {
 } pffmg_state;
 
 const char* pffmg_last_error(void);
-/* ABI version: 2 (struct_size guards; pffmg_state.phi_coef). */
-#define PFFMG_ABI_VERSION 2
+/* ABI version: 3 (struct_size guards; pffmg_state.phi_coef; pffmg_lattice.tiles3d). */
+#define PFFMG_ABI_VERSION 3
 int pffmg_version(void);
 int pffmg_device_sm_count(int* out);
 

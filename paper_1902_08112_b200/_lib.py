@@ -20,7 +20,7 @@ c_double_p = C.POINTER(C.c_double)
 vp = C.c_void_p
 
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class _Sized(C.Structure):
@@ -40,7 +40,8 @@ class Lattice(_Sized):
                 ("vrow_off", vp), ("vrow_lo", vp), ("vrow_hi", vp),
                 ("crow_lo", vp), ("crow_hi", vp),
                 ("own_lo", C.c_int32), ("own_hi", C.c_int32),
-                ("plane0", C.c_int32), ("order", C.c_int32)]
+                ("plane0", C.c_int32), ("order", C.c_int32),
+                ("tiles3d", vp), ("n_tiles3d", C.c_int32)]
 
 
 class State(_Sized):

@@ -47,6 +47,20 @@ int sm_count() {
     return cached;
 }
 
+int check_device() {
+    static int first = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        set_error("cudaGetDevice failed");
+        return PFFMG_ERR_CUDA;
+    }
+    if (first < 0) first = dev;
+    PFFMG_REQUIRE(dev == first,
+                  "libpffmg serves one GPU per process: it was first used on device %d, now called on device %d",
+                  first, dev);
+    return PFFMG_OK;
+}
+
 int make_lat(const pffmg_lattice* in, Lat* out) {
     PFFMG_REQUIRE(in, "null lattice");
     PFFMG_REQUIRE(in->struct_size == (int32_t)sizeof(pffmg_lattice),
@@ -89,6 +103,10 @@ int make_lat(const pffmg_lattice* in, Lat* out) {
     out->crow_lo = in->crow_lo;
     out->crow_hi = in->crow_hi;
     out->plane0 = in->plane0;
+    PFFMG_REQUIRE(in->tiles3d == nullptr || in->n_tiles3d > 0, "tiles3d given with n_tiles3d = %d",
+                  in->n_tiles3d);
+    out->tiles3d = in->tiles3d;
+    out->n_tiles3d = in->tiles3d ? in->n_tiles3d : 0;
     out->order = order;
     const int nplanes = order == 2 ? 2 * in->ny + 1 : (in->dim == 3 ? in->nz : in->ny) + 1;
     if (in->own_lo == 0 && in->own_hi == 0) {
@@ -130,6 +148,7 @@ int make_consts(const pffmg_lattice* lat, const pffmg_state* st, Consts* K) {
     K->k_phi = st->g_c * st->eps;
     K->band = st->split_band;
     K->eps = st->eps;
+    PFFMG_ONE_DEVICE();                 // after the argument checks (they need no GPU)
     return PFFMG_OK;
 }
 

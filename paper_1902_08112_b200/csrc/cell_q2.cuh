@@ -8,6 +8,10 @@
 // integration is the transposed pass.
 #pragma once
 
+#ifndef PFFMG_Q2_UNROLL_QY
+#define PFFMG_Q2_UNROLL_QY 0
+#endif
+
 #include "cellops_miehe.cuh"
 
 namespace pffmg {
@@ -302,7 +306,11 @@ __device__ __forceinline__ void cell_q2_rows(Load&& load, const double* __restri
 #pragma unroll
         for (int n = 0; n < 9; ++n) o[k][n] = 0.0;
     const bool cpl = MODE == M_FULL && !nocoup;
+#if PFFMG_Q2_UNROLL_QY
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
     for (int qy = 0; qy < 3; ++qy) {
         double By[3], Dy[3];
 #pragma unroll

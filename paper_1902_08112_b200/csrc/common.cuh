@@ -29,6 +29,17 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int sm_count();
 
+// libpffmg serves ONE GPU per process (the launch-shape, occupancy and
+// reduction-scratch caches are set up for the first device used): every
+// entry point that touches device state checks the current device against
+// that first one and fails loudly instead of mixing devices.
+int check_device();
+#define PFFMG_ONE_DEVICE()                          \
+    do {                                            \
+        const int rc_ = ::pffmg::check_device();    \
+        if (rc_) return rc_;                        \
+    } while (0)
+
 // ----------------------------------------------------------------- lattice
 
 // Kernel-side copy of pffmg_lattice (passed by value).
@@ -44,6 +55,8 @@ struct Lat {
     int own_lo, own_hi;    // finalised vertex planes of the last axis (always set by make_lat)
     int plane0;            // global index of local plane 0 along the last axis
     int order;             // 1 = Q1, 2 = Q2 (2D box, nodes on the half-spacing lattice)
+    const int32_t* __restrict__ tiles3d;   // occupied PFFMG_TILE3^2-column x-y tiles (NULL: all)
+    int n_tiles3d;
 };
 
 int make_lat(const pffmg_lattice* in, Lat* out);

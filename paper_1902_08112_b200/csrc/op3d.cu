@@ -11,7 +11,6 @@
 namespace pffmg {
 
 constexpr int TY3D = 8;    // generic kernel
-constexpr int TY3T = 8;    // streaming kernel
 
 template <int MODE, int EPI, bool ISO, bool MIE = false>
 static void set_smem(size_t smem) {
@@ -23,85 +22,85 @@ static void set_smem(size_t smem) {
     }
 }
 
-// Planes per CTA of the streaming kernel: each CTA marches `per` vertex
-// planes after a one-plane warm-up, so the cost of a launch is about
-//   ceil(active tiles x ceil(planes / per) / (SMs x resident CTAs)) x (per + c0)
-// waves of plane steps (c0 = warm-up + ring fill, ~2 plane steps).  `frac`
-// estimates the share of x-y tile columns that hold vertices (non-box
-// lattices leave whole columns empty, and those CTAs exit at once).
-static int planes_per_cta(int64_t columns, int planes, int occ, double frac) {
-    static const int forced = [] {
-        const char* e = getenv("PFFMG_3D_PLANES");
+template <int MODE, int EPI, int TX, bool RHO, bool BOX, bool PRE, bool TAB = false>
+static void launch_t(const OpArgs& A0, int planes, cudaStream_t s) {
+    using MI = ModeInfo<3, MODE>;
+    using TL = Tile3<TX>;
+    constexpr int NCO = MI::NCO;
+    constexpr bool STAGE = MODE == M_UBLK || (MODE == M_FULL && (EPI == E_CHEB || EPI == E_CHEB0));
+    constexpr size_t smem = TL::template smem<TAB ? MI::NV : MI::NF, NCO, STAGE ? EpiIn<NCO, EPI>::NL : 0>();
+    auto kern = op3dt_kernel<MODE, EPI, TX, RHO, BOX, PRE, TAB>;
+    static int occ = 0;
+    if (occ == 0) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T3_NT, smem) != cudaSuccess || occ < 1)
+            occ = 1;
+    }
+    // persistent grid: one wave of resident CTAs sharing the (tile, plane)
+    // items equally (op3dt_kernel); never more CTAs than items
+    const Lat& L = A0.L;
+    const bool listed = TX - 1 == PFFMG_TILE3 && L.tiles3d != nullptr;
+    const int64_t ntiles = listed ? L.n_tiles3d
+                                  : (int64_t)((L.nx + 1 + TX - 2) / (TX - 1)) * ((L.ny + 1 + TL::TY - 2) / (TL::TY - 1));
+    const int64_t items = ntiles * (A0.ends ? 2 : planes);
+    static const int cap = [] {
+        const char* e = getenv("PFFMG_3D_CTAS");      // tuning: CTAs per SM of the persistent grid
         return e ? atoi(e) : 0;
     }();
-    if (forced > 0) return forced;
-    const int64_t slots = (int64_t)sm_count() * (occ > 0 ? occ : 1);
-    const int64_t active = (int64_t)std::ceil((double)columns * frac);
-    int best = 32;
-    double best_cost = 1e300;
-    for (int per = 2; per <= 32; ++per) {
-        const int64_t ctas = active * ((planes + per - 1) / per);
-        const int64_t waves = (ctas + slots - 1) / slots;
-        const double cost = (double)waves * (std::min(per, planes) + 2.0);
-        if (cost < best_cost - 1e-9) {
-            best_cost = cost;
-            best = per;
-        }
+    int64_t g = (int64_t)sm_count() * (cap > 0 ? cap : occ);
+    if (g > items) g = items;
+    if (g < 1) g = 1;
+    // schedule (op3dt_kernel): persistent tile-major for the FP64-bound full
+    // operator and on listed (non-box) lattices; the strips x tiles grid,
+    // whose concurrent CTAs share halo planes in L2, for the lighter modes of
+    // box lattices (measured: cfg5 phi block 216 -> 163 us, u block 390 -> 373 us;
+    // full operator and the cfg4 L-prism better persistent, 153 -> 136 us)
+    static const int forced_sched = [] {
+        const char* e = getenv("PFFMG_3D_SCHED");    // tuning: 1 persistent, 2 grid
+        return e ? atoi(e) : 0;
+    }();
+    static const int forced = [] {
+        const char* e = getenv("PFFMG_3D_PLANES");   // tuning: strip height of the grid schedule
+        return e ? atoi(e) : 0;
+    }();
+    OpArgs A = A0;
+    A.sched = forced_sched ? forced_sched : ((MODE == M_FULL || listed || A0.ends) ? 1 : 2);
+    if (A0.ends) A.sched = 1;
+    if (A.sched == 2) {
+        // strips: about half a resident CTA's share of planes per tile, 8..32
+        // planes, balanced so the last strip is not a sliver
+        const int64_t share = items / g;
+        int S = forced > 0 ? forced : (int)std::min<int64_t>(32, std::max<int64_t>(8, share / 2));
+        S = std::max(1, std::min(S, planes));
+        const int nstrips = (planes + S - 1) / S;
+        S = (planes + nstrips - 1) / nstrips;
+        A.planes_per_cta = S;
+        g = (int64_t)nstrips * ntiles;
     }
-    return best;
+    const dim3 grid((unsigned)g);
+    pdl_launch(kern, grid, dim3(T3_NT), smem, s, A);
 }
 
-template <int MODE, int EPI, bool RHO, bool BOX, bool PRE, bool TAB = false>
-static void launch_t(const OpArgs& A0, int gx, int gy, int planes, double frac, size_t smem, cudaStream_t s) {
-    auto kern = op3dt_kernel<MODE, EPI, TY3T, RHO, BOX, PRE, TAB>;
-    static size_t done = 0;
-    static int occ = 0;
-    if (done < smem) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        done = smem;
-        occ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * TY3T, smem) != cudaSuccess) occ = 1;
-    }
-    OpArgs A = A0;
-    int per;
-    if (TAB) {
-        // light, HBM-bound phi block (4 CTAs/SM): latency-bound unless the
-        // grid fills the resident slots several times over
-        per = planes_per_cta((int64_t)gx * gy, planes, occ, frac);
-    } else {
-        // FP64-bound modes: ~2 CTAs of work per SM per wave, strips of 1..32
-        // planes (measured sweep)
-        static const int forced = [] {
-            const char* e = getenv("PFFMG_3D_PLANES");
-            return e ? atoi(e) : 0;
-        }();
-        const int64_t sms = sm_count();
-        int64_t p = ((int64_t)planes * gx * gy + 2LL * sms - 1) / (2LL * sms);
-        per = (int)(p < 1 ? 1 : (p > 32 ? 32 : p));
-        if (forced > 0) per = forced;
-    }
-    if (A.ends) per = 1;
-    A.planes_per_cta = per;
-    const dim3 grid(gx, gy, (unsigned)((planes + per - 1) / per));
-    pdl_launch(kern, grid, dim3(32 * TY3T), smem, s, A);
+// Tile shape of the streaming kernel: 16 x 16 cells (default) or 32 x 8
+// (PFFMG_3D_TX=32).
+static int tile_tx() {
+    static const int tx = [] {
+        const char* e = getenv("PFFMG_3D_TX");
+        return (e && atoi(e) == 32) ? 32 : 16;
+    }();
+    return tx;
 }
 
 template <int MODE, int EPI>
 static int launch_stream(const OpArgs& A, cudaStream_t s) {
     const Lat& L = A.L;
-    using MI = ModeInfo<3, MODE>;
-    const int gx = (L.nx + 1 + 29) / 30;
-    const int gy = (L.ny + 1 + TY3T - 2) / (TY3T - 1);
     const int planes = A.ends ? 2 : L.own_hi - L.own_lo;
-    const double frac = std::min(1.0, (double)L.V / ((double)(L.nx + 1) * (L.ny + 1) * (L.nz + 1)));
-    constexpr int ROWS = TY3T + 1;
     const bool tab = MODE == M_PBLK && A.ptab != nullptr;
-    const size_t smem = sizeof(double) * (4 * (tab ? MI::NV : MI::NF) * ROWS * 32 + TY3T * MI::NCO * 2 * 32 +
-                                          ((MODE == M_UBLK || (MODE == M_FULL && (EPI == E_CHEB || EPI == E_CHEB0)))
-                                               ? 32 * TY3T * EpiIn<MI::NCO, EPI>::NL * MI::NCO : 0)) +
-                        4 * ROWS * 48 + 4 * ROWS * sizeof(int);
     const bool rho = A.rho != nullptr, box = L.vrow_off == nullptr, pre = A.premasked != 0;
-#define PFFMG_T(R, B, P, T) launch_t<MODE, EPI, R, B, P, T>(A, gx, gy, planes, frac, smem, s)
+    const bool t32 = tile_tx() == 32;
+#define PFFMG_T(R, B, P, T)                                                        \
+    (t32 ? launch_t<MODE, EPI, 32, R, B, P, T>(A, planes, s)                       \
+         : launch_t<MODE, EPI, 16, R, B, P, T>(A, planes, s))
     if constexpr (MODE == M_PBLK) {
         if (tab) {                       // the table already holds rho
             if (box) { if (pre) PFFMG_T(false, true, true, true); else PFFMG_T(false, true, false, true); }

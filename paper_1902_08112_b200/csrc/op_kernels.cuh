@@ -43,6 +43,7 @@ struct OpArgs {
     int x_add_din;                     // CHEB: x = (x + d_in) + d_out instead of x += d_out
     int planes_per_cta;
     int nseg;                          // 2D warp kernel: 30-column segments per row
+    int sched;                         // work schedule of the streaming kernels (tuning, see launchers)
     int premasked;                     // PFFMG_HINT_PREMASKED
     int ends;                          // PFFMG_HINT_ENDS: strips = {own_lo}, {own_hi - 1}
     int split;                         // 0 NoSplit, 1 Miehe spectral split (2D)

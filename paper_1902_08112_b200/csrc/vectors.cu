@@ -31,6 +31,7 @@ struct Scratch {
 // concurrent per-level CG-Lanczos branches of the recorded setup graph) must
 // not share the partials / last-block counter.
 static int scratch(cudaStream_t stream, Scratch** out) {
+    PFFMG_ONE_DEVICE();
     static std::mutex mu;
     static std::unordered_map<cudaStream_t, Scratch*> table;
     std::lock_guard<std::mutex> lock(mu);
@@ -912,6 +913,7 @@ __global__ void __launch_bounds__(MGS_T, 1) mgs_coop_kernel(const double* __rest
 
 static int mgs_coop(const double* Vb, int64_t ld, int j, double* w, int64_t n, double* h, double* ctl,
                     cudaStream_t s) {
+    PFFMG_ONE_DEVICE();
     static int grid = -1;
     static int64_t cap = 0;
     static double* part = nullptr;

@@ -396,6 +396,29 @@ def _info_from_arrays(mesh):
     return LatticeInfo(dim, ncell, mesh.cell_size, V, is_box, rows, cell_perm)
 
 
+TILE3 = 15      # PFFMG_TILE3 (include/pffmg.h): vertex columns per 3D streaming-kernel tile edge
+
+
+def occupied_tiles3d(info):
+    """pffmg_lattice.tiles3d of a 3D non-box lattice: the ascending indices
+    bx + ntx*by of the TILE3 x TILE3 vertex-column tiles that hold a vertex
+    (None for 2D and box lattices, whose tiles are all occupied)."""
+    if info.dim != 3 or info.rows is None:
+        return None
+    _, vlo, vhi, _, _ = info.rows
+    nxv, nyv = int(info.ncell[0]) + 1, int(info.ncell[1]) + 1
+    ntx, nty = -(-nxv // TILE3), -(-nyv // TILE3)
+    vlo = np.asarray(vlo).reshape(-1, nyv)          # rows r = y + (ny+1) z
+    vhi = np.asarray(vhi).reshape(-1, nyv)
+    occ = np.zeros((nty, ntx), dtype=bool)
+    for bx in range(ntx):
+        lo, hi = bx * TILE3, min((bx + 1) * TILE3, nxv)
+        hit = ((vhi > vlo) & (vlo < hi) & (vhi > lo)).any(axis=0)     # per vertex row y
+        for by in range(nty):
+            occ[by, bx] = hit[by * TILE3:(by + 1) * TILE3].any()
+    return np.flatnonzero(occ.ravel()).astype(np.int32)
+
+
 class DeviceLattice:
     """pffmg_lattice + the device row tables backing it."""
 
@@ -424,6 +447,11 @@ class DeviceLattice:
         L.own_lo, L.own_hi = int(info.own[0]), int(info.own[1])
         L.plane0 = int(getattr(info, "plane_lo", 0))
         L.order = int(getattr(info, "order", 1))
+        tiles = occupied_tiles3d(info)
+        if tiles is not None:
+            t = torch.as_tensor(tiles, device="cuda")
+            self._tables.append(t)
+            L.tiles3d, L.n_tiles3d = t.data_ptr(), int(t.numel())
         self.struct = L
         self.ref = C.byref(L)
         self._rows = {}

@@ -160,3 +160,94 @@ def test_q2_fused_descent_and_entry_match_separate_kernels(monkeypatch):
                                             params, M.SplitKind.NOSPLIT)
         out.append(mgsolve.vcycle(ctxs, mgsolve.PreconditionerKind.FULL, r))
     assert torch.equal(out[0], out[1])
+
+
+def _cfg3_oracle_op(prob, mask):
+    """The Q2 oracle's operator of a cfg3 problem (CPU, test infrastructure)."""
+    levels = q2.q2_hierarchy(-20.0, 20.0, 8, prob.n_levels)
+    T = q2.Q2Tables(levels[-1], prob.n_levels - 1)
+    p = prob.params
+    mat = jacobian.Material(mu=p.mu, lam=p.lam, g_c=p.g_c, kappa=p.kappa, eps=p.eps,
+                            pressure_fn=p.pressure_fn)
+    s = prob.state
+    st = jacobian.State(U=s.U, U_prev1=s.U_prev1, U_prev2=s.U_prev2, t=s.t, t_prev1=s.t_prev1,
+                        t_prev2=s.t_prev2, phi_tilde=s.phi_tilde)
+    return T, jacobian.JacobianOperator(T, st, mask.is_constrained, mat)
+
+
+@pytest.mark.slow
+def test_cfg3_full_size_operator_matches_oracle():
+    """cfg3 at its BASELINE size (512^2 Q2 cells, 3.15M DoFs): the vmult (FULL
+    mode, unmasked input), both blocks and the block-diagonal operator against
+    the Q2 oracle -- every warp segment / strip seam of the staged Q2 kernel
+    at the benchmarked size."""
+    from paper_1902_08112_b200 import _lib, configs
+    from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, SplitKind
+    prob = configs.make("cfg3")
+    mask = prob.dirichlet.combined_with(prob.active, np.zeros(prob.n_dofs))
+    cm = ConstraintMask(mask.is_constrained, mask.inhomogeneity)
+    op = PhaseFieldOperator(prob.disc.finest, prob.state, cm, prob.params, SplitKind.NOSPLIT)
+    T, ref = _cfg3_oracle_op(prob, mask)
+    v = prob.v
+    d = T.dim * T.n_vertices
+    assert rel_err(op.apply(v), ref.apply(v)) <= TOL
+    assert rel_err(op.apply_block(0, v[:d]), ref.apply_block(0, v[:d])) <= TOL
+    assert rel_err(op.apply_block(1, v[d:]), ref.apply_block(1, v[d:])) <= TOL
+    vd = torch.as_tensor(v, device="cuda")
+    bd = torch.empty_like(vd)
+    op.apply_dev(_lib.BLOCKDIAG, vd, bd)
+    want = np.concatenate([ref.apply_block(0, v[:d]), ref.apply_block(1, v[d:])])
+    assert rel_err(bd.cpu().numpy(), want) <= TOL
+
+
+_AB_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_1902_08112_b200 import _lib, configs
+from paper_1902_08112_b200.model import ConstraintMask, PhaseFieldOperator, SplitKind
+prob = configs.make("cfg3", 5)
+mask = prob.dirichlet.combined_with(prob.active, np.zeros(prob.n_dofs))
+op = PhaseFieldOperator(prob.disc.finest, prob.state, ConstraintMask(mask.is_constrained, mask.inhomogeneity),
+                        prob.params, SplitKind.NOSPLIT)
+v = torch.as_tensor(prob.v, device="cuda")
+d = 2 * op.V
+outs = [op.apply(v), op.apply_block(0, v[:d]), op.apply_block(1, v[d:])]
+b = torch.empty_like(v)
+op.apply_dev(_lib.BLOCKDIAG, v, b)
+outs.append(b)
+g = torch.Generator(device="cuda").manual_seed(1)
+r0 = torch.randn(v.numel(), dtype=torch.float64, device="cuda", generator=g)
+x = torch.randn(v.numel(), dtype=torch.float64, device="cuda", generator=g)
+inv = torch.rand(v.numel(), dtype=torch.float64, device="cuda", generator=g) + 1.0
+cf = torch.tensor([0.3, 0.2], dtype=torch.float64, device="cuda")
+vp = v.clone()
+vp[torch.as_tensor(mask.is_constrained, device="cuda")] = 0.0
+d2, r = torch.empty_like(v), r0.clone()
+op.cheb_step_bd(vp, d2, r, x, inv, cf, cf, pre=True)
+outs += [d2, r, x]
+res = torch.empty_like(v)
+op.residual_dev(_lib.FULL, v, r0, res)
+outs.append(res)
+np.savez(sys.argv[2], *[o.cpu().numpy() for o in outs])
+"""
+
+
+def test_q2_staged_kernel_equals_unstaged(tmp_path):
+    """The staged Q2 kernel (cp.async node-row ring) is bitwise the per-cell
+    __ldg kernel on a 128^2-cell cfg3 level: vmult, both blocks, the
+    block-diagonal operator, a block-diagonal Chebyshev step (pre-masked
+    input) and the V-cycle residual."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "ab.py"
+    script.write_text(_AB_SCRIPT)
+    res = {}
+    for flag in ("1", "0"):
+        env = dict(os.environ, PFFMG_Q2_STAGED=flag)
+        path = tmp_path / f"out{flag}.npz"
+        subprocess.run([sys.executable, str(script), root, str(path)], env=env, check=True, timeout=600)
+        res[flag] = np.load(path)
+    for k in res["1"].files:
+        assert np.array_equal(res["1"][k], res["0"][k]), k

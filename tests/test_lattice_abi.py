@@ -69,7 +69,7 @@ def test_library_exports_every_header_symbol():
 
 def test_library_reports_argument_errors_without_a_gpu():
     lib = _lib.load()
-    assert lib.pffmg_version() == 2
+    assert lib.pffmg_version() == 3
     rc = lib.pffmg_apply(None, None, -1, None, None, None)
     assert rc == 1
     assert b"null" in lib.pffmg_last_error()

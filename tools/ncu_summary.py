@@ -68,6 +68,8 @@ def main():
     ap.add_argument("--name", required=True)
     ap.add_argument("--bench")
     ap.add_argument("--note", default="")
+    ap.add_argument("--src-sha", default=None,
+                    help="bench.src_sha() of the sources the capture ran (default: the bench line's)")
     a = ap.parse_args()
     h, units, rows = raw(a.rep)
     kernels = []
@@ -120,6 +122,9 @@ def main():
                                   for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]))]
     if a.bench:
         summary["bench_line"] = json.load(open(a.bench))
+        if a.src_sha is None:
+            a.src_sha = summary["bench_line"].get("roofline", {}).get("profile", {}).get("src_sha")
+    summary["src_sha"] = a.src_sha
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"ncu_{a.name}.json"), "w") as f:
         json.dump(summary, f, indent=1)
