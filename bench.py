@@ -549,6 +549,16 @@ def measure_config(name, hbm, steps=20, solve=True):
     g = golden_full(name)
     res = {"vmult_ms": per * 1e3, "value": prob.n_dofs / per * 1e-9, "unit": "GDoF/s",
            "frac_BC": b_c / per * 1e-9 / hbm, "frac_BF": b_f / per * 1e-9 / hbm, "n_dofs": prob.n_dofs}
+    # this config's ncu capture (profiles/ncu_vmult_<cfg>_r*.json) when it was
+    # taken from the current sources: DRAM traffic and FP64 rate of the kernel
+    prof_name, pj, fresh = profile_for(name)
+    if pj and fresh:
+        traffic, flops = pj.get("dram_bytes_per_launch"), pj.get("fp64_flops_per_launch")
+        res["profile"] = {"file": prof_name, "traffic": traffic,
+                          "frac_ncu": traffic / per * 1e-9 / hbm if traffic else None,
+                          "fp64_tflops": flops / per * 1e-12 if flops else None,
+                          "fp64_frac": flops / per * 1e-12 / FP64_PEAK_TFLOPS if flops else None,
+                          "kernel_us_ncu": (pj.get("kernels") or [{}])[0].get("duration_us")}
     if solve is not None:
         res.update({"newton_step_ms": solve["ms_per_newton_step"], "setup_ms": solve["setup_ms"],
                     "gmres_ms": solve["gmres_ms"], "gmres_iters": solve["gmres_iters"],

@@ -9,7 +9,7 @@
 #pragma once
 
 #ifndef PFFMG_Q2_UNROLL_QY
-#define PFFMG_Q2_UNROLL_QY 0
+#define PFFMG_Q2_UNROLL_QY 1
 #endif
 
 #include "cellops_miehe.cuh"

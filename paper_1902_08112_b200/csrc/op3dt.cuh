@@ -20,6 +20,7 @@
 namespace pffmg {
 
 constexpr int T3_NT = 256;                        // threads per CTA of the streaming kernel
+constexpr int T3_RING = 5;                        // staged vertex planes: cz, cz+1 read, cz+2 ready, cz+3 landing
 
 template <int TX>
 struct Tile3 {
@@ -29,7 +30,8 @@ struct Tile3 {
     // dynamic shared memory of one instantiation (doubles / bytes)
     template <int NF, int NCO, int NLE>
     static constexpr size_t smem() {
-        return sizeof(double) * (4 * NF * PL + TY * NCO * 2 * TX + (size_t)T3_NT * NLE * NCO) + 4 * PL;
+        return sizeof(double) * (T3_RING * NF * PL + 2 * TY * NCO * 2 * TX + (size_t)T3_NT * NLE * NCO) +
+               T3_RING * PL;
     }
 };
 
@@ -48,15 +50,15 @@ __global__ void __launch_bounds__(T3_NT, MODE == M_FULL ? PFFMG_3D_FULL_MINB : (
     constexpr int SLOT = NF * PL;                // doubles per staged plane
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* sv = reinterpret_cast<double*>(smem_raw);                          // [4][NF][ROWS][COLS]
-    double* sy = sv + 4 * SLOT;                                                 // [TY][NCO][2][TX]
+    double* sv = reinterpret_cast<double*>(smem_raw);                          // [T3_RING][NF][ROWS][COLS]
+    double* sy0 = sv + T3_RING * SLOT;                                          // [2][TY][NCO][2][TX]
     // epilogue operands staged in shared memory where a register prefetch
     // spills (u block, and the Chebyshev variants of FULL); elsewhere they
     // stay in registers (ncu: staging costs the table phi block and RESID ~4%)
     constexpr bool STAGE = MODE == M_UBLK || (MODE == M_FULL && (EPI == E_CHEB || EPI == E_CHEB0));
     constexpr int NLE = STAGE ? EpiIn<NCO, EPI>::NL : 0;                        // staged epilogue operands
-    double* sepi = sy + TY * NCO * 2 * TX;                                      // [T3_NT][NLE][NCO]
-    unsigned char* sfl = reinterpret_cast<unsigned char*>(sepi + T3_NT * NLE * NCO);   // [4][PL]
+    double* sepi = sy0 + 2 * TY * NCO * 2 * TX;                                 // [T3_NT][NLE][NCO]
+    unsigned char* sfl = reinterpret_cast<unsigned char*>(sepi + T3_NT * NLE * NCO);   // [T3_RING][PL]
 
     const Lat& L = A.L;
     const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
@@ -202,40 +204,54 @@ __global__ void __launch_bounds__(T3_NT, MODE == M_FULL ? PFFMG_3D_FULL_MINB : (
     };
 
     if (!BOX) {
-        for (int z = vz0 - 1; z <= vz0 + 2; ++z) fetch_rows(z);
+        for (int z = vz0 - 1; z <= vz0 + 3; ++z) fetch_rows(z);
         cp_async_commit();
         cp_async_wait<0>();
         __syncthreads();
     }
     {
+        // planes vz0-1, vz0 and (if the run has it) vz0+1 into slots 0, 1, 2
         issue(vz0 - 1, 0);
-        unsigned fl0[EPT];
+        unsigned fl0[EPT], fl1[EPT];
 #pragma unroll
         for (int j = 0; j < EPT; ++j) fl0[j] = ifl[j];
         issue(vz0, 1);
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) fl1[j] = ifl[j];
+        const bool third = vz0 + 1 <= vz1;
+        if (third) issue(vz0 + 1, 2);
         cp_async_commit();
         cp_async_wait<0>();
         finish(0, fl0);
-        finish(1, ifl);
+        finish(1, fl1);
+        if (third) finish(2, ifl);
+        __syncthreads();
     }
     double carry[NCO];
 #pragma unroll
     for (int k = 0; k < NCO; ++k) carry[k] = 0.0;
 
-    int it = 0;
-    for (int cz = vz0 - 1; cz < vz1; ++cz, ++it) {
-        const int s0 = it & 3, s1 = (it + 1) & 3;
+    // One barrier per plane step.  Step `it` reads planes cz (slot s0) and
+    // cz+1 (s1), writes its y partials to sy[it & 1], and lands + finishes
+    // plane cz+3 (slot s3, the slot of plane cz-2); the single barrier between
+    // the y-partial writes and reads also orders every thread's finish of
+    // plane cz+2 (previous step) before the next step reads it, and every read
+    // of a slot before it is refilled two steps later.
+    int it = 0, s0 = 0;
+    for (int cz = vz0 - 1; cz < vz1; ++cz, ++it, s0 = s0 == T3_RING - 1 ? 0 : s0 + 1) {
+        const int s1 = s0 == T3_RING - 1 ? 0 : s0 + 1;
+        const int s3 = s0 >= 2 ? s0 - 2 : s0 + 3;
+        double* sy = sy0 + (it & 1) * (TY * NCO * 2 * TX);
         // vertex finalised this iteration and its epilogue operands (loaded early)
         const int vid_f = (ty >= 1 && tx >= 1 && cz >= vz0) ? vid_of(cx, ty, cz) : -1;
         double* eslot = sepi + tid * (NLE * NCO);
         EpiIn<NCO, EPI> ein;
         if (STAGE && vid_f >= 0) epi_stage<NCO, EPI>(A, vid_f, eslot);   // committed with the plane below
         if (!STAGE && vid_f >= 0) epi_load<NCO, EPI>(A, vid_f, ein);
-        if (cz + 4 <= vz1 + 1) fetch_rows(cz + 4);     // committed with the plane below
-        const bool issued = cz + 2 <= vz1;
-        if (issued) issue(cz + 2, (it + 2) & 3);
+        if (cz + 5 <= vz1 + 1) fetch_rows(cz + 5);     // committed with the plane below
+        const bool issued = cz + 3 <= vz1;
+        if (issued) issue(cz + 3, s3);
         cp_async_commit();
-        __syncthreads();                         // planes cz, cz+1 finished by every thread
 
         const double* p0 = sv + s0 * SLOT;
         const double* p1 = sv + s1 * SLOT;
@@ -279,7 +295,7 @@ __global__ void __launch_bounds__(T3_NT, MODE == M_FULL ? PFFMG_3D_FULL_MINB : (
         };
         cell3_iso<MODE, RHO, Corners, decltype(emit)&, TAB>(C, rq, A.K, A.I, emit, tq,
                                                             (int64_t)L.nx * L.ny * L.nz);
-        __syncthreads();                         // y partials visible; planes fully read
+        __syncthreads();                         // y partials visible (see the loop head)
 
         if (ty >= 1) {
             double acc[NCO], top[NCO];
@@ -309,9 +325,9 @@ __global__ void __launch_bounds__(T3_NT, MODE == M_FULL ? PFFMG_3D_FULL_MINB : (
 #pragma unroll
             for (int k = 0; k < NCO; ++k) carry[k] = top[k];
         }
-        if (issued) {                            // plane cz+2: flags + masking before the next step's barrier
+        if (issued) {                            // plane cz+3: flags + masking before the next step's barrier
             cp_async_wait<0>();
-            finish((it + 2) & 3, ifl);
+            finish(s3, ifl);
         }
     }
     cp_async_wait<0>();

@@ -25,6 +25,7 @@ run on the rank's slab lattice (`own_lo/own_hi/plane0` of pffmg_lattice):
 from __future__ import annotations
 
 import copy
+import os
 
 import numpy as np
 import torch
@@ -38,6 +39,10 @@ from .lattice import device_lattice, info_from_mesh
 
 from .model import DeviceMask, LinearizationState, PhaseFieldOperator
 
+
+# overlap the ghost-plane exchange of the V-cycle stencils with their interior
+# planes (PFFMG_DIST_OVERLAP=0: exchange, then the whole stencil)
+OVERLAP = os.environ.get("PFFMG_DIST_OVERLAP", "1") != "0"
 
 class _Level:
     def __init__(self, l, info_g, slab, rank, world, group):
@@ -233,6 +238,29 @@ class DistGMG:
         lev = self.L[l]
         if lev.sharded:
             lev.halo.exchange(vec, n_comp, persistent=True)     # level buffers of the cycle
+
+    def overlap_plan(self, l):
+        """Row scopes (interior, [boundary...]) of a halo-overlapped stencil on
+        level l (PhaseFieldOperator.scope), or None when the level is
+        replicated or too thin to have interior planes.  Q1: interior planes
+        [lo+1, hi-1) read no ghost plane, the two boundary planes go in one
+        PFFMG_HINT_ENDS launch; Q2: node rows [lo+1, hi-2), then [lo, lo+1)
+        and [hi-2, hi) (as DistributedOperator.apply_local)."""
+        lev = self.L[l]
+        if not lev.sharded or not OVERLAP:
+            return None
+        lo, hi = lev.info.own
+        if hi - lo < 4:
+            return None
+        if getattr(lev.info, "order", 1) == 2:
+            return ("rows", lo + 1, hi - 2), [("rows", lo, lo + 1), ("rows", hi - 2, hi)]
+        return ("rows", lo + 1, hi - 1), ["ends"]
+
+    def halo_start(self, l, vec, n_comp):
+        return self.L[l].halo.start(vec, n_comp, persistent=True)
+
+    def halo_finish(self, l, handle):
+        self.L[l].halo.finish(handle)
 
     def restrict(self, l, fine, coarse, n_comp, comp0):
         """coarse (level l) = masked P^T fine (level l+1); agglomerated into a replicated level."""

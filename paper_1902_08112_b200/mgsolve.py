@@ -712,6 +712,26 @@ class _NativeCycle:
         if self.comm is not None:
             self.comm.halo(L.index, vec, n_comp)
 
+    def _stencil(self, L, vec, n_comp, call):
+        """`call()` (one operator kernel on level L reading `vec`) after a
+        refresh of vec's ghost planes.  Slab-distributed levels overlap the
+        exchange with the interior planes (their cells read owned planes
+        only) and finish the boundary planes once it has landed."""
+        comm = self.comm
+        plan = comm.overlap_plan(L.index) if comm is not None else None
+        if plan is None:
+            self._halo(L, vec, n_comp)
+            call()
+            return
+        interior, ends = plan
+        h = comm.halo_start(L.index, vec, n_comp)
+        with L.op.scope(interior):
+            call()
+        comm.halo_finish(L.index, h)
+        for sc in ends:
+            with L.op.scope(sc):
+                call()
+
     def _restrict(self, l, fine, coarse, n_comp, comp0, coarse_flags):
         if self.comm is not None:
             self.comm.restrict(l, fine, coarse, n_comp, comp0)
@@ -741,26 +761,24 @@ class _NativeCycle:
                 x.zero_()
                 r.copy_(rhs)
             else:
-                self._halo(L, x, nk)
-                op.residual_dev(k, x, rhs, r, pre=pre)
+                self._stencil(L, x, nk, lambda: op.residual_dev(k, x, rhs, r, pre=pre))
             for _ in range(prm.degree):
                 _lib.call("pffmg_jacobi_update_dc", _lib.ptr(r), _lib.ptr(inv), _lib.ptr(theta),
                           _lib.ptr(x), nb, s)
-                self._halo(L, x, nk)
-                op.residual_dev(k, x, rhs, r, pre=pre)
+                self._stencil(L, x, nk, lambda: op.residual_dev(k, x, rhs, r, pre=pre))
             return
         if x_is_zero:                                      # r = b; d = inv r / theta; x = d
             _lib.call("pffmg_cheb_init_zero_dc", _lib.ptr(rhs), _lib.ptr(inv), _lib.ptr(theta),
                       _lib.ptr(r), _lib.ptr(d_in), _lib.ptr(x), nb, s)
             pending = False
         else:                                              # r = b - A x; d = inv r / theta
-            self._halo(L, x, L.dim if k == 0 else 1)
-            op.cheb_init_dc(k, x, rhs, r, d_in, inv, theta, pre=pre)
+            self._stencil(L, x, L.dim if k == 0 else 1,
+                          lambda: op.cheb_init_dc(k, x, rhs, r, d_in, inv, theta, pre=pre))
             pending = True                                 # x += d folded into the next step
         for i in range(prm.degree - 1):
             c = coef[off + 1 + 2 * i: off + 3 + 2 * i]
-            self._halo(L, d_in, L.dim if k == 0 else 1)
-            op.cheb_step_dc(k, d_in, d_out, r, x, inv, c, pending, pre=pre)
+            self._stencil(L, d_in, L.dim if k == 0 else 1,
+                          lambda: op.cheb_step_dc(k, d_in, d_out, r, x, inv, c, pending, pre=pre))
             pending = False
             d_in, d_out = d_out, d_in
         if pending:                                        # degree 1 from a non-zero x
@@ -793,14 +811,13 @@ class _NativeCycle:
                       L.dim * L.V, _lib.ptr(r), _lib.ptr(d_in), _lib.ptr(x), L.n, s)
             pending = False
         else:
-            self._halo(L, x, L.dim + 1)
-            op.cheb_init_bd(x, rhs, r, d_in, inv, tu, tp, pre=pre)
+            self._stencil(L, x, L.dim + 1, lambda: op.cheb_init_bd(x, rhs, r, d_in, inv, tu, tp, pre=pre))
             pending = True
         common = min(pu.degree, pp.degree) - 1
         for i in range(common):
-            self._halo(L, d_in, L.dim + 1)
-            op.cheb_step_bd(d_in, d_out, r, x, inv, coef[ou + 1 + 2 * i: ou + 3 + 2 * i],
-                            coef[op_ + 1 + 2 * i: op_ + 3 + 2 * i], pending, pre=pre)
+            cu, cp = coef[ou + 1 + 2 * i: ou + 3 + 2 * i], coef[op_ + 1 + 2 * i: op_ + 3 + 2 * i]
+            self._stencil(L, d_in, L.dim + 1,
+                          lambda: op.cheb_step_bd(d_in, d_out, r, x, inv, cu, cp, pending, pre=pre))
             pending = False
             d_in, d_out = d_out, d_in
         if pending:                                        # degree 1 from a non-zero x
@@ -809,9 +826,9 @@ class _NativeCycle:
             b = L.blk(k)
             di, do = d_in[b], d_out[b]
             for i in range(common, prm.degree - 1):
-                self._halo(L, di, L.dim if k == 0 else 1)
-                op.cheb_step_dc(k, di, do, r[b], x[b], inv[b], coef[o + 1 + 2 * i: o + 3 + 2 * i],
-                                False, pre=pre)
+                c = coef[o + 1 + 2 * i: o + 3 + 2 * i]
+                self._stencil(L, di, L.dim if k == 0 else 1,
+                              lambda: op.cheb_step_dc(k, di, do, r[b], x[b], inv[b], c, False, pre=pre))
                 di, do = do, di
 
     def _smooth(self, l, x_is_zero, init_done=False):
@@ -843,8 +860,7 @@ class _NativeCycle:
             return
         L, Lc = self.levels[l], self.levels[l - 1]
         self._smooth(l, True, init_done)
-        self._halo(L, L.x, L.dim + 1)
-        L.op.residual_dev(_lib.FULL, L.x, L.r, L.res, pre=True)
+        self._stencil(L, L.x, L.dim + 1, lambda: L.op.residual_dev(_lib.FULL, L.x, L.r, L.res, pre=True))
         if self._fused_descent_ok(l - 1):
             ou, _, _ = self.slot[("s", l - 1, 0)]
             op_, _, _ = self.slot[("s", l - 1, 1)]
@@ -867,8 +883,7 @@ class _NativeCycle:
         self._cheb(L, k, ("s", l, k), True)
         ncomp = L.dim if k == 0 else 1
         comp0 = 0 if k == 0 else L.dim
-        self._halo(L, L.x[b], ncomp)
-        L.op.residual_dev(k, L.x[b], L.r[b], L.res[b], pre=True)
+        self._stencil(L, L.x[b], ncomp, lambda: L.op.residual_dev(k, L.x[b], L.r[b], L.res[b], pre=True))
         self._restrict(l - 1, L.res[b], Lc.r[Lc.blk(k)], ncomp, comp0, Lc.flags)
         self._block_cycle(k, l - 1)
         self._prolongate(l - 1, Lc.x[Lc.blk(k)], L.x[b], ncomp, comp0, L.flags)

@@ -20,6 +20,7 @@ from dataclasses import dataclass, replace
 from enum import Enum
 from typing import Callable, Optional
 
+import contextlib
 import os
 
 import numpy as np
@@ -201,6 +202,12 @@ class PhaseFieldOperator:
         st_ends.hints = 2
         self._st_ends = st_ends
         self._stp_ends = ctypes.byref(st_ends)
+        st_pre_ends = _lib.State()
+        ctypes.pointer(st_pre_ends)[0] = st
+        st_pre_ends.hints = 3
+        self._st_pre_ends = st_pre_ends
+        self._stp_pre_ends = ctypes.byref(st_pre_ends)
+        self._scope = None          # row scope of the slab-overlapped stencils (see scope())
         # per-QP a_phiphi of the phi block, cached like _build_caches does
         # (model.py:260, 304-308): NoSplit Q2 and isotropic Q1 levels (phi
         # block, block-diagonal smoother)
@@ -212,7 +219,7 @@ class PhaseFieldOperator:
                 and os.environ.get("PFFMG_PHI_TABLE", "1") != "0"):
             if _ptab is not None:            # a table already built from this state (mgsolve._Session)
                 self._ptab = _ptab
-                for st in (self._st, self._st_pre, self._st_ends):
+                for st in (self._st, self._st_pre, self._st_ends, self._st_pre_ends):
                     st.phi_coef = _ptab.data_ptr()
             else:
                 self._ptab = empty((9 if order == 2 else 1 << self.dim) * self.lat.n_lattice_cells)
@@ -223,10 +230,10 @@ class PhaseFieldOperator:
         work on the current stream; graph-capturable) and point the states at it."""
         if self._ptab is None:
             return
-        for st in (self._st, self._st_pre, self._st_ends):
+        for st in (self._st, self._st_pre, self._st_ends, self._st_pre_ends):
             st.phi_coef = None
         _lib.call("pffmg_phi_coef", self.lat.ref, self._stp, _lib.ptr(self._ptab), _lib.stream())
-        for st in (self._st, self._st_pre, self._st_ends):
+        for st in (self._st, self._st_pre, self._st_ends, self._st_pre_ends):
             st.phi_coef = self._ptab.data_ptr()
 
     def _rebind(self, U, phi_tilde, flags):
@@ -235,7 +242,7 @@ class PhaseFieldOperator:
         self._U, self._pt, self._flags = U, phi_tilde, flags
         if self._ptab is not None:
             self._ptab = self._ptab.clone()
-        for st in (self._st, self._st_pre, self._st_ends):
+        for st in (self._st, self._st_pre, self._st_ends, self._st_pre_ends):
             st.U = U.data_ptr()
             st.phi_tilde = phi_tilde.data_ptr()
             st.flags = flags.data_ptr()
@@ -309,10 +316,28 @@ class PhaseFieldOperator:
 
     # -- device-level entry points (no conversions) --------------------------
     def _sp(self, pre):
+        if self._scope == "ends":
+            return self._stp_pre_ends if pre else self._stp_ends
         return self._stp_pre if pre else self._stp
 
+    def _lref(self):
+        sc = self._scope
+        return self.lat.ref if sc is None or sc == "ends" else self.lat.rows(sc[1], sc[2])
+
+    @contextlib.contextmanager
+    def scope(self, sc):
+        """Restrict the *_dev stencil calls to some vertex planes of a slab:
+        ("rows", lo, hi) finalises planes [lo, hi) only, "ends" the first and
+        the last owned plane (PFFMG_HINT_ENDS) -- the interior / boundary
+        halves of a halo-overlapped stencil (dist_solver.DistGMG)."""
+        old, self._scope = self._scope, sc
+        try:
+            yield self
+        finally:
+            self._scope = old
+
     def apply_dev(self, which, x, out, pre=False):
-        _lib.call("pffmg_apply", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(out),
+        _lib.call("pffmg_apply", self._lref(), self._sp(pre), which, _lib.ptr(x), _lib.ptr(out),
                   _lib.stream())
 
     def apply_rows_dev(self, which, x, out, lo, hi, pre=False):
@@ -326,7 +351,7 @@ class PhaseFieldOperator:
                   _lib.stream())
 
     def residual_dev(self, which, x, b, out, pre=False):
-        _lib.call("pffmg_residual", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
+        _lib.call("pffmg_residual", self._lref(), self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
                   _lib.ptr(out), _lib.stream())
 
     def semilinear_dev(self, out):
@@ -337,32 +362,32 @@ class PhaseFieldOperator:
         _lib.call("pffmg_diagonal", self.lat.ref, self._stp, _lib.ptr(out), _lib.stream())
 
     def cheb_step_dev(self, which, d_in, d_out, r, x, inv, c_dd, c_dr, x_add_din=False, pre=False):
-        _lib.call("pffmg_cheb_step", self.lat.ref, self._sp(pre), which, _lib.ptr(d_in),
+        _lib.call("pffmg_cheb_step", self._lref(), self._sp(pre), which, _lib.ptr(d_in),
                   _lib.ptr(d_out), _lib.ptr(r), _lib.ptr(x), _lib.ptr(inv), c_dd, c_dr,
                   int(x_add_din), _lib.stream())
 
     def cheb_init_dev(self, which, x, b, r, d, inv, theta, pre=False):
-        _lib.call("pffmg_cheb_init", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
+        _lib.call("pffmg_cheb_init", self._lref(), self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
                   _lib.ptr(r), _lib.ptr(d), _lib.ptr(inv), theta, _lib.stream())
 
     # device-coefficient forms: scalars read from `coef` (a CUDA tensor view) at run time
     def cheb_step_dc(self, which, d_in, d_out, r, x, inv, coef, x_add_din=False, pre=False):
-        _lib.call("pffmg_cheb_step_dc", self.lat.ref, self._sp(pre), which, _lib.ptr(d_in),
+        _lib.call("pffmg_cheb_step_dc", self._lref(), self._sp(pre), which, _lib.ptr(d_in),
                   _lib.ptr(d_out), _lib.ptr(r), _lib.ptr(x), _lib.ptr(inv), _lib.ptr(coef),
                   int(x_add_din), _lib.stream())
 
     def cheb_step_bd(self, d_in, d_out, r, x, inv, coef_u, coef_p, x_add_din=False, pre=False):
         """Both diagonal blocks' Chebyshev steps in one kernel (full-length vectors)."""
-        _lib.call("pffmg_cheb_step_bd", self.lat.ref, self._sp(pre), _lib.ptr(d_in), _lib.ptr(d_out),
+        _lib.call("pffmg_cheb_step_bd", self._lref(), self._sp(pre), _lib.ptr(d_in), _lib.ptr(d_out),
                   _lib.ptr(r), _lib.ptr(x), _lib.ptr(inv), _lib.ptr(coef_u), _lib.ptr(coef_p),
                   int(x_add_din), _lib.stream())
 
     def cheb_init_bd(self, x, b, r, d, inv, theta_u, theta_p, pre=False):
-        _lib.call("pffmg_cheb_init_bd", self.lat.ref, self._sp(pre), _lib.ptr(x), _lib.ptr(b), _lib.ptr(r),
+        _lib.call("pffmg_cheb_init_bd", self._lref(), self._sp(pre), _lib.ptr(x), _lib.ptr(b), _lib.ptr(r),
                   _lib.ptr(d), _lib.ptr(inv), _lib.ptr(theta_u), _lib.ptr(theta_p), _lib.stream())
 
     def cheb_init_dc(self, which, x, b, r, d, inv, theta, pre=False):
-        _lib.call("pffmg_cheb_init_dc", self.lat.ref, self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
+        _lib.call("pffmg_cheb_init_dc", self._lref(), self._sp(pre), which, _lib.ptr(x), _lib.ptr(b),
                   _lib.ptr(r), _lib.ptr(d), _lib.ptr(inv), _lib.ptr(theta), _lib.stream())
 
     # -- helpers ---------------------------------------------------------------
