@@ -51,3 +51,6 @@ for k, (n, t, ds) in sorted(rows.items(), key=lambda kv: -kv[1][1]):
     print(f"{t:9.1f} us {n:4d}x  max {max(ds):7.1f}  min {min(ds):6.1f}  {k}")
 short = [e.time_range.end - e.time_range.start for e in ev]
 print("kernels < 5 us:", sum(1 for d in short if d < 5), "total", sum(d for d in short if d < 5))
+if os.environ.get("PFFMG_VC_SEQ"):
+    for e in ev:
+        print(f"{e.time_range.start - ev[0].time_range.start:9.1f} {e.time_range.end - e.time_range.start:7.1f}  {e.name[:70]}")
