@@ -240,6 +240,10 @@ COARSE_KERNEL = os.environ.get("PFFMG_COARSE_KERNEL", "1") != "0"
 # Restriction into a level fused with that level's smoother start from x = 0
 # (pffmg_restrict_init_bd); PFFMG_FUSED_DESCENT=0: separate kernels.
 FUSED_DESCENT = os.environ.get("PFFMG_FUSED_DESCENT", "1") != "0"
+# block-diagonal smoothing kernel (both blocks per launch) on levels with fewer
+# vertices than these; larger levels run the two block kernels per step
+BD_MAXV2 = int(os.environ.get("PFFMG_BD_MAXV2", str(1 << 40)))
+BD_MAXV3 = int(os.environ.get("PFFMG_BD_MAXV3", str(1 << 17)))
 
 
 def build_level_contexts(disc, state, active_mask, dirichlet_mask, params, split,
@@ -624,7 +628,7 @@ class _Level:
         # (launch-latency-bound) 3D levels; large 3D levels are FP64-bound and
         # run faster as two block kernels (measured, cfg4)
         self.index = ctx.level
-        self.bd_ok = self.dim == 2 or self.V < (1 << 17)
+        self.bd_ok = self.V < (BD_MAXV2 if self.dim == 2 else BD_MAXV3)
         info = op.lat.info
         self.coarse_ok = (int(np.prod(info.ncell)) <= 256 and tuple(info.own) == (0, 0)
                           and coarse_smem_bytes(self.dim, int(np.prod(info.ncell)), self.V,
