@@ -131,6 +131,12 @@ const char* pffmg_last_error(void);
 #define PFFMG_ABI_VERSION 3
 int pffmg_version(void);
 int pffmg_device_sm_count(int* out);
+/* Programmatic dependent launch of the library's kernels (on by default;
+ * PFFMG_PDL=0 in the environment disables it for good): on = 0 makes every
+ * later launch of this process fully stream-ordered, on = 1 restores it.
+ * *previous (optional) receives the old setting.  Used around multi-stream
+ * graph captures, where early-launched dependents would hold SM slots. */
+int pffmg_set_pdl(int on, int* previous);
 
 /* ---------------------------------------------------------------- operator */
 
@@ -201,6 +207,15 @@ int pffmg_cheb_init_dc(const pffmg_lattice* lat, const pffmg_state* st, int whic
 int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st, int which,
                      const double* h_v, double* h_out, double* d_v, double* d_out,
                      const int64_t* h_plane_off, int n_strips, void* stream);
+
+/* The same for ORDINARY (pageable) host memory, e.g. the numpy arrays the
+ * reference's drivers pass to PhaseFieldOperator.apply (model.py:368-375):
+ * host threads (PFFMG_COPY_THREADS, default half the cores, at most 16) stage
+ * the strips through page-locked buffers the library keeps, overlapped with
+ * the link copies and the stencil.  Synchronous: h_out is complete on return. */
+int pffmg_apply_pageable(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                         const double* h_v, double* h_out, double* d_v, double* d_out,
+                         const int64_t* h_plane_off, int n_strips, void* stream);
 
 /* Boundary load (model.py:511-547): sum over the n_faces boundary faces
  * (face_cell[i] = lattice cell index cx + nx (cy + ny cz), face_id[i] =

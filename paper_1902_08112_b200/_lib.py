@@ -57,6 +57,7 @@ class State(_Sized):
 _SIGS = {
     "pffmg_version": [],
     "pffmg_device_sm_count": [C.POINTER(C.c_int)],
+    "pffmg_set_pdl": [C.c_int, C.POINTER(C.c_int)],
     "pffmg_apply": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp],
     "pffmg_residual": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp],
     "pffmg_diagonal": [C.POINTER(Lattice), C.POINTER(State), vp, vp],
@@ -67,6 +68,7 @@ _SIGS = {
     "pffmg_cheb_init": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp,
                         C.c_double, vp],
     "pffmg_apply_host": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, C.c_int, vp],
+    "pffmg_apply_pageable": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, C.c_int, vp],
     "pffmg_qoi": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp],
     "pffmg_boundary_load": [C.POINTER(Lattice), C.POINTER(State), vp, vp, C.c_int64, C.c_int, vp, vp, vp],
     "pffmg_coarse_cheb": [C.POINTER(Lattice), C.POINTER(State), vp, vp, vp, vp, vp, vp, C.c_int, vp, C.c_int, vp],

@@ -1,5 +1,6 @@
 // Error state, device queries and host-side construction of the kernel
 // argument structs for libpffmg.
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
@@ -27,13 +28,17 @@ int check_launch(const char* what) {
     return PFFMG_OK;
 }
 
+static std::atomic<int> g_pdl_on{1};
+
 bool pdl_enabled() {
     static const bool on = [] {
         const char* e = getenv("PFFMG_PDL");
         return !(e && e[0] == '0');
     }();
-    return on;
+    return on && g_pdl_on.load(std::memory_order_relaxed) != 0;
 }
+
+int pdl_set(int on) { return g_pdl_on.exchange(on ? 1 : 0); }
 
 int sm_count() {
     static int cached = 0;
@@ -159,6 +164,12 @@ using namespace pffmg;
 extern "C" const char* pffmg_last_error(void) { return g_err; }
 
 extern "C" int pffmg_version(void) { return PFFMG_ABI_VERSION; }
+
+extern "C" int pffmg_set_pdl(int on, int* previous) {
+    const int prev = pdl_set(on);
+    if (previous) *previous = prev;
+    return PFFMG_OK;
+}
 
 extern "C" int pffmg_device_sm_count(int* out) {
     PFFMG_REQUIRE(out, "null out");

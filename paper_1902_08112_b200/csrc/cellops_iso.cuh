@@ -128,9 +128,9 @@ __device__ __forceinline__ void mass_transpose(double (&f)[1 << D], const Consts
         for (int i = 0; i < (1 << D); ++i) {
             if (i & (1 << a)) continue;
             const int j = i | (1 << a);
-            const double f0 = f[i], f1 = f[j];
-            f[i] = fma(K.omg0, f0, K.omg1 * f1);
-            f[j] = fma(K.g0, f0, K.g1 * f1);
+            const double f0 = f[i], f1 = f[j], d = f1 - f0;   // symmetric Gauss points: see SFr::deriv_T
+            f[i] = fma(K.g0, d, f0);
+            f[j] = fma(-K.g0, d, f1);
         }
     }
 }

@@ -257,9 +257,11 @@ struct SFr {
             for (int i = 0; i < NR; ++i) {
                 if (i & (1 << ab)) continue;
                 const int k = i | (1 << ab);
-                const double f0 = r[i], f1 = r[k];
-                r[i] = fma(K.omg0, f0, K.omg1 * f1);
-                r[k] = fma(K.g0, f0, K.g1 * f1);
+                // B^T of a pair; the Gauss points are symmetric (omg0 = g1, omg1 = g0,
+                // g0 + g1 = 1), so (g1 f0 + g0 f1, g0 f0 + g1 f1) = (f0 + g0 d, f1 - g0 d)
+                const double f0 = r[i], f1 = r[k], d = f1 - f0;
+                r[i] = fma(K.g0, d, f0);
+                r[k] = fma(-K.g0, d, f1);
             }
         }
 #pragma unroll
@@ -279,7 +281,20 @@ struct SFr {
 // chain (a V-cycle, a CG run) is scheduled while the previous one drains, and
 // waits for its completion (and memory flush) before touching data.  The wait
 // returns at once when there is no prerequisite grid.  PFFMG_PDL=0 disables it.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+//
+// PFFMG_PDL_EARLY (compile time): right after its own wait a kernel lets its
+// dependents launch (griddepcontrol.launch_dependents); they park in their
+// wait until this grid has completed and flushed, so a single-stream chain
+// overlaps every launch with the previous kernel.  Parked dependents hold SM
+// slots, which costs a multi-stream graph its concurrency: pffmg_set_pdl(0)
+// switches the launch attribute off for such sections (the setup graph).
+__device__ __forceinline__ void pdl_wait() {
+#ifdef PFFMG_PDL_EARLY
+    asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
+#else
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
 
 bool pdl_enabled();
 

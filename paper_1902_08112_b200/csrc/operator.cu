@@ -2,8 +2,12 @@
 // the per-dimension kernel instantiations (op2d.cu, op3d.cu; kernels in
 // op_kernels.cuh).  Replaces reference model.py:368-413 and the vector
 // updates of mgsolve.py:82-113 / 227 (fused epilogues).
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
+#include <thread>
+#include <vector>
 
 #include "op_launch.cuh"
 
@@ -118,8 +122,12 @@ namespace pffmg {
 namespace {
 struct PipeRes {
     cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t ev[2 * 64 + 2] = {};
+    cudaEvent_t ev[3 * 64 + 2] = {};
     bool ok = false;
+    // page-locked staging of pffmg_apply_pageable (grown on demand, kept)
+    double* stage_in = nullptr;
+    double* stage_out = nullptr;
+    size_t stage_cap = 0;
 };
 PipeRes& pipe_res() {
     static thread_local PipeRes R;
@@ -187,7 +195,7 @@ extern "C" int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st,
     const size_t pitch = (size_t)V * sizeof(double);
     cudaEvent_t* ein = R.ev;          // [K]
     cudaEvent_t* ek = R.ev + 64;      // [K]
-    cudaEvent_t e0 = R.ev[128], edone = R.ev[129];
+    cudaEvent_t e0 = R.ev[192], edone = R.ev[193];
     cudaEventRecord(e0, s);           // d_v / d_out free once prior work on `stream` is done
     cudaStreamWaitEvent(R.h2d, e0, 0);
     cudaStreamWaitEvent(R.d2h, e0, 0);
@@ -220,6 +228,176 @@ extern "C" int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st,
     cudaEventRecord(edone, R.d2h);
     cudaStreamWaitEvent(s, edone, 0);  // the caller's stream orders after the last copy
     return check_launch("pffmg_apply_host");
+}
+
+namespace pffmg {
+namespace {
+int copy_threads() {
+    static const int t = [] {
+        const char* e = getenv("PFFMG_COPY_THREADS");
+        int n = e ? atoi(e) : (int)(std::thread::hardware_concurrency() / 2);
+        return n < 1 ? 1 : (n > 16 ? 16 : n);
+    }();
+    return t;
+}
+}  // namespace
+}  // namespace pffmg
+
+// Host-buffer apply for ORDINARY (pageable) memory -- what a numpy caller
+// (the reference's drivers) hands over.  A pageable cudaMemcpy is staged by
+// the driver on one thread; here copy_threads() host threads move the strips
+// of v into a page-locked staging buffer (kept between calls) while earlier
+// strips are already on the link, and move finished output strips out of the
+// second staging buffer while later strips are still being computed.  The
+// stencil launches are those of pffmg_apply_host.  Synchronous: h_out is
+// complete when the call returns.
+extern "C" int pffmg_apply_pageable(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                                    const double* h_v, double* h_out, double* d_v, double* d_out,
+                                    const int64_t* h_plane_off, int n_strips, void* stream) {
+    PFFMG_REQUIRE(lat && st && h_v && h_out && d_v && d_out && d_v != d_out, "pffmg_apply_pageable: bad pointers");
+    PFFMG_REQUIRE(which == PFFMG_FULL || which == PFFMG_UBLOCK || which == PFFMG_PBLOCK,
+                  "pffmg_apply_pageable: bad which %d", which);
+    const bool q2 = lat->order == 2;
+    const int nplanes = q2 ? 2 * lat->ny + 1 : (lat->dim == 3 ? lat->nz : lat->ny) + 1;
+    PFFMG_REQUIRE(lat->own_lo == 0 && (lat->own_hi == 0 || lat->own_hi == nplanes),
+                  "pffmg_apply_pageable: needs a whole (non-slab) lattice");
+    PFFMG_REQUIRE(lat->vrow_off == nullptr || h_plane_off != nullptr,
+                  "pffmg_apply_pageable: non-box lattices need host plane offsets");
+    int K = n_strips < 1 ? 1 : (n_strips > 64 ? 64 : n_strips);
+    if (K > nplanes) K = nplanes;
+    if (q2) K = 1;
+    PipeRes& R = pipe_res();
+    PFFMG_REQUIRE(R.ok, "pffmg_apply_pageable: could not create copy streams/events");
+    const cudaStream_t s = as_stream(stream);
+    const int64_t V = lat->n_vertices;
+    const int nc = which == PFFMG_FULL ? lat->dim + 1 : (which == PFFMG_UBLOCK ? lat->dim : 1);
+    const size_t need = (size_t)nc * (size_t)V;
+    if (R.stage_cap < need) {
+        if (R.stage_in) cudaFreeHost(R.stage_in);
+        if (R.stage_out) cudaFreeHost(R.stage_out);
+        R.stage_in = R.stage_out = nullptr;
+        R.stage_cap = 0;
+        if (cudaHostAlloc((void**)&R.stage_in, need * sizeof(double), cudaHostAllocDefault) != cudaSuccess ||
+            cudaHostAlloc((void**)&R.stage_out, need * sizeof(double), cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("pffmg_apply_pageable: could not allocate %zu bytes of page-locked staging",
+                      2 * need * sizeof(double));
+            return PFFMG_ERR_CUDA;
+        }
+        R.stage_cap = need;
+    }
+    double* const pin = R.stage_in;
+    double* const pout = R.stage_out;
+    const int64_t per_plane = q2 ? (int64_t)(2 * lat->nx + 1)
+                                 : (lat->dim == 3 ? (int64_t)(lat->nx + 1) * (lat->ny + 1) : (int64_t)(lat->nx + 1));
+    auto off = [&](int p) -> int64_t { return h_plane_off ? h_plane_off[p] : (int64_t)p * per_plane; };
+    int wsum = 0, wcum[65] = {0};
+    for (int i = 0; i < K; ++i) {
+        wsum += min(i + 1, K - i);
+        wcum[i + 1] = wsum;
+    }
+    int64_t lo[65];
+    int pb[65];
+    for (int i = 0; i <= K; ++i) {
+        pb[i] = (int)(((int64_t)nplanes * wcum[i]) / wsum);
+        lo[i] = off(pb[i]);
+    }
+    const int T = copy_threads();
+    std::atomic<int> in_done[64], out_ready[64];
+    for (int i = 0; i < K; ++i) {
+        in_done[i].store(0, std::memory_order_relaxed);
+        out_ready[i].store(0, std::memory_order_relaxed);
+    }
+    // worker t moves its share of every strip (all components): in, then out
+    auto worker = [&](int t) {
+        auto span = [&](int i, int64_t* a, int64_t* n) {
+            const int64_t len = lo[i + 1] - lo[i];
+            const int64_t c0 = (len * t / T) & ~(int64_t)7, c1 = t + 1 == T ? len : ((len * (t + 1) / T) & ~(int64_t)7);
+            *a = lo[i] + c0;
+            *n = c1 - c0;
+        };
+        for (int i = 0; i < K; ++i) {
+            int64_t a, n;
+            span(i, &a, &n);
+            if (n > 0)
+                for (int c = 0; c < nc; ++c) memcpy(pin + c * V + a, h_v + c * V + a, (size_t)n * sizeof(double));
+            in_done[i].fetch_add(1, std::memory_order_release);
+        }
+        for (int i = 0; i < K; ++i) {
+            int r;
+            while ((r = out_ready[i].load(std::memory_order_acquire)) == 0) std::this_thread::yield();
+            if (r < 0) return;                       // aborted
+            int64_t a, n;
+            span(i, &a, &n);
+            if (n > 0)
+                for (int c = 0; c < nc; ++c) memcpy(h_out + c * V + a, pout + c * V + a, (size_t)n * sizeof(double));
+        }
+    };
+    std::vector<std::thread> pool;
+    pool.reserve(T - 1);
+    for (int t = 1; t < T; ++t) pool.emplace_back(worker, t);
+    // the calling thread orchestrates the device side; it joins the copy-out as worker 0
+    const size_t pitch = (size_t)V * sizeof(double);
+    cudaEvent_t* ein = R.ev;
+    cudaEvent_t* ek = R.ev + 64;
+    cudaEvent_t* eo = R.ev + 128;
+    cudaEvent_t e0 = R.ev[192];
+    cudaEventRecord(e0, s);
+    cudaStreamWaitEvent(R.h2d, e0, 0);
+    cudaStreamWaitEvent(R.d2h, e0, 0);
+    pffmg_lattice sub = *lat;
+    int rc = PFFMG_OK;
+    auto stencil = [&](int i) {                      // strip i: needs the copies of strips i and i+1
+        cudaStreamWaitEvent(s, ein[i + 1 < K ? i + 1 : K - 1], 0);
+        if (!q2) {
+            sub.own_lo = pb[i];
+            sub.own_hi = pb[i + 1];
+        }
+        if (rc == PFFMG_OK && (q2 || sub.own_hi > sub.own_lo)) rc = pffmg_apply(&sub, st, which, d_v, d_out, stream);
+        cudaEventRecord(ek[i], s);
+        cudaStreamWaitEvent(R.d2h, ek[i], 0);
+        if (lo[i + 1] > lo[i])
+            cudaMemcpy2DAsync(pout + lo[i], pitch, d_out + lo[i], pitch, (size_t)(lo[i + 1] - lo[i]) * sizeof(double),
+                              nc, cudaMemcpyDeviceToHost, R.d2h);
+        cudaEventRecord(eo[i], R.d2h);
+    };
+    for (int i = 0; i < K; ++i) {
+        {   // this thread's share of strip i
+            const int64_t len = lo[i + 1] - lo[i];
+            const int64_t c1 = T == 1 ? len : ((len / T) & ~(int64_t)7);
+            if (c1 > 0)
+                for (int c = 0; c < nc; ++c) memcpy(pin + c * V + lo[i], h_v + c * V + lo[i], (size_t)c1 * sizeof(double));
+            in_done[i].fetch_add(1, std::memory_order_release);
+        }
+        while (in_done[i].load(std::memory_order_acquire) < T) std::this_thread::yield();
+        if (lo[i + 1] > lo[i])
+            cudaMemcpy2DAsync(d_v + lo[i], pitch, pin + lo[i], pitch, (size_t)(lo[i + 1] - lo[i]) * sizeof(double), nc,
+                              cudaMemcpyHostToDevice, R.h2d);
+        cudaEventRecord(ein[i], R.h2d);
+        if (i >= 1) stencil(i - 1);
+    }
+    stencil(K - 1);
+    for (int i = 0; i < K; ++i) {
+        const bool good = cudaEventSynchronize(eo[i]) == cudaSuccess && rc == PFFMG_OK;
+        out_ready[i].store(good ? 1 : -1, std::memory_order_release);
+        if (!good) {
+            for (int k = i + 1; k < K; ++k) out_ready[k].store(-1, std::memory_order_release);
+            if (rc == PFFMG_OK) {
+                set_error("pffmg_apply_pageable: copy-out failed: %s", cudaGetErrorString(cudaGetLastError()));
+                rc = PFFMG_ERR_CUDA;
+            }
+            break;
+        }
+        const int64_t len = lo[i + 1] - lo[i];
+        const int64_t c1 = T == 1 ? len : ((len / T) & ~(int64_t)7);
+        if (c1 > 0)
+            for (int c = 0; c < nc; ++c) memcpy(h_out + c * V + lo[i], pout + c * V + lo[i], (size_t)c1 * sizeof(double));
+    }
+    for (auto& th : pool) th.join();
+    cudaEventRecord(R.ev[193], R.d2h);
+    cudaStreamWaitEvent(s, R.ev[193], 0);
+    if (rc) return rc;
+    return check_launch("pffmg_apply_pageable");
 }
 
 extern "C" int pffmg_residual(const pffmg_lattice* lat, const pffmg_state* st, int which,

@@ -240,6 +240,9 @@ COARSE_KERNEL = os.environ.get("PFFMG_COARSE_KERNEL", "1") != "0"
 # Restriction into a level fused with that level's smoother start from x = 0
 # (pffmg_restrict_init_bd); PFFMG_FUSED_DESCENT=0: separate kernels.
 FUSED_DESCENT = os.environ.get("PFFMG_FUSED_DESCENT", "1") != "0"
+# The multi-stream setup (2L concurrent CG-Lanczos chains) launches with
+# programmatic dependent launch (PFFMG_SETUP_PDL=0: fully stream-ordered).
+SETUP_PDL = os.environ.get("PFFMG_SETUP_PDL", "1") != "0"
 # block-diagonal smoothing kernel (both blocks per launch) on levels with fewer
 # vertices than these; larger levels run the two block kernels per step
 BD_MAXV2 = int(os.environ.get("PFFMG_BD_MAXV2", str(1 << 40)))
@@ -379,6 +382,16 @@ class _Session:
         streams right after -- the fine level's chains (the critical path) no
         longer wait for the coarse levels' setup kernels.  The 2L chains are
         independent (each stream has its own reduction scratch in libpffmg)."""
+        if not SETUP_PDL:
+            prev = _lib.C.c_int(1)
+            _lib.call("pffmg_set_pdl", 0, _lib.C.byref(prev))
+            try:
+                return self._device_setup_body()
+            finally:
+                _lib.call("pffmg_set_pdl", prev.value, None)
+        return self._device_setup_body()
+
+    def _device_setup_body(self):
         D, s = self.D, _lib.stream()
         main = torch.cuda.current_stream()
         if self._streams is None:

@@ -271,6 +271,9 @@ class PhaseFieldOperator:
         Pinned host tensors take the pipelined host path (pffmg_apply_host)."""
         if _pinned_f64(v) and (out is None or _pinned_f64(out)) and self.lat.info.own == (0, 0):
             return self._apply_host(v, out)
+        if (PAGEABLE_PIPELINE and _plain_f64(v) and (out is None or _plain_f64(out, True))
+                and v.size == self.n_dofs >= PAGEABLE_MIN and self.lat.info.own == (0, 0)):
+            return self._apply_pageable(v, out)
         x = dev(v)
         if x.numel() != self.n_dofs:
             raise ValueError(f"expected {self.n_dofs} dofs, got {x.numel()}")
@@ -295,6 +298,25 @@ class PhaseFieldOperator:
                   _lib.ptr(bufs[0]), _lib.ptr(bufs[1]), None if po is None else po.ctypes.data,
                   strips, _lib.stream())
         torch.cuda.current_stream().synchronize()
+        return out
+
+    def _apply_pageable(self, v, out):
+        """numpy in / numpy out (what the reference's drivers pass): threaded
+        staging through the library's page-locked buffers, pipelined with the
+        link copies and the stencil (pffmg_apply_pageable)."""
+        n = self.n_dofs
+        if out is None:
+            out = np.empty(n, dtype=np.float64)
+        elif out.size != n:
+            raise ValueError(f"expected {n} dofs, got {out.size}")
+        bufs = getattr(self, "_host_bufs", None)
+        if bufs is None:
+            bufs = self._host_bufs = (empty(n), empty(n))
+        po = self.lat.plane_off_host
+        strips = int(max(1, min(8, round(8 * n / (4 << 20)))))
+        _lib.call("pffmg_apply_pageable", self.lat.ref, self._stp, _lib.FULL, v.ctypes.data, out.ctypes.data,
+                  _lib.ptr(bufs[0]), _lib.ptr(bufs[1]), None if po is None else po.ctypes.data,
+                  strips, _lib.stream())
         return out
 
     def apply_block(self, which, v_block):
@@ -409,6 +431,17 @@ def _modulus_table(space, lat, params):
         coords = _lattice_qp_coords(space.mesh)
         table = np.asarray(params.modulus_field(coords), dtype=float).reshape(ncell_lat, Q)
     return dev(table.ravel())
+
+
+# numpy vectors of at least PAGEABLE_MIN dofs go through pffmg_apply_pageable
+# (PFFMG_PAGEABLE_PIPELINE=0: plain pageable copies around the device apply)
+PAGEABLE_PIPELINE = os.environ.get("PFFMG_PAGEABLE_PIPELINE", "1") != "0"
+PAGEABLE_MIN = 1 << 17
+
+
+def _plain_f64(a, writeable=False):
+    return (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.ndim == 1
+            and a.flags.c_contiguous and a.flags.aligned and (a.flags.writeable or not writeable))
 
 
 def _pinned_f64(t):

@@ -205,6 +205,39 @@ def test_pinned_host_apply_pipeline_is_exact(golden, name):
         assert torch.equal(out, ref), strips
 
 
+@pytest.mark.parametrize("name", ["cfg1", "lshape", "lprism", "cube"])
+def test_pageable_host_apply_pipeline_is_exact(golden, name, monkeypatch):
+    """pffmg_apply_pageable (numpy in / out: threaded staging through page-locked
+    buffers, pipelined with the copies and the stencil) gives bit-identical
+    results to the device apply for any strip count; PhaseFieldOperator.apply
+    takes it for numpy vectors above PAGEABLE_MIN dofs."""
+    from paper_1902_08112_b200 import _lib, model
+    g = golden["operator"]
+    op, tag = _op(g, name, "masked")
+    v = np.ascontiguousarray(g[f"{tag}/v"], dtype=np.float64)
+    ref = op.apply(torch.as_tensor(v).cuda()).cpu().numpy()
+    calls = []
+    real = _lib.call
+    monkeypatch.setattr(_lib, "call", lambda name_, *a: (calls.append(name_), real(name_, *a))[1])
+    monkeypatch.setattr(model, "PAGEABLE_MIN", 1)
+    got = op.apply(v)                                             # public path, numpy -> numpy
+    assert "pffmg_apply_pageable" in calls
+    assert isinstance(got, np.ndarray) and np.array_equal(got, ref)
+    out = np.full_like(v, np.nan)
+    assert op.apply(v, out=out) is out and np.array_equal(out, ref)
+    monkeypatch.setattr(model, "PAGEABLE_PIPELINE", False)        # plain copies: same values
+    calls.clear()
+    assert np.array_equal(op.apply(v), ref) and "pffmg_apply_pageable" not in calls
+    d_in, d_out = torch.empty(v.size, dtype=torch.float64, device="cuda"), torch.empty(v.size, dtype=torch.float64,
+                                                                                      device="cuda")
+    po = op.lat.plane_off_host
+    for strips in (1, 2, 3, 7, 64):
+        out[:] = np.nan
+        real("pffmg_apply_pageable", op.lat.ref, op._stp, _lib.FULL, v.ctypes.data, out.ctypes.data,
+             _lib.ptr(d_in), _lib.ptr(d_out), None if po is None else po.ctypes.data, strips, _lib.stream())
+        assert np.array_equal(out, ref), strips
+
+
 @pytest.mark.parametrize("name", list(MESHES))
 @pytest.mark.parametrize("split", ["none", "miehe"])
 def test_blockdiag_operator_equals_blocks(golden, name, split):

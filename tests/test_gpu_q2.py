@@ -78,6 +78,13 @@ def test_q2_operator_matches_oracle(split, band, mod):
     # pinned host path
     vh = torch.as_tensor(v).pin_memory()
     assert rel_err(op.apply(vh).numpy(), ref.apply(v)) <= TOL
+    # numpy path through the threaded pageable pipeline (one strip for Q2)
+    M_min = M.PAGEABLE_MIN
+    try:
+        M.PAGEABLE_MIN = 1
+        assert np.array_equal(op.apply(v), out)
+    finally:
+        M.PAGEABLE_MIN = M_min
 
 
 def test_q2_transfers_match_oracle():
