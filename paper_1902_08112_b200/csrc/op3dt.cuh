@@ -277,9 +277,14 @@ __global__ void __launch_bounds__(T3_NT, MODE == M_FULL ? PFFMG_3D_FULL_MINB : (
         const double* rq = (RHO && cell) ? A.rho + lcell * 8 : A.rho;
         const double* tq = (TAB && cell) ? A.ptab + lcell : A.ptab;
         double vp[NCO][2];                       // this vertex column's (y=0) partials, per z corner
+        // absent cells (lattice edges, the L-prism's missing quadrant) contribute
+        // nothing; warps holding none skip the selects (a warp-uniform branch)
+        const bool any_absent = __any_sync(0xffffffffu, !cell);
         auto emit = [&](int k, double (&o)[8]) {
+            if (any_absent) {
 #pragma unroll
-            for (int n = 0; n < 8; ++n) o[n] = cell ? o[n] : 0.0;
+                for (int n = 0; n < 8; ++n) o[n] = cell ? o[n] : 0.0;
+            }
 #pragma unroll
             for (int zb = 0; zb < 2; ++zb)
 #pragma unroll

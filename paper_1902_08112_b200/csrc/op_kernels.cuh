@@ -356,7 +356,12 @@ op2dw_kernel(const OpArgs A) {
                 else
                     cell_kernel<D, MODE>(cv, rq, A.K, o);
             }
-            if (BRANCHLESS) {
+            // Lane 31's outputs are never used (its left corners belong to a
+            // vertex it does not finalise, its right corners are shuffled to
+            // nobody), so only warps holding an absent cell in lanes 0..30 --
+            // the lattice's edge columns / rows -- need the select: a
+            // warp-uniform branch around it.
+            if (BRANCHLESS && __any_sync(0xffffffffu, !cell && lane < 31)) {
 #pragma unroll
                 for (int k = 0; k < NCO; ++k)
 #pragma unroll
