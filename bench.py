@@ -608,7 +608,7 @@ def measure_strong(name, ws, rank, args):
     res = {"config": name, "n_dofs": prob.n_dofs, "n_gpus": ws, "vmult_ms": per * 1e3,
            "value": prob.n_dofs / per * 1e-9, "unit": "GDoF/s",
            "what": "z-slab sharded fused vmult, halo exchange overlapped with the interior planes, "
-                   "time = max over ranks (the single-GPU figure: configs.cfg5 of the N = 1 line)"}
+                   f"time = max over ranks (the single-GPU figure: configs.{name} of the N = 1 line)"}
     del v, out, dop, flush
     torch.cuda.empty_cache()
     if not args.no_solve:

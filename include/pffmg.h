@@ -249,6 +249,19 @@ int pffmg_cheb_init_zero_bd(const double* b, const double* invdiag, const double
                             const double* theta_p, int64_t n_u, double* r, double* d, double* x,
                             int64_t n, void* stream);
 
+/* "Lean" x = 0 start: the start's residual is the right-hand side and its
+ * iterate is d, so pffmg_cheb_init_zero(_dc/_bd), pffmg_masked_copy_init_bd and
+ * pffmg_restrict_init_bd accept r = x = NULL (only d is stored), and the FIRST
+ * step of the recurrence (mgsolve.py:108-111) then goes through these entry
+ * points: the residual is read from `rhs`, x is not read (x_old = 0 + d_in), and
+ * r, d_out, x are written.  Bit-identical to the full init + pffmg_cheb_step_*. */
+int pffmg_cheb_first_dc(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                        const double* d_in, const double* rhs, double* d_out, double* r, double* x,
+                        const double* invdiag, const double* coef, void* stream);
+int pffmg_cheb_first_bd(const pffmg_lattice* lat, const pffmg_state* st, const double* d_in,
+                        const double* rhs, double* d_out, double* r, double* x, const double* invdiag,
+                        const double* coef_u, const double* coef_p, void* stream);
+
 /* The whole coarse_solve of the V-cycle (mgsolve.py:209-218) in one launch for
  * small whole levels (<= 256 lattice cells): both blocks' Chebyshev
  * recurrences from x = 0 with degrees deg_u / deg_p and the coefficient

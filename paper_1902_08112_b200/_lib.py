@@ -73,6 +73,8 @@ _SIGS = {
     "pffmg_boundary_load": [C.POINTER(Lattice), C.POINTER(State), vp, vp, C.c_int64, C.c_int, vp, vp, vp],
     "pffmg_coarse_cheb": [C.POINTER(Lattice), C.POINTER(State), vp, vp, vp, vp, vp, vp, C.c_int, vp, C.c_int, vp],
     "pffmg_cheb_step_bd": [C.POINTER(Lattice), C.POINTER(State), vp, vp, vp, vp, vp, vp, vp, C.c_int, vp],
+    "pffmg_cheb_first_bd": [C.POINTER(Lattice), C.POINTER(State), vp, vp, vp, vp, vp, vp, vp, vp, vp],
+    "pffmg_cheb_first_dc": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, vp, vp, vp],
     "pffmg_cheb_init_bd": [C.POINTER(Lattice), C.POINTER(State), vp, vp, vp, vp, vp, vp, vp, vp],
     "pffmg_cheb_init_zero_bd": [vp, vp, vp, vp, C.c_int64, vp, vp, vp, C.c_int64, vp],
     "pffmg_cheb_step_dc": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, vp,

@@ -40,7 +40,9 @@ struct OpArgs {
     const double* __restrict__ coef;   // if set, c1/c2 are read from device memory (coef[0], coef[1])
     const double* __restrict__ coef2;  // block-diagonal mode: the phase-field component's coefficients
     int nocoup;                        // FULL mode without the G_phiu coupling (block-diagonal operator)
-    int x_add_din;                     // CHEB: x = (x + d_in) + d_out instead of x += d_out
+    int x_add_din;                     // CHEB: 1: x = (x + d_in) + d_out instead of x += d_out;
+                                       // 2: first step after the x = 0 start: x_old = 0 + d_in, x is not read
+    const double* __restrict__ r_in;   // CHEB: residual read from here (written to r) if set
     int planes_per_cta;
     int nseg;                          // 2D warp kernel: 30-column segments per row
     int sched;                         // work schedule of the streaming kernels (tuning, see launchers)
@@ -66,9 +68,9 @@ __device__ __forceinline__ void epi_load(const OpArgs& A, int64_t vid, EpiIn<NCO
     for (int k = 0; k < NCO; ++k) {
         const int64_t g = (int64_t)k * V + vid;
         if (EPI == E_CHEB) {
-            e.a[0][k] = A.r[g];
+            e.a[0][k] = A.r_in ? __ldg(A.r_in + g) : A.r[g];
             e.a[1][k] = __ldg(A.inv + g);
-            e.a[2][k] = A.x[g];
+            e.a[2][k] = A.x_add_din == 2 ? 0.0 : A.x[g];
         } else if (EPI == E_CHEB0) {
             e.a[0][k] = __ldg(A.b + g);
             e.a[1][k] = __ldg(A.inv + g);
@@ -89,9 +91,9 @@ __device__ __forceinline__ void epi_stage(const OpArgs& A, int64_t vid, double* 
     for (int k = 0; k < NCO; ++k) {
         const int64_t g = (int64_t)k * V + vid;
         if (EPI == E_CHEB) {
-            cp_async8(slot + 0 * NCO + k, A.r + g, true);
+            cp_async8(slot + 0 * NCO + k, (A.r_in ? A.r_in : A.r) + g, true);
             cp_async8(slot + 1 * NCO + k, A.inv + g, true);
-            cp_async8(slot + 2 * NCO + k, A.x + g, true);
+            if (A.x_add_din != 2) cp_async8(slot + 2 * NCO + k, A.x + g, true);
         } else if (EPI == E_CHEB0) {
             cp_async8(slot + 0 * NCO + k, A.b + g, true);
             cp_async8(slot + 1 * NCO + k, A.inv + g, true);
@@ -140,8 +142,9 @@ __device__ __forceinline__ void epilogue(const OpArgs& A, int64_t vid, uint8_t f
             const double dn = c1 * vin[k] + c2 * (e.a[1][k] * rr);
             A.r[g] = rr;
             A.dout[g] = dn;
-            const double xo = e.a[2][k];
-            A.x[g] = A.x_add_din ? (xo + vin[k]) + dn : xo + dn;
+            // (2: x was started as 0.0 + d_in by the x = 0 init, which did not store it)
+            const double xo = A.x_add_din == 2 ? 0.0 + vin[k] : e.a[2][k];
+            A.x[g] = A.x_add_din == 1 ? (xo + vin[k]) + dn : xo + dn;
         } else {                                                 // E_CHEB0: mgsolve.py:95, 105
             const double rr = e.a[0][k] - Av;
             A.r[g] = rr;

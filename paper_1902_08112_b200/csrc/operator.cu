@@ -506,6 +506,51 @@ extern "C" int pffmg_cheb_step_bd(const pffmg_lattice* lat, const pffmg_state* s
     return dispatch_which<E_CHEB>(A, PFFMG_BLOCKDIAG, as_stream(stream), "pffmg_cheb_step_bd");
 }
 
+// First Chebyshev step after the x = 0 start (mgsolve.py:95, 103-111 with
+// x = 0): the start's residual is the right-hand side itself and its iterate
+// is d_in, so the step reads r from `rhs`, never reads x, and writes r, d_out
+// and x -- the init then stores d only (r / x = NULL in the *_init_zero* /
+// *_init_bd entry points).  Bit-identical to init + pffmg_cheb_step_*.
+extern "C" int pffmg_cheb_first_dc(const pffmg_lattice* lat, const pffmg_state* st, int which,
+                                   const double* d_in, const double* rhs, double* d_out, double* r, double* x,
+                                   const double* invdiag, const double* coef, void* stream) {
+    OpArgs A;
+    int rc = fill_args(lat, st, &A);
+    if (rc) return rc;
+    PFFMG_REQUIRE(d_in && rhs && d_out && r && x && invdiag && coef && d_in != d_out && x != d_in && r != rhs,
+                  "pffmg_cheb_first_dc: bad pointers");
+    A.v = d_in;
+    A.dout = d_out;
+    A.r_in = rhs;
+    A.r = r;
+    A.x = x;
+    A.inv = invdiag;
+    A.coef = coef;
+    A.x_add_din = 2;
+    return dispatch_which<E_CHEB>(A, which, as_stream(stream), "pffmg_cheb_first_dc");
+}
+
+extern "C" int pffmg_cheb_first_bd(const pffmg_lattice* lat, const pffmg_state* st, const double* d_in,
+                                   const double* rhs, double* d_out, double* r, double* x, const double* invdiag,
+                                   const double* coef_u, const double* coef_p, void* stream) {
+    OpArgs A;
+    int rc = fill_args(lat, st, &A);
+    if (rc) return rc;
+    PFFMG_REQUIRE(d_in && rhs && d_out && r && x && invdiag && coef_u && coef_p && d_in != d_out && x != d_in &&
+                      r != rhs,
+                  "pffmg_cheb_first_bd: bad pointers");
+    A.v = d_in;
+    A.dout = d_out;
+    A.r_in = rhs;
+    A.r = r;
+    A.x = x;
+    A.inv = invdiag;
+    A.coef = coef_u;
+    A.coef2 = coef_p;
+    A.x_add_din = 2;
+    return dispatch_which<E_CHEB>(A, PFFMG_BLOCKDIAG, as_stream(stream), "pffmg_cheb_first_bd");
+}
+
 extern "C" int pffmg_cheb_init_bd(const pffmg_lattice* lat, const pffmg_state* st, const double* x,
                                   const double* b, double* r, double* d, const double* invdiag,
                                   const double* theta_u, const double* theta_p, void* stream) {

@@ -126,9 +126,11 @@ __global__ void restrict_init_bd_kernel(Lat Lc, Lat Lf, const double* __restrict
         const double ri = ((fl >> k) & 1) ? 0.0 : acc[k];
         const double di = (__ldg(inv + g) * ri) / (k < D ? thu : thp);
         vc[g] = ri;
-        r[g] = ri;
         d[g] = di;
-        x[g] = 0.0 + di;
+        if (r) {                                 // (NULL: the first step is pffmg_cheb_first_bd)
+            r[g] = ri;
+            x[g] = 0.0 + di;
+        }
     }
 }
 
@@ -427,7 +429,7 @@ extern "C" int pffmg_restrict_init_bd(const pffmg_lattice* coarse, const pffmg_l
     int rc = check_pair(coarse, fine, &Lc, &Lf, &q2);
     if (rc) return rc;
     PFFMG_REQUIRE(!q2, "pffmg_restrict_init_bd: Q1 lattices only");
-    PFFMG_REQUIRE(vf && vc && coarse_flags && invdiag && theta_u && theta_p && r && d && x,
+    PFFMG_REQUIRE(vf && vc && coarse_flags && invdiag && theta_u && theta_p && d && !r == !x,
                   "pffmg_restrict_init_bd: bad arguments");
     if (Lc.dim == 3)
         pdl_launch(restrict_init_bd_kernel<3>, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf,

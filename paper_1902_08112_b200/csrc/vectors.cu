@@ -332,9 +332,11 @@ __global__ void masked_copy_init_bd_k(const uint8_t* f, int64_t V, int nc, const
         const double ri = ((f[v] >> c) & 1) ? 0.0 : in[i];
         const double di = (inv[i] * ri) / (c < nc - 1 ? thu : thp);
         rhs[i] = ri;
-        r[i] = ri;
         d[i] = di;
-        x[i] = 0.0 + di;
+        if (r) {                                   // (NULL: the first step is pffmg_cheb_first_*)
+            r[i] = ri;
+            x[i] = 0.0 + di;
+        }
     }
 }
 __global__ void reciprocal_k(const double* d, double* o, int64_t n) {
@@ -348,9 +350,11 @@ __global__ void cheb_init_zero_k(const double* b, const double* inv, double thet
     GRID_STRIDE(i, n) {
         const double ri = b[i];
         const double di = (inv[i] * ri) / theta;   // mgsolve.py:105
-        r[i] = ri;
         d[i] = di;
-        x[i] = 0.0 + di;                           // x = zeros; x += d
+        if (r) {
+            r[i] = ri;
+            x[i] = 0.0 + di;                       // x = zeros; x += d
+        }
     }
 }
 __global__ void jacobi_update_k(const double* r, const double* inv, double theta_v, const double* theta_p,
@@ -425,7 +429,7 @@ extern "C" int pffmg_masked_copy(const uint8_t* flags, int64_t V, int comp0, int
 extern "C" int pffmg_masked_copy_init_bd(const uint8_t* flags, int64_t V, int n_comp, const double* in,
                                          double* rhs, const double* invdiag, const double* theta_u,
                                          const double* theta_p, double* r, double* d, double* x, void* stream) {
-    PFFMG_REQUIRE(flags && in && rhs && invdiag && theta_u && theta_p && r && d && x && V >= 0 && n_comp >= 2 &&
+    PFFMG_REQUIRE(flags && in && rhs && invdiag && theta_u && theta_p && d && !r == !x && V >= 0 && n_comp >= 2 &&
                       n_comp <= 4,
                   "pffmg_masked_copy_init_bd: bad args");
     pdl_launch(masked_copy_init_bd_k, dim3(vgrid(V * n_comp)), dim3(256), 0, as_stream(stream), flags, V, n_comp, in,
@@ -445,7 +449,7 @@ extern "C" int pffmg_cheb_init_zero(const double* b, const double* invdiag, doub
 }
 extern "C" int pffmg_cheb_init_zero_dc(const double* b, const double* invdiag, const double* theta, double* r,
                                        double* d, double* x, int64_t n, void* stream) {
-    PFFMG_REQUIRE(b && invdiag && theta && r && d && x, "pffmg_cheb_init_zero_dc: bad args");
+    PFFMG_REQUIRE(b && invdiag && theta && d && !r == !x, "pffmg_cheb_init_zero_dc: bad args");
     pdl_launch(cheb_init_zero_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), b, invdiag, 0.0, theta, r, d, x, n);
     VCHECK("pffmg_cheb_init_zero_dc");
 }
@@ -456,15 +460,17 @@ __global__ void cheb_init_zero_bd_k(const double* b, const double* inv, const do
     GRID_STRIDE(i, n) {
         const double ri = b[i];
         const double di = (inv[i] * ri) / (i < n_u ? thu : thp);
-        r[i] = ri;
         d[i] = di;
-        x[i] = 0.0 + di;
+        if (r) {
+            r[i] = ri;
+            x[i] = 0.0 + di;
+        }
     }
 }
 extern "C" int pffmg_cheb_init_zero_bd(const double* b, const double* invdiag, const double* theta_u,
                                        const double* theta_p, int64_t n_u, double* r, double* d, double* x,
                                        int64_t n, void* stream) {
-    PFFMG_REQUIRE(b && invdiag && theta_u && theta_p && r && d && x && n_u >= 0 && n_u <= n,
+    PFFMG_REQUIRE(b && invdiag && theta_u && theta_p && d && !r == !x && n_u >= 0 && n_u <= n,
                   "pffmg_cheb_init_zero_bd: bad args");
     pdl_launch(cheb_init_zero_bd_k, dim3(vgrid(n)), dim3(256), 0, as_stream(stream), b, invdiag, theta_u, theta_p, n_u, r, d, x, n);
     VCHECK("pffmg_cheb_init_zero_bd");

@@ -240,6 +240,10 @@ COARSE_KERNEL = os.environ.get("PFFMG_COARSE_KERNEL", "1") != "0"
 # Restriction into a level fused with that level's smoother start from x = 0
 # (pffmg_restrict_init_bd); PFFMG_FUSED_DESCENT=0: separate kernels.
 FUSED_DESCENT = os.environ.get("PFFMG_FUSED_DESCENT", "1") != "0"
+# x = 0 starts store d only and the first Chebyshev step reads r from the
+# right-hand side and x from d (pffmg_cheb_first_*); PFFMG_LEAN_START=0: the
+# start writes r, d, x and every step is a pffmg_cheb_step_*.
+LEAN_START = os.environ.get("PFFMG_LEAN_START", "1") != "0"
 # The multi-stream setup (2L concurrent CG-Lanczos chains) launches with
 # programmatic dependent launch (PFFMG_SETUP_PDL=0: fully stream-ordered).
 SETUP_PDL = os.environ.get("PFFMG_SETUP_PDL", "1") != "0"
@@ -784,9 +788,10 @@ class _NativeCycle:
                           _lib.ptr(x), nb, s)
                 self._stencil(L, x, nk, lambda: op.residual_dev(k, x, rhs, r, pre=pre))
             return
+        lean = x_is_zero and LEAN_START and prm.degree >= 2
         if x_is_zero:                                      # r = b; d = inv r / theta; x = d
             _lib.call("pffmg_cheb_init_zero_dc", _lib.ptr(rhs), _lib.ptr(inv), _lib.ptr(theta),
-                      _lib.ptr(r), _lib.ptr(d_in), _lib.ptr(x), nb, s)
+                      None if lean else _lib.ptr(r), _lib.ptr(d_in), None if lean else _lib.ptr(x), nb, s)
             pending = False
         else:                                              # r = b - A x; d = inv r / theta
             self._stencil(L, x, L.dim if k == 0 else 1,
@@ -794,8 +799,12 @@ class _NativeCycle:
             pending = True                                 # x += d folded into the next step
         for i in range(prm.degree - 1):
             c = coef[off + 1 + 2 * i: off + 3 + 2 * i]
-            self._stencil(L, d_in, L.dim if k == 0 else 1,
-                          lambda: op.cheb_step_dc(k, d_in, d_out, r, x, inv, c, pending, pre=pre))
+            if lean and i == 0:                            # r read from rhs, x = d_in + d_out
+                self._stencil(L, d_in, L.dim if k == 0 else 1,
+                              lambda: op.cheb_first_dc(k, d_in, rhs, d_out, r, x, inv, c, pre=pre))
+            else:
+                self._stencil(L, d_in, L.dim if k == 0 else 1,
+                              lambda: op.cheb_step_dc(k, d_in, d_out, r, x, inv, c, pending, pre=pre))
             pending = False
             d_in, d_out = d_out, d_in
         if pending:                                        # degree 1 from a non-zero x
@@ -806,6 +815,11 @@ class _NativeCycle:
         _, pp, degp = self.slot[sp]
         return not (not BLOCKDIAG_SMOOTH or not L.bd_ok or degu or degp or
                     (pu.degree != pp.degree and not x_is_zero))
+
+    def _lean_pair(self, L, su, sp):
+        """The block-diagonal x = 0 start of (su, sp) stores d only (see LEAN_START)."""
+        return (LEAN_START and self._bd_pair_ok(L, su, sp, True) and
+                min(self.slot[su][1].degree, self.slot[sp][1].degree) >= 2)
 
     def _cheb_pair(self, L, su, sp, x_is_zero, pre=True, init_done=False):
         """Chebyshev on both diagonal blocks (independent, mgsolve.py:200-206) with
@@ -821,11 +835,13 @@ class _NativeCycle:
         op, coef, s = L.op, self.coef, _lib.stream()
         x, r, rhs, inv, d_in, d_out = L.x, L.cr, L.r, L.inv, L.d0, L.d1
         tu, tp = coef[ou:ou + 1], coef[op_:op_ + 1]
+        lean = x_is_zero and self._lean_pair(L, su, sp)
         if x_is_zero and init_done:
             pending = False
         elif x_is_zero:
             _lib.call("pffmg_cheb_init_zero_bd", _lib.ptr(rhs), _lib.ptr(inv), _lib.ptr(tu), _lib.ptr(tp),
-                      L.dim * L.V, _lib.ptr(r), _lib.ptr(d_in), _lib.ptr(x), L.n, s)
+                      L.dim * L.V, None if lean else _lib.ptr(r), _lib.ptr(d_in),
+                      None if lean else _lib.ptr(x), L.n, s)
             pending = False
         else:
             self._stencil(L, x, L.dim + 1, lambda: op.cheb_init_bd(x, rhs, r, d_in, inv, tu, tp, pre=pre))
@@ -833,8 +849,12 @@ class _NativeCycle:
         common = min(pu.degree, pp.degree) - 1
         for i in range(common):
             cu, cp = coef[ou + 1 + 2 * i: ou + 3 + 2 * i], coef[op_ + 1 + 2 * i: op_ + 3 + 2 * i]
-            self._stencil(L, d_in, L.dim + 1,
-                          lambda: op.cheb_step_bd(d_in, d_out, r, x, inv, cu, cp, pending, pre=pre))
+            if lean and i == 0:
+                self._stencil(L, d_in, L.dim + 1,
+                              lambda: op.cheb_first_bd(d_in, rhs, d_out, r, x, inv, cu, cp, pre=pre))
+            else:
+                self._stencil(L, d_in, L.dim + 1,
+                              lambda: op.cheb_step_bd(d_in, d_out, r, x, inv, cu, cp, pending, pre=pre))
             pending = False
             d_in, d_out = d_out, d_in
         if pending:                                        # degree 1 from a non-zero x
@@ -881,8 +901,10 @@ class _NativeCycle:
         if self._fused_descent_ok(l - 1):
             ou, _, _ = self.slot[("s", l - 1, 0)]
             op_, _, _ = self.slot[("s", l - 1, 1)]
+            lean = self._lean_pair(Lc, ("s", l - 1, 0), ("s", l - 1, 1))
             self.disc.restrict_init_bd_dev(L.res, Lc.r, l - 1, Lc.flags, Lc.inv, self.coef[ou:ou + 1],
-                                           self.coef[op_:op_ + 1], Lc.cr, Lc.d0, Lc.x)
+                                           self.coef[op_:op_ + 1], None if lean else Lc.cr, Lc.d0,
+                                           None if lean else Lc.x)
             self._cycle(l - 1, init_done=True)
         else:
             self._restrict(l - 1, L.res, Lc.r, L.dim + 1, 0, Lc.flags)
@@ -930,10 +952,11 @@ class _NativeCycle:
                 t = len(self.levels) - 1
                 ou, _, _ = self.slot[("s", t, 0)]
                 op_, _, _ = self.slot[("s", t, 1)]
+                lean = self._lean_pair(top, ("s", t, 0), ("s", t, 1))
                 _lib.call("pffmg_masked_copy_init_bd", _lib.ptr(top.flags), top.V, top.dim + 1, _lib.ptr(r),
                           _lib.ptr(top.r), _lib.ptr(top.inv), _lib.ptr(self.coef[ou:ou + 1]),
-                          _lib.ptr(self.coef[op_:op_ + 1]), _lib.ptr(top.cr), _lib.ptr(top.d0),
-                          _lib.ptr(top.x), _lib.stream())
+                          _lib.ptr(self.coef[op_:op_ + 1]), None if lean else _lib.ptr(top.cr),
+                          _lib.ptr(top.d0), None if lean else _lib.ptr(top.x), _lib.stream())
             else:
                 _lib.call("pffmg_masked_copy", _lib.ptr(top.flags), top.V, 0, top.dim + 1,
                           _lib.ptr(r), _lib.ptr(top.r), _lib.stream())

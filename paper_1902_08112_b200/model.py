@@ -404,6 +404,17 @@ class PhaseFieldOperator:
                   _lib.ptr(r), _lib.ptr(x), _lib.ptr(inv), _lib.ptr(coef_u), _lib.ptr(coef_p),
                   int(x_add_din), _lib.stream())
 
+    def cheb_first_bd(self, d_in, rhs, d_out, r, x, inv, coef_u, coef_p, pre=False):
+        """First step after the lean x = 0 start (r = rhs, x = d_in not stored): both blocks."""
+        _lib.call("pffmg_cheb_first_bd", self._lref(), self._sp(pre), _lib.ptr(d_in), _lib.ptr(rhs),
+                  _lib.ptr(d_out), _lib.ptr(r), _lib.ptr(x), _lib.ptr(inv), _lib.ptr(coef_u), _lib.ptr(coef_p),
+                  _lib.stream())
+
+    def cheb_first_dc(self, which, d_in, rhs, d_out, r, x, inv, coef, pre=False):
+        """First step after the lean x = 0 start of one block."""
+        _lib.call("pffmg_cheb_first_dc", self._lref(), self._sp(pre), which, _lib.ptr(d_in), _lib.ptr(rhs),
+                  _lib.ptr(d_out), _lib.ptr(r), _lib.ptr(x), _lib.ptr(inv), _lib.ptr(coef), _lib.stream())
+
     def cheb_init_bd(self, x, b, r, d, inv, theta_u, theta_p, pre=False):
         _lib.call("pffmg_cheb_init_bd", self._lref(), self._sp(pre), _lib.ptr(x), _lib.ptr(b), _lib.ptr(r),
                   _lib.ptr(d), _lib.ptr(inv), _lib.ptr(theta_u), _lib.ptr(theta_p), _lib.stream())

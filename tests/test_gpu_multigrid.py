@@ -294,6 +294,32 @@ def test_fused_descent_and_entry_match_separate_kernels(golden, name, monkeypatc
     assert torch.equal(out[0], out[1])
 
 
+@pytest.mark.parametrize("name", MG)
+@pytest.mark.parametrize("kind", ["full", "block_diag"])
+@pytest.mark.parametrize("bd", [True, False])
+def test_lean_chebyshev_start_matches_full_start(golden, name, kind, bd, monkeypatch):
+    """x = 0 starts that store d only + pffmg_cheb_first_* (the first step reads r
+    from the right-hand side and x from d) are bitwise the full start + step, in
+    the block-diagonal and the per-block smoothers, FULL and BLOCK_DIAG cycles."""
+    from paper_1902_08112_b200 import _lib, mgsolve
+    g = golden["multigrid"]
+    r = torch.as_tensor(g[f"{name}/r"], device="cuda")
+    pk = mgsolve.PreconditionerKind.FULL if kind == "full" else mgsolve.PreconditionerKind.BLOCK_DIAG
+    monkeypatch.setattr(mgsolve, "BLOCKDIAG_SMOOTH", bd)
+    out, seen = [], []
+    real = _lib.call
+    monkeypatch.setattr(_lib, "call", lambda n_, *a: (seen.append(n_), real(n_, *a))[1])
+    for flag in (True, False):
+        monkeypatch.setattr(mgsolve, "LEAN_START", flag)
+        mgsolve._Session._cache.clear()
+        mgsolve._NativeCycle._cache.clear()
+        seen.clear()
+        disc, ctxs = _contexts(g, name)
+        out.append(mgsolve.vcycle(ctxs, pk, r))
+        assert any(n_.startswith("pffmg_cheb_first") for n_ in seen) == flag
+    assert torch.equal(out[0], out[1])
+
+
 def test_gmres_restart_above_64():
     """Restart lengths above the one-launch MGS bound (64) take the multi-launch
     Arnoldi path and still match the oracle (reference krylov.py:50-136 accepts any m)."""

@@ -143,8 +143,10 @@ def test_q2_vcycle_and_gmres_match_oracle():
     assert rel_err(x, xo) <= 1e-6
 
 
-def test_q2_fused_descent_and_entry_match_separate_kernels(monkeypatch):
-    """The fused descent / V-cycle entry on Q2 levels are bitwise the separate kernels."""
+@pytest.mark.parametrize("flag_name", ["FUSED_DESCENT", "LEAN_START"])
+def test_q2_fused_descent_and_entry_match_separate_kernels(monkeypatch, flag_name):
+    """The fused descent / V-cycle entry and the lean Chebyshev start (d-only
+    x = 0 start + pffmg_cheb_first_*) on Q2 levels are bitwise the separate kernels."""
     from paper_1902_08112_b200 import mgsolve
     from paper_1902_08112_b200 import model as M
     levels, tables, tr = _oracle()
@@ -157,7 +159,7 @@ def test_q2_fused_descent_and_entry_match_separate_kernels(monkeypatch):
     r = torch.as_tensor(rng.standard_normal(n), device="cuda")
     out = []
     for flag in (True, False):
-        monkeypatch.setattr(mgsolve, "FUSED_DESCENT", flag)
+        monkeypatch.setattr(mgsolve, flag_name, flag)
         mgsolve._Session._cache.clear()
         mgsolve._NativeCycle._cache.clear()
         disc = _product()
