@@ -475,6 +475,29 @@ def newton_step_fn(prob, mask):
     return newton_step
 
 
+def newton_step_numpy_fn(prob, mask):
+    """The same Newton step with numpy state, masks and right-hand side in and a
+    numpy solution out -- what the reference's own driver (ActiveSetSolver.solve_step
+    through patch.install) exchanges with the twins every step."""
+    from paper_1902_08112_b200 import krylov, mgsolve
+    from paper_1902_08112_b200 import model as M
+    ctl = krylov.SolverControl(abs_tol=0.0, rel_tol=1e-8, restart=30, max_iters=1000)
+
+    def newton_step():
+        t0 = time.perf_counter()
+        R = M.residual(prob.disc.finest, prob.state, prob.dirichlet, prob.params, M.SplitKind.NOSPLIT)
+        R = -np.asarray(R)
+        R[mask.is_constrained] = 0.0
+        ctxs = mgsolve.build_level_contexts(prob.disc, prob.state, prob.active, prob.dirichlet,
+                                            prob.params, M.SplitKind.NOSPLIT)
+        pc = mgsolve.VCyclePreconditioner(ctxs, degree=prob.degree)
+        x, its = krylov.gmres(ctxs[-1].op.apply, pc, R, ctl)
+        assert isinstance(x, np.ndarray)
+        return time.perf_counter() - t0, its
+
+    return newton_step
+
+
 def solve_bytes(newton_step):
     """Algorithmic bytes and launches of one Newton step, from the launch list of
     an eager run (PFFMG_GRAPHS=0: the kernels the graphs replay) through
@@ -514,6 +537,14 @@ def measure_solve(prob, mask, hbm, with_bytes=True):
            "control": "GMRES(30) rel 1e-8 abs 0, V(1,1) FULL, Chebyshev deg %d" % prob.degree,
            "timing": "wall clock, median of 3 after one warm-up"}
     if with_bytes:
+        step_np = newton_step_numpy_fn(prob, mask)
+        step_np()
+        ts = [step_np() for _ in range(3)]
+        out["numpy_io"] = {"ms_per_newton_step": float(np.median([t[0] for t in ts])) * 1e3,
+                           "gmres_iters": ts[-1][1],
+                           "what": "the same step with numpy state / masks / right-hand side in and a numpy "
+                                   "solution out (the reference driver's calling convention; pageable copies "
+                                   "through pffmg_copy_h2d / _d2h)"}
         b = solve_bytes(newton_step)
         t = setup_s + gmres_s
         out["hbm"] = {"bytes_F": b["bytes_F"], "bytes_C": b["bytes_C"], "launches": b["launches"],

@@ -17,6 +17,7 @@
 #ifndef PFFMG_H
 #define PFFMG_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -216,6 +217,13 @@ int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st, int which,
 int pffmg_apply_pageable(const pffmg_lattice* lat, const pffmg_state* st, int which,
                          const double* h_v, double* h_out, double* d_v, double* d_out,
                          const int64_t* h_plane_off, int n_strips, void* stream);
+
+/* Copies between ORDINARY (pageable) host memory and device memory for the
+ * numpy-facing twins: 4 MiB chunks through a ring of page-locked slots, filled /
+ * drained by host threads (PFFMG_COPY_THREADS) while earlier chunks are on the
+ * link.  Ordered after prior work on `stream`; synchronous (complete on return). */
+int pffmg_copy_h2d(const void* host, void* device, size_t bytes, void* stream);
+int pffmg_copy_d2h(const void* device, void* host, size_t bytes, void* stream);
 
 /* Boundary load (model.py:511-547): sum over the n_faces boundary faces
  * (face_cell[i] = lattice cell index cx + nx (cy + ny cz), face_id[i] =

@@ -68,6 +68,8 @@ _SIGS = {
     "pffmg_cheb_init": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp,
                         C.c_double, vp],
     "pffmg_apply_host": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, C.c_int, vp],
+    "pffmg_copy_h2d": [vp, vp, C.c_size_t, vp],
+    "pffmg_copy_d2h": [vp, vp, C.c_size_t, vp],
     "pffmg_apply_pageable": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp, vp, vp, vp, C.c_int, vp],
     "pffmg_qoi": [C.POINTER(Lattice), C.POINTER(State), C.c_int, vp, vp],
     "pffmg_boundary_load": [C.POINTER(Lattice), C.POINTER(State), vp, vp, C.c_int64, C.c_int, vp, vp, vp],

@@ -9,6 +9,8 @@ moves the user's own data, never the pffmg kernels, to the host.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -21,6 +23,13 @@ def is_tensor(a):
     return isinstance(a, torch.Tensor)
 
 
+# numpy arrays of at least THREADED_MIN bytes cross the link through libpffmg's
+# threaded page-locked staging (pffmg_copy_h2d / _d2h) instead of the driver's
+# single-threaded pageable copy (PFFMG_THREADED_COPIES=0: plain torch copies)
+THREADED_COPIES = os.environ.get("PFFMG_THREADED_COPIES", "1") != "0"
+THREADED_MIN = 1 << 20
+
+
 def dev(a, dtype=F64):
     """float64 (or dtype) contiguous CUDA tensor view/copy of `a`."""
     if isinstance(a, torch.Tensor):
@@ -30,16 +39,45 @@ def dev(a, dtype=F64):
             a = a.to(dtype)
         return a.contiguous()
     arr = np.ascontiguousarray(np.asarray(a), dtype=_np_dtype(dtype))
+    if THREADED_COPIES and arr.nbytes >= THREADED_MIN:
+        out = torch.empty(arr.shape, dtype=dtype, device="cuda")
+        _lib.call("pffmg_copy_h2d", arr.ctypes.data, _lib.ptr(out), arr.nbytes, _lib.stream())
+        return out
     return torch.from_numpy(arr).to("cuda")
 
 
+_NP_OF = {torch.float64: np.float64, torch.uint8: np.uint8, torch.bool: np.bool_,
+          torch.int64: np.int64, torch.int32: np.int32}
+
+
 def _np_dtype(dtype):
-    return {torch.float64: np.float64, torch.uint8: np.uint8, torch.bool: np.bool_,
-            torch.int64: np.int64, torch.int32: np.int32}[dtype]
+    return _NP_OF[dtype]
+
+
+def copy_into(buf, src, dtype=F64):
+    """buf (a contiguous CUDA tensor) <- src (tensor or numpy array of the same size)."""
+    if isinstance(src, torch.Tensor):
+        buf.copy_(src)
+        return buf
+    arr = np.ascontiguousarray(np.asarray(src), dtype=_np_dtype(dtype))
+    if arr.size != buf.numel():
+        raise ValueError(f"expected {buf.numel()} entries, got {arr.size}")
+    if THREADED_COPIES and arr.nbytes >= THREADED_MIN and buf.is_contiguous() and buf.dtype == dtype:
+        _lib.call("pffmg_copy_h2d", arr.ctypes.data, _lib.ptr(buf), arr.nbytes, _lib.stream())
+    else:
+        buf.copy_(torch.from_numpy(arr).reshape(buf.shape))
+    return buf
 
 
 def host(t):
-    return t.detach().cpu().numpy()
+    t = t.detach()
+    nbytes = t.numel() * t.element_size()
+    if THREADED_COPIES and t.is_cuda and nbytes >= THREADED_MIN and t.dtype in _NP_OF:
+        t = t.contiguous()
+        out = np.empty(tuple(t.shape), dtype=_NP_OF[t.dtype])
+        _lib.call("pffmg_copy_d2h", _lib.ptr(t), out.ctypes.data, nbytes, _lib.stream())
+        return out
+    return t.cpu().numpy()
 
 
 def like(out, ref, dst=None):

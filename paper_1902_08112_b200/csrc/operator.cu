@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <thread>
 #include <vector>
 
@@ -398,6 +399,125 @@ extern "C" int pffmg_apply_pageable(const pffmg_lattice* lat, const pffmg_state*
     cudaStreamWaitEvent(s, R.ev[193], 0);
     if (rc) return rc;
     return check_launch("pffmg_apply_pageable");
+}
+
+// Pageable host <-> device copies for the numpy-facing twins (states, masks,
+// right-hand sides and results of a Newton step driven by the reference's own
+// Python loop): COPY_CH-byte chunks through a ring of page-locked slots, host
+// threads filling / draining the slots while earlier chunks are on the link.
+// Synchronous.  dir = 0: host -> device, 1: device -> host.
+namespace pffmg {
+namespace {
+constexpr size_t COPY_CH = (size_t)4 << 20;
+constexpr int COPY_SLOTS = 8;
+
+int threaded_copy(int dir, const void* src, void* dst, size_t bytes, cudaStream_t s, const char* what) {
+    PFFMG_REQUIRE(src && dst, "%s: null pointer", what);
+    if (bytes == 0) return PFFMG_OK;
+    PipeRes& R = pipe_res();
+    PFFMG_REQUIRE(R.ok, "%s: could not create copy streams/events", what);
+    const size_t need = COPY_SLOTS * COPY_CH / sizeof(double);
+    if (R.stage_cap < need) {
+        if (R.stage_in) cudaFreeHost(R.stage_in);
+        if (R.stage_out) cudaFreeHost(R.stage_out);
+        R.stage_in = R.stage_out = nullptr;
+        R.stage_cap = 0;
+        if (cudaHostAlloc((void**)&R.stage_in, need * sizeof(double), cudaHostAllocDefault) != cudaSuccess ||
+            cudaHostAlloc((void**)&R.stage_out, need * sizeof(double), cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("%s: could not allocate page-locked staging", what);
+            return PFFMG_ERR_CUDA;
+        }
+        R.stage_cap = need;
+    }
+    char* const ring = reinterpret_cast<char*>(dir == 0 ? R.stage_in : R.stage_out);
+    const int n = (int)((bytes + COPY_CH - 1) / COPY_CH);
+    const int T = copy_threads();
+    // filled[k]: workers that finished chunk k (h2d: slot written; d2h: slot drained)
+    // go[k]: chunk k's slot may be touched by the workers (h2d: free; d2h: landed); -1 aborts
+    std::unique_ptr<std::atomic<int>[]> filled(new std::atomic<int>[n]), go(new std::atomic<int>[n]);
+    for (int k = 0; k < n; ++k) {
+        filled[k].store(0, std::memory_order_relaxed);
+        go[k].store(dir == 0 && k < COPY_SLOTS ? 1 : 0, std::memory_order_relaxed);
+    }
+    auto chunk_len = [&](int k) { return k + 1 < n ? COPY_CH : bytes - (size_t)k * COPY_CH; };
+    auto worker = [&](int t) {
+        for (int k = 0; k < n; ++k) {
+            int g;
+            while ((g = go[k].load(std::memory_order_acquire)) == 0) std::this_thread::yield();
+            if (g < 0) return;
+            const size_t len = chunk_len(k);
+            const size_t a = (len * t / T) & ~(size_t)63, b = t + 1 == T ? len : ((len * (t + 1) / T) & ~(size_t)63);
+            char* slot = ring + (size_t)(k % COPY_SLOTS) * COPY_CH;
+            if (b > a) {
+                if (dir == 0)
+                    memcpy(slot + a, static_cast<const char*>(src) + (size_t)k * COPY_CH + a, b - a);
+                else
+                    memcpy(static_cast<char*>(dst) + (size_t)k * COPY_CH + a, slot + a, b - a);
+            }
+            filled[k].fetch_add(1, std::memory_order_release);
+        }
+    };
+    std::vector<std::thread> pool;
+    pool.reserve(T);
+    for (int t = 0; t < T; ++t) pool.emplace_back(worker, t);
+    const cudaStream_t cs = dir == 0 ? R.h2d : R.d2h;
+    cudaEvent_t* ev = R.ev;                       // [COPY_SLOTS] of the ring
+    cudaEvent_t e0 = R.ev[192];
+    cudaEventRecord(e0, s);                       // the device buffer is ready / free on `stream`
+    cudaStreamWaitEvent(cs, e0, 0);
+    bool good = true;
+    auto abort_all = [&]() {
+        good = false;
+        for (int k = 0; k < n; ++k) go[k].store(-1, std::memory_order_release);
+    };
+    if (dir == 0) {
+        constexpr int AHEAD = COPY_SLOTS - 2;     // link copies in flight before a slot is recycled
+        for (int k = 0; k < n && good; ++k) {
+            while (filled[k].load(std::memory_order_acquire) < T) std::this_thread::yield();
+            cudaMemcpyAsync(static_cast<char*>(dst) + (size_t)k * COPY_CH, ring + (size_t)(k % COPY_SLOTS) * COPY_CH,
+                            chunk_len(k), cudaMemcpyHostToDevice, cs);
+            cudaEventRecord(ev[k % COPY_SLOTS], cs);
+            const int j = k - AHEAD;              // chunk j's copy done -> its slot serves chunk j + SLOTS
+            if (j >= 0 && j + COPY_SLOTS < n) {
+                if (cudaEventSynchronize(ev[j % COPY_SLOTS]) != cudaSuccess) abort_all();
+                else go[j + COPY_SLOTS].store(1, std::memory_order_release);
+            }
+        }
+        if (good && cudaStreamSynchronize(cs) != cudaSuccess) abort_all();
+    } else {
+        for (int k = 0; k <= n && good; ++k) {
+            if (k < n) {
+                if (k >= COPY_SLOTS)              // the slot's previous chunk has been drained
+                    while (filled[k - COPY_SLOTS].load(std::memory_order_acquire) < T) std::this_thread::yield();
+                cudaMemcpyAsync(ring + (size_t)(k % COPY_SLOTS) * COPY_CH,
+                                static_cast<const char*>(src) + (size_t)k * COPY_CH, chunk_len(k),
+                                cudaMemcpyDeviceToHost, cs);
+                cudaEventRecord(ev[k % COPY_SLOTS], cs);
+            }
+            const int j = k - 1;
+            if (j >= 0) {
+                if (cudaEventSynchronize(ev[j % COPY_SLOTS]) != cudaSuccess) abort_all();
+                else go[j].store(1, std::memory_order_release);
+            }
+        }
+    }
+    for (auto& th : pool) th.join();
+    if (!good) {
+        set_error("%s: copy failed: %s", what, cudaGetErrorString(cudaGetLastError()));
+        return PFFMG_ERR_CUDA;
+    }
+    return PFFMG_OK;
+}
+}  // namespace
+}  // namespace pffmg
+
+extern "C" int pffmg_copy_h2d(const void* host, void* device, size_t bytes, void* stream) {
+    return threaded_copy(0, host, device, bytes, as_stream(stream), "pffmg_copy_h2d");
+}
+
+extern "C" int pffmg_copy_d2h(const void* device, void* host, size_t bytes, void* stream) {
+    return threaded_copy(1, device, host, bytes, as_stream(stream), "pffmg_copy_d2h");
 }
 
 extern "C" int pffmg_residual(const pffmg_lattice* lat, const pffmg_state* st, int which,

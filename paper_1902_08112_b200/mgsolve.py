@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .arrays import DeviceCallable, dev, empty, flags_buffer, host, is_tensor, like, pack_flags, zeros
+from .arrays import DeviceCallable, copy_into, dev, empty, flags_buffer, host, is_tensor, like, pack_flags, zeros
 from .fem import Discretization
 from .krylov import cg_lanczos_dev, estimate_spectrum, lanczos_extremes, lanczos_extremes_batch, probe_vector
 from .model import DeviceMask, LinearizationState, PhaseFieldOperator
@@ -452,7 +452,7 @@ class _Session:
         L, nc = self.L, self.nc
         for buf, src in ((self.U[-1], state.U), (self.P1[-1], state.U_prev1),
                          (self.P2[-1], state.U_prev2), (self.PT[-1], state.phi_tilde)):
-            buf.copy_(src if is_tensor(src) else torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64)))
+            copy_into(buf, src)
         m = dev(fine_bool, torch.uint8) if not is_tensor(fine_bool) else fine_bool.to(torch.uint8).contiguous()
         _lib.call("pffmg_pack_flags", _lib.ptr(m), nc, self.Vs[-1], _lib.ptr(self.flags[-1]), _lib.stream())
         if not self.use_graph:
