@@ -23,11 +23,16 @@ def is_tensor(a):
     return isinstance(a, torch.Tensor)
 
 
-# numpy arrays of at least THREADED_MIN bytes cross the link through libpffmg's
+# large numpy arrays cross the link through libpffmg's
 # threaded page-locked staging (pffmg_copy_h2d / _d2h) instead of the driver's
 # single-threaded pageable copy (PFFMG_THREADED_COPIES=0: plain torch copies)
 THREADED_COPIES = os.environ.get("PFFMG_THREADED_COPIES", "1") != "0"
-THREADED_MIN = 1 << 20
+# measured on the B200 hosts (tools/copybench.py): host -> device beats torch's
+# pageable copy from ~16 MiB on (28 vs 21 GB/s at 25 MB, 37 vs 12 at 100 MB; below,
+# the pool threads' wake-up costs more than it saves), device -> host from a few
+# MiB on (30 vs 17 GB/s at 8 MB, 46 vs 18 at 25 MB, 40 vs 2 at 100 MB)
+THREADED_MIN_H2D = 16 << 20
+THREADED_MIN_D2H = 4 << 20
 
 
 def dev(a, dtype=F64):
@@ -39,7 +44,7 @@ def dev(a, dtype=F64):
             a = a.to(dtype)
         return a.contiguous()
     arr = np.ascontiguousarray(np.asarray(a), dtype=_np_dtype(dtype))
-    if THREADED_COPIES and arr.nbytes >= THREADED_MIN:
+    if THREADED_COPIES and arr.nbytes >= THREADED_MIN_H2D:
         out = torch.empty(arr.shape, dtype=dtype, device="cuda")
         _lib.call("pffmg_copy_h2d", arr.ctypes.data, _lib.ptr(out), arr.nbytes, _lib.stream())
         return out
@@ -62,7 +67,7 @@ def copy_into(buf, src, dtype=F64):
     arr = np.ascontiguousarray(np.asarray(src), dtype=_np_dtype(dtype))
     if arr.size != buf.numel():
         raise ValueError(f"expected {buf.numel()} entries, got {arr.size}")
-    if THREADED_COPIES and arr.nbytes >= THREADED_MIN and buf.is_contiguous() and buf.dtype == dtype:
+    if THREADED_COPIES and arr.nbytes >= THREADED_MIN_H2D and buf.is_contiguous() and buf.dtype == dtype:
         _lib.call("pffmg_copy_h2d", arr.ctypes.data, _lib.ptr(buf), arr.nbytes, _lib.stream())
     else:
         buf.copy_(torch.from_numpy(arr).reshape(buf.shape))
@@ -72,7 +77,7 @@ def copy_into(buf, src, dtype=F64):
 def host(t):
     t = t.detach()
     nbytes = t.numel() * t.element_size()
-    if THREADED_COPIES and t.is_cuda and nbytes >= THREADED_MIN and t.dtype in _NP_OF:
+    if THREADED_COPIES and t.is_cuda and nbytes >= THREADED_MIN_D2H and t.dtype in _NP_OF:
         t = t.contiguous()
         out = np.empty(tuple(t.shape), dtype=_NP_OF[t.dtype])
         _lib.call("pffmg_copy_d2h", _lib.ptr(t), out.ctypes.data, nbytes, _lib.stream())

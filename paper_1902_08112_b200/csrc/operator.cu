@@ -2,8 +2,12 @@
 // the per-dimension kernel instantiations (op2d.cu, op3d.cu; kernels in
 // op_kernels.cuh).  Replaces reference model.py:368-413 and the vector
 // updates of mgsolve.py:82-113 / 227 (fused epilogues).
+#include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -241,6 +245,115 @@ int copy_threads() {
     }();
     return t;
 }
+
+// The host threads of the pageable paths: created once and parked on a
+// condition variable between calls (creating a thread in a process with a
+// CUDA context costs ~150 us, more than a 4 MiB chunk's copy).  Never
+// destroyed: the threads would outlive a static object at exit.  A job owns
+// its state (shared_ptr captured by value) and tracks its own completion, so
+// nobody waits for a thread that wakes late; it just finds nothing to do.
+class CopyPool {
+  public:
+    static CopyPool& get() {
+        static CopyPool* p = new CopyPool(copy_threads());
+        return *p;
+    }
+    std::mutex exclusive;                  // one job at a time: held by the caller for the whole call
+    void start(std::function<void(int)> fn) {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            job_ = std::move(fn);
+            ++gen_;
+        }
+        cv_.notify_all();
+    }
+
+  private:
+    explicit CopyPool(int n) {
+        for (int t = 0; t < n; ++t) std::thread([this, t] { loop(t); }).detach();
+    }
+    void loop(int t) {
+        unsigned long long seen = 0;
+        for (;;) {
+            std::function<void(int)> job;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                job = job_;
+            }
+            job(t);
+        }
+    }
+    std::mutex m_;
+    std::condition_variable cv_;
+    std::function<void(int)> job_;
+    unsigned long long gen_ = 0;
+};
+}  // namespace
+}  // namespace pffmg
+
+namespace pffmg {
+namespace {
+// Shared state of the host copies of one pffmg_apply_pageable call (see
+// CopyJob below for why it is shared with the pool threads): pieces of at most
+// PIECE doubles, claimed in order -- every strip's copy-in pieces, then every
+// strip's copy-out pieces (which wait for the strip to land).
+struct StripJob {
+    struct Piece { int strip; int64_t off; int64_t len; };       // off: element offset incl. the component
+    static constexpr int64_t PIECE = 64 << 10;
+    const double* h_v = nullptr;
+    double* h_out = nullptr;
+    double* pin = nullptr;
+    double* pout = nullptr;
+    int K = 0;
+    std::vector<Piece> pieces;
+    int in_cnt[64] = {0};
+    std::atomic<int> in_done[64], out_ready[64];
+    std::atomic<long long> next{0}, out_done{0};
+    std::atomic<int> inflight{0};
+
+    void run_piece(long long q) {                // q already claimed
+        const long long P = (long long)pieces.size();
+        const Piece& pc = pieces[(size_t)(q % P)];
+        if (q < P) {
+            memcpy(pin + pc.off, h_v + pc.off, (size_t)pc.len * sizeof(double));
+            in_done[pc.strip].fetch_add(1, std::memory_order_release);
+        } else {
+            int r;
+            while ((r = out_ready[pc.strip].load(std::memory_order_acquire)) == 0) std::this_thread::yield();
+            if (r > 0) {
+                memcpy(h_out + pc.off, pout + pc.off, (size_t)pc.len * sizeof(double));
+                out_done.fetch_add(1, std::memory_order_release);
+            }
+        }
+        inflight.fetch_sub(1, std::memory_order_release);
+    }
+    void work() {
+        const long long total = 2 * (long long)pieces.size();
+        for (;;) {
+            inflight.fetch_add(1, std::memory_order_acquire);
+            const long long q = next.fetch_add(1, std::memory_order_relaxed);
+            if (q >= total) {
+                inflight.fetch_sub(1, std::memory_order_release);
+                return;
+            }
+            run_piece(q);
+        }
+    }
+    bool help() {                                // the caller: one piece that cannot block
+        const long long P = (long long)pieces.size();
+        long long q = next.load(std::memory_order_relaxed);
+        if (q >= 2 * P) return false;
+        if (q >= P && out_ready[pieces[(size_t)(q - P)].strip].load(std::memory_order_acquire) == 0) return false;
+        inflight.fetch_add(1, std::memory_order_acquire);
+        if (next.compare_exchange_strong(q, q + 1, std::memory_order_relaxed))
+            run_piece(q);
+        else
+            inflight.fetch_sub(1, std::memory_order_release);
+        return true;
+    }
+};
 }  // namespace
 }  // namespace pffmg
 
@@ -303,41 +416,25 @@ extern "C" int pffmg_apply_pageable(const pffmg_lattice* lat, const pffmg_state*
         pb[i] = (int)(((int64_t)nplanes * wcum[i]) / wsum);
         lo[i] = off(pb[i]);
     }
-    const int T = copy_threads();
-    std::atomic<int> in_done[64], out_ready[64];
+    CopyPool& pool = CopyPool::get();
+    std::lock_guard<std::mutex> pool_guard(pool.exclusive);
+    auto J = std::make_shared<StripJob>();
+    J->h_v = h_v;
+    J->h_out = h_out;
+    J->pin = pin;
+    J->pout = pout;
+    J->K = K;
     for (int i = 0; i < K; ++i) {
-        in_done[i].store(0, std::memory_order_relaxed);
-        out_ready[i].store(0, std::memory_order_relaxed);
+        J->in_done[i].store(0, std::memory_order_relaxed);
+        J->out_ready[i].store(0, std::memory_order_relaxed);
+        for (int c = 0; c < nc; ++c)
+            for (int64_t a = lo[i]; a < lo[i + 1]; a += StripJob::PIECE) {
+                J->pieces.push_back({i, (int64_t)c * V + a, std::min<int64_t>(StripJob::PIECE, lo[i + 1] - a)});
+                ++J->in_cnt[i];
+            }
     }
-    // worker t moves its share of every strip (all components): in, then out
-    auto worker = [&](int t) {
-        auto span = [&](int i, int64_t* a, int64_t* n) {
-            const int64_t len = lo[i + 1] - lo[i];
-            const int64_t c0 = (len * t / T) & ~(int64_t)7, c1 = t + 1 == T ? len : ((len * (t + 1) / T) & ~(int64_t)7);
-            *a = lo[i] + c0;
-            *n = c1 - c0;
-        };
-        for (int i = 0; i < K; ++i) {
-            int64_t a, n;
-            span(i, &a, &n);
-            if (n > 0)
-                for (int c = 0; c < nc; ++c) memcpy(pin + c * V + a, h_v + c * V + a, (size_t)n * sizeof(double));
-            in_done[i].fetch_add(1, std::memory_order_release);
-        }
-        for (int i = 0; i < K; ++i) {
-            int r;
-            while ((r = out_ready[i].load(std::memory_order_acquire)) == 0) std::this_thread::yield();
-            if (r < 0) return;                       // aborted
-            int64_t a, n;
-            span(i, &a, &n);
-            if (n > 0)
-                for (int c = 0; c < nc; ++c) memcpy(h_out + c * V + a, pout + c * V + a, (size_t)n * sizeof(double));
-        }
-    };
-    std::vector<std::thread> pool;
-    pool.reserve(T - 1);
-    for (int t = 1; t < T; ++t) pool.emplace_back(worker, t);
-    // the calling thread orchestrates the device side; it joins the copy-out as worker 0
+    const long long P = (long long)J->pieces.size();
+    pool.start([J](int) { J->work(); });         // the calling thread orchestrates the device side and helps
     const size_t pitch = (size_t)V * sizeof(double);
     cudaEvent_t* ein = R.ev;
     cudaEvent_t* ek = R.ev + 64;
@@ -363,14 +460,8 @@ extern "C" int pffmg_apply_pageable(const pffmg_lattice* lat, const pffmg_state*
         cudaEventRecord(eo[i], R.d2h);
     };
     for (int i = 0; i < K; ++i) {
-        {   // this thread's share of strip i
-            const int64_t len = lo[i + 1] - lo[i];
-            const int64_t c1 = T == 1 ? len : ((len / T) & ~(int64_t)7);
-            if (c1 > 0)
-                for (int c = 0; c < nc; ++c) memcpy(pin + c * V + lo[i], h_v + c * V + lo[i], (size_t)c1 * sizeof(double));
-            in_done[i].fetch_add(1, std::memory_order_release);
-        }
-        while (in_done[i].load(std::memory_order_acquire) < T) std::this_thread::yield();
+        while (J->in_done[i].load(std::memory_order_acquire) < J->in_cnt[i])
+            if (!J->help()) std::this_thread::yield();
         if (lo[i + 1] > lo[i])
             cudaMemcpy2DAsync(d_v + lo[i], pitch, pin + lo[i], pitch, (size_t)(lo[i + 1] - lo[i]) * sizeof(double), nc,
                               cudaMemcpyHostToDevice, R.h2d);
@@ -380,21 +471,21 @@ extern "C" int pffmg_apply_pageable(const pffmg_lattice* lat, const pffmg_state*
     stencil(K - 1);
     for (int i = 0; i < K; ++i) {
         const bool good = cudaEventSynchronize(eo[i]) == cudaSuccess && rc == PFFMG_OK;
-        out_ready[i].store(good ? 1 : -1, std::memory_order_release);
+        J->out_ready[i].store(good ? 1 : -1, std::memory_order_release);
         if (!good) {
-            for (int k = i + 1; k < K; ++k) out_ready[k].store(-1, std::memory_order_release);
+            for (int k = i + 1; k < K; ++k) J->out_ready[k].store(-1, std::memory_order_release);
             if (rc == PFFMG_OK) {
                 set_error("pffmg_apply_pageable: copy-out failed: %s", cudaGetErrorString(cudaGetLastError()));
                 rc = PFFMG_ERR_CUDA;
             }
             break;
         }
-        const int64_t len = lo[i + 1] - lo[i];
-        const int64_t c1 = T == 1 ? len : ((len / T) & ~(int64_t)7);
-        if (c1 > 0)
-            for (int c = 0; c < nc; ++c) memcpy(h_out + c * V + lo[i], pout + c * V + lo[i], (size_t)c1 * sizeof(double));
+        J->help();
     }
-    for (auto& th : pool) th.join();
+    while (rc == PFFMG_OK && J->out_done.load(std::memory_order_acquire) < P)   // drain with the pool
+        if (!J->help()) std::this_thread::yield();
+    // no thread may still be inside a memcpy on the caller's buffers
+    while (J->inflight.load(std::memory_order_acquire) > 0) std::this_thread::yield();
     cudaEventRecord(R.ev[193], R.d2h);
     cudaStreamWaitEvent(s, R.ev[193], 0);
     if (rc) return rc;
@@ -410,6 +501,70 @@ namespace pffmg {
 namespace {
 constexpr size_t COPY_CH = (size_t)4 << 20;
 constexpr int COPY_SLOTS = 8;
+
+// Shared state of one threaded copy: owned jointly by the caller and by every
+// pool thread that picked the job up, so a thread that wakes after the copy
+// has finished (a parked thread of a virtualised host can take ~1 ms to wake)
+// finds no piece left and touches nothing else -- the caller never waits for it.
+struct CopyJob {
+    int dir = 0;
+    const char* src = nullptr;
+    char* dst = nullptr;
+    char* ring = nullptr;
+    size_t bytes = 0;
+    int n = 0;                                   // chunks
+    long long total = 0;                         // pieces
+    std::atomic<long long> next{0}, done{0};
+    std::atomic<int> inflight{0};
+    // go[k]: chunk k's slot may be touched (h2d: free; d2h: landed); -1 aborts
+    // filled[k]: pieces of chunk k done (h2d: slot written; d2h: slot drained)
+    std::unique_ptr<std::atomic<int>[]> go, filled;
+    static constexpr size_t PIECE = (size_t)512 << 10;
+    static constexpr int PPC = (int)(COPY_CH / PIECE);          // pieces per full chunk
+
+    size_t chunk_len(int k) const { return k + 1 < n ? COPY_CH : bytes - (size_t)k * COPY_CH; }
+    int pieces_of(int k) const { return (int)((chunk_len(k) + PIECE - 1) / PIECE); }
+    // copy piece q (already claimed); waits for its chunk to become touchable
+    void copy_piece(long long q) {
+        const int k = (int)(q / PPC), pi = (int)(q % PPC);
+        int g;
+        while ((g = go[k].load(std::memory_order_acquire)) == 0) std::this_thread::yield();
+        if (g > 0) {
+            const size_t len = chunk_len(k);
+            const size_t a = (size_t)pi * PIECE, b = a + PIECE < len ? a + PIECE : len;
+            char* slot = ring + (size_t)(k % COPY_SLOTS) * COPY_CH;
+            if (dir == 0)
+                memcpy(slot + a, src + (size_t)k * COPY_CH + a, b - a);
+            else
+                memcpy(dst + (size_t)k * COPY_CH + a, slot + a, b - a);
+            filled[k].fetch_add(1, std::memory_order_release);
+            done.fetch_add(1, std::memory_order_release);
+        }
+        inflight.fetch_sub(1, std::memory_order_release);
+    }
+    void work() {                                // pool threads: pieces in order until none is left
+        for (;;) {
+            inflight.fetch_add(1, std::memory_order_acquire);
+            const long long q = next.fetch_add(1, std::memory_order_relaxed);
+            if (q >= total) {
+                inflight.fetch_sub(1, std::memory_order_release);
+                return;
+            }
+            copy_piece(q);
+            if (go[(int)(q / PPC)].load(std::memory_order_relaxed) < 0) return;
+        }
+    }
+    bool help() {                                // the caller: one piece, only if its chunk is touchable now
+        long long q = next.load(std::memory_order_relaxed);
+        if (q >= total || go[(int)(q / PPC)].load(std::memory_order_acquire) <= 0) return false;
+        inflight.fetch_add(1, std::memory_order_acquire);
+        if (next.compare_exchange_strong(q, q + 1, std::memory_order_relaxed))
+            copy_piece(q);
+        else
+            inflight.fetch_sub(1, std::memory_order_release);
+        return true;
+    }
+};
 
 int threaded_copy(int dir, const void* src, void* dst, size_t bytes, cudaStream_t s, const char* what) {
     PFFMG_REQUIRE(src && dst, "%s: null pointer", what);
@@ -430,37 +585,23 @@ int threaded_copy(int dir, const void* src, void* dst, size_t bytes, cudaStream_
         }
         R.stage_cap = need;
     }
-    char* const ring = reinterpret_cast<char*>(dir == 0 ? R.stage_in : R.stage_out);
-    const int n = (int)((bytes + COPY_CH - 1) / COPY_CH);
-    const int T = copy_threads();
-    // filled[k]: workers that finished chunk k (h2d: slot written; d2h: slot drained)
-    // go[k]: chunk k's slot may be touched by the workers (h2d: free; d2h: landed); -1 aborts
-    std::unique_ptr<std::atomic<int>[]> filled(new std::atomic<int>[n]), go(new std::atomic<int>[n]);
+    CopyPool& pool = CopyPool::get();
+    std::lock_guard<std::mutex> pool_guard(pool.exclusive);
+    auto J = std::make_shared<CopyJob>();
+    J->dir = dir;
+    J->src = static_cast<const char*>(src);
+    J->dst = static_cast<char*>(dst);
+    J->ring = reinterpret_cast<char*>(dir == 0 ? R.stage_in : R.stage_out);
+    J->bytes = bytes;
+    const int n = J->n = (int)((bytes + COPY_CH - 1) / COPY_CH);
+    J->total = (long long)(n - 1) * CopyJob::PPC + J->pieces_of(n - 1);
+    J->go.reset(new std::atomic<int>[n]);
+    J->filled.reset(new std::atomic<int>[n]);
     for (int k = 0; k < n; ++k) {
-        filled[k].store(0, std::memory_order_relaxed);
-        go[k].store(dir == 0 && k < COPY_SLOTS ? 1 : 0, std::memory_order_relaxed);
+        J->filled[k].store(0, std::memory_order_relaxed);
+        J->go[k].store(dir == 0 && k < COPY_SLOTS ? 1 : 0, std::memory_order_relaxed);
     }
-    auto chunk_len = [&](int k) { return k + 1 < n ? COPY_CH : bytes - (size_t)k * COPY_CH; };
-    auto worker = [&](int t) {
-        for (int k = 0; k < n; ++k) {
-            int g;
-            while ((g = go[k].load(std::memory_order_acquire)) == 0) std::this_thread::yield();
-            if (g < 0) return;
-            const size_t len = chunk_len(k);
-            const size_t a = (len * t / T) & ~(size_t)63, b = t + 1 == T ? len : ((len * (t + 1) / T) & ~(size_t)63);
-            char* slot = ring + (size_t)(k % COPY_SLOTS) * COPY_CH;
-            if (b > a) {
-                if (dir == 0)
-                    memcpy(slot + a, static_cast<const char*>(src) + (size_t)k * COPY_CH + a, b - a);
-                else
-                    memcpy(static_cast<char*>(dst) + (size_t)k * COPY_CH + a, slot + a, b - a);
-            }
-            filled[k].fetch_add(1, std::memory_order_release);
-        }
-    };
-    std::vector<std::thread> pool;
-    pool.reserve(T);
-    for (int t = 0; t < T; ++t) pool.emplace_back(worker, t);
+    pool.start([J](int) { J->work(); });
     const cudaStream_t cs = dir == 0 ? R.h2d : R.d2h;
     cudaEvent_t* ev = R.ev;                       // [COPY_SLOTS] of the ring
     cudaEvent_t e0 = R.ev[192];
@@ -469,40 +610,45 @@ int threaded_copy(int dir, const void* src, void* dst, size_t bytes, cudaStream_
     bool good = true;
     auto abort_all = [&]() {
         good = false;
-        for (int k = 0; k < n; ++k) go[k].store(-1, std::memory_order_release);
+        for (int k = 0; k < n; ++k) J->go[k].store(-1, std::memory_order_release);
+    };
+    auto await_chunk = [&](int k) {               // all pieces of chunk k done; the caller helps meanwhile
+        while (J->filled[k].load(std::memory_order_acquire) < J->pieces_of(k))
+            if (!J->help()) std::this_thread::yield();
     };
     if (dir == 0) {
         constexpr int AHEAD = COPY_SLOTS - 2;     // link copies in flight before a slot is recycled
         for (int k = 0; k < n && good; ++k) {
-            while (filled[k].load(std::memory_order_acquire) < T) std::this_thread::yield();
-            cudaMemcpyAsync(static_cast<char*>(dst) + (size_t)k * COPY_CH, ring + (size_t)(k % COPY_SLOTS) * COPY_CH,
-                            chunk_len(k), cudaMemcpyHostToDevice, cs);
+            await_chunk(k);
+            cudaMemcpyAsync(J->dst + (size_t)k * COPY_CH, J->ring + (size_t)(k % COPY_SLOTS) * COPY_CH,
+                            J->chunk_len(k), cudaMemcpyHostToDevice, cs);
             cudaEventRecord(ev[k % COPY_SLOTS], cs);
             const int j = k - AHEAD;              // chunk j's copy done -> its slot serves chunk j + SLOTS
             if (j >= 0 && j + COPY_SLOTS < n) {
                 if (cudaEventSynchronize(ev[j % COPY_SLOTS]) != cudaSuccess) abort_all();
-                else go[j + COPY_SLOTS].store(1, std::memory_order_release);
+                else J->go[j + COPY_SLOTS].store(1, std::memory_order_release);
             }
         }
         if (good && cudaStreamSynchronize(cs) != cudaSuccess) abort_all();
     } else {
         for (int k = 0; k <= n && good; ++k) {
             if (k < n) {
-                if (k >= COPY_SLOTS)              // the slot's previous chunk has been drained
-                    while (filled[k - COPY_SLOTS].load(std::memory_order_acquire) < T) std::this_thread::yield();
-                cudaMemcpyAsync(ring + (size_t)(k % COPY_SLOTS) * COPY_CH,
-                                static_cast<const char*>(src) + (size_t)k * COPY_CH, chunk_len(k),
-                                cudaMemcpyDeviceToHost, cs);
+                if (k >= COPY_SLOTS) await_chunk(k - COPY_SLOTS);   // the slot's previous chunk has been drained
+                cudaMemcpyAsync(J->ring + (size_t)(k % COPY_SLOTS) * COPY_CH, J->src + (size_t)k * COPY_CH,
+                                J->chunk_len(k), cudaMemcpyDeviceToHost, cs);
                 cudaEventRecord(ev[k % COPY_SLOTS], cs);
             }
             const int j = k - 1;
             if (j >= 0) {
                 if (cudaEventSynchronize(ev[j % COPY_SLOTS]) != cudaSuccess) abort_all();
-                else go[j].store(1, std::memory_order_release);
+                else J->go[j].store(1, std::memory_order_release);
             }
         }
+        while (good && J->done.load(std::memory_order_acquire) < J->total)   // drain with the pool
+            if (!J->help()) std::this_thread::yield();
     }
-    for (auto& th : pool) th.join();
+    // no thread may still be inside a memcpy on the caller's buffers
+    while (J->inflight.load(std::memory_order_acquire) > 0) std::this_thread::yield();
     if (!good) {
         set_error("%s: copy failed: %s", what, cudaGetErrorString(cudaGetLastError()));
         return PFFMG_ERR_CUDA;

@@ -447,7 +447,7 @@ def _modulus_table(space, lat, params):
 # numpy vectors of at least PAGEABLE_MIN dofs go through pffmg_apply_pageable
 # (PFFMG_PAGEABLE_PIPELINE=0: plain pageable copies around the device apply)
 PAGEABLE_PIPELINE = os.environ.get("PFFMG_PAGEABLE_PIPELINE", "1") != "0"
-PAGEABLE_MIN = 1 << 17
+PAGEABLE_MIN = 1 << 20
 
 
 def _plain_f64(a, writeable=False):
