@@ -525,7 +525,7 @@ def measure_solve(prob, mask, hbm, with_bytes=True):
     import torch
     newton_step = newton_step_fn(prob, mask)
     newton_step()                                   # warm (graph capture, probes)
-    runs = [newton_step() for _ in range(3)]
+    runs = [newton_step() for _ in range(5 if with_bytes else 3)]
     setup_s = float(np.median([r[0] for r in runs]))
     gmres_s = float(np.median([r[1] for r in runs]))
     its = runs[-1][2]
@@ -535,7 +535,8 @@ def measure_solve(prob, mask, hbm, with_bytes=True):
            "rhs": "Newton RHS -A(U), constrained rows zeroed, from the GPU residual kernel",
            "resident": "state U, Dirichlet mask and active set on the device (as the Newton loop holds them)",
            "control": "GMRES(30) rel 1e-8 abs 0, V(1,1) FULL, Chebyshev deg %d" % prob.degree,
-           "timing": "wall clock, median of 3 after one warm-up"}
+           "timing": "wall clock, median of %d after one warm-up" % len(runs),
+           "ms_per_newton_step_runs": [round((r[0] + r[1]) * 1e3, 3) for r in runs]}
     if with_bytes:
         step_np = newton_step_numpy_fn(prob, mask)
         step_np()
