@@ -183,9 +183,12 @@ extern "C" int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st,
     const int64_t per_plane = q2 ? (int64_t)(2 * lat->nx + 1)
                                  : (lat->dim == 3 ? (int64_t)(lat->nx + 1) * (lat->ny + 1) : (int64_t)(lat->nx + 1));
     auto off = [&](int p) -> int64_t { return h_plane_off ? h_plane_off[p] : (int64_t)p * per_plane; };
-    // Strip i's kernel waits for the copies of strips i and i+1, and the copy out
-    // of the last strip runs alone: small strips at both ends shorten the
-    // exposed head and tail (triangular weights 1, 2, .., 2, 1).
+    // Strip i's kernel finalises planes [bound(i), bound(i+1)) and reads one plane
+    // more on either side, so copy-in chunk i carries planes up to bound(i+1) + 1
+    // (hbound): the kernel then waits for its own chunk only and the copy out of
+    // strip i starts one chunk earlier.  The copy out of the last strip runs
+    // alone: small strips at both ends shorten the exposed head and tail
+    // (triangular weights 1, 2, .., 2, 1).
     static const int tri = [] {
         const char* e = getenv("PFFMG_PIPE_TRI");
         return e ? atoi(e) : 1;
@@ -197,6 +200,7 @@ extern "C" int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st,
         wcum[i + 1] = wsum;
     }
     auto bound = [&](int i) -> int { return (int)(((int64_t)nplanes * wcum[i]) / wsum); };
+    auto hbound = [&](int i) -> int { return i == 0 ? 0 : (i == K ? nplanes : min(bound(i) + 1, nplanes)); };
     const size_t pitch = (size_t)V * sizeof(double);
     cudaEvent_t* ein = R.ev;          // [K]
     cudaEvent_t* ek = R.ev + 64;      // [K]
@@ -205,16 +209,20 @@ extern "C" int pffmg_apply_host(const pffmg_lattice* lat, const pffmg_state* st,
     cudaStreamWaitEvent(R.h2d, e0, 0);
     cudaStreamWaitEvent(R.d2h, e0, 0);
     // (copies of a few MiB: much smaller ones serialise the two directions on this link)
-    for (int i = 0; i < K; ++i) {
-        const int64_t a = off(bound(i)), b = off(bound(i + 1));
+    auto copy_in = [&](int i) {
+        const int64_t a = off(hbound(i)), b = off(hbound(i + 1));
         if (b > a)
             cudaMemcpy2DAsync(d_v + a, pitch, h_v + a, pitch, (size_t)(b - a) * sizeof(double), nc,
                               cudaMemcpyHostToDevice, R.h2d);
         cudaEventRecord(ein[i], R.h2d);
-    }
+    };
     pffmg_lattice sub = *lat;
+    // enqueue order: the copy engine stays one chunk ahead of the stencils, and
+    // the first stencil is submitted before the later chunks' API calls
+    copy_in(0);
     for (int i = 0; i < K; ++i) {
-        cudaStreamWaitEvent(s, ein[i + 1 < K ? i + 1 : K - 1], 0);
+        if (i + 1 < K) copy_in(i + 1);
+        cudaStreamWaitEvent(s, ein[i], 0);
         if (lat->order != 2) {
             sub.own_lo = bound(i);
             sub.own_hi = bound(i + 1);
@@ -297,7 +305,7 @@ namespace pffmg {
 namespace {
 // Shared state of the host copies of one pffmg_apply_pageable call (see
 // CopyJob below for why it is shared with the pool threads): pieces of at most
-// PIECE doubles, claimed in order -- every strip's copy-in pieces, then every
+// PIECE doubles, claimed in order -- every chunk's copy-in pieces, then every
 // strip's copy-out pieces (which wait for the strip to land).
 struct StripJob {
     struct Piece { int strip; int64_t off; int64_t len; };       // off: element offset incl. the component
@@ -307,19 +315,20 @@ struct StripJob {
     double* pin = nullptr;
     double* pout = nullptr;
     int K = 0;
-    std::vector<Piece> pieces;
+    std::vector<Piece> in_pieces, out_pieces;    // claimed in this order: all copy-in, then all copy-out
     int in_cnt[64] = {0};
     std::atomic<int> in_done[64], out_ready[64];
     std::atomic<long long> next{0}, out_done{0};
     std::atomic<int> inflight{0};
 
     void run_piece(long long q) {                // q already claimed
-        const long long P = (long long)pieces.size();
-        const Piece& pc = pieces[(size_t)(q % P)];
-        if (q < P) {
+        const long long PI = (long long)in_pieces.size();
+        if (q < PI) {
+            const Piece& pc = in_pieces[(size_t)q];
             memcpy(pin + pc.off, h_v + pc.off, (size_t)pc.len * sizeof(double));
             in_done[pc.strip].fetch_add(1, std::memory_order_release);
         } else {
+            const Piece& pc = out_pieces[(size_t)(q - PI)];
             int r;
             while ((r = out_ready[pc.strip].load(std::memory_order_acquire)) == 0) std::this_thread::yield();
             if (r > 0) {
@@ -330,7 +339,7 @@ struct StripJob {
         inflight.fetch_sub(1, std::memory_order_release);
     }
     void work() {
-        const long long total = 2 * (long long)pieces.size();
+        const long long total = (long long)(in_pieces.size() + out_pieces.size());
         for (;;) {
             inflight.fetch_add(1, std::memory_order_acquire);
             const long long q = next.fetch_add(1, std::memory_order_relaxed);
@@ -342,10 +351,11 @@ struct StripJob {
         }
     }
     bool help() {                                // the caller: one piece that cannot block
-        const long long P = (long long)pieces.size();
+        const long long PI = (long long)in_pieces.size();
         long long q = next.load(std::memory_order_relaxed);
-        if (q >= 2 * P) return false;
-        if (q >= P && out_ready[pieces[(size_t)(q - P)].strip].load(std::memory_order_acquire) == 0) return false;
+        if (q >= PI + (long long)out_pieces.size()) return false;
+        if (q >= PI && out_ready[out_pieces[(size_t)(q - PI)].strip].load(std::memory_order_acquire) == 0)
+            return false;
         inflight.fetch_add(1, std::memory_order_acquire);
         if (next.compare_exchange_strong(q, q + 1, std::memory_order_relaxed))
             run_piece(q);
@@ -410,11 +420,13 @@ extern "C" int pffmg_apply_pageable(const pffmg_lattice* lat, const pffmg_state*
         wsum += min(i + 1, K - i);
         wcum[i + 1] = wsum;
     }
-    int64_t lo[65];
+    int64_t lo[65], hlo[65];                     // strip bounds (elements): copy-out / stencil, copy-in
     int pb[65];
     for (int i = 0; i <= K; ++i) {
         pb[i] = (int)(((int64_t)nplanes * wcum[i]) / wsum);
         lo[i] = off(pb[i]);
+        // copy-in chunk i carries one plane more than strip i finalises (see pffmg_apply_host)
+        hlo[i] = i == 0 ? 0 : off(i == K ? nplanes : min(pb[i] + 1, nplanes));
     }
     CopyPool& pool = CopyPool::get();
     std::lock_guard<std::mutex> pool_guard(pool.exclusive);
@@ -428,12 +440,15 @@ extern "C" int pffmg_apply_pageable(const pffmg_lattice* lat, const pffmg_state*
         J->in_done[i].store(0, std::memory_order_relaxed);
         J->out_ready[i].store(0, std::memory_order_relaxed);
         for (int c = 0; c < nc; ++c)
-            for (int64_t a = lo[i]; a < lo[i + 1]; a += StripJob::PIECE) {
-                J->pieces.push_back({i, (int64_t)c * V + a, std::min<int64_t>(StripJob::PIECE, lo[i + 1] - a)});
+            for (int64_t a = hlo[i]; a < hlo[i + 1]; a += StripJob::PIECE) {
+                J->in_pieces.push_back({i, (int64_t)c * V + a, std::min<int64_t>(StripJob::PIECE, hlo[i + 1] - a)});
                 ++J->in_cnt[i];
             }
+        for (int c = 0; c < nc; ++c)
+            for (int64_t a = lo[i]; a < lo[i + 1]; a += StripJob::PIECE)
+                J->out_pieces.push_back({i, (int64_t)c * V + a, std::min<int64_t>(StripJob::PIECE, lo[i + 1] - a)});
     }
-    const long long P = (long long)J->pieces.size();
+    const long long P = (long long)J->out_pieces.size();
     pool.start([J](int) { J->work(); });         // the calling thread orchestrates the device side and helps
     const size_t pitch = (size_t)V * sizeof(double);
     cudaEvent_t* ein = R.ev;
@@ -445,8 +460,8 @@ extern "C" int pffmg_apply_pageable(const pffmg_lattice* lat, const pffmg_state*
     cudaStreamWaitEvent(R.d2h, e0, 0);
     pffmg_lattice sub = *lat;
     int rc = PFFMG_OK;
-    auto stencil = [&](int i) {                      // strip i: needs the copies of strips i and i+1
-        cudaStreamWaitEvent(s, ein[i + 1 < K ? i + 1 : K - 1], 0);
+    auto stencil = [&](int i) {                      // strip i: needs copy-in chunks 0..i
+        cudaStreamWaitEvent(s, ein[i], 0);
         if (!q2) {
             sub.own_lo = pb[i];
             sub.own_hi = pb[i + 1];
@@ -462,13 +477,12 @@ extern "C" int pffmg_apply_pageable(const pffmg_lattice* lat, const pffmg_state*
     for (int i = 0; i < K; ++i) {
         while (J->in_done[i].load(std::memory_order_acquire) < J->in_cnt[i])
             if (!J->help()) std::this_thread::yield();
-        if (lo[i + 1] > lo[i])
-            cudaMemcpy2DAsync(d_v + lo[i], pitch, pin + lo[i], pitch, (size_t)(lo[i + 1] - lo[i]) * sizeof(double), nc,
-                              cudaMemcpyHostToDevice, R.h2d);
+        if (hlo[i + 1] > hlo[i])
+            cudaMemcpy2DAsync(d_v + hlo[i], pitch, pin + hlo[i], pitch, (size_t)(hlo[i + 1] - hlo[i]) * sizeof(double),
+                              nc, cudaMemcpyHostToDevice, R.h2d);
         cudaEventRecord(ein[i], R.h2d);
-        if (i >= 1) stencil(i - 1);
+        stencil(i);
     }
-    stencil(K - 1);
     for (int i = 0; i < K; ++i) {
         const bool good = cudaEventSynchronize(eo[i]) == cudaSuccess && rc == PFFMG_OK;
         J->out_ready[i].store(good ? 1 : -1, std::memory_order_release);
