@@ -4,6 +4,8 @@
 // CSR built from lattice keys) as gather stencils -- no atomics, each output
 // written by exactly one thread, summation in increasing input-id order like
 // the CSR products -- and fuses the V-cycle masking of mgsolve.py:228-234.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace pffmg {
@@ -16,6 +18,23 @@ namespace pffmg {
 // owned rows / planes (no 64-bit index divisions per point).
 __device__ __forceinline__ bool grid_point(const Lat& L, int& x, int& y, int& z) {
     x = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+    if (x > L.nx) return false;
+    if (L.dim == 3) {
+        y = (int)blockIdx.y;
+        z = (int)blockIdx.z + L.own_lo;
+    } else {
+        y = (int)blockIdx.y + L.own_lo;
+        z = 0;
+    }
+    return true;
+}
+
+// Component-parallel variant: gridDim.x = gx * ncomp blocks, component k = blockIdx.x / gx
+// (a coarse vertex's gather of 9 / 27 fine values per component is then one
+// thread's work: 3-4x more threads in flight on the small coarse grids).
+__device__ __forceinline__ bool grid_point_comp(const Lat& L, int gx, int& x, int& y, int& z, int& k) {
+    k = (int)blockIdx.x / gx;
+    x = (int)(((int)blockIdx.x - k * gx) * blockDim.x + threadIdx.x);
     if (x > L.nx) return false;
     if (L.dim == 3) {
         y = (int)blockIdx.y;
@@ -47,9 +66,89 @@ __device__ __forceinline__ void fine_of(const Lat& Lc, const Lat& Lf, int x, int
     }
 }
 
+// (P^T vf)[c] of one component (vfk = that component's fine vector): fine
+// neighbours in increasing id order, the CSR product order of fem.py:323-339.
+template <int D>
+__device__ __forceinline__ double restrict_gather(const Lat& Lc, const Lat& Lf, int x, int y, int z,
+                                                  const double* __restrict__ vfk) {
+    constexpr int zlo = D == 3 ? -1 : 0, zhi = D == 3 ? 1 : 0;
+    constexpr int NT = D == 3 ? 27 : 9;
+    double val[NT];
+    int t = 0;
+#pragma unroll
+    for (int c = zlo; c <= zhi; ++c)
+#pragma unroll
+        for (int b = -1; b <= 1; ++b)
+#pragma unroll
+            for (int a = -1; a <= 1; ++a, ++t) {
+                int fx, fy, fz;
+                fine_of(Lc, Lf, x, y, z, a, b, c, fx, fy, fz);
+                const int64_t fid = vertex_id(Lf, fx, fy, fz);
+                val[t] = fid >= 0 ? __ldg(vfk + fid) : 0.0;      // all loads in flight before the sum
+            }
+    double acc = 0.0;
+    t = 0;
+#pragma unroll
+    for (int c = zlo; c <= zhi; ++c)
+#pragma unroll
+        for (int b = -1; b <= 1; ++b)
+#pragma unroll
+            for (int a = -1; a <= 1; ++a, ++t) {
+                const double w = (a ? 0.5 : 1.0) * (b ? 0.5 : 1.0) * (c ? 0.5 : 1.0);
+                acc += w * val[t];
+            }
+    return acc;
+}
+
 // vc[k] = sum_{fine f} P[f, c] vf[k][f]  for owned coarse vertices c, then masking.
 template <int D>
-__global__ void restrict_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vf,
+__global__ void restrict_kernel(Lat Lc, Lat Lf, int gx, int comp0, const double* __restrict__ vf,
+                                double* __restrict__ vc, const uint8_t* __restrict__ cflags) {
+    pdl_wait();
+    int x, y, z, k;
+    if (!grid_point_comp(Lc, gx, x, y, z, k)) return;
+    const int64_t cid = vertex_id(Lc, x, y, z);
+    if (cid < 0) return;
+    const uint8_t fl = cflags ? cflags[cid] : 0;
+    const double acc = restrict_gather<D>(Lc, Lf, x, y, z, vf + (int64_t)k * Lf.V);
+    vc[(int64_t)k * Lc.V + cid] = ((fl >> (comp0 + k)) & 1) ? 0.0 : acc;
+}
+
+// Restriction of all components into the coarse level's right-hand side fused
+// with the start of its block-diagonal Chebyshev smoother from x = 0
+// (mgsolve.py:95, 103-106; the arithmetic of cheb_init_zero_bd_k): per coarse
+// dof rc = (P^T vf)[masked]; vc = r = rc; d = inv rc / theta_block; x = d.
+template <int D>
+__global__ void restrict_init_bd_kernel(Lat Lc, Lat Lf, int gx, const double* __restrict__ vf,
+                                        double* __restrict__ vc, const uint8_t* __restrict__ cflags,
+                                        const double* __restrict__ inv, const double* __restrict__ tu,
+                                        const double* __restrict__ tp, double* __restrict__ r,
+                                        double* __restrict__ d, double* __restrict__ x) {
+    pdl_wait();
+    int X, Y, Z, k;
+    if (!grid_point_comp(Lc, gx, X, Y, Z, k)) return;
+    const int64_t cid = vertex_id(Lc, X, Y, Z);
+    if (cid < 0) return;
+    const uint8_t fl = cflags[cid];
+    const int64_t g = (int64_t)k * Lc.V + cid;
+    const double iv = __ldg(inv + g);
+    const double th = k < D ? *tu : *tp;
+    const double acc = restrict_gather<D>(Lc, Lf, X, Y, Z, vf + (int64_t)k * Lf.V);
+    const double ri = ((fl >> k) & 1) ? 0.0 : acc;
+    const double di = (iv * ri) / th;
+    vc[g] = ri;
+    d[g] = di;
+    if (r) {                                     // (NULL: the first step is pffmg_cheb_first_bd)
+        r[g] = ri;
+        x[g] = 0.0 + di;
+    }
+}
+
+// All components of a coarse vertex in one thread (large levels, 3D: the
+// 9 / 27 fine ids of the vertex are looked up once).
+// vc[k] = sum_{fine f} P[f, c] vf[k][f]  for owned coarse vertices c, then masking.
+template <int D>
+__global__ void restrict_all_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vf,
                                 double* __restrict__ vc, const uint8_t* __restrict__ cflags) {
     pdl_wait();
     int x, y, z;
@@ -90,7 +189,7 @@ __global__ void restrict_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const doub
 // (mgsolve.py:95, 103-106; the arithmetic of cheb_init_zero_bd_k): per coarse
 // dof rc = (P^T vf)[masked]; vc = r = rc; d = inv rc / theta_block; x = d.
 template <int D>
-__global__ void restrict_init_bd_kernel(Lat Lc, Lat Lf, const double* __restrict__ vf, double* __restrict__ vc,
+__global__ void restrict_init_bd_all_kernel(Lat Lc, Lat Lf, const double* __restrict__ vf, double* __restrict__ vc,
                                         const uint8_t* __restrict__ cflags, const double* __restrict__ inv,
                                         const double* __restrict__ tu, const double* __restrict__ tp,
                                         double* __restrict__ r, double* __restrict__ d, double* __restrict__ x) {
@@ -137,8 +236,8 @@ __global__ void restrict_init_bd_kernel(Lat Lc, Lat Lf, const double* __restrict
 // vf[k][f] (=|+=) sum_c P[f, c] vc[k][c] for owned fine vertices, zeroed where
 // the fine dof is constrained.  Coarse corners in bit order (x fastest), as
 // the COO entries of fem.py:323-339; corners with a zero weight are skipped.
-template <int D>
-__global__ void prolongate_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vc,
+template <int D, int NC>
+__global__ void prolongate_kernel(Lat Lc, Lat Lf, int comp0, const double* __restrict__ vc,
                                   double* __restrict__ vf, const uint8_t* __restrict__ fflags,
                                   int accumulate) {
     pdl_wait();
@@ -147,6 +246,9 @@ __global__ void prolongate_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const do
     const int64_t fid = vertex_id(Lf, X, Y, Z);
     if (fid < 0) return;
     const uint8_t fl = fflags ? fflags[fid] : 0;
+    double cur[NC];                              // the fine values first: the long (DRAM) loads
+#pragma unroll
+    for (int k = 0; k < NC; ++k) cur[k] = accumulate ? vf[(int64_t)k * Lf.V + fid] : 0.0;
     // global coordinate along the cut axis decides the parity
     const int Yg = D == 3 ? Y : Y + Lf.plane0, Zg = D == 3 ? Z + Lf.plane0 : 0;
     const int shY = D == 3 ? 0 : Lc.plane0, shZ = D == 3 ? Lc.plane0 : 0;
@@ -162,19 +264,33 @@ __global__ void prolongate_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const do
         const bool used = !((bx && !ox) || (by && !oy) || (bz && !oz));
         cid[bits] = used ? vertex_id(Lc, bx ? hix : lox, by ? hiy : loy, D == 3 ? (bz ? hiz : loz) : 0) : -1;
     }
+    double cval[NC][1 << D];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        if (k >= ncomp) break;
+    for (int k = 0; k < NC; ++k)
+#pragma unroll
+        for (int bits = 0; bits < (1 << D); ++bits)
+            cval[k][bits] = cid[bits] >= 0 ? __ldg(vc + (int64_t)k * Lc.V + cid[bits]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
         double acc = 0.0;
 #pragma unroll
         for (int bits = 0; bits < (1 << D); ++bits)
-            if (cid[bits] >= 0) acc += w * __ldg(vc + (int64_t)k * Lc.V + cid[bits]);
+            if (cid[bits] >= 0) acc += w * cval[k][bits];
         const int64_t g = (int64_t)k * Lf.V + fid;
         if ((fl >> (comp0 + k)) & 1) acc = 0.0;
-        if (accumulate)
-            vf[g] += acc;
-        else
-            vf[g] = acc;
+        vf[g] = accumulate ? cur[k] + acc : acc;
+    }
+}
+
+template <int D>
+static void launch_prolongate(const Lat& Lc, const Lat& Lf, int n_comp, int comp0, const double* vc, double* vf,
+                              const uint8_t* fine_flags, int accumulate, cudaStream_t s) {
+    const dim3 g = grid_points(Lf, 128), b(128);
+    switch (n_comp) {
+        case 1: pdl_launch(prolongate_kernel<D, 1>, g, b, 0, s, Lc, Lf, comp0, vc, vf, fine_flags, accumulate); break;
+        case 2: pdl_launch(prolongate_kernel<D, 2>, g, b, 0, s, Lc, Lf, comp0, vc, vf, fine_flags, accumulate); break;
+        case 3: pdl_launch(prolongate_kernel<D, 3>, g, b, 0, s, Lc, Lf, comp0, vc, vf, fine_flags, accumulate); break;
+        default: pdl_launch(prolongate_kernel<D, 4>, g, b, 0, s, Lc, Lf, comp0, vc, vf, fine_flags, accumulate); break;
     }
 }
 
@@ -344,6 +460,19 @@ static dim3 grid_for(int64_t n) {
     return dim3((unsigned)b);
 }
 
+// Restriction into small 2D levels runs one thread per (coarse vertex,
+// component): the launch then has 3x the threads to hide the latency of the
+// gather (cfg2 V-cycle 621 -> 609 us, cfg1 159 -> 152 us).  Large 2D levels
+// (full-size restriction 16.4 -> 20.5 us) and 3D levels (27 taps: cfg4 37 ->
+// 70 us) keep all components of a vertex in one thread.
+static bool comp_parallel(const Lat& Lc) {
+    static const int64_t maxv = [] {
+        const char* e = getenv("PFFMG_RESTRICT_CP_MAXV");       // tuning: largest coarse level taking it
+        return e ? (int64_t)atoll(e) : (int64_t)1 << 17;
+    }();
+    return Lc.dim == 2 && Lc.V <= maxv;
+}
+
 }  // namespace pffmg
 
 using namespace pffmg;
@@ -361,12 +490,18 @@ extern "C" int pffmg_restrict(const pffmg_lattice* coarse, const pffmg_lattice* 
         pdl_launch(restrict_q2_kernel, dim3(grid_for((int64_t)(Lc.nx + 1) * (Lc.own_hi - Lc.own_lo))), dim3(256), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vf, vc, coarse_flags);
         return check_launch("pffmg_restrict");
     }
-    if (Lc.dim == 3)
-        pdl_launch(restrict_kernel<3>, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vf, vc,
-                                                                               coarse_flags);
-    else
-        pdl_launch(restrict_kernel<2>, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vf,
-                                                                                vc, coarse_flags);
+    dim3 g = grid_points(Lc, 128);
+    if (Lc.dim == 3) {
+        pdl_launch(restrict_all_kernel<3>, g, dim3(128), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vf, vc,
+                   coarse_flags);
+    } else if (comp_parallel(Lc)) {
+        const int gx = (int)g.x;
+        g.x *= (unsigned)n_comp;                 // one thread per (coarse vertex, component)
+        pdl_launch(restrict_kernel<2>, g, dim3(128), 0, as_stream(stream), Lc, Lf, gx, comp0, vf, vc, coarse_flags);
+    } else {
+        pdl_launch(restrict_all_kernel<2>, g, dim3(128), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vf, vc,
+                   coarse_flags);
+    }
     return check_launch("pffmg_restrict");
 }
 
@@ -384,9 +519,9 @@ extern "C" int pffmg_prolongate(const pffmg_lattice* coarse, const pffmg_lattice
         return check_launch("pffmg_prolongate");
     }
     if (Lf.dim == 3)
-        pdl_launch(prolongate_kernel<3>, dim3(grid_points(Lf, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
+        launch_prolongate<3>(Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate, as_stream(stream));
     else
-        pdl_launch(prolongate_kernel<2>, dim3(grid_points(Lf, 128)), dim3(128), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
+        launch_prolongate<2>(Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate, as_stream(stream));
     return check_launch("pffmg_prolongate");
 }
 
@@ -431,11 +566,18 @@ extern "C" int pffmg_restrict_init_bd(const pffmg_lattice* coarse, const pffmg_l
     PFFMG_REQUIRE(!q2, "pffmg_restrict_init_bd: Q1 lattices only");
     PFFMG_REQUIRE(vf && vc && coarse_flags && invdiag && theta_u && theta_p && d && !r == !x,
                   "pffmg_restrict_init_bd: bad arguments");
-    if (Lc.dim == 3)
-        pdl_launch(restrict_init_bd_kernel<3>, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf,
-                   vf, vc, coarse_flags, invdiag, theta_u, theta_p, r, d, x);
-    else
-        pdl_launch(restrict_init_bd_kernel<2>, dim3(grid_points(Lc, 128)), dim3(128), 0, as_stream(stream), Lc, Lf,
-                   vf, vc, coarse_flags, invdiag, theta_u, theta_p, r, d, x);
+    dim3 g = grid_points(Lc, 128);
+    if (Lc.dim == 3) {
+        pdl_launch(restrict_init_bd_all_kernel<3>, g, dim3(128), 0, as_stream(stream), Lc, Lf, vf, vc, coarse_flags,
+                   invdiag, theta_u, theta_p, r, d, x);
+    } else if (comp_parallel(Lc)) {
+        const int gx = (int)g.x;
+        g.x *= (unsigned)(Lc.dim + 1);           // one thread per (coarse vertex, component)
+        pdl_launch(restrict_init_bd_kernel<2>, g, dim3(128), 0, as_stream(stream), Lc, Lf, gx, vf, vc, coarse_flags,
+                   invdiag, theta_u, theta_p, r, d, x);
+    } else {
+        pdl_launch(restrict_init_bd_all_kernel<2>, g, dim3(128), 0, as_stream(stream), Lc, Lf, vf, vc, coarse_flags,
+                   invdiag, theta_u, theta_p, r, d, x);
+    }
     return check_launch("pffmg_restrict_init_bd");
 }
