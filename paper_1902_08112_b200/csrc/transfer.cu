@@ -329,68 +329,90 @@ __device__ __forceinline__ int q2_prolong_taps(int j, int (&idx)[3], double (&w)
 // Lc / Lf are the NODE lattices (nx = 2 * cells): nxn = nx + 1 nodes per row.
 // Slabs: the output lattice's owned node rows only; tap parities and the
 // coarse/fine row pairing use global rows (local row + plane0).
-__global__ void restrict_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vf,
+// One thread per (coarse node, component): blockIdx.y = owned coarse row,
+// blockIdx.z = component; the (up to 5 x 5) fine values are loaded before the
+// sum, which keeps the increasing-fine-id order of the CSR product.
+__global__ void restrict_q2_kernel(Lat Lc, Lat Lf, int comp0, const double* __restrict__ vf,
                                    double* __restrict__ vc, const uint8_t* __restrict__ cflags) {
     pdl_wait();
     const int nxc = Lc.nx + 1, nxf = Lf.nx + 1, nyf = Lf.ny + 1;
-    const int64_t npts = (int64_t)nxc * (Lc.own_hi - Lc.own_lo);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(i % nxc), y = Lc.own_lo + (int)(i / nxc);
-        const int yg = y + Lc.plane0;
-        int ox[5], oy[5];
-        double wx[5], wy[5];
-        const int nx5 = q2_restrict_taps(x, ox, wx), ny5 = q2_restrict_taps(yg, oy, wy);
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int b = 0; b < ny5; ++b) {                    // increasing fine id (CSR order)
-            const int fy = 2 * yg + oy[b] - Lf.plane0;
-            if (fy < 0 || fy >= nyf) continue;
-            for (int a = 0; a < nx5; ++a) {
-                const int fx = 2 * x + ox[a];
-                if (fx < 0 || fx >= nxf) continue;
-                const int64_t fid = (int64_t)fy * nxf + fx;
-                const double w = wx[a] * wy[b];
+    const int x = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+    if (x >= nxc) return;
+    const int y = Lc.own_lo + (int)blockIdx.y, k = (int)blockIdx.z;
+    const int yg = y + Lc.plane0;
+    int ox[5], oy[5];
+    double wx[5], wy[5];
+    const int nx5 = q2_restrict_taps(x, ox, wx), ny5 = q2_restrict_taps(yg, oy, wy);
+    const double* __restrict__ vfk = vf + (int64_t)k * Lf.V;
+    double val[25];
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (k < ncomp) acc[k] += w * __ldg(vf + (int64_t)k * Lf.V + fid);
-            }
-        }
-        const int64_t cid = (int64_t)y * nxc + x;
-        const uint8_t fl = cflags ? cflags[cid] : 0;
+    for (int b = 0; b < 5; ++b) {
+        const int fy = 2 * yg + oy[b < ny5 ? b : 0] - Lf.plane0;
+        const bool oky = b < ny5 && fy >= 0 && fy < nyf;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (k >= ncomp) break;
-            vc[(int64_t)k * Lc.V + cid] = ((fl >> (comp0 + k)) & 1) ? 0.0 : acc[k];
+        for (int a = 0; a < 5; ++a) {
+            const int fx = 2 * x + ox[a < nx5 ? a : 0];
+            const bool ok = oky && a < nx5 && fx >= 0 && fx < nxf;
+            val[5 * b + a] = ok ? __ldg(vfk + (int64_t)fy * nxf + fx) : 0.0;
         }
     }
+    double acc = 0.0;
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+        const int fy = 2 * yg + oy[b < ny5 ? b : 0] - Lf.plane0;
+        if (!(b < ny5 && fy >= 0 && fy < nyf)) continue;
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+            const int fx = 2 * x + ox[a < nx5 ? a : 0];
+            if (!(a < nx5 && fx >= 0 && fx < nxf)) continue;
+            acc += (wx[a] * wy[b]) * val[5 * b + a];
+        }
+    }
+    const int64_t cid = (int64_t)y * nxc + x;
+    const uint8_t fl = cflags ? cflags[cid] : 0;
+    vc[(int64_t)k * Lc.V + cid] = ((fl >> (comp0 + k)) & 1) ? 0.0 : acc;
 }
 
-__global__ void prolongate_q2_kernel(Lat Lc, Lat Lf, int ncomp, int comp0, const double* __restrict__ vc,
+// blockIdx.y = owned fine row; NC components per thread, the fine values and
+// the (up to 3 x 3) coarse values loaded before the sums.
+template <int NC>
+__global__ void prolongate_q2_kernel(Lat Lc, Lat Lf, int comp0, const double* __restrict__ vc,
                                      double* __restrict__ vf, const uint8_t* __restrict__ fflags,
                                      int accumulate) {
     pdl_wait();
     const int nxc = Lc.nx + 1, nxf = Lf.nx + 1;
-    const int64_t npts = (int64_t)nxf * (Lf.own_hi - Lf.own_lo);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npts;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int X = (int)(i % nxf), Y = Lf.own_lo + (int)(i / nxf);
-        int ix[3], iy[3];
-        double wx[3], wy[3];
-        const int nx3 = q2_prolong_taps(X, ix, wx), ny3 = q2_prolong_taps(Y + Lf.plane0, iy, wy);
-        const int64_t fid = (int64_t)Y * nxf + X;
-        const uint8_t fl = fflags ? fflags[fid] : 0;
-        for (int k = 0; k < ncomp; ++k) {
-            double acc = 0.0;
-            for (int b = 0; b < ny3; ++b)
-                for (int a = 0; a < nx3; ++a)
-                    acc += (wx[a] * wy[b]) * vc[(int64_t)k * Lc.V + (int64_t)(iy[b] - Lc.plane0) * nxc + ix[a]];
-            const int64_t g = (int64_t)k * Lf.V + fid;
-            if ((fl >> (comp0 + k)) & 1) acc = 0.0;
-            if (accumulate)
-                vf[g] += acc;
-            else
-                vf[g] = acc;
-        }
+    const int X = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+    if (X >= nxf) return;
+    const int Y = Lf.own_lo + (int)blockIdx.y;
+    const int64_t fid = (int64_t)Y * nxf + X;
+    double cur[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) cur[k] = accumulate ? vf[(int64_t)k * Lf.V + fid] : 0.0;
+    int ix[3], iy[3];
+    double wx[3], wy[3];
+    const int nx3 = q2_prolong_taps(X, ix, wx), ny3 = q2_prolong_taps(Y + Lf.plane0, iy, wy);
+    const uint8_t fl = fflags ? fflags[fid] : 0;
+    double cv[NC][9];
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                cv[k][3 * b + a] = (b < ny3 && a < nx3)
+                                       ? __ldg(vc + (int64_t)k * Lc.V + (int64_t)(iy[b] - Lc.plane0) * nxc + ix[a])
+                                       : 0.0;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        double acc = 0.0;
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                if (b < ny3 && a < nx3) acc += (wx[a] * wy[b]) * cv[k][3 * b + a];
+        const int64_t g = (int64_t)k * Lf.V + fid;
+        if ((fl >> (comp0 + k)) & 1) acc = 0.0;
+        vf[g] = accumulate ? cur[k] + acc : acc;
     }
 }
 
@@ -452,13 +474,6 @@ static int check_pair(const pffmg_lattice* c, const pffmg_lattice* f, Lat* Lc, L
     return PFFMG_OK;
 }
 
-static dim3 grid_for(int64_t n) {
-    int64_t b = (n + 255) / 256;
-    const int64_t cap = (int64_t)sm_count() * 16;
-    if (b > cap) b = cap;
-    if (b < 1) b = 1;
-    return dim3((unsigned)b);
-}
 
 // Restriction into small 2D levels runs one thread per (coarse vertex,
 // component): the launch then has 3x the threads to hide the latency of the
@@ -487,7 +502,9 @@ extern "C" int pffmg_restrict(const pffmg_lattice* coarse, const pffmg_lattice* 
     PFFMG_REQUIRE(vf && vc && n_comp >= 1 && comp0 >= 0 && comp0 + n_comp <= Lc.dim + 1,
                   "pffmg_restrict: bad arguments");
     if (q2) {
-        pdl_launch(restrict_q2_kernel, dim3(grid_for((int64_t)(Lc.nx + 1) * (Lc.own_hi - Lc.own_lo))), dim3(256), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vf, vc, coarse_flags);
+        pdl_launch(restrict_q2_kernel,
+                   dim3((unsigned)((Lc.nx + 1 + 127) / 128), (unsigned)(Lc.own_hi - Lc.own_lo), (unsigned)n_comp),
+                   dim3(128), 0, as_stream(stream), Lc, Lf, comp0, vf, vc, coarse_flags);
         return check_launch("pffmg_restrict");
     }
     dim3 g = grid_points(Lc, 128);
@@ -515,7 +532,13 @@ extern "C" int pffmg_prolongate(const pffmg_lattice* coarse, const pffmg_lattice
     PFFMG_REQUIRE(vf && vc && n_comp >= 1 && comp0 >= 0 && comp0 + n_comp <= Lc.dim + 1,
                   "pffmg_prolongate: bad arguments");
     if (q2) {
-        pdl_launch(prolongate_q2_kernel, dim3(grid_for((int64_t)(Lf.nx + 1) * (Lf.own_hi - Lf.own_lo))), dim3(256), 0, as_stream(stream), Lc, Lf, n_comp, comp0, vc, vf, fine_flags, accumulate);
+        const dim3 g((unsigned)((Lf.nx + 1 + 127) / 128), (unsigned)(Lf.own_hi - Lf.own_lo)), b(128);
+        const cudaStream_t s = as_stream(stream);
+        switch (n_comp) {
+            case 1: pdl_launch(prolongate_q2_kernel<1>, g, b, 0, s, Lc, Lf, comp0, vc, vf, fine_flags, accumulate); break;
+            case 2: pdl_launch(prolongate_q2_kernel<2>, g, b, 0, s, Lc, Lf, comp0, vc, vf, fine_flags, accumulate); break;
+            default: pdl_launch(prolongate_q2_kernel<3>, g, b, 0, s, Lc, Lf, comp0, vc, vf, fine_flags, accumulate); break;
+        }
         return check_launch("pffmg_prolongate");
     }
     if (Lf.dim == 3)
