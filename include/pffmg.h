@@ -294,7 +294,7 @@ int pffmg_restrict(const pffmg_lattice* coarse, const pffmg_lattice* fine, int n
  * dim+1 components with constrained coarse entries 0, fused with the coarse
  * level's block-diagonal Chebyshev start from x = 0: r = vc, d = invdiag vc /
  * theta (theta_u for the displacement block, theta_p for phi; device scalars),
- * x = d.  Q1 lattices. */
+ * x = d. */
 int pffmg_restrict_init_bd(const pffmg_lattice* coarse, const pffmg_lattice* fine, const double* vf,
                            double* vc, const uint8_t* coarse_flags, const double* invdiag,
                            const double* theta_u, const double* theta_p, double* r, double* d,

@@ -332,8 +332,14 @@ __device__ __forceinline__ int q2_prolong_taps(int j, int (&idx)[3], double (&w)
 // One thread per (coarse node, component): blockIdx.y = owned coarse row,
 // blockIdx.z = component; the (up to 5 x 5) fine values are loaded before the
 // sum, which keeps the increasing-fine-id order of the CSR product.
+// With d set (pffmg_restrict_init_bd on Q2 levels): all components from comp0 =
+// 0, fused with the coarse level's block-diagonal Chebyshev start from x = 0
+// (the arithmetic of cheb_init_zero_bd_k; r / x optional as there).
 __global__ void restrict_q2_kernel(Lat Lc, Lat Lf, int comp0, const double* __restrict__ vf,
-                                   double* __restrict__ vc, const uint8_t* __restrict__ cflags) {
+                                   double* __restrict__ vc, const uint8_t* __restrict__ cflags,
+                                   const double* __restrict__ inv, const double* __restrict__ tu,
+                                   const double* __restrict__ tp, double* __restrict__ r,
+                                   double* __restrict__ d, double* __restrict__ xs) {
     pdl_wait();
     const int nxc = Lc.nx + 1, nxf = Lf.nx + 1, nyf = Lf.ny + 1;
     const int x = (int)(blockIdx.x * blockDim.x + threadIdx.x);
@@ -370,7 +376,17 @@ __global__ void restrict_q2_kernel(Lat Lc, Lat Lf, int comp0, const double* __re
     }
     const int64_t cid = (int64_t)y * nxc + x;
     const uint8_t fl = cflags ? cflags[cid] : 0;
-    vc[(int64_t)k * Lc.V + cid] = ((fl >> (comp0 + k)) & 1) ? 0.0 : acc;
+    const int64_t g = (int64_t)k * Lc.V + cid;
+    const double ri = ((fl >> (comp0 + k)) & 1) ? 0.0 : acc;
+    vc[g] = ri;
+    if (d) {
+        const double di = (__ldg(inv + g) * ri) / (k < 2 ? *tu : *tp);
+        d[g] = di;
+        if (r) {
+            r[g] = ri;
+            xs[g] = 0.0 + di;
+        }
+    }
 }
 
 // blockIdx.y = owned fine row; NC components per thread, the fine values and
@@ -504,7 +520,9 @@ extern "C" int pffmg_restrict(const pffmg_lattice* coarse, const pffmg_lattice* 
     if (q2) {
         pdl_launch(restrict_q2_kernel,
                    dim3((unsigned)((Lc.nx + 1 + 127) / 128), (unsigned)(Lc.own_hi - Lc.own_lo), (unsigned)n_comp),
-                   dim3(128), 0, as_stream(stream), Lc, Lf, comp0, vf, vc, coarse_flags);
+                   dim3(128), 0, as_stream(stream), Lc, Lf, comp0, vf, vc, coarse_flags, (const double*)nullptr,
+                   (const double*)nullptr, (const double*)nullptr, (double*)nullptr, (double*)nullptr,
+                   (double*)nullptr);
         return check_launch("pffmg_restrict");
     }
     dim3 g = grid_points(Lc, 128);
@@ -586,9 +604,14 @@ extern "C" int pffmg_restrict_init_bd(const pffmg_lattice* coarse, const pffmg_l
     bool q2 = false;
     int rc = check_pair(coarse, fine, &Lc, &Lf, &q2);
     if (rc) return rc;
-    PFFMG_REQUIRE(!q2, "pffmg_restrict_init_bd: Q1 lattices only");
     PFFMG_REQUIRE(vf && vc && coarse_flags && invdiag && theta_u && theta_p && d && !r == !x,
                   "pffmg_restrict_init_bd: bad arguments");
+    if (q2) {
+        pdl_launch(restrict_q2_kernel,
+                   dim3((unsigned)((Lc.nx + 1 + 127) / 128), (unsigned)(Lc.own_hi - Lc.own_lo), 3u), dim3(128), 0,
+                   as_stream(stream), Lc, Lf, 0, vf, vc, coarse_flags, invdiag, theta_u, theta_p, r, d, x);
+        return check_launch("pffmg_restrict_init_bd");
+    }
     dim3 g = grid_points(Lc, 128);
     if (Lc.dim == 3) {
         pdl_launch(restrict_init_bd_all_kernel<3>, g, dim3(128), 0, as_stream(stream), Lc, Lf, vf, vc, coarse_flags,

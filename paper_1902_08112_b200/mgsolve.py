@@ -875,7 +875,6 @@ class _NativeCycle:
         """Restriction into level l can carry level l's smoother start (x = 0)."""
         Lc = self.levels[l]
         return (FUSED_DESCENT and self.comm is None and l >= 1 and
-                getattr(Lc.op.lat.info, "order", 1) == 1 and
                 self._bd_pair_ok(Lc, ("s", l, 0), ("s", l, 1), True))
 
     def _coarse_into_x(self, pre=True):
