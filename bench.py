@@ -721,13 +721,22 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
 
     def load_for(seconds):
-        """Keep the GPU busy with the same work so nvidia-smi sees it under load."""
+        """Keep the GPU busy with the same work so nvidia-smi sees it under load.
+        With several ranks every step is a halo exchange, so all ranks must run
+        the same number of steps: they agree after every batch (max over ranks
+        of "my time is not up yet") instead of each watching its own clock."""
         t_end = time.perf_counter() + seconds
-        while time.perf_counter() < t_end:
+        more = True
+        while more:
             for _ in range(20):
                 flush.zero_()
                 step()
             torch.cuda.synchronize()
+            more = time.perf_counter() < t_end
+            if ws > 1:
+                f = torch.tensor([1.0 if more else 0.0], device="cuda" if args.backend == "nccl" else "cpu")
+                torch.distributed.all_reduce(f, op=torch.distributed.ReduceOp.MAX)
+                more = bool(f.item() > 0.0)
 
     barrier = (lambda: torch.distributed.barrier()) if ws > 1 else None
     with Clocks(local) as clk:
@@ -923,6 +932,9 @@ def run_gpu(args):
 
 
 def main():
+    if os.environ.get("PFFMG_BENCH_WATCHDOG"):      # debugging aid: dump every thread's stack after N seconds
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["PFFMG_BENCH_WATCHDOG"]), exit=False)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
